@@ -1,0 +1,202 @@
+/*
+ * sacd.h -- C ABI of the B200-native SaCD hot path (libsacd.so).
+ *
+ * Saturating Coordinate Descent for sparse nonnegative CP tensor factorization,
+ * arXiv 2003.03572 ("the paper"; line numbers "P:n" refer to PAPER.md).  The problem the
+ * library solves is the paper's problem statement: given a sparse 3-way tensor X as the
+ * set Omega of observed cells (q,p,s) with values x_qps (Table 2) and a rank R
+ * (P:171), find nonnegative U (Q x R), V (P x R), W (S x R) minimising
+ *     f(U,V,W) = || X - [[U,V,W]] ||^2                    (eq:ntf; Eq 6-7)
+ * by `maxiters` sweeps of Algorithm 1 from a random initialisation.  The
+ * readings of ambiguous passages are listed in DESIGN.md section 3 (C1-C19).
+ *
+ * Conventions for every entry point
+ *   - Every call returns an int status (sacd_status); no C++ exception crosses the ABI.
+ *     A thread-local message for the last failure is available from sacd_last_error().
+ *   - SACD_ECUDA / SACD_ENCCL are sticky: after one, only sacd_free() is valid.
+ *   - Matrices are row-major.  "Host" pointers are ordinary CPU memory; arguments marked
+ *     "host or device" may be either (detected with cudaPointerGetAttributes).
+ *   - A context is used from one host thread at a time.  All device memory, streams,
+ *     events and graphs are owned by the context and released by sacd_free().
+ *   - Calls are stream-ordered on the context's stream; calls that return data to the
+ *     host synchronise that stream before returning.
+ */
+#ifndef SACD_H
+#define SACD_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SACD_ABI_VERSION 1
+
+typedef struct sacd_ctx sacd_ctx; /* opaque; owned by the library until sacd_free */
+
+typedef enum {
+  SACD_OK = 0,
+  SACD_EINVAL = -1,     /* bad argument: dims < 1, rank not in [1,256], nnz < 0, bad options   */
+  SACD_ERANGE = -2,     /* a coordinate index >= its mode length                              */
+  SACD_EDUP = -3,       /* duplicate (q,p,s) (Omega is a set, Table 2)           */
+  SACD_ENONFINITE = -4, /* NaN or Inf value                                                   */
+  SACD_ENOMEM = -5,     /* device or host allocation failed                                   */
+  SACD_ECUDA = -6,      /* CUDA error (sticky)                                                */
+  SACD_ENCCL = -7,      /* NCCL error (sticky)                                                */
+  SACD_ESTATE = -8      /* bad mode / ld / call order                                         */
+} sacd_status;
+
+/* Lipschitz constant used in the importance (Eq 20). */
+enum {
+  SACD_L_DIAG = 0, /* L_r = h_rr, the Gram-Hadamard diagonal (Eq 15): default (C5)    */
+  SACD_L_FROB = 1  /* L = ||H||_F, Alg 1 line "L = ||H||" literally (Lemma 1)    */
+};
+
+/* Element selection. */
+enum {
+  SACD_VARIANT_GS_LAGGED = 0, /* Alg 1 selection with the lagged ti branch (C10) */
+  SACD_VARIANT_SELECT_OFF = 1 /* the k==1 rule (z > 0) every sweep: projected GS CD            */
+};
+
+/* Arithmetic precision of factors, z_prev, MTTKRP and the row update (Grams, H and all
+ * reductions are fp64 in both). */
+enum { SACD_F64 = 0, SACD_F32 = 1 };
+
+/* Branch of the selection rule for one mode pass (C10). */
+enum { SACD_BR_AUTO = -1, SACD_BR_FIRST = 0, SACD_BR_EQ24 = 1, SACD_BR_EQ27 = 2 };
+
+typedef struct {
+  uint32_t struct_size;       /* = sizeof(sacd_options) (ABI versioning)                    */
+  int32_t precision;          /* SACD_F64 (default) | SACD_F32                              */
+  int32_t l_mode;             /* SACD_L_DIAG (default) | SACD_L_FROB                        */
+  int32_t variant;            /* SACD_VARIANT_GS_LAGGED (default) | SACD_VARIANT_SELECT_OFF */
+  int32_t device;             /* CUDA ordinal; -1 = the calling thread's current device      */
+  int32_t world_size, rank;   /* slice sharding across GPUs (1, 0 = single GPU)             */
+  const void *nccl_unique_id; /* 128 bytes from sacd_nccl_unique_id() on rank 0 (G > 1)     */
+  void *stream;               /* cudaStream_t to run on, or NULL = library-owned stream     */
+  int32_t use_graph;          /* 1 (default): sacd_iterate replays a captured CUDA graph    */
+  int32_t profile;            /* 1: time every kernel class with CUDA events (no graph)     */
+  int32_t nnz_per_item;       /* MTTKRP work-item size in nonzeros (0 = default)            */
+  int32_t reserved[7];
+} sacd_options;
+
+/* Per-sweep statistics (device-side ring, read by sacd_stats). */
+typedef struct {
+  int32_t k;             /* sweep index, 1-based                                            */
+  int32_t branch[3];     /* SACD_BR_* used for U, V, W                                      */
+  double objective;      /* f^k after the W pass (Eq 6-7 via the Gram identity, C1)          */
+  double fit;            /* 1 - sqrt(f)/||X|| (C16)                                          */
+  double ti[3];          /* total importance ti^k per mode (Eq 25)                    */
+  int64_t E[3];          /* #elements selected (Lemma 4)                              */
+  int64_t E_changed[3];  /* #selected with a nonzero step (C14)                              */
+} sacd_iter_stats;
+
+typedef struct {
+  int64_t dims[3];
+  int64_t nnz;      /* this rank's nonzeros (all of them for G = 1)                         */
+  int32_t rank;     /* R                                                                    */
+  int32_t pitch;    /* factor row pitch on device (R rounded up to the kernel tile)          */
+  int32_t precision;
+  int32_t l_mode, variant;
+  int32_t k;        /* completed sweeps                                                      */
+  int32_t mode_a[3], mode_b[3]; /* the "a" (shorter) and "b" other modes of each layout     */
+  double xnorm2;    /* ||X||^2 in fp64                                                       */
+  int64_t items[3]; /* MTTKRP work items per mode                                            */
+  int64_t split_rows[3];
+  int64_t device_bytes;
+} sacd_info;
+
+void sacd_default_options(sacd_options *opt);
+
+/* Build a context: validate the COO tensor, copy it to the device, build the three
+ * mode-sorted layouts (Table 2 slices Omega^U_q, Omega^V_p, Omega^W_s; key (i_n, i_a, i_b)
+ * with a the shorter other mode), compute ||X||^2 (fp64), initialise the factors
+ * uniformly in [0,1) from `seed` (Alg 1 input; reading C12) and their Grams, and
+ * capture the sweep graph.
+ *   coords : host or device, nnz x 3 uint32 (q,p,s), 0-based.   vals : host or device, fp32.
+ *   dims   : host, {Q, P, S}, each >= 1 and < 2^32.              rank : 1..256.
+ * Errors: EINVAL, ERANGE, EDUP, ENONFINITE, ENOMEM, ECUDA.  nnz == 0 is legal.
+ * The caller keeps ownership of coords/vals and may free them when the call returns. */
+int sacd_init(sacd_ctx **out, const uint32_t *coords, const float *vals, int64_t nnz, const int64_t dims[3],
+              int32_t rank, uint64_t seed, const sacd_options *opt);
+
+/* Run n_sweeps sweeps of Alg 1 (each: U, V, W mode updates, then the objective),
+ * asynchronously on the context stream; k += n_sweeps. */
+int sacd_iterate(sacd_ctx *ctx, int32_t n_sweeps);
+
+/* Block until all queued work of the context has finished. */
+int sacd_sync(sacd_ctx *ctx);
+
+/* Objective f (Eq 6-7, all cells, C1) and fit = 1 - sqrt(f)/||X|| after the last completed
+ * sweep (k = 0: the initial factors).  Synchronous. */
+int sacd_fit(sacd_ctx *ctx, double *objective, double *fit);
+
+/* Copy factor `mode` (0=U, 1=V, 2=W) into host memory `out` (I_mode rows, leading
+ * dimension ld >= rank, fp64).  Errors: ESTATE for a bad mode or ld. */
+int sacd_factors(sacd_ctx *ctx, int32_t mode, double *out, int64_t ld);
+
+/* Copy up to `cap` per-sweep records, oldest first, into host `out`; *n_out = count. */
+int sacd_stats(sacd_ctx *ctx, sacd_iter_stats *out, int32_t cap, int32_t *n_out);
+
+int sacd_get_info(sacd_ctx *ctx, sacd_info *out);
+
+void sacd_free(sacd_ctx *ctx);
+
+const char *sacd_last_error(void);
+
+/* --------------------------------------------------------------------------------------
+ * Component entry points (teacher forcing, parity tests and kernel timing).  Each runs the
+ * same kernels the sweep runs.
+ * ------------------------------------------------------------------------------------ */
+
+/* Overwrite factor `mode` from host fp64 `in` (ld >= rank; columns >= rank ignored) and
+ * refresh its Gram.  Values are rounded to the context precision. */
+int sacd_set_factors(sacd_ctx *ctx, int32_t mode, const double *in, int64_t ld);
+
+/* Read / overwrite the previous importances z^{k-1} of `mode` (Alg 1). */
+int sacd_get_zprev(sacd_ctx *ctx, int32_t mode, double *out, int64_t ld);
+int sacd_set_zprev(sacd_ctx *ctx, int32_t mode, const double *in, int64_t ld);
+
+/* Sparse MTTKRP for `mode` with the current factors:
+ *   M_(i,r) = sum_{e in Omega^(mode)_i} x_e a_(e,r) b_(e,r)   (Eq 9 first term, P:340;
+ *   column form P:623-625, 655, 682), written to host `out` (I_mode x ld, fp64). */
+int sacd_mttkrp(sacd_ctx *ctx, int32_t mode, double *out, int64_t ld);
+
+/* Time `reps` back-to-back launches of the MTTKRP of `mode` with CUDA events on the context
+ * stream; *ms = mean milliseconds per launch. */
+int sacd_time_mttkrp(sacd_ctx *ctx, int32_t mode, int32_t reps, double *ms);
+
+/* Gram G_mode = F^T F (fp64, R x R, host `out`), and H = G_a * G_b for `mode` (Eq 10 /
+ * ppdei / ppdet: the Hadamard product of the OTHER factors' Grams). */
+int sacd_gram(sacd_ctx *ctx, int32_t mode, double *out);
+int sacd_hessian(sacd_ctx *ctx, int32_t mode, double *out);
+
+/* One mode update (MTTKRP, H, the column-wise SaCD step, Gram refresh) with the selection
+ * branch `branch` (SACD_BR_AUTO = the device rule C10, which also advances the history).
+ * Optional host outputs: decisions (I_mode x rank bytes, 1 = element selected), ti, E,
+ * E_changed.  Synchronous. */
+int sacd_mode_update(sacd_ctx *ctx, int32_t mode, int32_t branch, uint8_t *decisions, double *ti, int64_t *E,
+                     int64_t *E_changed);
+
+/* Copy the mode-sorted layout of `mode` to host: idx_a/idx_b/val have nnz entries (the
+ * indices in modes mode_a/mode_b of sacd_info), row_ptr has I_mode + 1 (int64). */
+int sacd_layout(sacd_ctx *ctx, int32_t mode, uint32_t *idx_a, uint32_t *idx_b, float *val, int64_t *row_ptr);
+
+/* Profiling (opt.profile = 1): per kernel class, total milliseconds and launch count
+ * accumulated by sacd_iterate since the last reset.  Classes: 0 mttkrp, 1 split-row
+ * fix-up, 2 hessian/branch, 3 SaCD row update, 4 Gram, 5 finalize/fit.  Synchronous. */
+#define SACD_NUM_KCLASS 6
+int sacd_profile_read(sacd_ctx *ctx, double ms[SACD_NUM_KCLASS], int64_t launches[SACD_NUM_KCLASS]);
+int sacd_profile_reset(sacd_ctx *ctx);
+
+/* ABI self-description for bindings: out = {SACD_ABI_VERSION, sizeof(sacd_options),
+ * sizeof(sacd_iter_stats), sizeof(sacd_info)}.  Needs no GPU. */
+int sacd_abi_sizes(int32_t out[4]);
+
+/* Multi-GPU: a fresh 128-byte NCCL unique id (rank 0), to be broadcast by the caller. */
+int sacd_nccl_unique_id(void *out128);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SACD_H */

@@ -1,0 +1,705 @@
+// capi.cu -- the C ABI of libsacd (include/sacd.h): context lifetime, the MTTKRP work
+// partition (host-side planning over row_ptr, done once at init), the sweep CUDA graph,
+// teacher-forcing entry points and profiling.
+#include <string.h>
+
+#include <algorithm>
+#include <new>
+#include <vector>
+
+#include "sacd_internal.cuh"
+
+struct sacd_ctx : public sacd::Context {};
+
+namespace sacd {
+
+static thread_local std::string g_err;
+void set_error(const std::string &m) { g_err = m; }
+
+// ------------------------------------------------------------------ profiling events
+static int prof_flush(Context &c) {
+  if (c.ev_pending.empty()) {
+    c.ev_next = 0;
+    return SACD_OK;
+  }
+  SACD_CUDA_TRY(cudaStreamSynchronize(c.stream));
+  for (auto &p : c.ev_pending) {
+    float ms = 0.f;
+    SACD_CUDA_TRY(cudaEventElapsedTime(&ms, c.ev_pool[p.second], c.ev_pool[p.second + 1]));
+    c.prof_ms[p.first] += ms;
+    c.prof_n[p.first] += 1;
+  }
+  c.ev_pending.clear();
+  c.ev_next = 0;
+  return SACD_OK;
+}
+
+int prof_begin(Context &c, int kclass) {
+  (void)kclass;
+  if (!c.opt.profile) return -1;
+  if (c.ev_next + 2 > 16384) {
+    if (prof_flush(c) != SACD_OK) return -1;
+  }
+  while (c.ev_pool.size() < c.ev_next + 2) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return -1;
+    c.ev_pool.push_back(e);
+  }
+  const int idx = (int)c.ev_next;
+  c.ev_next += 2;
+  if (cudaEventRecord(c.ev_pool[idx], c.stream) != cudaSuccess) return -1;
+  return idx;
+}
+
+int prof_end(Context &c, int kclass, int idx) {
+  if (idx < 0) return SACD_OK;
+  SACD_CUDA_TRY(cudaEventRecord(c.ev_pool[idx + 1], c.stream));
+  c.ev_pending.push_back({kclass, idx});
+  return SACD_OK;
+}
+
+// ------------------------------------------------------------------ MTTKRP work partition
+// Items hold whole rows with <= T nonzeros in total and <= maxrows rows; a row with more
+// than T nonzeros is cut into ceil(nnz/T) row-relative segments, each writing a partial
+// slot that k_fixup sums in slot order (deterministic).
+static void build_items(const std::vector<long long> &rp, long long I, long long T, long long maxrows,
+                        std::vector<WorkItem> &items, std::vector<SplitRow> &splits, long long &nslots) {
+  items.clear();
+  splits.clear();
+  nslots = 0;
+  long long i = 0;
+  while (i < I) {
+    const long long li = rp[i + 1] - rp[i];
+    if (li > T) {
+      const long long nseg = (li + T - 1) / T;
+      SplitRow sr;
+      sr.slot0 = nslots;
+      sr.nslots = nseg;
+      sr.row = (int)i;
+      sr.pad = 0;
+      for (long long s = 0; s < nseg; ++s) {
+        WorkItem w;
+        w.nz0 = rp[i] + s * T;
+        w.nz1 = std::min(rp[i] + (s + 1) * T, rp[i + 1]);
+        w.row0 = (int)i;
+        w.row1 = (int)(i + 1);
+        w.slot = nslots++;
+        items.push_back(w);
+      }
+      splits.push_back(sr);
+      ++i;
+      continue;
+    }
+    long long j = i, tot = 0;
+    while (j < I && j - i < maxrows) {
+      const long long l = rp[j + 1] - rp[j];
+      if (l > T) break;
+      if (tot + l > T && j > i) break;
+      tot += l;
+      ++j;
+    }
+    WorkItem w;
+    w.nz0 = rp[i];
+    w.nz1 = rp[j];
+    w.row0 = (int)i;
+    w.row1 = (int)j;
+    w.slot = -1;
+    items.push_back(w);
+    i = j;
+  }
+}
+
+static int capture_graph(Context &c) {
+  if (c.graph_exec) {
+    cudaGraphExecDestroy(c.graph_exec);
+    c.graph_exec = nullptr;
+  }
+  if (c.graph) {
+    cudaGraphDestroy(c.graph);
+    c.graph = nullptr;
+  }
+  if (!c.opt.use_graph || c.opt.profile) return SACD_OK;
+  SACD_CUDA_TRY(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
+  int rc = SACD_OK;
+  for (int n = 0; n < 3 && rc == SACD_OK; ++n) rc = launch_mode_update(c, n, SACD_BR_AUTO, n == 0, n == 2, nullptr);
+  cudaGraph_t g = nullptr;
+  cudaError_t e = cudaStreamEndCapture(c.stream, &g);
+  if (rc != SACD_OK) {
+    if (g) cudaGraphDestroy(g);
+    return rc;
+  }
+  SACD_CUDA_TRY(e);
+  c.graph = g;
+  SACD_CUDA_TRY(cudaGraphInstantiate(&c.graph_exec, c.graph, 0));
+  return SACD_OK;
+}
+
+static int sweep_eager(Context &c) {
+  for (int n = 0; n < 3; ++n) SACD_TRY(launch_mode_update(c, n, SACD_BR_AUTO, n == 0, n == 2, nullptr));
+  return SACD_OK;
+}
+
+static void destroy(sacd_ctx *c) {
+  if (!c) return;
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
+  if (c->graph) cudaGraphDestroy(c->graph);
+  for (auto e : c->ev_pool) cudaEventDestroy(e);
+  for (int n = 0; n < 3; ++n) {
+    ModeData &m = c->m[n];
+    cudaFree(m.idx_a);
+    cudaFree(m.idx_b);
+    cudaFree(m.val);
+    cudaFree(m.row_ptr);
+    cudaFree(m.items);
+    cudaFree(m.splits);
+    cudaFree(m.F);
+    cudaFree(m.Z);
+    cudaFree(m.G);
+  }
+  cudaFree(c->st);
+  cudaFree(c->M);
+  cudaFree(c->partial);
+  cudaFree(c->Hr);
+  cudaFree(c->Hd);
+  cudaFree(c->row_part);
+  cudaFree(c->cnt_part);
+  cudaFree(c->gram_part);
+  cudaFree(c->decisions);
+  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+static int other_modes(const long long dims[3], int n, int *a, int *b) {
+  const int o1 = (n + 1) % 3, o2 = (n + 2) % 3;
+  const int lo = std::min(o1, o2), hi = std::max(o1, o2);
+  if (dims[hi] < dims[lo]) {
+    *a = hi;
+    *b = lo;
+  } else {
+    *a = lo;
+    *b = hi;
+  }
+  return 0;
+}
+
+#define CTX_CHECK(ctx)                                              \
+  do {                                                              \
+    if (!(ctx)) {                                                   \
+      set_error("null context");                                    \
+      return SACD_EINVAL;                                           \
+    }                                                               \
+    if ((ctx)->dead) {                                              \
+      set_error("context is dead after a CUDA/NCCL error");         \
+      return SACD_ECUDA;                                            \
+    }                                                               \
+    if (cudaSetDevice((ctx)->device) != cudaSuccess) {              \
+      set_error("cudaSetDevice failed");                            \
+      return SACD_ECUDA;                                            \
+    }                                                               \
+  } while (0)
+
+// Any ECUDA/ENCCL result kills the context (sticky).
+static int sticky(Context *c, int rc) {
+  if (rc == SACD_ECUDA || rc == SACD_ENCCL) c->dead = true;
+  return rc;
+}
+
+static int init_impl(Context *c, const uint32_t *coords, const float *vals, uint64_t seed) {
+  const size_t rs = real_size(*c);
+  cudaStream_t s = c->stream;
+  SACD_CUDA_TRY(cudaMalloc(&c->st, sizeof(DevState)));
+  SACD_CUDA_TRY(cudaMemsetAsync(c->st, 0, sizeof(DevState), s));
+  for (int n = 0; n < 3; ++n) {
+    c->m[n].I = c->dims[n];
+    other_modes(c->dims, n, &c->m[n].a, &c->m[n].b);
+  }
+  // tensor to device (host or device source; UVA picks the direction)
+  uint32_t *dc = nullptr;
+  float *dv = nullptr;
+  const size_t ne = (size_t)(c->nnz > 0 ? c->nnz : 1);
+  SACD_CUDA_TRY(cudaMallocAsync(&dc, ne * 12, s));
+  SACD_CUDA_TRY(cudaMallocAsync(&dv, ne * 4, s));
+  if (c->nnz > 0) {
+    SACD_CUDA_TRY(cudaMemcpyAsync(dc, coords, (size_t)c->nnz * 12, cudaMemcpyDefault, s));
+    SACD_CUDA_TRY(cudaMemcpyAsync(dv, vals, (size_t)c->nnz * 4, cudaMemcpyDefault, s));
+  }
+  int rc = build_layouts(*c, dc, dv);
+  cudaFreeAsync(dc, s);
+  cudaFreeAsync(dv, s);
+  SACD_TRY(rc);
+
+  // partitions
+  const long long T = c->opt.nnz_per_item > 0 ? c->opt.nnz_per_item : 512;
+  long long max_slots = 1, maxI = 1;
+  for (int n = 0; n < 3; ++n) {
+    ModeData &md = c->m[n];
+    std::vector<long long> rp((size_t)md.I + 1);
+    SACD_CUDA_TRY(cudaMemcpyAsync(rp.data(), md.row_ptr, rp.size() * 8, cudaMemcpyDeviceToHost, s));
+    SACD_CUDA_TRY(cudaStreamSynchronize(s));
+    std::vector<WorkItem> items;
+    std::vector<SplitRow> splits;
+    long long nslots = 0;
+    build_items(rp, md.I, T, 32, items, splits, nslots);
+    md.n_items = (long long)items.size();
+    md.n_splits = (long long)splits.size();
+    md.n_slots = nslots;
+    SACD_CUDA_TRY(cudaMalloc(&md.items, std::max<size_t>(1, items.size()) * sizeof(WorkItem)));
+    SACD_CUDA_TRY(cudaMalloc(&md.splits, std::max<size_t>(1, splits.size()) * sizeof(SplitRow)));
+    if (!items.empty())
+      SACD_CUDA_TRY(cudaMemcpy(md.items, items.data(), items.size() * sizeof(WorkItem), cudaMemcpyHostToDevice));
+    if (!splits.empty())
+      SACD_CUDA_TRY(
+          cudaMemcpy(md.splits, splits.data(), splits.size() * sizeof(SplitRow), cudaMemcpyHostToDevice));
+    max_slots = std::max(max_slots, nslots);
+    maxI = std::max(maxI, md.I);
+    c->device_bytes += (long long)(items.size() * sizeof(WorkItem) + splits.size() * sizeof(SplitRow));
+  }
+  // factors, z_prev, Grams, scratch
+  const int P = c->pitch, R = c->R;
+  for (int n = 0; n < 3; ++n) {
+    ModeData &md = c->m[n];
+    SACD_CUDA_TRY(cudaMalloc(&md.F, (size_t)md.I * P * rs));
+    SACD_CUDA_TRY(cudaMalloc(&md.Z, (size_t)md.I * P * rs));
+    SACD_CUDA_TRY(cudaMemsetAsync(md.Z, 0, (size_t)md.I * P * rs, s));
+    SACD_CUDA_TRY(cudaMalloc(&md.G, (size_t)R * R * 8));
+    c->device_bytes += (long long)(2 * (size_t)md.I * P * rs + (size_t)R * R * 8);
+  }
+  c->max_row_blocks = (maxI + 31) / 32 + 1;  // >= ceil(I / rows_per_block) for every pitch
+  c->gram_blocks = (int)std::min<long long>(296, std::max<long long>(1, (maxI + 63) / 64));
+  SACD_CUDA_TRY(cudaMalloc(&c->M, (size_t)maxI * P * rs));
+  SACD_CUDA_TRY(cudaMalloc(&c->partial, (size_t)max_slots * P * rs));
+  SACD_CUDA_TRY(cudaMalloc(&c->Hr, (size_t)P * P * rs));
+  SACD_CUDA_TRY(cudaMalloc(&c->Hd, (size_t)R * R * 8));
+  SACD_CUDA_TRY(cudaMalloc(&c->row_part, (size_t)c->max_row_blocks * 2 * 8));
+  SACD_CUDA_TRY(cudaMalloc(&c->cnt_part, (size_t)c->max_row_blocks * 2 * 8));
+  SACD_CUDA_TRY(cudaMalloc(&c->gram_part, (size_t)c->gram_blocks * R * R * 8));
+  c->device_bytes += (long long)((size_t)maxI * P * rs + (size_t)max_slots * P * rs + (size_t)P * P * rs +
+                                 (size_t)c->max_row_blocks * 32 + (size_t)c->gram_blocks * R * R * 8 +
+                                 sizeof(DevState));
+  SACD_TRY(launch_setup(*c));
+  SACD_TRY(launch_init_factors(*c, seed));
+  for (int n = 0; n < 3; ++n) SACD_TRY(launch_gram(*c, n));
+  SACD_TRY(launch_initial_fit(*c));
+  SACD_CUDA_TRY(cudaStreamSynchronize(s));
+  SACD_TRY(capture_graph(*c));
+  SACD_CUDA_TRY(cudaStreamSynchronize(s));
+  return SACD_OK;
+}
+
+template <typename T>
+static int dev_read(Context *c, T *dst, const void *src, size_t bytes) {
+  SACD_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c->stream));
+  SACD_CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return SACD_OK;
+}
+
+// factor-like matrix (Real, pitch) -> host fp64 with leading dimension ld
+static int read_matrix(Context *c, const void *src, long long rows, double *out, long long ld) {
+  double *tmp = nullptr;
+  cudaStream_t s = c->stream;
+  SACD_CUDA_TRY(cudaMallocAsync(&tmp, (size_t)std::max(1LL, rows) * c->R * 8, s));
+  int rc = launch_convert_out(*c, src, rows, tmp);
+  if (rc == SACD_OK) {
+    cudaError_t e = cudaMemcpy2DAsync(out, (size_t)ld * 8, tmp, (size_t)c->R * 8, (size_t)c->R * 8, (size_t)rows,
+                                      cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) {
+      set_error(std::string("read_matrix: ") + cudaGetErrorString(e));
+      rc = SACD_ECUDA;
+    }
+  }
+  cudaFreeAsync(tmp, s);
+  return rc;
+}
+
+static int write_matrix(Context *c, void *dst, long long rows, const double *in, long long ld) {
+  double *tmp = nullptr;
+  cudaStream_t s = c->stream;
+  SACD_CUDA_TRY(cudaMallocAsync(&tmp, (size_t)std::max(1LL, rows) * c->R * 8, s));
+  cudaError_t e = cudaMemcpy2DAsync(tmp, (size_t)c->R * 8, in, (size_t)ld * 8, (size_t)c->R * 8, (size_t)rows,
+                                    cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) {
+    set_error(std::string("write_matrix: ") + cudaGetErrorString(e));
+    return SACD_ECUDA;
+  }
+  int rc = launch_convert_in(*c, tmp, rows, dst);
+  cudaFreeAsync(tmp, s);
+  if (rc == SACD_OK) {
+    e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) {
+      set_error(std::string("write_matrix: ") + cudaGetErrorString(e));
+      rc = SACD_ECUDA;
+    }
+  }
+  return rc;
+}
+
+}  // namespace sacd
+
+using namespace sacd;
+
+extern "C" {
+
+const char *sacd_last_error(void) { return g_err.c_str(); }
+
+void sacd_default_options(sacd_options *o) {
+  if (!o) return;
+  memset(o, 0, sizeof(*o));
+  o->struct_size = sizeof(sacd_options);
+  o->precision = SACD_F64;
+  o->l_mode = SACD_L_DIAG;
+  o->variant = SACD_VARIANT_GS_LAGGED;
+  o->device = -1;
+  o->world_size = 1;
+  o->rank = 0;
+  o->use_graph = 1;
+}
+
+int sacd_init(sacd_ctx **out, const uint32_t *coords, const float *vals, int64_t nnz, const int64_t dims[3],
+              int32_t rank, uint64_t seed, const sacd_options *opt) {
+  if (!out || !dims) {
+    set_error("sacd_init: null argument");
+    return SACD_EINVAL;
+  }
+  *out = nullptr;
+  sacd_options o;
+  sacd_default_options(&o);
+  if (opt) {
+    if (opt->struct_size != sizeof(sacd_options)) {
+      set_error("sacd_init: options struct_size mismatch");
+      return SACD_EINVAL;
+    }
+    o = *opt;
+  }
+  if (nnz < 0 || nnz > 2000000000LL || rank < 1 || rank > 256 || (nnz > 0 && (!coords || !vals))) {
+    set_error("sacd_init: bad nnz/rank/pointers");
+    return SACD_EINVAL;
+  }
+  for (int n = 0; n < 3; ++n)
+    if (dims[n] < 1 || dims[n] > 2147483647LL) {
+      set_error("sacd_init: dims must be in [1, 2^31)");
+      return SACD_EINVAL;
+    }
+  if ((double)dims[0] * (double)dims[1] * (double)dims[2] >= 1.8e19) {
+    set_error("sacd_init: Q*P*S must fit in 64 bits");
+    return SACD_EINVAL;
+  }
+  if ((o.precision != SACD_F64 && o.precision != SACD_F32) || (o.l_mode != SACD_L_DIAG && o.l_mode != SACD_L_FROB) ||
+      (o.variant != SACD_VARIANT_GS_LAGGED && o.variant != SACD_VARIANT_SELECT_OFF)) {
+    set_error("sacd_init: bad option value");
+    return SACD_EINVAL;
+  }
+  if (o.world_size != 1 || o.rank != 0) {
+    set_error("sacd_init: world_size > 1 requires the NCCL build (not in this library)");
+    return SACD_EINVAL;
+  }
+  sacd_ctx *c = new (std::nothrow) sacd_ctx();
+  if (!c) {
+    set_error("sacd_init: host allocation failed");
+    return SACD_ENOMEM;
+  }
+  c->opt = o;
+  if (o.device >= 0) {
+    c->device = o.device;
+  } else if (cudaGetDevice(&c->device) != cudaSuccess) {
+    set_error("sacd_init: no CUDA device");
+    delete c;
+    return SACD_ECUDA;
+  }
+  if (cudaSetDevice(c->device) != cudaSuccess) {
+    set_error("sacd_init: cudaSetDevice failed");
+    delete c;
+    return SACD_ECUDA;
+  }
+  for (int n = 0; n < 3; ++n) c->dims[n] = dims[n];
+  c->nnz = nnz;
+  c->R = rank;
+  int p = 8;
+  while (p < rank) p <<= 1;
+  c->pitch = p;
+  if (o.stream) {
+    c->stream = (cudaStream_t)o.stream;
+  } else {
+    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+      set_error("sacd_init: stream creation failed");
+      delete c;
+      return SACD_ECUDA;
+    }
+    c->own_stream = true;
+  }
+  const int rc = init_impl(c, coords, vals, seed);
+  if (rc != SACD_OK) {
+    destroy(c);
+    return rc;
+  }
+  *out = c;
+  return SACD_OK;
+}
+
+int sacd_iterate(sacd_ctx *c, int32_t n) {
+  CTX_CHECK(c);
+  if (n < 0) {
+    set_error("sacd_iterate: n < 0");
+    return SACD_EINVAL;
+  }
+  for (int i = 0; i < n; ++i) {
+    if (c->graph_exec) {
+      cudaError_t e = cudaGraphLaunch(c->graph_exec, c->stream);
+      if (e != cudaSuccess) {
+        set_error(std::string("cudaGraphLaunch: ") + cudaGetErrorString(e));
+        return sticky(c, SACD_ECUDA);
+      }
+    } else {
+      const int rc = sweep_eager(*c);
+      if (rc != SACD_OK) return sticky(c, rc);
+    }
+  }
+  return SACD_OK;
+}
+
+int sacd_sync(sacd_ctx *c) {
+  CTX_CHECK(c);
+  cudaError_t e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) {
+    set_error(std::string("sacd_sync: ") + cudaGetErrorString(e));
+    return sticky(c, SACD_ECUDA);
+  }
+  return SACD_OK;
+}
+
+int sacd_fit(sacd_ctx *c, double *objective, double *fit) {
+  CTX_CHECK(c);
+  double v[2];
+  const int rc = dev_read(c, v, reinterpret_cast<const char *>(c->st) + offsetof(DevState, f), sizeof(v));
+  if (rc != SACD_OK) return sticky(c, rc);
+  if (objective) *objective = v[0];
+  if (fit) *fit = v[1];
+  return SACD_OK;
+}
+
+int sacd_factors(sacd_ctx *c, int32_t mode, double *out, int64_t ld) {
+  CTX_CHECK(c);
+  if (mode < 0 || mode > 2 || ld < c->R || !out) {
+    set_error("sacd_factors: bad mode/ld/out");
+    return SACD_ESTATE;
+  }
+  return sticky(c, read_matrix(c, c->m[mode].F, c->m[mode].I, out, ld));
+}
+
+int sacd_get_zprev(sacd_ctx *c, int32_t mode, double *out, int64_t ld) {
+  CTX_CHECK(c);
+  if (mode < 0 || mode > 2 || ld < c->R || !out) {
+    set_error("sacd_get_zprev: bad mode/ld/out");
+    return SACD_ESTATE;
+  }
+  return sticky(c, read_matrix(c, c->m[mode].Z, c->m[mode].I, out, ld));
+}
+
+int sacd_set_zprev(sacd_ctx *c, int32_t mode, const double *in, int64_t ld) {
+  CTX_CHECK(c);
+  if (mode < 0 || mode > 2 || ld < c->R || !in) {
+    set_error("sacd_set_zprev: bad mode/ld/in");
+    return SACD_ESTATE;
+  }
+  return sticky(c, write_matrix(c, c->m[mode].Z, c->m[mode].I, in, ld));
+}
+
+int sacd_set_factors(sacd_ctx *c, int32_t mode, const double *in, int64_t ld) {
+  CTX_CHECK(c);
+  if (mode < 0 || mode > 2 || ld < c->R || !in) {
+    set_error("sacd_set_factors: bad mode/ld/in");
+    return SACD_ESTATE;
+  }
+  int rc = write_matrix(c, c->m[mode].F, c->m[mode].I, in, ld);
+  if (rc == SACD_OK) rc = launch_gram(*c, mode);
+  if (rc == SACD_OK && cudaStreamSynchronize(c->stream) != cudaSuccess) rc = SACD_ECUDA;
+  return sticky(c, rc);
+}
+
+int sacd_mttkrp(sacd_ctx *c, int32_t mode, double *out, int64_t ld) {
+  CTX_CHECK(c);
+  if (mode < 0 || mode > 2 || ld < c->R || !out) {
+    set_error("sacd_mttkrp: bad mode/ld/out");
+    return SACD_ESTATE;
+  }
+  int rc = launch_mttkrp(*c, mode, c->M);
+  if (rc == SACD_OK) rc = read_matrix(c, c->M, c->m[mode].I, out, ld);
+  return sticky(c, rc);
+}
+
+int sacd_time_mttkrp(sacd_ctx *c, int32_t mode, int32_t reps, double *ms) {
+  CTX_CHECK(c);
+  if (mode < 0 || mode > 2 || reps < 1 || !ms) {
+    set_error("sacd_time_mttkrp: bad args");
+    return SACD_EINVAL;
+  }
+  const int saved = c->opt.profile;
+  c->opt.profile = 0;
+  cudaEvent_t e0, e1;
+  SACD_CUDA_TRY(cudaEventCreate(&e0));
+  SACD_CUDA_TRY(cudaEventCreate(&e1));
+  int rc = launch_mttkrp(*c, mode, c->M);  // warm-up
+  SACD_CUDA_TRY(cudaEventRecord(e0, c->stream));
+  for (int i = 0; i < reps && rc == SACD_OK; ++i) rc = launch_mttkrp(*c, mode, c->M);
+  SACD_CUDA_TRY(cudaEventRecord(e1, c->stream));
+  SACD_CUDA_TRY(cudaEventSynchronize(e1));
+  float t = 0.f;
+  SACD_CUDA_TRY(cudaEventElapsedTime(&t, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  c->opt.profile = saved;
+  *ms = (double)t / reps;
+  return sticky(c, rc);
+}
+
+int sacd_gram(sacd_ctx *c, int32_t mode, double *out) {
+  CTX_CHECK(c);
+  if (mode < 0 || mode > 2 || !out) {
+    set_error("sacd_gram: bad mode/out");
+    return SACD_ESTATE;
+  }
+  return sticky(c, dev_read(c, out, c->m[mode].G, (size_t)c->R * c->R * 8));
+}
+
+int sacd_hessian(sacd_ctx *c, int32_t mode, double *out) {
+  CTX_CHECK(c);
+  if (mode < 0 || mode > 2 || !out) {
+    set_error("sacd_hessian: bad mode/out");
+    return SACD_ESTATE;
+  }
+  int rc = launch_hessian_only(*c, mode);
+  if (rc == SACD_OK) rc = dev_read(c, out, c->Hd, (size_t)c->R * c->R * 8);
+  return sticky(c, rc);
+}
+
+int sacd_mode_update(sacd_ctx *c, int32_t mode, int32_t branch, uint8_t *decisions, double *ti, int64_t *E,
+                     int64_t *Ech) {
+  CTX_CHECK(c);
+  if (mode < 0 || mode > 2 || branch < -1 || branch > 2) {
+    set_error("sacd_mode_update: bad mode/branch");
+    return SACD_ESTATE;
+  }
+  const size_t nd = (size_t)c->m[mode].I * c->R;
+  uint8_t *dd = nullptr;
+  if (decisions) {
+    SACD_CUDA_TRY(cudaMallocAsync(&dd, std::max<size_t>(1, nd), c->stream));
+  }
+  int rc = launch_mode_update(*c, mode, branch, false, false, dd);
+  if (rc == SACD_OK && decisions) rc = dev_read(c, decisions, dd, nd);
+  if (dd) cudaFreeAsync(dd, c->stream);
+  if (rc == SACD_OK) {
+    double t;
+    long long e[2];
+    rc = dev_read(c, &t, reinterpret_cast<const char *>(c->st) + offsetof(DevState, ti_cur) + mode * 8, 8);
+    if (rc == SACD_OK) rc = dev_read(c, &e[0], reinterpret_cast<const char *>(c->st) + offsetof(DevState, E) + mode * 8, 8);
+    if (rc == SACD_OK)
+      rc = dev_read(c, &e[1], reinterpret_cast<const char *>(c->st) + offsetof(DevState, Ech) + mode * 8, 8);
+    if (rc == SACD_OK) {
+      if (ti) *ti = t;
+      if (E) *E = e[0];
+      if (Ech) *Ech = e[1];
+    }
+  }
+  return sticky(c, rc);
+}
+
+int sacd_layout(sacd_ctx *c, int32_t mode, uint32_t *idx_a, uint32_t *idx_b, float *val, int64_t *row_ptr) {
+  CTX_CHECK(c);
+  if (mode < 0 || mode > 2) {
+    set_error("sacd_layout: bad mode");
+    return SACD_ESTATE;
+  }
+  ModeData &md = c->m[mode];
+  int rc = SACD_OK;
+  if (rc == SACD_OK && idx_a && c->nnz) rc = dev_read(c, idx_a, md.idx_a, (size_t)c->nnz * 4);
+  if (rc == SACD_OK && idx_b && c->nnz) rc = dev_read(c, idx_b, md.idx_b, (size_t)c->nnz * 4);
+  if (rc == SACD_OK && val && c->nnz) rc = dev_read(c, val, md.val, (size_t)c->nnz * 4);
+  if (rc == SACD_OK && row_ptr) rc = dev_read(c, row_ptr, md.row_ptr, (size_t)(md.I + 1) * 8);
+  return sticky(c, rc);
+}
+
+int sacd_stats(sacd_ctx *c, sacd_iter_stats *out, int32_t cap, int32_t *n_out) {
+  CTX_CHECK(c);
+  int cnt = 0;
+  int rc = dev_read(c, &cnt, reinterpret_cast<const char *>(c->st) + offsetof(DevState, ring_count), sizeof(int));
+  if (rc != SACD_OK) return sticky(c, rc);
+  const int avail = std::min(cnt, kRing);
+  const int n = std::min(avail, std::max(0, (int)cap));
+  const int first = cnt - avail;  // oldest retained record
+  for (int i = 0; i < n && out; ++i) {
+    const int slot = (first + i) % kRing;
+    rc = dev_read(c, out + i, reinterpret_cast<const char *>(c->st) + offsetof(DevState, ring) +
+                                  (size_t)slot * sizeof(sacd_iter_stats),
+                  sizeof(sacd_iter_stats));
+    if (rc != SACD_OK) return sticky(c, rc);
+  }
+  if (n_out) *n_out = out ? n : avail;
+  return SACD_OK;
+}
+
+int sacd_get_info(sacd_ctx *c, sacd_info *o) {
+  CTX_CHECK(c);
+  if (!o) return SACD_EINVAL;
+  memset(o, 0, sizeof(*o));
+  for (int n = 0; n < 3; ++n) {
+    o->dims[n] = c->dims[n];
+    o->mode_a[n] = c->m[n].a;
+    o->mode_b[n] = c->m[n].b;
+    o->items[n] = c->m[n].n_items;
+    o->split_rows[n] = c->m[n].n_splits;
+  }
+  o->nnz = c->nnz;
+  o->rank = c->R;
+  o->pitch = c->pitch;
+  o->precision = c->opt.precision;
+  o->l_mode = c->opt.l_mode;
+  o->variant = c->opt.variant;
+  o->device_bytes = c->device_bytes;
+  int k = 0;
+  int rc = dev_read(c, &k, reinterpret_cast<const char *>(c->st) + offsetof(DevState, k), sizeof(int));
+  if (rc == SACD_OK)
+    rc = dev_read(c, &o->xnorm2, reinterpret_cast<const char *>(c->st) + offsetof(DevState, xnorm2), 8);
+  o->k = k;
+  return sticky(c, rc);
+}
+
+int sacd_profile_read(sacd_ctx *c, double ms[SACD_NUM_KCLASS], int64_t launches[SACD_NUM_KCLASS]) {
+  CTX_CHECK(c);
+  const int rc = prof_flush(*c);
+  if (rc != SACD_OK) return sticky(c, rc);
+  for (int i = 0; i < SACD_NUM_KCLASS; ++i) {
+    if (ms) ms[i] = c->prof_ms[i];
+    if (launches) launches[i] = c->prof_n[i];
+  }
+  return SACD_OK;
+}
+
+int sacd_profile_reset(sacd_ctx *c) {
+  CTX_CHECK(c);
+  const int rc = prof_flush(*c);
+  for (int i = 0; i < SACD_NUM_KCLASS; ++i) {
+    c->prof_ms[i] = 0;
+    c->prof_n[i] = 0;
+  }
+  return sticky(c, rc);
+}
+
+int sacd_abi_sizes(int32_t out[4]) {
+  if (!out) return SACD_EINVAL;
+  out[0] = SACD_ABI_VERSION;
+  out[1] = (int32_t)sizeof(sacd_options);
+  out[2] = (int32_t)sizeof(sacd_iter_stats);
+  out[3] = (int32_t)sizeof(sacd_info);
+  return SACD_OK;
+}
+
+int sacd_nccl_unique_id(void *out128) {
+  (void)out128;
+  set_error("sacd_nccl_unique_id: this library was built without NCCL");
+  return SACD_ENCCL;
+}
+
+void sacd_free(sacd_ctx *c) { destroy(c); }
+
+}  // extern "C"

@@ -1,0 +1,722 @@
+// kernels.cu -- the SaCD sweep on B200 (sm_100a): sparse MTTKRP, Gram-Hadamard H,
+// the fused column-wise SaCD row update, Gram refresh and the objective.
+//
+// Paper: arXiv 2003.03572 ("P:n" = PAPER.md line n).  Readings C1-C19: DESIGN.md s3.
+//   MTTKRP      m_ir = sum_{e in Omega^(n)_i} x_e a_(e,r) b_(e,r)      Eq 9
+//   H           H = G_a * G_b                                         Eq 10
+//   row update  for r = 0..R-1 (Gauss-Seidel within the row, C9):
+//                 g = -m_r + sum_j u_j h_jr                           Eq 14
+//                 u' = max(0, u_r - g/h_rr), d = u' - u_r              Eq 11-13
+//                 z = -g d - (L_r/2) d^2                               Eq 20
+//                 select: FIRST z>0 | EQ24 z-zprev>0 | EQ27 zprev-z>0  Alg 1, Eq 24/27
+//                 if selected u_r <- u'; zprev_r <- z                  P:598 (C8)
+//   objective   f = ||X||^2 - 2 sum_s w_s.m^W_s + 1^T(G_U*G_V*G_W)1   Eq 6-7, C1
+//
+// Determinism: no floating-point atomics anywhere; every reduction has a fixed order, so
+// reruns are bitwise identical (unchanged elements recompute the same z exactly).
+#include <math.h>
+
+#include "sacd_internal.cuh"
+
+namespace sacd {
+
+namespace {
+
+// ------------------------------------------------------------------ small helpers
+template <typename Real>
+struct V16;
+template <>
+struct V16<float> {
+  using T = float4;
+  static constexpr int N = 4;
+  __device__ static inline void get(const T &v, float *o) { o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w; }
+  __device__ static inline T make(const float *o) { return make_float4(o[0], o[1], o[2], o[3]); }
+};
+template <>
+struct V16<double> {
+  using T = double2;
+  static constexpr int N = 2;
+  __device__ static inline void get(const T &v, double *o) { o[0] = v.x; o[1] = v.y; }
+  __device__ static inline T make(const double *o) { return make_double2(o[0], o[1]); }
+};
+
+// Streaming loads for the nonzero arrays: read once per pass, keep L1 for factor rows.
+__device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t *p) {
+  uint32_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ float ld_stream_f32(const float *p) {
+  float v;
+  asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  return v;
+}
+
+// Reading C12: rand(seed, tag, ctr) = mix64(mix64(seed ^ tag) + (ctr + 1) * golden)
+__device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+template <int RT>
+__host__ __device__ constexpr int rows_per_block() {
+  return RT <= 64 ? 128 : (RT == 128 ? 64 : 32);
+}
+
+template <typename Real, int RT>
+__host__ __device__ constexpr bool h_in_smem() {
+  return (size_t)RT * RT * sizeof(Real) <= 64 * 1024;
+}
+
+template <typename Real, int RT>
+__host__ __device__ constexpr size_t rows_smem_bytes() {
+  return (h_in_smem<Real, RT>() ? (size_t)RT * RT * sizeof(Real) : 0) +
+         (size_t)rows_per_block<RT>() * (RT + 1) * sizeof(Real);
+}
+
+template <int RT>
+__host__ __device__ constexpr int gram_tg() {
+  return RT <= 16 ? RT : (RT <= 128 ? 16 : 32);
+}
+
+// ------------------------------------------------------------------ init (Alg 1 input, C12)
+template <typename Real>
+__global__ void k_init_factors(Real *__restrict__ F, long long I, int R, int RT, unsigned long long seed,
+                               unsigned long long off) {
+  const unsigned long long base = mix64(seed ^ 1ULL);  // tag INIT = 1
+  for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < I * RT;
+       x += (long long)gridDim.x * blockDim.x) {
+    const long long i = x / RT;
+    const int r = (int)(x - i * RT);
+    Real v = Real(0);
+    if (r < R) {
+      const unsigned long long ctr = off + (unsigned long long)i * R + r;
+      const unsigned long long u = mix64(base + (ctr + 1ULL) * 0x9E3779B97F4A7C15ULL);
+      v = (Real)((double)(u >> 40) * (1.0 / 16777216.0));
+    }
+    F[x] = v;
+  }
+}
+
+// ------------------------------------------------------------------ sparse MTTKRP
+// One warp per work item.  Lanes tile the row's R columns with 16-byte vectors (float4 /
+// double2); when a row needs fewer than 32 lanes, the warp splits into G groups that take
+// every G-th nonzero of the row and are combined by a fixed xor-shuffle tree at row end.
+template <typename Real, int RT>
+__global__ void __launch_bounds__(256) k_mttkrp(const WorkItem *__restrict__ items, long long n_items,
+                                                const long long *__restrict__ row_ptr,
+                                                const uint32_t *__restrict__ ia, const uint32_t *__restrict__ ib,
+                                                const float *__restrict__ val, const Real *__restrict__ A,
+                                                const Real *__restrict__ B, Real *__restrict__ M,
+                                                Real *__restrict__ partial) {
+  using VV = V16<Real>;
+  using VT = typename VV::T;
+  constexpr int VEC = VV::N;
+  constexpr int NV = RT / VEC;
+  constexpr int LPN = NV < 32 ? NV : 32;
+  constexpr int VPL = NV / LPN;
+  constexpr int G = 32 / LPN;
+  const int lane = threadIdx.x & 31;
+  const long long item = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (item >= n_items) return;
+  const WorkItem it = items[item];
+  const int grp = lane / LPN, sub = lane % LPN;
+  for (int row = it.row0; row < it.row1; ++row) {
+    long long s = row_ptr[row], t = row_ptr[row + 1];
+    if (s < it.nz0) s = it.nz0;
+    if (t > it.nz1) t = it.nz1;
+    Real acc[VPL][VEC];
+#pragma unroll
+    for (int v = 0; v < VPL; ++v)
+#pragma unroll
+      for (int c = 0; c < VEC; ++c) acc[v][c] = Real(0);
+    for (long long e = s + grp; e < t; e += G) {
+      const Real x = (Real)ld_stream_f32(val + e);
+      const VT *ap = reinterpret_cast<const VT *>(A + (long long)ld_stream_u32(ia + e) * RT);
+      const VT *bp = reinterpret_cast<const VT *>(B + (long long)ld_stream_u32(ib + e) * RT);
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) {
+        Real av[VEC], bv[VEC];
+        VV::get(__ldg(ap + sub + v * LPN), av);
+        VV::get(__ldg(bp + sub + v * LPN), bv);
+#pragma unroll
+        for (int c = 0; c < VEC; ++c) acc[v][c] = fma(x * av[c], bv[c], acc[v][c]);
+      }
+    }
+#pragma unroll
+    for (int off = LPN; off < 32; off <<= 1)
+#pragma unroll
+      for (int v = 0; v < VPL; ++v)
+#pragma unroll
+        for (int c = 0; c < VEC; ++c) acc[v][c] += __shfl_xor_sync(0xffffffffu, acc[v][c], off);
+    if (grp == 0) {
+      Real *dst = (it.slot >= 0) ? partial + it.slot * RT : M + (long long)row * RT;
+      VT *dv = reinterpret_cast<VT *>(dst);
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) dv[sub + v * LPN] = VV::make(acc[v]);
+    }
+  }
+}
+
+// Heavy rows split across items: M_row = sum of the row's partials in slot order.
+template <typename Real, int RT>
+__global__ void k_fixup(const SplitRow *__restrict__ splits, long long n, const Real *__restrict__ partial,
+                        Real *__restrict__ M) {
+  const long long sidx = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (sidx >= n) return;
+  const SplitRow sr = splits[sidx];
+  for (int c = lane; c < RT; c += 32) {
+    Real s = Real(0);
+    for (long long k = 0; k < sr.nslots; ++k) s += partial[(sr.slot0 + k) * RT + c];
+    M[(long long)sr.row * RT + c] = s;
+  }
+}
+
+// ------------------------------------------------------------------ H, L and the branch
+// H = G_a * G_b (Eq 10), L = ||H||_F (Alg 1), branch by reading C10.
+template <typename Real, int RT>
+__global__ void __launch_bounds__(256) k_prepare(int mode, int R, const double *__restrict__ Ga,
+                                                 const double *__restrict__ Gb, double *__restrict__ Hd,
+                                                 Real *__restrict__ Hr, DevState *st, int branch_override,
+                                                 int begin_sweep, int variant, int write_state) {
+  __shared__ double red[256];
+  double ss = 0.0;
+  for (int x = threadIdx.x; x < RT * RT; x += blockDim.x) {
+    const int r = x / RT, t = x - (x / RT) * RT;
+    double h = 0.0;
+    if (r < R && t < R) {
+      h = Ga[r * R + t] * Gb[r * R + t];
+      Hd[r * R + t] = h;
+      ss += h * h;
+    }
+    Hr[x] = (Real)h;
+  }
+  red[threadIdx.x] = ss;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0 && write_state) {
+    if (begin_sweep) st->k += 1;
+    int br;
+    if (branch_override >= 0) br = branch_override;
+    else if (variant == SACD_VARIANT_SELECT_OFF || st->nhist[mode] == 0) br = SACD_BR_FIRST;
+    else if (st->nhist[mode] == 1) br = SACD_BR_EQ24;
+    else br = (st->ti1[mode] > st->ti2[mode]) ? SACD_BR_EQ27 : SACD_BR_EQ24;
+    st->branch[mode] = br;
+    st->Lfrob[mode] = sqrt(red[0]);
+  }
+}
+
+// ------------------------------------------------------------------ fused row update
+// One thread per row (rows are independent given A and B: Eq ucap).  The block's
+// rows are staged in shared memory with an odd stride (RT+1) so the per-thread column
+// walk is bank-conflict free; H is staged in shared memory when it fits.
+template <typename Real, int RT>
+__global__ void __launch_bounds__(rows_per_block<RT>())
+    k_sacd_rows(long long I, int R, int mode, int l_mode, const Real *__restrict__ M, Real *__restrict__ F,
+                Real *__restrict__ Z, const Real *__restrict__ Hr, const DevState *__restrict__ st,
+                uint8_t *__restrict__ dec, double *__restrict__ ti_part, double *__restrict__ md_part,
+                long long *__restrict__ e_part, long long *__restrict__ ech_part) {
+  constexpr int TR = rows_per_block<RT>();
+  constexpr int US = RT + 1;
+  constexpr bool HS = h_in_smem<Real, RT>();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Real *Hs = reinterpret_cast<Real *>(smem_raw);
+  Real *Us = reinterpret_cast<Real *>(smem_raw + (HS ? (size_t)RT * RT * sizeof(Real) : 0));
+  __shared__ double red_d[2][TR / 32];
+  __shared__ long long red_l[2][TR / 32];
+
+  const int tid = threadIdx.x;
+  const long long row0 = (long long)blockIdx.x * TR;
+  const int nrows = (int)min((long long)TR, I - row0);
+  if (HS) {
+    for (int x = tid; x < RT * RT; x += TR) Hs[x] = Hr[x];
+  }
+  const Real *Fg = F + row0 * RT;
+  for (int x = tid; x < nrows * RT; x += TR) Us[(x / RT) * US + (x % RT)] = Fg[x];
+  __syncthreads();
+  const Real *H = HS ? Hs : Hr;
+  const int branch = st->branch[mode];
+  const Real Lf = (Real)st->Lfrob[mode];
+
+  double ti = 0.0, md = 0.0;
+  long long E = 0, Ech = 0;
+  if (tid < nrows) {
+    const long long row = row0 + tid;
+    Real *u = Us + tid * US;
+    const Real *m = M + row * RT;
+    Real *zp = Z + row * RT;
+    for (int r = 0; r < R; ++r) {
+      const Real *Hrow = H + r * RT;  // H is symmetric: row r == column r
+      const Real h = Hrow[r];
+      Real z = Real(0);
+      bool sel = false;
+      if (h != Real(0)) {
+        Real s = Real(0);
+#pragma unroll 4
+        for (int j = 0; j < R; ++j) s = fma(u[j], Hrow[j], s);
+        const Real g = s - m[r];                       // Eq 14
+        const Real ur = u[r];
+        const Real un = fmax(Real(0), ur - g / h);     // Eq 11-13
+        const Real d = un - ur;                        // Eq 12
+        const Real L = l_mode ? Lf : h;
+        z = -g * d - (L * Real(0.5)) * d * d;          // Eq 20
+        const Real zpr = zp[r];
+        sel = (branch == SACD_BR_FIRST) ? (z > Real(0))
+                                        : ((branch == SACD_BR_EQ24) ? (z - zpr > Real(0)) : (zpr - z > Real(0)));
+        if (sel) {
+          u[r] = un;
+          E += 1;
+          if (d != Real(0)) Ech += 1;
+        }
+      }
+      zp[r] = z;
+      ti += (double)z;
+      if (dec) dec[row * R + r] = (uint8_t)sel;
+    }
+    for (int r = 0; r < R; ++r) md += (double)u[r] * (double)m[r];
+  }
+  __syncthreads();
+  Real *Fo = F + row0 * RT;
+  for (int x = tid; x < nrows * RT; x += TR) Fo[x] = Us[(x / RT) * US + (x % RT)];
+
+  // fixed-order block reduction of (ti, md, E, Ech)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ti += __shfl_xor_sync(0xffffffffu, ti, o);
+    md += __shfl_xor_sync(0xffffffffu, md, o);
+    E += __shfl_xor_sync(0xffffffffu, E, o);
+    Ech += __shfl_xor_sync(0xffffffffu, Ech, o);
+  }
+  const int w = tid >> 5;
+  if ((tid & 31) == 0) {
+    red_d[0][w] = ti;
+    red_d[1][w] = md;
+    red_l[0][w] = E;
+    red_l[1][w] = Ech;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double a = 0.0, b = 0.0;
+    long long c = 0, d = 0;
+    for (int k = 0; k < TR / 32; ++k) {
+      a += red_d[0][k];
+      b += red_d[1][k];
+      c += red_l[0][k];
+      d += red_l[1][k];
+    }
+    ti_part[blockIdx.x] = a;
+    md_part[blockIdx.x] = b;
+    e_part[blockIdx.x] = c;
+    ech_part[blockIdx.x] = d;
+  }
+}
+
+// sum_r F_ir M_ir per row block (initial objective f^0)
+template <typename Real, int RT>
+__global__ void k_fm_dot(long long I, int R, const Real *__restrict__ F, const Real *__restrict__ M,
+                         double *__restrict__ ti_part, double *__restrict__ md_part, long long *__restrict__ e_part,
+                         long long *__restrict__ ech_part) {
+  constexpr int TR = rows_per_block<RT>();
+  __shared__ double red[TR];
+  const long long row = (long long)blockIdx.x * TR + threadIdx.x;
+  double s = 0.0;
+  if (row < I)
+    for (int r = 0; r < R; ++r) s += (double)F[row * RT + r] * (double)M[row * RT + r];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0;
+    for (int k = 0; k < TR; ++k) a += red[k];
+    md_part[blockIdx.x] = a;
+    ti_part[blockIdx.x] = 0.0;
+    e_part[blockIdx.x] = 0;
+    ech_part[blockIdx.x] = 0;
+  }
+}
+
+// ------------------------------------------------------------------ Gram G = F^T F (fp64)
+// Fixed grid: blockIdx.x = a contiguous row range, blockIdx.y = a pair (bi <= bj) of GT-wide
+// column panels (one pair unless R > 128).  Each thread owns a T x T tile; inside a
+// diagonal panel pair only tiles with ty <= tx work.  Partials are reduced in block order.
+template <int RT>
+__host__ __device__ constexpr int gram_gt() {
+  return RT < 128 ? RT : 128;
+}
+
+template <typename Real, int RT>
+__global__ void __launch_bounds__(gram_tg<gram_gt<RT>()>() * gram_tg<gram_gt<RT>()>())
+    k_gram_partial(long long I, int R, const Real *__restrict__ F, double *__restrict__ part) {
+  constexpr int GT = gram_gt<RT>();
+  constexpr int TG = gram_tg<GT>();
+  constexpr int T = GT / TG;
+  constexpr int CH = GT >= 128 ? 16 : 32;
+  __shared__ double Fa[CH][GT + 1];
+  __shared__ double Fb[CH][GT + 1];
+  // panel pair from blockIdx.y (row-major over the upper triangle of NB x NB panels)
+  constexpr int NB = RT / GT;
+  int bi = 0, bj = 0;
+  {
+    int y = blockIdx.y;
+    for (int a = 0; a < NB; ++a) {
+      if (y < NB - a) {
+        bi = a;
+        bj = a + y;
+        break;
+      }
+      y -= NB - a;
+    }
+  }
+  const int tid = threadIdx.x;
+  const int ty = tid / TG, tx = tid % TG;
+  const bool active = (bi != bj) || (ty <= tx);
+  const long long per = (I + gridDim.x - 1) / gridDim.x;
+  const long long i0 = (long long)blockIdx.x * per;
+  const long long i1 = min(I, i0 + per);
+  double acc[T][T];
+#pragma unroll
+  for (int a = 0; a < T; ++a)
+#pragma unroll
+    for (int b = 0; b < T; ++b) acc[a][b] = 0.0;
+  for (long long c0 = i0; c0 < i1; c0 += CH) {
+    const int nr = (int)min((long long)CH, i1 - c0);
+    __syncthreads();
+    for (int x = tid; x < nr * GT; x += TG * TG) {
+      const int k = x / GT, col = x % GT;
+      Fa[k][col] = (double)F[(c0 + k) * RT + bi * GT + col];
+      Fb[k][col] = (double)F[(c0 + k) * RT + bj * GT + col];
+    }
+    __syncthreads();
+    if (active) {
+      for (int k = 0; k < nr; ++k) {
+        double av[T], bv[T];
+#pragma unroll
+        for (int a = 0; a < T; ++a) av[a] = Fa[k][ty * T + a];
+#pragma unroll
+        for (int b = 0; b < T; ++b) bv[b] = Fb[k][tx * T + b];
+#pragma unroll
+        for (int a = 0; a < T; ++a)
+#pragma unroll
+          for (int b = 0; b < T; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
+      }
+    }
+  }
+  if (active) {
+    double *p = part + (long long)blockIdx.x * R * R;
+#pragma unroll
+    for (int a = 0; a < T; ++a)
+#pragma unroll
+      for (int b = 0; b < T; ++b) {
+        const int r = bi * GT + ty * T + a, t = bj * GT + tx * T + b;
+        if (r < R && t < R) p[r * R + t] = acc[a][b];
+      }
+  }
+}
+
+// G[r][t] = sum over blocks (in order) of the upper-triangle partial; mirrored exactly.
+__global__ void k_gram_reduce(int R, int nblk, const double *__restrict__ part, double *__restrict__ G) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= R * R) return;
+  const int r = x / R, t = x % R;
+  const int src = (r <= t) ? (r * R + t) : (t * R + r);
+  // (an entry with r <= t lies in tile (r/T, t/T), which has ty <= tx, so it was written)
+  double s = 0.0;
+  for (int b = 0; b < nblk; ++b) s += part[(long long)b * R * R + src];
+  G[x] = s;
+}
+
+// ------------------------------------------------------------------ finalize a mode pass
+// flags: 1 = record the pass (ti/E/history), 2 = compute f (needs all three Grams),
+//        4 = push a stats-ring record (end of sweep)
+__global__ void __launch_bounds__(1024) k_finalize(int mode, long long nblk, const double *__restrict__ ti_part,
+                                                   const double *__restrict__ md_part,
+                                                   const long long *__restrict__ e_part,
+                                                   const long long *__restrict__ ech_part, const double *G0,
+                                                   const double *G1, const double *G2, int R, DevState *st,
+                                                   int flags) {
+  __shared__ double sd[3][1024];
+  __shared__ long long sl[2][1024];
+  const int tid = threadIdx.x;
+  double ti = 0.0, md = 0.0, mn = 0.0;
+  long long E = 0, Ech = 0;
+  for (long long b = tid; b < nblk; b += 1024) {
+    ti += ti_part[b];
+    md += md_part[b];
+    E += e_part[b];
+    Ech += ech_part[b];
+  }
+  if (flags & 2)
+    for (int x = tid; x < R * R; x += 1024) mn += G0[x] * G1[x] * G2[x];
+  sd[0][tid] = ti;
+  sd[1][tid] = md;
+  sd[2][tid] = mn;
+  sl[0][tid] = E;
+  sl[1][tid] = Ech;
+  __syncthreads();
+  for (int o = 512; o > 0; o >>= 1) {
+    if (tid < o) {
+      sd[0][tid] += sd[0][tid + o];
+      sd[1][tid] += sd[1][tid + o];
+      sd[2][tid] += sd[2][tid + o];
+      sl[0][tid] += sl[0][tid + o];
+      sl[1][tid] += sl[1][tid + o];
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    if (flags & 1) {
+      st->ti_cur[mode] = sd[0][0];
+      st->E[mode] = sl[0][0];
+      st->Ech[mode] = sl[1][0];
+      st->ti2[mode] = st->ti1[mode];
+      st->ti1[mode] = sd[0][0];
+      st->nhist[mode] += 1;
+    }
+    if (mode == 2) st->mdot = sd[1][0];
+    if (flags & 2) {
+      const double f = st->xnorm2 - 2.0 * sd[1][0] + sd[2][0];
+      st->f = f;
+      st->fit = st->xnorm2 > 0.0 ? 1.0 - sqrt(f > 0.0 ? f : 0.0) / sqrt(st->xnorm2) : 0.0;
+    }
+    if (flags & 4) {
+      sacd_iter_stats &rec = st->ring[st->ring_count % kRing];
+      rec.k = st->k;
+      rec.objective = st->f;
+      rec.fit = st->fit;
+      for (int n = 0; n < 3; ++n) {
+        rec.branch[n] = st->branch[n];
+        rec.ti[n] = st->ti_cur[n];
+        rec.E[n] = st->E[n];
+        rec.E_changed[n] = st->Ech[n];
+      }
+      st->ring_count += 1;
+    }
+  }
+}
+
+template <typename Real>
+__global__ void k_convert_in(const double *__restrict__ src, long long rows, int R, int RT, Real *__restrict__ dst) {
+  for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < rows * RT;
+       x += (long long)gridDim.x * blockDim.x) {
+    const long long i = x / RT;
+    const int r = (int)(x - i * RT);
+    dst[x] = r < R ? (Real)src[i * R + r] : Real(0);
+  }
+}
+
+template <typename Real>
+__global__ void k_convert_out(const Real *__restrict__ src, long long rows, int R, int RT, double *__restrict__ dst) {
+  for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < rows * R;
+       x += (long long)gridDim.x * blockDim.x) {
+    const long long i = x / R;
+    const int r = (int)(x - i * R);
+    dst[x] = (double)src[i * RT + r];
+  }
+}
+
+inline int grid1d(long long n, int block = 256) {
+  long long g = (n + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > 148 * 32) g = 148 * 32;
+  return (int)g;
+}
+
+// ------------------------------------------------------------------ launch implementations
+template <typename Real, int RT>
+struct Impl {
+  static int mttkrp(Context &c, int mode, void *out_v) {
+    Real *out = reinterpret_cast<Real *>(out_v);
+    ModeData &md = c.m[mode];
+    const Real *A = reinterpret_cast<const Real *>(c.m[md.a].F);
+    const Real *B = reinterpret_cast<const Real *>(c.m[md.b].F);
+    int pe = prof_begin(c, 0);
+    if (md.n_items > 0) {
+      const int wpb = 8;
+      const long long blocks = (md.n_items + wpb - 1) / wpb;
+      k_mttkrp<Real, RT><<<(unsigned)blocks, wpb * 32, 0, c.stream>>>(
+          md.items, md.n_items, md.row_ptr, md.idx_a, md.idx_b, md.val, A, B, out,
+          reinterpret_cast<Real *>(c.partial));
+    }
+    SACD_CUDA_TRY(cudaGetLastError());
+    SACD_TRY(prof_end(c, 0, pe));
+    if (md.n_splits > 0) {
+      pe = prof_begin(c, 1);
+      const long long blocks = (md.n_splits + 7) / 8;
+      k_fixup<Real, RT><<<(unsigned)blocks, 256, 0, c.stream>>>(md.splits, md.n_splits,
+                                                                 reinterpret_cast<const Real *>(c.partial), out);
+      SACD_CUDA_TRY(cudaGetLastError());
+      SACD_TRY(prof_end(c, 1, pe));
+    }
+    return SACD_OK;
+  }
+
+  static int gram(Context &c, int mode) {
+    ModeData &md = c.m[mode];
+    constexpr int GT = gram_gt<RT>();
+    constexpr int TG = gram_tg<GT>();
+    constexpr int NB = RT / GT;
+    int pe = prof_begin(c, 4);
+    k_gram_partial<Real, RT><<<dim3(c.gram_blocks, NB * (NB + 1) / 2), TG * TG, 0, c.stream>>>(md.I, c.R, reinterpret_cast<const Real *>(md.F),
+                                                                    c.gram_part);
+    k_gram_reduce<<<(c.R * c.R + 255) / 256, 256, 0, c.stream>>>(c.R, c.gram_blocks, c.gram_part, md.G);
+    SACD_CUDA_TRY(cudaGetLastError());
+    return prof_end(c, 4, pe);
+  }
+
+  static int prepare(Context &c, int mode, int branch_override, bool begin_sweep, int write_state) {
+    ModeData &md = c.m[mode];
+    int pe = prof_begin(c, 2);
+    k_prepare<Real, RT><<<1, 256, 0, c.stream>>>(mode, c.R, c.m[md.a].G, c.m[md.b].G, c.Hd,
+                                                 reinterpret_cast<Real *>(c.Hr), c.st, branch_override,
+                                                 begin_sweep ? 1 : 0, c.opt.variant, write_state);
+    SACD_CUDA_TRY(cudaGetLastError());
+    return prof_end(c, 2, pe);
+  }
+
+  static int mode_update(Context &c, int mode, int branch_override, bool begin_sweep, bool end_sweep,
+                         uint8_t *dec) {
+    ModeData &md = c.m[mode];
+    Real *M = reinterpret_cast<Real *>(c.M);
+    SACD_TRY(mttkrp(c, mode, M));
+    SACD_TRY(prepare(c, mode, branch_override, begin_sweep, 1));
+    constexpr int TR = rows_per_block<RT>();
+    constexpr size_t smem = rows_smem_bytes<Real, RT>();
+    const long long nblk = (md.I + TR - 1) / TR;
+    double *ti_part = c.row_part, *md_part = c.row_part + c.max_row_blocks;
+    long long *e_part = c.cnt_part, *ech_part = c.cnt_part + c.max_row_blocks;
+    int pe = prof_begin(c, 3);
+    k_sacd_rows<Real, RT><<<(unsigned)nblk, TR, smem, c.stream>>>(
+        md.I, c.R, mode, c.opt.l_mode, M, reinterpret_cast<Real *>(md.F), reinterpret_cast<Real *>(md.Z),
+        reinterpret_cast<const Real *>(c.Hr), c.st, dec, ti_part, md_part, e_part, ech_part);
+    SACD_CUDA_TRY(cudaGetLastError());
+    SACD_TRY(prof_end(c, 3, pe));
+    SACD_TRY(gram(c, mode));
+    pe = prof_begin(c, 5);
+    const int flags = 1 | (end_sweep ? 6 : 0);
+    k_finalize<<<1, 1024, 0, c.stream>>>(mode, nblk, ti_part, md_part, e_part, ech_part, c.m[0].G, c.m[1].G,
+                                         c.m[2].G, c.R, c.st, flags);
+    SACD_CUDA_TRY(cudaGetLastError());
+    return prof_end(c, 5, pe);
+  }
+
+  static int initial_fit(Context &c) {
+    Real *M = reinterpret_cast<Real *>(c.M);
+    SACD_TRY(mttkrp(c, 2, M));
+    ModeData &md = c.m[2];
+    constexpr int TR = rows_per_block<RT>();
+    const long long nblk = (md.I + TR - 1) / TR;
+    double *ti_part = c.row_part, *md_part = c.row_part + c.max_row_blocks;
+    long long *e_part = c.cnt_part, *ech_part = c.cnt_part + c.max_row_blocks;
+    k_fm_dot<Real, RT><<<(unsigned)nblk, TR, 0, c.stream>>>(md.I, c.R, reinterpret_cast<const Real *>(md.F), M,
+                                                            ti_part, md_part, e_part, ech_part);
+    k_finalize<<<1, 1024, 0, c.stream>>>(2, nblk, ti_part, md_part, e_part, ech_part, c.m[0].G, c.m[1].G, c.m[2].G,
+                                         c.R, c.st, 2);
+    SACD_CUDA_TRY(cudaGetLastError());
+    return SACD_OK;
+  }
+
+  static int setup(Context &c) {
+    constexpr size_t smem = rows_smem_bytes<Real, RT>();
+    SACD_CUDA_TRY(cudaFuncSetAttribute(k_sacd_rows<Real, RT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    return SACD_OK;
+  }
+};
+
+#define SACD_DISPATCH(c, EXPR)                                   \
+  do {                                                           \
+    const bool f64_ = (c).opt.precision == SACD_F64;             \
+    switch ((c).pitch) {                                         \
+      case 8:                                                    \
+        if (f64_) { using I_ = Impl<double, 8>; return EXPR; }   \
+        else { using I_ = Impl<float, 8>; return EXPR; }         \
+      case 16:                                                   \
+        if (f64_) { using I_ = Impl<double, 16>; return EXPR; }  \
+        else { using I_ = Impl<float, 16>; return EXPR; }        \
+      case 32:                                                   \
+        if (f64_) { using I_ = Impl<double, 32>; return EXPR; }  \
+        else { using I_ = Impl<float, 32>; return EXPR; }        \
+      case 64:                                                   \
+        if (f64_) { using I_ = Impl<double, 64>; return EXPR; }  \
+        else { using I_ = Impl<float, 64>; return EXPR; }        \
+      case 128:                                                  \
+        if (f64_) { using I_ = Impl<double, 128>; return EXPR; } \
+        else { using I_ = Impl<float, 128>; return EXPR; }       \
+      case 256:                                                  \
+        if (f64_) { using I_ = Impl<double, 256>; return EXPR; } \
+        else { using I_ = Impl<float, 256>; return EXPR; }       \
+      default:                                                   \
+        set_error("bad pitch");                                  \
+        return SACD_EINVAL;                                      \
+    }                                                            \
+  } while (0)
+
+}  // namespace
+
+size_t real_size(const Context &c) { return c.opt.precision == SACD_F64 ? 8 : 4; }
+
+long long rows_block_for(const Context &c) {
+  switch (c.pitch) {
+    case 128: return 64;
+    case 256: return 32;
+    default: return 128;
+  }
+}
+
+int launch_setup(Context &c) { SACD_DISPATCH(c, I_::setup(c)); }
+
+int launch_init_factors(Context &c, uint64_t seed) {
+  unsigned long long off = 0;
+  for (int n = 0; n < 3; ++n) {
+    ModeData &md = c.m[n];
+    if (c.opt.precision == SACD_F64)
+      k_init_factors<double><<<grid1d(md.I * c.pitch), 256, 0, c.stream>>>(reinterpret_cast<double *>(md.F), md.I,
+                                                                             c.R, c.pitch, seed, off);
+    else
+      k_init_factors<float><<<grid1d(md.I * c.pitch), 256, 0, c.stream>>>(reinterpret_cast<float *>(md.F), md.I,
+                                                                            c.R, c.pitch, seed, off);
+    off += (unsigned long long)md.I * c.R;
+  }
+  SACD_CUDA_TRY(cudaGetLastError());
+  return SACD_OK;
+}
+
+int launch_mttkrp(Context &c, int mode, void *out) { SACD_DISPATCH(c, I_::mttkrp(c, mode, out)); }
+
+int launch_gram(Context &c, int mode) { SACD_DISPATCH(c, I_::gram(c, mode)); }
+
+int launch_hessian_only(Context &c, int mode) { SACD_DISPATCH(c, I_::prepare(c, mode, -1, false, 0)); }
+
+int launch_mode_update(Context &c, int mode, int branch_override, bool begin_sweep, bool end_sweep,
+                       uint8_t *decisions_dev) {
+  SACD_DISPATCH(c, I_::mode_update(c, mode, branch_override, begin_sweep, end_sweep, decisions_dev));
+}
+
+int launch_initial_fit(Context &c) { SACD_DISPATCH(c, I_::initial_fit(c)); }
+
+int launch_convert_in(Context &c, const double *src_dev, long long rows, void *dst) {
+  if (c.opt.precision == SACD_F64)
+    k_convert_in<double><<<grid1d(rows * c.pitch), 256, 0, c.stream>>>(src_dev, rows, c.R, c.pitch,
+                                                                        reinterpret_cast<double *>(dst));
+  else
+    k_convert_in<float><<<grid1d(rows * c.pitch), 256, 0, c.stream>>>(src_dev, rows, c.R, c.pitch,
+                                                                       reinterpret_cast<float *>(dst));
+  SACD_CUDA_TRY(cudaGetLastError());
+  return SACD_OK;
+}
+
+int launch_convert_out(Context &c, const void *src, long long rows, double *dst_dev) {
+  if (c.opt.precision == SACD_F64)
+    k_convert_out<double><<<grid1d(rows * c.R), 256, 0, c.stream>>>(reinterpret_cast<const double *>(src), rows, c.R,
+                                                                     c.pitch, dst_dev);
+  else
+    k_convert_out<float><<<grid1d(rows * c.R), 256, 0, c.stream>>>(reinterpret_cast<const float *>(src), rows, c.R,
+                                                                    c.pitch, dst_dev);
+  SACD_CUDA_TRY(cudaGetLastError());
+  return SACD_OK;
+}
+
+}  // namespace sacd

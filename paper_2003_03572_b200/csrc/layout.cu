@@ -1,0 +1,193 @@
+// layout.cu -- per-mode sorted nonzero layout, built once on device by sacd_init.
+//
+// The paper's slices Omega^U_q, Omega^V_p, Omega^W_s (Table 2) become,
+// per mode n, the nonzeros sorted by the key (i_n, i_a, i_b) where a is the shorter other
+// mode (ties -> lower mode id) and b the remaining one; row_ptr[i] .. row_ptr[i+1] is the
+// slice of row i.  This replaces the unfolding X_(n) (Lemma 4), which
+// is never materialised.  Keys are unique (duplicates are rejected), so the order
+// is unique and equals the oracle's bit for bit.
+//
+// Steps (all on device): validate -> 64-bit keys -> cub radix sort of (key, position) ->
+// duplicate check -> gather idx_a, idx_b, val -> row_ptr by binary search -> ||X||^2.
+#include <cub/device/device_radix_sort.cuh>
+
+#include "sacd_internal.cuh"
+
+namespace sacd {
+
+namespace {
+
+__global__ void k_validate(const uint32_t *__restrict__ coords, const float *__restrict__ vals, long long nnz,
+                           long long d0, long long d1, long long d2, int *__restrict__ flags) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nnz;
+       e += (long long)gridDim.x * blockDim.x) {
+    const uint32_t q = coords[3 * e], p = coords[3 * e + 1], s = coords[3 * e + 2];
+    if (q >= d0 || p >= d1 || s >= d2) atomicOr(flags, 1);
+    if (!isfinite(vals[e])) atomicOr(flags, 2);
+  }
+}
+
+__global__ void k_make_keys(const uint32_t *__restrict__ coords, long long nnz, int n, int a, int b,
+                            unsigned long long Ia, unsigned long long Ib, unsigned long long *__restrict__ keys,
+                            uint32_t *__restrict__ pos) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nnz;
+       e += (long long)gridDim.x * blockDim.x) {
+    const unsigned long long in = coords[3 * e + n], ia = coords[3 * e + a], ib = coords[3 * e + b];
+    keys[e] = (in * Ia + ia) * Ib + ib;
+    pos[e] = (uint32_t)e;
+  }
+}
+
+__global__ void k_check_dup(const unsigned long long *__restrict__ keys, long long nnz, int *__restrict__ flags) {
+  for (long long e = 1 + blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nnz;
+       e += (long long)gridDim.x * blockDim.x)
+    if (keys[e] == keys[e - 1]) atomicOr(flags, 4);
+}
+
+__global__ void k_gather(const uint32_t *__restrict__ coords, const float *__restrict__ vals,
+                         const uint32_t *__restrict__ pos, long long nnz, int a, int b, uint32_t *__restrict__ ia,
+                         uint32_t *__restrict__ ib, float *__restrict__ v) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nnz;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long p = pos[e];
+    ia[e] = coords[3 * p + a];
+    ib[e] = coords[3 * p + b];
+    v[e] = vals[p];
+  }
+}
+
+// row_ptr[i] = #keys < i * (Ia*Ib)   (lower bound), i = 0..I
+__global__ void k_row_ptr(const unsigned long long *__restrict__ keys, long long nnz, long long I,
+                          unsigned long long stride, long long *__restrict__ row_ptr) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i <= I;
+       i += (long long)gridDim.x * blockDim.x) {
+    const unsigned long long target = (unsigned long long)i * stride;
+    long long lo = 0, hi = nnz;
+    while (lo < hi) {
+      const long long mid = (lo + hi) >> 1;
+      if (keys[mid] < target) lo = mid + 1;
+      else hi = mid;
+    }
+    row_ptr[i] = lo;
+  }
+}
+
+// ||X||^2 = sum x^2 in fp64: fixed grid of per-block partials, then one block in order.
+constexpr int kNormBlocks = 296;
+__global__ void k_norm_partial(const float *__restrict__ v, long long nnz, double *__restrict__ part) {
+  __shared__ double sh[256];
+  const long long per = (nnz + gridDim.x - 1) / gridDim.x;
+  const long long e0 = blockIdx.x * per, e1 = min(nnz, e0 + per);
+  double s = 0.0;
+  for (long long e = e0 + threadIdx.x; e < e1; e += blockDim.x) s += (double)v[e] * (double)v[e];
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
+}
+
+__global__ void k_norm_final(const double *__restrict__ part, int n, DevState *st) {
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < n; i++) s += part[i];
+    st->xnorm2 = s;
+  }
+}
+
+inline int grid_for(long long n) {
+  long long g = (n + 255) / 256;
+  if (g < 1) g = 1;
+  if (g > 148 * 16) g = 148 * 16;
+  return (int)g;
+}
+
+int bits_for(unsigned long long maxkey) {
+  int b = 1;
+  while (b < 64 && (maxkey >> b) != 0) b++;
+  return b;
+}
+
+}  // namespace
+
+int build_layouts(Context &c, const uint32_t *coords, const float *vals) {
+  const long long nnz = c.nnz;
+  cudaStream_t s = c.stream;
+  int *flags = nullptr;
+  SACD_CUDA_TRY(cudaMallocAsync(&flags, sizeof(int), s));
+  SACD_CUDA_TRY(cudaMemsetAsync(flags, 0, sizeof(int), s));
+  if (nnz > 0)
+    k_validate<<<grid_for(nnz), 256, 0, s>>>(coords, vals, nnz, c.dims[0], c.dims[1], c.dims[2], flags);
+  int hflags = 0;
+  SACD_CUDA_TRY(cudaMemcpyAsync(&hflags, flags, sizeof(int), cudaMemcpyDeviceToHost, s));
+  SACD_CUDA_TRY(cudaStreamSynchronize(s));
+  if (hflags & 1) {
+    set_error("sacd_init: coordinate index out of range");
+    cudaFreeAsync(flags, s);
+    return SACD_ERANGE;
+  }
+  if (hflags & 2) {
+    set_error("sacd_init: non-finite value");
+    cudaFreeAsync(flags, s);
+    return SACD_ENONFINITE;
+  }
+
+  unsigned long long *keys = nullptr, *keys2 = nullptr;
+  uint32_t *pos = nullptr, *pos2 = nullptr;
+  void *temp = nullptr;
+  size_t temp_bytes = 0;
+  const size_t ne = (size_t)(nnz > 0 ? nnz : 1);
+  SACD_CUDA_TRY(cudaMallocAsync(&keys, ne * 8, s));
+  SACD_CUDA_TRY(cudaMallocAsync(&keys2, ne * 8, s));
+  SACD_CUDA_TRY(cudaMallocAsync(&pos, ne * 4, s));
+  SACD_CUDA_TRY(cudaMallocAsync(&pos2, ne * 4, s));
+  if (nnz > 0) {
+    SACD_CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, keys, keys2, pos, pos2, (int)nnz, 0, 64, s));
+    SACD_CUDA_TRY(cudaMallocAsync(&temp, temp_bytes, s));
+  }
+  for (int n = 0; n < 3; n++) {
+    ModeData &md = c.m[n];
+    const int a = md.a, b = md.b;
+    const unsigned long long Ia = (unsigned long long)c.dims[a], Ib = (unsigned long long)c.dims[b];
+    SACD_CUDA_TRY(cudaMallocAsync(&md.idx_a, ne * 4, s));
+    SACD_CUDA_TRY(cudaMallocAsync(&md.idx_b, ne * 4, s));
+    SACD_CUDA_TRY(cudaMallocAsync(&md.val, ne * 4, s));
+    SACD_CUDA_TRY(cudaMallocAsync(&md.row_ptr, (size_t)(md.I + 1) * 8, s));
+    c.device_bytes += (long long)ne * 12 + (md.I + 1) * 8;
+    if (nnz > 0) {
+      k_make_keys<<<grid_for(nnz), 256, 0, s>>>(coords, nnz, n, a, b, Ia, Ib, keys, pos);
+      const int end_bit = bits_for((unsigned long long)c.dims[n] * Ia * Ib - 1ULL);
+      SACD_CUDA_TRY(
+          cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys, keys2, pos, pos2, (int)nnz, 0, end_bit, s));
+      k_check_dup<<<grid_for(nnz), 256, 0, s>>>(keys2, nnz, flags);
+      k_gather<<<grid_for(nnz), 256, 0, s>>>(coords, vals, pos2, nnz, a, b, md.idx_a, md.idx_b, md.val);
+    }
+    k_row_ptr<<<grid_for(md.I + 1), 256, 0, s>>>(keys2, nnz, md.I, Ia * Ib, md.row_ptr);
+    SACD_CUDA_TRY(cudaGetLastError());
+  }
+  SACD_CUDA_TRY(cudaMemcpyAsync(&hflags, flags, sizeof(int), cudaMemcpyDeviceToHost, s));
+  // ||X||^2 in mode-0 layout order
+  double *part = nullptr;
+  SACD_CUDA_TRY(cudaMallocAsync(&part, kNormBlocks * sizeof(double), s));
+  k_norm_partial<<<kNormBlocks, 256, 0, s>>>(c.m[0].val, nnz, part);
+  k_norm_final<<<1, 32, 0, s>>>(part, kNormBlocks, c.st);
+  SACD_CUDA_TRY(cudaGetLastError());
+  SACD_CUDA_TRY(cudaStreamSynchronize(s));
+  cudaFreeAsync(part, s);
+  cudaFreeAsync(keys, s);
+  cudaFreeAsync(keys2, s);
+  cudaFreeAsync(pos, s);
+  cudaFreeAsync(pos2, s);
+  if (temp) cudaFreeAsync(temp, s);
+  cudaFreeAsync(flags, s);
+  SACD_CUDA_TRY(cudaStreamSynchronize(s));
+  if (hflags & 4) {
+    set_error("sacd_init: duplicate coordinate");
+    return SACD_EDUP;
+  }
+  return SACD_OK;
+}
+
+}  // namespace sacd

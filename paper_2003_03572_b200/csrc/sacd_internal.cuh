@@ -1,0 +1,142 @@
+// sacd_internal.cuh -- internal declarations of libsacd (B200 / sm_100a).
+// The public ABI is include/sacd.h; nothing here crosses it.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/sacd.h"
+
+namespace sacd {
+
+// ------------------------------------------------------------------ errors
+void set_error(const std::string &msg);
+
+struct Status {
+  int code;
+};
+
+#define SACD_CUDA_TRY(call)                                                                    \
+  do {                                                                                         \
+    cudaError_t e_ = (call);                                                                   \
+    if (e_ != cudaSuccess) {                                                                   \
+      ::sacd::set_error(std::string(#call) + ": " + cudaGetErrorString(e_) + " @" + __FILE__ + \
+                        ":" + std::to_string(__LINE__));                                       \
+      return (e_ == cudaErrorMemoryAllocation) ? SACD_ENOMEM : SACD_ECUDA;                     \
+    }                                                                                          \
+  } while (0)
+
+#define SACD_TRY(call)          \
+  do {                          \
+    int rc_ = (call);           \
+    if (rc_ != SACD_OK) return rc_; \
+  } while (0)
+
+// ------------------------------------------------------------------ device structures
+// One MTTKRP work item: either whole rows [row0,row1) whose nonzeros are [nz0,nz1), or
+// (slot >= 0) one segment [nz0,nz1) of a heavy row row0 whose partial goes to `slot`.
+struct WorkItem {
+  long long nz0, nz1;
+  int row0, row1;
+  long long slot;
+};
+
+struct SplitRow {
+  long long slot0, nslots;
+  int row, pad;
+};
+
+constexpr int kRing = 4096;
+
+// Device-resident control state: everything the sweep graph needs to decide on device.
+struct DevState {
+  int k;                 // completed/started sweeps
+  int nhist[3];          // number of ti values recorded per mode
+  double ti1[3], ti2[3]; // ti^{k-1}, ti^{k-2} per mode (reading C10)
+  int branch[3];         // branch used by the latest pass of each mode
+  double Lfrob[3];       // ||H||_F of the latest pass of each mode
+  double ti_cur[3];
+  long long E[3], Ech[3];
+  double xnorm2;
+  double f, fit;
+  double mdot;           // sum_i sum_r w_ir m^W_ir of the latest W pass
+  int ring_count;
+  sacd_iter_stats ring[kRing];
+};
+
+struct ModeData {
+  long long I = 0;
+  int a = 0, b = 0;               // the other modes ("a" = shorter)
+  uint32_t *idx_a = nullptr, *idx_b = nullptr;
+  float *val = nullptr;
+  long long *row_ptr = nullptr;   // I+1
+  WorkItem *items = nullptr;
+  long long n_items = 0;
+  SplitRow *splits = nullptr;
+  long long n_splits = 0, n_slots = 0;
+  void *F = nullptr;              // Real[I * pitch]
+  void *Z = nullptr;              // Real[I * pitch]  (z_prev)
+  double *G = nullptr;            // fp64 R x R Gram of F
+};
+
+struct Context {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  bool dead = false;
+  sacd_options opt{};
+  long long dims[3]{};
+  long long nnz = 0;
+  int R = 0, pitch = 0;           // pitch = kernel tile RT (8..256)
+  ModeData m[3];
+  DevState *st = nullptr;         // device
+  // scratch
+  void *M = nullptr;              // Real[maxI * pitch]
+  void *partial = nullptr;        // Real[max slots * pitch]
+  void *Hr = nullptr;             // Real[pitch * pitch]
+  double *Hd = nullptr;           // R x R
+  double *row_part = nullptr;     // 4 * max row blocks (ti, mdot) as doubles
+  long long *cnt_part = nullptr;  // 2 * max row blocks (E, Ech)
+  double *gram_part = nullptr;    // gram blocks * R * R
+  uint8_t *decisions = nullptr;   // teacher-forced only
+  long long max_row_blocks = 0;
+  int gram_blocks = 0;
+  long long device_bytes = 0;
+  // graph
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t graph_exec = nullptr;
+  // profiling
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<std::pair<int, int>> ev_pending;  // (class, pool index of start)
+  size_t ev_next = 0;
+  double prof_ms[SACD_NUM_KCLASS]{};
+  long long prof_n[SACD_NUM_KCLASS]{};
+  bool world_multi = false;
+};
+
+size_t real_size(const Context &c);
+
+// layout.cu
+int build_layouts(Context &c, const uint32_t *coords_dev, const float *vals_dev);
+
+// kernels.cu
+int launch_init_factors(Context &c, uint64_t seed);
+int launch_mttkrp(Context &c, int mode, void *out_M);
+int launch_mode_update(Context &c, int mode, int branch_override, bool begin_sweep, bool end_sweep,
+                       uint8_t *decisions_dev);
+int launch_gram(Context &c, int mode);
+int launch_initial_fit(Context &c);
+int launch_convert_in(Context &c, const double *src_dev, long long rows, void *dst);
+int launch_convert_out(Context &c, const void *src, long long rows, double *dst_dev);
+int launch_hessian_only(Context &c, int mode);
+int launch_setup(Context &c);
+long long rows_block_for(const Context &c);
+
+// profiling helpers (kernels.cu uses them around launches)
+int prof_begin(Context &c, int kclass);
+int prof_end(Context &c, int kclass, int start_idx);
+
+}  // namespace sacd

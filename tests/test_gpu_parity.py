@@ -1,0 +1,272 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 CPU oracle on the same
+seeded inputs.  Bit-exact for the layout and the init; the north-star tolerances for
+floating point: relative objective error <= 1e-4 per sweep and max relative factor error
+<= 1e-3 (column-relative floor) after 10 sweeps."""
+import numpy as np
+import pytest
+
+import oracle as O
+import sacd_inputs as SI
+
+pytestmark = pytest.mark.gpu
+
+F_TOL = 1e-4
+FACTOR_TOL = 1e-3
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2003_03572_b200 import build
+    build.build()
+
+
+def S(*a, **k):
+    from paper_2003_03572_b200.sacd import Sacd
+    return Sacd(*a, **k)
+
+
+def factor_err(Fg, Fo):
+    """max_{i,r} |Fg - Fo| / max(|Fo|, 1e-3 * max_i |Fo[:, r]|)"""
+    floor = 1e-3 * np.abs(Fo).max(axis=0, keepdims=True)
+    den = np.maximum(np.abs(Fo), floor)
+    den = np.where(den == 0, 1.0, den)
+    return float((np.abs(Fg - Fo) / den).max())
+
+
+def ragged_tensor(dims, nnz, seed, heavy_rows=((0, 0, 300),)):
+    """Uniform tensor plus heavy slices (mode, index, count) to force split rows."""
+    cfg = SI.custom_config(dims, nnz, 4, cid=seed)
+    c = SI.make_coords(cfg).numpy()
+    extra = []
+    rng = np.random.default_rng(seed)
+    for mode, idx, cnt in heavy_rows:
+        e = rng.integers(0, dims, size=(cnt, 3))
+        e[:, mode] = idx
+        extra.append(e)
+    c = np.concatenate([c] + extra)
+    key = (c[:, 0] * dims[1] + c[:, 1]) * dims[2] + c[:, 2]
+    _, first = np.unique(key, return_index=True)
+    c = c[np.sort(first)]
+    v = (1.0 - SI.unit24_t(SI.rand_t(seed, SI.TAG_VALUE, SI.torch.from_numpy(
+        (c[:, 0] * dims[1] + c[:, 1]) * dims[2] + c[:, 2]))).numpy()).astype(np.float32)
+    return c.astype(np.uint32), v
+
+
+# ----------------------------------------------------------------------------- layout / init
+@pytest.mark.parametrize("nnz_per_item", [0, 16])
+def test_layout_bit_exact(nnz_per_item):
+    dims = (37, 23, 51)
+    c, v = ragged_tensor(dims, 3000, 5, heavy_rows=((0, 3, 400), (1, 7, 300), (2, 50, 500)))
+    with S(c, v, dims, 6, 1, nnz_per_item=nnz_per_item) as g:
+        info = g.info()
+        assert info["nnz"] == len(v)
+        for n in range(3):
+            ia, ib, vv, rp = g.layout(n)
+            oa, ob, ov, orp = O.layout(c, v, dims, n)
+            assert (info["mode_a"][n], info["mode_b"][n]) == O.other_modes(dims, n)
+            assert np.array_equal(ia, oa) and np.array_equal(ib, ob)
+            assert np.array_equal(vv.view(np.uint32), ov.view(np.uint32))
+            assert np.array_equal(rp, orp)
+        if nnz_per_item == 16:
+            assert min(info["split_rows"]) > 0
+        assert info["xnorm2"] == pytest.approx(float((v.astype(np.float64) ** 2).sum()), rel=1e-14)
+
+
+@pytest.mark.parametrize("precision", ["f64", "f32"])
+@pytest.mark.parametrize("R", [1, 5, 16, 64, 256])
+def test_init_bit_exact(precision, R):
+    dims = (30, 20, 10)
+    c, v = SI.tiny_tensor(dims, 0.05, 3)
+    with S(c.numpy(), v.numpy(), dims, R, 77, precision=precision) as g:
+        Fo = O.init_factors(dims, R, 77)
+        for n in range(3):
+            assert np.array_equal(g.factors(n), Fo[n])   # 24-bit dyadic values are exact in fp32 too
+
+
+def test_errors_dup_range_nonfinite():
+    from paper_2003_03572_b200.sacd import SacdError, SACD_EDUP, SACD_ERANGE, SACD_ENONFINITE
+    dims = (4, 4, 4)
+    with pytest.raises(SacdError) as e:
+        S(np.array([[0, 0, 0], [0, 0, 0]], np.uint32), np.ones(2, np.float32), dims, 2, 1)
+    assert e.value.code == SACD_EDUP
+    with pytest.raises(SacdError) as e:
+        S(np.array([[0, 0, 0], [0, 4, 0]], np.uint32), np.ones(2, np.float32), dims, 2, 1)
+    assert e.value.code == SACD_ERANGE
+    with pytest.raises(SacdError) as e:
+        S(np.array([[0, 0, 0]], np.uint32), np.array([np.inf], np.float32), dims, 2, 1)
+    assert e.value.code == SACD_ENONFINITE
+
+
+# ----------------------------------------------------------------------------- teacher-forced kernels
+@pytest.mark.parametrize("R", [1, 5, 8, 16, 33, 64, 128, 256])
+@pytest.mark.parametrize("precision", ["f64", "f32"])
+def test_mttkrp_gram_hessian(R, precision):
+    dims = (41, 29, 57)
+    c, v = ragged_tensor(dims, 4000, 11, heavy_rows=((0, 2, 600), (2, 9, 700)))
+    F = O.init_factors(dims, R, 3)
+    with S(c, v, dims, R, 3, precision=precision, nnz_per_item=64) as g:
+        tol = 1e-12 if precision == "f64" else 1e-5
+        for n in range(3):
+            Mo = O.mttkrp(c, v, dims, n, F)
+            Mg = g.mttkrp(n)
+            scale = np.maximum(np.abs(Mo).max(axis=0, keepdims=True), 1e-30)
+            assert (np.abs(Mg - Mo) / scale).max() <= tol
+            Go = O.gram(F[n])
+            assert np.abs(g.gram(n) - Go).max() <= tol * np.abs(Go).max()
+            Ho = O.mode_hessian(F, dims, n)
+            assert np.abs(g.hessian(n) - Ho).max() <= tol * np.abs(Ho).max()
+
+
+@pytest.mark.parametrize("R", [3, 16, 64, 128])
+@pytest.mark.parametrize("branch", [0, 1, 2])
+@pytest.mark.parametrize("l_mode", ["diag", "frob"])
+def test_one_pass_teacher_forced_f64(R, branch, l_mode):
+    """One mode pass from identical state: decisions identical, factors / z to fp64 noise."""
+    dims = (60, 45, 33)
+    c, v = ragged_tensor(dims, 5000, 21, heavy_rows=((1, 4, 500),))
+    F = O.init_factors(dims, R, 9)
+    rng = np.random.default_rng(R + 10 * branch)
+    with S(c, v, dims, R, 9, l_mode=l_mode, nnz_per_item=128) as g:
+        for n in range(3):
+            Z0 = rng.random((dims[n], R)) * 0.1
+            g.set_zprev(n, Z0)
+            out = g.mode_update(n, branch=branch, decisions=True)
+            M = O.mttkrp(c, v, dims, n, F)
+            H = O.mode_hessian(F, dims, n)
+            Fn, zp, ti, E, Ech, md, dec = O.mode_pass(M, H, F[n], Z0, branch,
+                                                     l_mode=O.L_DIAG if l_mode == "diag" else O.L_FROB,
+                                                     decisions=True)
+            assert np.array_equal(out["decisions"], dec)
+            assert out["E"] == E and out["E_changed"] == Ech
+            assert factor_err(g.factors(n), Fn) <= 1e-9
+            assert np.abs(g.get_zprev(n) - zp).max() <= 1e-9 * max(1.0, np.abs(zp).max())
+            assert abs(out["ti"] - ti) <= 1e-9 * max(1.0, abs(ti))
+            F[n] = Fn                       # keep GPU and oracle states identical for the next mode
+            g.set_factors(n, Fn)
+
+
+def test_one_pass_teacher_forced_f32_flip_census():
+    """fp32 state: decisions agree except near-ties (|z| <= 1e-6 max|z| for the FIRST rule)."""
+    dims, R = (80, 60, 40), 16
+    c, v = ragged_tensor(dims, 8000, 4, heavy_rows=())
+    F = O.init_factors(dims, R, 2)
+    with S(c, v, dims, R, 2, precision="f32") as g:
+        for n in range(3):
+            Z0 = np.zeros((dims[n], R))
+            out = g.mode_update(n, branch=0, decisions=True)
+            M = O.mttkrp(c, v, dims, n, F)
+            H = O.mode_hessian(F, dims, n)
+            Fn, zp, ti, E, Ech, md, dec = O.mode_pass(M, H, F[n], Z0, 0, decisions=True)
+            mism = out["decisions"] != dec
+            if mism.any():   # FIRST: sp = z, a near-tie means z ~ 0 relative to the pass
+                tie = np.abs(zp) <= 1e-6 * np.abs(zp).max()
+                assert tie[mism].all()
+            F[n] = g.factors(n)
+            g.set_factors(n, F[n])
+
+
+# ----------------------------------------------------------------------------- end to end
+def run_pair(c, v, dims, R, seed, K, **kw):
+    precision = kw.pop("precision", "f64")
+    with S(c, v, dims, R, seed, precision=precision, **kw) as g:
+        f0 = g.fit()[0]
+        g.iterate(K)
+        st = g.stats()
+        Fg = g.factors()
+        fg = np.array([f0] + [s["objective"] for s in st])
+        Eg = np.array([s["E"] for s in st])
+        brg = np.array([s["branch"] for s in st])
+    l_mode = {"diag": O.L_DIAG, "frob": O.L_FROB}[kw.get("l_mode", "diag")]
+    variant = {"gs": O.VAR_GS_LAGGED, "select_off": O.VAR_SELECT_OFF}[kw.get("variant", "gs")]
+    ora = O.sacd_run(c, v, dims, R, seed, K, l_mode=l_mode, variant=variant)
+    return fg, Fg, Eg, brg, ora
+
+
+def check_pair(fg, Fg, Eg, brg, ora, f_tol=F_TOL, factor_tol=FACTOR_TOL):
+    fo = ora["f"]
+    rel = np.abs(fg - fo) / np.maximum(fo, 1e-300)
+    assert rel.max() <= f_tol, rel
+    # explained energy ||X||^2 - f, when it is not negligible
+    ex_o = ora["xnorm2"] - fo
+    ex_g = ora["xnorm2"] - fg
+    big = ex_o > 1e-3 * ora["xnorm2"]
+    if big.any():
+        assert (np.abs(ex_g - ex_o)[big] / ex_o[big]).max() <= f_tol
+    for n in range(3):
+        assert factor_err(Fg[n], ora["F"][n]) <= factor_tol
+    assert np.array_equal(brg, ora["branch"])
+    return rel.max()
+
+
+@pytest.mark.parametrize("variant", ["gs", "select_off"])
+@pytest.mark.parametrize("l_mode", ["diag", "frob"])
+def test_end_to_end_c1(variant, l_mode):
+    cfg = SI.CONFIGS["c1"]
+    c, v = SI.make_tensor(cfg)
+    c, v = c.numpy(), v.numpy()
+    fg, Fg, Eg, brg, ora = run_pair(c, v, cfg.dims, cfg.rank, cfg.seed, cfg.iters, variant=variant, l_mode=l_mode)
+    check_pair(fg, Fg, Eg, brg, ora)
+    assert np.array_equal(Eg, ora["E"])
+
+
+def test_end_to_end_c2_10_sweeps():
+    cfg = SI.CONFIGS["c2"]
+    c, v = SI.make_tensor(cfg)
+    c, v = c.numpy(), v.numpy()
+    fg, Fg, Eg, brg, ora = run_pair(c, v, cfg.dims, cfg.rank, cfg.seed, 10)
+    check_pair(fg, Fg, Eg, brg, ora)
+
+
+@pytest.mark.parametrize("R", [1, 8, 33, 128])
+def test_end_to_end_ragged_ranks(R):
+    dims = (300, 200, 50)
+    c, v = ragged_tensor(dims, 20000, 8, heavy_rows=((2, 1, 3000), (0, 5, 900)))
+    fg, Fg, Eg, brg, ora = run_pair(c, v, dims, R, 17, 10, nnz_per_item=256)
+    check_pair(fg, Fg, Eg, brg, ora)
+
+
+def test_empty_tensor():
+    dims = (5, 4, 3)
+    with S(np.zeros((0, 3), np.uint32), np.zeros(0, np.float32), dims, 3, 1) as g:
+        g.iterate(2)
+        f, fit = g.fit()
+        assert f == 0.0
+        for n in range(3):
+            assert (g.factors(n) == 0).all()
+
+
+def test_deterministic_and_graph_equals_eager():
+    cfg = SI.CONFIGS["c1"]
+    c, v = SI.make_tensor(cfg)
+    res = []
+    for use_graph in (True, True, False):
+        with S(c.numpy(), v.numpy(), cfg.dims, cfg.rank, cfg.seed, use_graph=use_graph) as g:
+            g.iterate(6)
+            res.append((g.factors(), [s["objective"] for s in g.stats()]))
+    for r in res[1:]:
+        assert all(np.array_equal(a, b) for a, b in zip(r[0], res[0][0]))
+        assert r[1] == res[0][1]
+
+
+def test_device_pointer_inputs():
+    import torch
+    cfg = SI.CONFIGS["c1"]
+    c, v = SI.make_tensor(cfg)
+    with S(c.cuda(), v.cuda(), cfg.dims, cfg.rank, cfg.seed) as g1, \
+            S(c.numpy(), v.numpy(), cfg.dims, cfg.rank, cfg.seed) as g2:
+        g1.iterate(3)
+        g2.iterate(3)
+        assert np.array_equal(g1.factors(0), g2.factors(0))
+
+
+def test_profile_mode_counts_launches():
+    cfg = SI.CONFIGS["c1"]
+    c, v = SI.make_tensor(cfg)
+    with S(c.numpy(), v.numpy(), cfg.dims, cfg.rank, cfg.seed, profile=True) as g:
+        g.profile_reset()
+        g.iterate(4)
+        p = g.profile_read()
+        assert p["mttkrp"][1] == 12 and p["rows"][1] == 12 and p["mttkrp"][0] > 0
