@@ -1,0 +1,363 @@
+#!/usr/bin/env python
+"""bench.py -- SaCD full sweeps/s (all modes) on B200, through libsacd's C ABI.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--precision f64]
+    python bench.py --impl reference ...       (the fp64 CPU oracle on the host cores)
+
+A "step" is one SaCD sweep (U, V and W mode updates: MTTKRP, Gram-Hadamard H, the fused
+column-wise SaCD row update, Gram refresh, objective) over the whole synthetic tensor of
+the configuration (BASELINE.json configs; default c4, the largest single-GPU one and the
+one the north star's scaling target names).  Inputs (the mode-sorted layouts: 3.6 GB for
+c4) are larger than the 126 MB L2, so no L2 flush is needed between sweeps.
+
+Prints ONE JSON line on rank 0 (see DESIGN.md section 7 for every field).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "SaCD full sweeps/sec (all modes) on sparse 3-way NTF"
+UNIT = "sweeps/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=None)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="sacd", choices=["sacd", "reference"])
+    p.add_argument("--config", default="c4")
+    p.add_argument("--rank", type=int, default=None, help="override R (c5 rank sweep)")
+    p.add_argument("--precision", default="f64", choices=["f64", "f32"])
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--nnz-per-item", type=int, default=0)
+    return p.parse_args()
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled every 50 ms while running."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.lines = []
+        self.proc = None
+        self.t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-i", str(self.index), "-lms", "50"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                smax.append(float(f[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, f[4:8]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- algorithmic bytes
+def algorithmic_bytes(cfg_dims, nnz, R, s):
+    """Per mode n: MTTKRP = 12 nnz (idx_a, idx_b, val) + 8 (I_n+1) (row_ptr)
+    + (I_a + I_b) R s (each other-factor row once) + I_n R s (M write);
+    row update = 5 I_n R s (M read, F read+write, z_prev read+write).
+    B_comp per sweep = sum over modes of MTTKRP + row update - M round trip."""
+    d = cfg_dims
+    out = {}
+    for n in range(3):
+        a, b = [m for m in range(3) if m != n]
+        mt = 12 * nnz + 8 * (d[n] + 1) + (d[a] + d[b]) * R * s + d[n] * R * s
+        rows = 5 * d[n] * R * s
+        out[n] = (mt, rows)
+    bcomp = sum(12 * nnz + 8 * (d[n] + 1) + (sum(d) - d[n]) * R * s + 4 * d[n] * R * s for n in range(3))
+    return out, bcomp
+
+
+# ----------------------------------------------------------------------------- oracle (CPU) leg
+def oracle_sweep_seconds(c, v, dims, R, seed, frac, reps=1):
+    """Wall seconds of ONE oracle sweep (oracle.sacd_run with K=1, layout build included)
+    on the sample 'every (1/frac)-th nonzero, full dims'."""
+    import oracle as O
+    step = max(1, int(round(1 / frac)))
+    cs, vs = np.ascontiguousarray(c[::step]), np.ascontiguousarray(v[::step])
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        O.sacd_run(cs, vs, dims, R, seed, 1)
+        ts.append(time.perf_counter() - t0)
+    return float(np.median(ts)), len(vs)
+
+
+def cpu_baseline(c, v, dims, R, seed, nnz, budget_s=30.0):
+    """Oracle sweeps/s for the FULL workload, extrapolated from two bounded samples with a
+    two-point model t(n) = a + b n (a = the nnz-independent Gram / row work, b = per-nonzero
+    work), both measured here on the host cores."""
+    import oracle as O
+    O.build()
+    cores = O.max_threads()
+    f1, f2 = 1 / 400, 1 / 200
+    t1, n1 = oracle_sweep_seconds(c, v, dims, R, seed, f1)
+    if t1 > budget_s / 2:
+        f2 = f1
+        t2, n2 = t1, n1
+        t_full = t1 * nnz / max(n1, 1)
+        how = f"one sample (every {int(1 / f1)}th nonzero, {n1} nnz, full dims), linear in nnz"
+    else:
+        t2, n2 = oracle_sweep_seconds(c, v, dims, R, seed, f2)
+        b = (t2 - t1) / max(n2 - n1, 1)
+        t_full = t2 + max(b, 0.0) * (nnz - n2)
+        how = (f"oracle.sacd_run K=1 (layout sort included) on every {int(1 / f1)}th and every "
+               f"{int(1 / f2)}th nonzero ({n1} / {n2} nnz, full dims): {t1:.2f} s / {t2:.2f} s, "
+               f"extrapolated t(n)=a+b*n to {nnz} nnz")
+    return {"value": 1.0 / t_full, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": how,
+            "sample_seconds": [t1, t2]}
+
+
+def run_reference(args, cfg, R):
+    """--impl reference: the fp64 oracle on the box's host cores (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import torch
+    import oracle as O
+    import sacd_inputs as SI
+    O.build()
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    c, v = SI.make_tensor(cfg, device=dev)
+    c, v = c.cpu().numpy().astype(np.uint32), v.cpu().numpy()
+    nnz = len(v)
+    frac = 1 / 200 if nnz > 5_000_000 else 1.0
+    K = args.steps if args.steps is not None else 5
+    step = max(1, int(round(1 / frac)))
+    cs, vs = np.ascontiguousarray(c[::step]), np.ascontiguousarray(v[::step])
+    for _ in range(args.warmup):
+        O.sacd_run(cs, vs, cfg.dims, R, cfg.seed, 1)
+    ts = []
+    for _ in range(K):
+        t0 = time.perf_counter()
+        O.sacd_run(cs, vs, cfg.dims, R, cfg.seed, 1)
+        ts.append(time.perf_counter() - t0)
+    t_sample = float(np.mean(ts))
+    if frac < 1.0:
+        t_half, n_half = oracle_sweep_seconds(c, v, cfg.dims, R, cfg.seed, frac / 2)
+        b = (t_sample - t_half) / max(len(vs) - n_half, 1)
+        t_full = t_sample + max(b, 0.0) * (nnz - len(vs))
+        sample = (f"each step = oracle.sacd_run K=1 (layout included) on every {step}th nonzero ({len(vs)} nnz, "
+                  f"full dims); full-workload time extrapolated t(n)=a+b*n with a second sample of {n_half} nnz")
+    else:
+        t_full = t_sample
+        sample = "full workload, one oracle sweep per step"
+    val = 1.0 / t_full
+    cores = O.max_threads()
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": K, "warmup": args.warmup, "ms_per_step": 1e3 * t_full, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg.name, "dims": list(cfg.dims), "nnz": cfg.nnz, "rank": R},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "gpu_launches": 0}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- GPU leg
+def main():
+    args = parse()
+    import sacd_inputs as SI
+    cfg = SI.CONFIGS[args.config]
+    R = args.rank or cfg.rank
+    if args.impl == "reference":
+        run_reference(args, cfg, R)
+        return
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2003_03572_b200 import build
+    if rank == 0 or world == 1:
+        build.build()
+    if world > 1:
+        dist.barrier()
+    from paper_2003_03572_b200.sacd import Sacd
+
+    K = args.steps if args.steps is not None else cfg.iters
+    W = args.warmup
+    s = 8 if args.precision == "f64" else 4
+
+    t_gen = time.perf_counter()
+    coords, vals = SI.make_tensor(cfg, device="cuda")
+    torch.cuda.synchronize()
+    t_gen = time.perf_counter() - t_gen
+    nnz = int(vals.shape[0])
+    stream = torch.cuda.Stream()
+
+    # ---- device-resident timed region (kernel-class events on the launching stream)
+    g = Sacd(coords, vals, cfg.dims, R, cfg.seed, precision=args.precision, stream=stream.cuda_stream,
+             profile=True, nnz_per_item=args.nnz_per_item, device=local)
+    info = g.info()
+    g.iterate(W)
+    g.sync()
+    g.profile_reset()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.15)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    g.iterate(K)
+    e1.record(stream)
+    e1.synchronize()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    clk = clocks.stop()
+    prof = g.profile_read()
+    f_final, fit_final = g.fit()
+    ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    value = world * K / (ms_max / 1e3)  # replicas: every rank runs the full workload
+
+    per_mode, bcomp = algorithmic_bytes(cfg.dims, nnz, R, s)
+    kc = {k: v for k, v in prof.items()}
+    dom = max(kc, key=lambda k: kc[k][0])
+    launches = sum(n for (_, n) in kc.values()) + sum(1 for k in ("gram",) for _ in range(kc[k][1]))  # gram = 2 kernels
+    mt_ms = kc["mttkrp"][0] / max(kc["mttkrp"][1], 1)
+    mt_bytes = sum(per_mode[n][0] for n in range(3)) / 3
+    rows_ms = kc["rows"][0] / max(kc["rows"][1], 1)
+    rows_bytes = sum(per_mode[n][1] for n in range(3)) / 3
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "MEASURED_PEAKS.json hbm_gbs (measured)" if "hbm_gbs" in peaks else "fallback 6650 GB/s"
+    traffic = None
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+        traffic = tr.get(f"{cfg.name}_R{R}_{args.precision}_mttkrp")
+    except Exception:
+        pass
+    if dom == "rows":
+        achieved = rows_bytes / (rows_ms / 1e3) / 1e9
+        dom_name, dom_bytes, dom_ms = "k_sacd_rows", rows_bytes, rows_ms
+    else:
+        achieved = mt_bytes / (mt_ms / 1e3) / 1e9
+        dom_name, dom_bytes, dom_ms = "k_mttkrp", mt_bytes, mt_ms
+    roofline = {"bound": "hbm", "kernel": dom_name, "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                "frac": achieved / hbm_peak, "traffic": traffic, "algorithmic_bytes_per_launch": dom_bytes,
+                "avg_launch_ms": dom_ms, "peak_source": peak_src,
+                "sweep_hbm_frac": (bcomp / (ms_max / K / 1e3) / 1e9) / hbm_peak,
+                "sweep_hbm_frac_8TBs": (bcomp / (ms_max / K / 1e3) / 1e9) / 8000.0,
+                "kernel_ms_per_sweep": {k: v[0] / K for k, v in kc.items()}}
+
+    # ---- end to end through the public API with host (pinned) buffers
+    e2e = None
+    if not args.no_e2e:
+        hc = coords.cpu().pin_memory()
+        hv = vals.cpu().pin_memory()
+        g.close()
+        del g
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        g2 = Sacd(hc, hv, cfg.dims, R, cfg.seed, precision=args.precision, stream=stream.cuda_stream,
+                  nnz_per_item=args.nnz_per_item, device=local)
+        g2.iterate(K)
+        Fs = g2.factors()
+        f2, _ = g2.fit()
+        t_e2e = time.perf_counter() - t0
+        te = torch.tensor([t_e2e], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        t_e2e = float(te.item())
+        g2.close()
+        h2d = nnz * 16
+        d2h = sum(x.nbytes for x in Fs) + 16
+        e2e = {"value": world * K / t_e2e, "unit": UNIT, "h2d_bytes_per_step": h2d / K, "d2h_bytes_per_step": d2h / K,
+               "seconds": t_e2e,
+               "what": "sacd_init from pinned host COO (H2D + device layout sort) + sacd_iterate(K) + "
+                       "sacd_factors (D2H, all modes) + sacd_fit; bytes per step = totals / K"}
+    else:
+        g.close()
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline(coords.cpu().numpy().astype(np.uint32), vals.cpu().numpy(), cfg.dims, R, cfg.seed,
+                               nnz)
+        except Exception as ex:  # the baseline must never break the bench line
+            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle", "sample": f"failed: {ex}"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
+                "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": args.precision, "data": "synthetic",
+                "config": {"workload": cfg.name, "dims": list(cfg.dims), "nnz": nnz, "rank": R,
+                           "parallelism": "replicas" if world > 1 else "single",
+                           "l2": "inputs larger than L2 (mode layouts %.2f GB > 126 MB), no flush" % (36 * nnz / 1e9),
+                           "b_comp_bytes_per_sweep": bcomp, "gen_seconds": t_gen,
+                           "mttkrp_items": info["items"], "split_rows": info["split_rows"],
+                           "objective_after": f_final, "fit_after": fit_final},
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+                "clocks": clk}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

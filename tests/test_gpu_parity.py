@@ -229,13 +229,19 @@ def test_end_to_end_ragged_ranks(R):
 
 
 def test_empty_tensor():
+    """nnz = 0: the U pass drives U to 0 (m = 0), after which h_rr = 0 for V and W, which are
+    then skipped (reading C11); f = 0 from sweep 1 on.  Same as the oracle."""
     dims = (5, 4, 3)
-    with S(np.zeros((0, 3), np.uint32), np.zeros(0, np.float32), dims, 3, 1) as g:
+    c, v = np.zeros((0, 3), np.uint32), np.zeros(0, np.float32)
+    with S(c, v, dims, 3, 1) as g:
         g.iterate(2)
         f, fit = g.fit()
-        assert f == 0.0
-        for n in range(3):
-            assert (g.factors(n) == 0).all()
+        Fg = g.factors()
+    ora = O.sacd_run(c, v, dims, 3, 1, 2)
+    assert f == 0.0 == ora["f"][-1]
+    assert (Fg[0] == 0).all()
+    for n in range(3):
+        assert np.array_equal(Fg[n], ora["F"][n])
 
 
 def test_deterministic_and_graph_equals_eager():
