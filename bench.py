@@ -118,81 +118,93 @@ def algorithmic_bytes(cfg_dims, nnz, R, s):
 
 
 # ----------------------------------------------------------------------------- oracle (CPU) leg
-def oracle_sweep_seconds(c, v, dims, R, seed, frac, reps=1):
-    """Wall seconds of ONE oracle sweep (oracle.sacd_run with K=1, layout build included)
-    on the sample 'every (1/frac)-th nonzero, full dims'."""
-    import oracle as O
-    step = max(1, int(round(1 / frac)))
-    cs, vs = np.ascontiguousarray(c[::step]), np.ascontiguousarray(v[::step])
-    ts = []
-    for _ in range(reps):
-        t0 = time.perf_counter()
-        O.sacd_run(cs, vs, dims, R, seed, 1)
-        ts.append(time.perf_counter() - t0)
-    return float(np.median(ts)), len(vs)
+class OracleSweepSample:
+    """The fp64 oracle's per-sweep work on a bounded sample, scaled to the full workload.
+
+    One oracle sweep (oracle.sacd_run) does, per mode n: Gram of the two other factors,
+    MTTKRP over all nonzeros, the row pass over all I_n rows; plus the three Grams for the
+    objective -- i.e. each factor's Gram three times.  The MTTKRP cost is linear in the
+    nonzeros and the Gram / row-pass cost linear in the rows, so we time
+      * oracle.mttkrp_layout on every `nz_step`-th nonzero (full dims), x nz_step, and
+      * 3 x oracle.gram + oracle.mode_pass on every `row_step`-th row, x row_step,
+    with the oracle's own functions, as they stand, on all host cores.  Layout building
+    (init work, not per sweep) is done untimed in the constructor."""
+
+    def __init__(self, c, v, dims, R, seed, nz_step, row_step):
+        import oracle as O
+        O.build()
+        self.O, self.dims, self.R = O, dims, R
+        self.nz_step, self.row_step = nz_step, row_step
+        self.F = O.init_factors(dims, R, seed)
+        cs, vs = np.ascontiguousarray(c[::nz_step]), np.ascontiguousarray(v[::nz_step])
+        self.n_sample = len(vs)
+        self.lay = [O.layout(cs, vs, dims, n) for n in range(3)]
+        self.H = [O.mode_hessian(self.F, dims, n) for n in range(3)]
+        self.rows = [np.ascontiguousarray(self.F[n][::row_step]) for n in range(3)]
+
+    def seconds(self):
+        O = self.O
+        t = 0.0
+        for n in range(3):
+            a, b = O.other_modes(self.dims, n)
+            ia, ib, vv, rp = self.lay[n]
+            t0 = time.perf_counter()
+            O.mttkrp_layout(rp, ia, ib, vv, self.F[a], self.F[b])
+            t += (time.perf_counter() - t0) * self.nz_step
+            Fs = self.rows[n]
+            Ms = np.zeros_like(Fs)
+            t0 = time.perf_counter()
+            for _ in range(3):
+                O.gram(Fs)
+            O.mode_pass(Ms, self.H[n], Fs, np.zeros_like(Fs), O.BR_FIRST)
+            t += (time.perf_counter() - t0) * self.row_step
+        return t
+
+    def describe(self, nnz):
+        return (f"oracle per-sweep work as it stands: mttkrp_layout on every {self.nz_step}th nonzero "
+                f"({self.n_sample} of {nnz}) x{self.nz_step}, plus 3 x gram + mode_pass on every "
+                f"{self.row_step}th row x{self.row_step}; layouts built untimed; all host cores")
 
 
-def cpu_baseline(c, v, dims, R, seed, nnz, budget_s=30.0):
-    """Oracle sweeps/s for the FULL workload, extrapolated from two bounded samples with a
-    two-point model t(n) = a + b n (a = the nnz-independent Gram / row work, b = per-nonzero
-    work), both measured here on the host cores."""
+def sample_steps(nnz, rows_total):
+    nz_step = max(1, nnz // 2_000_000)
+    row_step = max(1, rows_total // 100_000)
+    return nz_step, row_step
+
+
+def cpu_baseline(c, v, dims, R, seed, nnz, reps=3):
     import oracle as O
-    O.build()
-    cores = O.max_threads()
-    f1, f2 = 1 / 400, 1 / 200
-    t1, n1 = oracle_sweep_seconds(c, v, dims, R, seed, f1)
-    if t1 > budget_s / 2:
-        f2 = f1
-        t2, n2 = t1, n1
-        t_full = t1 * nnz / max(n1, 1)
-        how = f"one sample (every {int(1 / f1)}th nonzero, {n1} nnz, full dims), linear in nnz"
-    else:
-        t2, n2 = oracle_sweep_seconds(c, v, dims, R, seed, f2)
-        b = (t2 - t1) / max(n2 - n1, 1)
-        t_full = t2 + max(b, 0.0) * (nnz - n2)
-        how = (f"oracle.sacd_run K=1 (layout sort included) on every {int(1 / f1)}th and every "
-               f"{int(1 / f2)}th nonzero ({n1} / {n2} nnz, full dims): {t1:.2f} s / {t2:.2f} s, "
-               f"extrapolated t(n)=a+b*n to {nnz} nnz")
-    return {"value": 1.0 / t_full, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": how,
-            "sample_seconds": [t1, t2]}
+    nz_step, row_step = sample_steps(nnz, sum(dims))
+    s = OracleSweepSample(c, v, dims, R, seed, nz_step, row_step)
+    ts = [s.seconds() for _ in range(reps)]
+    t = float(np.median(ts))
+    return {"value": 1.0 / t, "unit": UNIT, "cores": O.max_threads(), "kind": "oracle",
+            "sample": s.describe(nnz) + f"; median of {reps}", "seconds_per_sweep": t}
 
 
 def run_reference(args, cfg, R):
-    """--impl reference: the fp64 oracle on the box's host cores (rank 0 only)."""
+    """--impl reference: the fp64 oracle on the box's host cores (rank 0 only); each step
+    is the sampled oracle sweep of OracleSweepSample, scaled to the full workload."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     import torch
     import oracle as O
     import sacd_inputs as SI
-    O.build()
     dev = "cuda" if torch.cuda.is_available() else "cpu"
     c, v = SI.make_tensor(cfg, device=dev)
     c, v = c.cpu().numpy().astype(np.uint32), v.cpu().numpy()
     nnz = len(v)
-    frac = 1 / 200 if nnz > 5_000_000 else 1.0
+    nz_step, row_step = sample_steps(nnz, sum(cfg.dims))
+    smp = OracleSweepSample(c, v, cfg.dims, R, cfg.seed, nz_step, row_step)
     K = args.steps if args.steps is not None else 5
-    step = max(1, int(round(1 / frac)))
-    cs, vs = np.ascontiguousarray(c[::step]), np.ascontiguousarray(v[::step])
     for _ in range(args.warmup):
-        O.sacd_run(cs, vs, cfg.dims, R, cfg.seed, 1)
-    ts = []
-    for _ in range(K):
-        t0 = time.perf_counter()
-        O.sacd_run(cs, vs, cfg.dims, R, cfg.seed, 1)
-        ts.append(time.perf_counter() - t0)
-    t_sample = float(np.mean(ts))
-    if frac < 1.0:
-        t_half, n_half = oracle_sweep_seconds(c, v, cfg.dims, R, cfg.seed, frac / 2)
-        b = (t_sample - t_half) / max(len(vs) - n_half, 1)
-        t_full = t_sample + max(b, 0.0) * (nnz - len(vs))
-        sample = (f"each step = oracle.sacd_run K=1 (layout included) on every {step}th nonzero ({len(vs)} nnz, "
-                  f"full dims); full-workload time extrapolated t(n)=a+b*n with a second sample of {n_half} nnz")
-    else:
-        t_full = t_sample
-        sample = "full workload, one oracle sweep per step"
+        smp.seconds()
+    ts = [smp.seconds() for _ in range(K)]
+    t_full = float(np.mean(ts))
     val = 1.0 / t_full
     cores = O.max_threads()
+    sample = smp.describe(nnz)
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
             "steps": K, "warmup": args.warmup, "ms_per_step": 1e3 * t_full, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",

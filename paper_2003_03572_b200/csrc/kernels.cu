@@ -121,6 +121,60 @@ __global__ void __launch_bounds__(256) k_mttkrp(const WorkItem *__restrict__ ite
   const long long item = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (item >= n_items) return;
   const WorkItem it = items[item];
+  if constexpr (G == 1) {
+    // One nonzero at a time per warp.  The warp loads 32 nonzeros' (idx_a, idx_b, x)
+    // with coalesced streaming loads and broadcasts them by shuffle; rows are walked
+    // warp-uniformly and flushed when the nonzero index crosses row_ptr[row+1].
+    int row = it.row0;
+    long long row_end = min(row_ptr[row + 1], it.nz1);
+    Real acc[VPL][VEC];
+#pragma unroll
+    for (int v = 0; v < VPL; ++v)
+#pragma unroll
+      for (int c = 0; c < VEC; ++c) acc[v][c] = Real(0);
+    auto flush = [&](int rr) {
+      Real *dst = (it.slot >= 0) ? partial + it.slot * RT : M + (long long)rr * RT;
+      VT *dv = reinterpret_cast<VT *>(dst);
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) {
+        dv[lane + v * 32] = VV::make(acc[v]);
+#pragma unroll
+        for (int c = 0; c < VEC; ++c) acc[v][c] = Real(0);
+      }
+    };
+    for (long long base = it.nz0; base < it.nz1; base += 32) {
+      const int cnt = (int)min(32LL, it.nz1 - base);
+      uint32_t my_a = 0, my_b = 0;
+      float my_x = 0.f;
+      if (lane < cnt) {
+        my_a = ld_stream_u32(ia + base + lane);
+        my_b = ld_stream_u32(ib + base + lane);
+        my_x = ld_stream_f32(val + base + lane);
+      }
+      for (int j = 0; j < cnt; ++j) {
+        while (base + j >= row_end) {
+          flush(row);
+          ++row;
+          row_end = min(row_ptr[row + 1], it.nz1);
+        }
+        const uint32_t ea = __shfl_sync(0xffffffffu, my_a, j);
+        const uint32_t eb = __shfl_sync(0xffffffffu, my_b, j);
+        const Real x = (Real)__shfl_sync(0xffffffffu, my_x, j);
+        const VT *ap = reinterpret_cast<const VT *>(A + (long long)ea * RT);
+        const VT *bp = reinterpret_cast<const VT *>(B + (long long)eb * RT);
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) {
+          Real av[VEC], bv[VEC];
+          VV::get(__ldg(ap + lane + v * 32), av);
+          VV::get(__ldg(bp + lane + v * 32), bv);
+#pragma unroll
+          for (int c = 0; c < VEC; ++c) acc[v][c] = fma(x * av[c], bv[c], acc[v][c]);
+        }
+      }
+    }
+    for (; row < it.row1; ++row) flush(row);   // the last row(s), including empty ones
+    return;
+  }
   const int grp = lane / LPN, sub = lane % LPN;
   for (int row = it.row0; row < it.row1; ++row) {
     long long s = row_ptr[row], t = row_ptr[row + 1];
@@ -159,17 +213,37 @@ __global__ void __launch_bounds__(256) k_mttkrp(const WorkItem *__restrict__ ite
   }
 }
 
-// Heavy rows split across items: M_row = sum of the row's partials in slot order.
+// Heavy rows split across items: M_row = sum of the row's partials.  One block per split
+// row; warp w sums slots w, w+8, ... and the 8 warp sums are combined in warp order, so the
+// result is deterministic.
 template <typename Real, int RT>
-__global__ void k_fixup(const SplitRow *__restrict__ splits, long long n, const Real *__restrict__ partial,
-                        Real *__restrict__ M) {
-  const long long sidx = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (sidx >= n) return;
-  const SplitRow sr = splits[sidx];
-  for (int c = lane; c < RT; c += 32) {
-    Real s = Real(0);
-    for (long long k = 0; k < sr.nslots; ++k) s += partial[(sr.slot0 + k) * RT + c];
+__global__ void __launch_bounds__(256) k_fixup(const SplitRow *__restrict__ splits, long long n,
+                                               const Real *__restrict__ partial, Real *__restrict__ M) {
+  constexpr int CPL = RT >= 32 ? RT / 32 : 1;  // columns per lane
+  __shared__ Real red[8][RT];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const SplitRow sr = splits[blockIdx.x];
+  Real acc[CPL];
+#pragma unroll
+  for (int q = 0; q < CPL; ++q) acc[q] = Real(0);
+  for (long long k = w; k < sr.nslots; k += 8) {
+    const Real *p = partial + (sr.slot0 + k) * RT;
+#pragma unroll
+    for (int q = 0; q < CPL; ++q) {
+      const int c = lane + 32 * q;
+      if (c < RT) acc[q] += p[c];
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < CPL; ++q) {
+    const int c = lane + 32 * q;
+    if (c < RT) red[w][c] = acc[q];
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < RT; c += 256) {
+    Real s = red[0][c];
+#pragma unroll
+    for (int k = 1; k < 8; ++k) s += red[k][c];
     M[(long long)sr.row * RT + c] = s;
   }
 }
@@ -545,8 +619,7 @@ struct Impl {
     SACD_TRY(prof_end(c, 0, pe));
     if (md.n_splits > 0) {
       pe = prof_begin(c, 1);
-      const long long blocks = (md.n_splits + 7) / 8;
-      k_fixup<Real, RT><<<(unsigned)blocks, 256, 0, c.stream>>>(md.splits, md.n_splits,
+      k_fixup<Real, RT><<<(unsigned)md.n_splits, 256, 0, c.stream>>>(md.splits, md.n_splits,
                                                                  reinterpret_cast<const Real *>(c.partial), out);
       SACD_CUDA_TRY(cudaGetLastError());
       SACD_TRY(prof_end(c, 1, pe));
