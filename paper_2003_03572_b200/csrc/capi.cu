@@ -230,7 +230,7 @@ static int init_impl(Context *c, const uint32_t *coords, const float *vals, uint
   SACD_TRY(rc);
 
   // partitions
-  const long long T = c->opt.nnz_per_item > 0 ? c->opt.nnz_per_item : 512;
+  const long long T = c->opt.nnz_per_item > 0 ? c->opt.nnz_per_item : 1024;
   long long max_slots = 1, maxI = 1;
   for (int n = 0; n < 3; ++n) {
     ModeData &md = c->m[n];

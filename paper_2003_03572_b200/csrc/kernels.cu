@@ -122,17 +122,36 @@ __global__ void __launch_bounds__(256) k_mttkrp(const WorkItem *__restrict__ ite
   if (item >= n_items) return;
   const WorkItem it = items[item];
   if constexpr (G == 1) {
-    // One nonzero at a time per warp.  The warp loads 32 nonzeros' (idx_a, idx_b, x)
-    // with coalesced streaming loads and broadcasts them by shuffle; rows are walked
-    // warp-uniformly and flushed when the nonzero index crosses row_ptr[row+1].
+    // One nonzero at a time per warp, lanes across the R columns.
+    //  * The warp loads 32 nonzeros' (idx_a, idx_b, x) with coalesced streaming loads and
+    //    broadcasts them by shuffle.
+    //  * Fiber factoring: the layout is sorted by (i_n, i_a, i_b), so a
+    //    run of equal i_a inside a row is a fiber and
+    //        m_i = sum_fibers a_(i_a) * ( sum_{e in fiber} x_e b_(i_b(e)) ),
+    //    one a-row gather per fiber instead of per nonzero.  The a-row load is issued when
+    //    the fiber starts and consumed when it closes; the next b-row is prefetched.
+    //  * Rows are walked warp-uniformly and flushed when the nonzero index crosses
+    //    row_ptr[row+1] (empty rows get zeros).
     int row = it.row0;
     long long row_end = min(row_ptr[row + 1], it.nz1);
-    Real acc[VPL][VEC];
+    Real acc[VPL][VEC], facc[VPL][VEC], arow[VPL][VEC], bcur[VPL][VEC], bnext[VPL][VEC];
 #pragma unroll
     for (int v = 0; v < VPL; ++v)
 #pragma unroll
-      for (int c = 0; c < VEC; ++c) acc[v][c] = Real(0);
+      for (int c = 0; c < VEC; ++c) acc[v][c] = facc[v][c] = arow[v][c] = Real(0);
+    uint32_t cur_a = 0xffffffffu;
+    auto close_fiber = [&]() {
+#pragma unroll
+      for (int v = 0; v < VPL; ++v)
+#pragma unroll
+        for (int c = 0; c < VEC; ++c) {
+          acc[v][c] = fma(arow[v][c], facc[v][c], acc[v][c]);
+          facc[v][c] = Real(0);
+        }
+      cur_a = 0xffffffffu;
+    };
     auto flush = [&](int rr) {
+      close_fiber();
       Real *dst = (it.slot >= 0) ? partial + it.slot * RT : M + (long long)rr * RT;
       VT *dv = reinterpret_cast<VT *>(dst);
 #pragma unroll
@@ -141,6 +160,11 @@ __global__ void __launch_bounds__(256) k_mttkrp(const WorkItem *__restrict__ ite
 #pragma unroll
         for (int c = 0; c < VEC; ++c) acc[v][c] = Real(0);
       }
+    };
+    auto load_row = [&](const Real *F, uint32_t idx, Real (&out)[VPL][VEC]) {
+      const VT *p = reinterpret_cast<const VT *>(F + (long long)idx * RT);
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) VV::get(__ldg(p + lane + v * 32), out[v]);
     };
     for (long long base = it.nz0; base < it.nz1; base += 32) {
       const int cnt = (int)min(32LL, it.nz1 - base);
@@ -151,25 +175,28 @@ __global__ void __launch_bounds__(256) k_mttkrp(const WorkItem *__restrict__ ite
         my_b = ld_stream_u32(ib + base + lane);
         my_x = ld_stream_f32(val + base + lane);
       }
+      load_row(B, __shfl_sync(0xffffffffu, my_b, 0), bcur);
       for (int j = 0; j < cnt; ++j) {
+        if (j + 1 < cnt) load_row(B, __shfl_sync(0xffffffffu, my_b, j + 1), bnext);
         while (base + j >= row_end) {
           flush(row);
           ++row;
           row_end = min(row_ptr[row + 1], it.nz1);
         }
         const uint32_t ea = __shfl_sync(0xffffffffu, my_a, j);
-        const uint32_t eb = __shfl_sync(0xffffffffu, my_b, j);
         const Real x = (Real)__shfl_sync(0xffffffffu, my_x, j);
-        const VT *ap = reinterpret_cast<const VT *>(A + (long long)ea * RT);
-        const VT *bp = reinterpret_cast<const VT *>(B + (long long)eb * RT);
-#pragma unroll
-        for (int v = 0; v < VPL; ++v) {
-          Real av[VEC], bv[VEC];
-          VV::get(__ldg(ap + lane + v * 32), av);
-          VV::get(__ldg(bp + lane + v * 32), bv);
-#pragma unroll
-          for (int c = 0; c < VEC; ++c) acc[v][c] = fma(x * av[c], bv[c], acc[v][c]);
+        if (ea != cur_a) {
+          close_fiber();
+          cur_a = ea;
+          load_row(A, ea, arow);
         }
+#pragma unroll
+        for (int v = 0; v < VPL; ++v)
+#pragma unroll
+          for (int c = 0; c < VEC; ++c) {
+            facc[v][c] = fma(x, bcur[v][c], facc[v][c]);
+            bcur[v][c] = bnext[v][c];
+          }
       }
     }
     for (; row < it.row1; ++row) flush(row);   // the last row(s), including empty ones
@@ -317,6 +344,10 @@ __global__ void __launch_bounds__(rows_per_block<RT>())
   const int branch = st->branch[mode];
   const Real Lf = (Real)st->Lfrob[mode];
 
+  using VV = V16<Real>;
+  using VT = typename VV::T;
+  constexpr int VEC = VV::N;
+  constexpr int C = 8;  // column block: each u_j read from shared memory feeds C FMAs
   double ti = 0.0, md = 0.0;
   long long E = 0, Ech = 0;
   if (tid < nrows) {
@@ -324,35 +355,70 @@ __global__ void __launch_bounds__(rows_per_block<RT>())
     Real *u = Us + tid * US;
     const Real *m = M + row * RT;
     Real *zp = Z + row * RT;
-    for (int r = 0; r < R; ++r) {
-      const Real *Hrow = H + r * RT;  // H is symmetric: row r == column r
-      const Real h = Hrow[r];
-      Real z = Real(0);
-      bool sel = false;
-      if (h != Real(0)) {
-        Real s = Real(0);
+    for (int c0 = 0; c0 < R; c0 += C) {
+      // (1) block gradient with the current row (columns < c0 already updated), Eq 14:
+      //     acc_q = sum_j u_j h_(j, c0+q)        (H symmetric)
+      Real acc[C];
+#pragma unroll
+      for (int q = 0; q < C; ++q) acc[q] = Real(0);
 #pragma unroll 4
-        for (int j = 0; j < R; ++j) s = fma(u[j], Hrow[j], s);
-        const Real g = s - m[r];                       // Eq 14
-        const Real ur = u[r];
-        const Real un = fmax(Real(0), ur - g / h);     // Eq 11-13
-        const Real d = un - ur;                        // Eq 12
-        const Real L = l_mode ? Lf : h;
-        z = -g * d - (L * Real(0.5)) * d * d;          // Eq 20
-        const Real zpr = zp[r];
-        sel = (branch == SACD_BR_FIRST) ? (z > Real(0))
-                                        : ((branch == SACD_BR_EQ24) ? (z - zpr > Real(0)) : (zpr - z > Real(0)));
-        if (sel) {
-          u[r] = un;
-          E += 1;
-          if (d != Real(0)) Ech += 1;
+      for (int j = 0; j < R; ++j) {
+        const Real uj = u[j];
+        const VT *hj = reinterpret_cast<const VT *>(H + j * RT + c0);
+#pragma unroll
+        for (int x = 0; x < C / VEC; ++x) {
+          Real hv[VEC];
+          VV::get(hj[x], hv);
+#pragma unroll
+          for (int y = 0; y < VEC; ++y) acc[x * VEC + y] = fma(uj, hv[y], acc[x * VEC + y]);
         }
       }
-      zp[r] = z;
-      ti += (double)z;
-      if (dec) dec[row * R + r] = (uint8_t)sel;
+      Real mv[C], zv[C], dl[C];
+#pragma unroll
+      for (int x = 0; x < C / VEC; ++x) {
+        VV::get(reinterpret_cast<const VT *>(m + c0)[x], mv + x * VEC);
+        VV::get(reinterpret_cast<const VT *>(zp + c0)[x], zv + x * VEC);
+      }
+      // (2) Gauss-Seidel inside the block (C9): column r sees the steps dl of columns
+      //     c0..r-1 through the correction sum_q' h_(r, c0+q') dl_q'.
+#pragma unroll
+      for (int q = 0; q < C; ++q) {
+        const int r = c0 + q;
+        dl[q] = Real(0);
+        if (r < R) {
+          const Real *Hr_ = H + r * RT;
+          const Real h = Hr_[r];
+          Real z = Real(0);
+          bool sel = false;
+          if (h != Real(0)) {
+            Real sg = acc[q];
+#pragma unroll
+            for (int qq = 0; qq < q; ++qq) sg = fma(Hr_[c0 + qq], dl[qq], sg);
+            const Real g = sg - mv[q];                     // Eq 14
+            const Real ur = u[r];
+            const Real un = fmax(Real(0), ur - g / h);     // Eq 11-13
+            const Real d = un - ur;                        // Eq 12
+            const Real L = l_mode ? Lf : h;
+            z = -g * d - (L * Real(0.5)) * d * d;          // Eq 20
+            const Real zpr = zv[q];
+            sel = (branch == SACD_BR_FIRST) ? (z > Real(0))
+                                            : ((branch == SACD_BR_EQ24) ? (z - zpr > Real(0)) : (zpr - z > Real(0)));
+            if (sel) {
+              u[r] = un;
+              dl[q] = d;
+              E += 1;
+              if (d != Real(0)) Ech += 1;
+            }
+          }
+          zv[q] = z;                                       // z_prev <- z always (C8)
+          ti += (double)z;                                 // Eq 25
+          md += (double)u[r] * (double)mv[q];
+          if (dec) dec[row * R + r] = (uint8_t)sel;
+        }
+      }
+#pragma unroll
+      for (int x = 0; x < C / VEC; ++x) reinterpret_cast<VT *>(zp + c0)[x] = VV::make(zv + x * VEC);
     }
-    for (int r = 0; r < R; ++r) md += (double)u[r] * (double)m[r];
   }
   __syncthreads();
   Real *Fo = F + row0 * RT;
