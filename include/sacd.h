@@ -36,7 +36,7 @@ typedef struct sacd_ctx sacd_ctx; /* opaque; owned by the library until sacd_fre
 
 typedef enum {
   SACD_OK = 0,
-  SACD_EINVAL = -1,     /* bad argument: dims < 1, rank not in [1,256], nnz < 0, bad options   */
+  SACD_EINVAL = -1,     /* bad argument: dims not in [1,2^30), rank not in [1,256], nnz < 0     */
   SACD_ERANGE = -2,     /* a coordinate index >= its mode length                              */
   SACD_EDUP = -3,       /* duplicate (q,p,s) (Omega is a set, Table 2)           */
   SACD_ENONFINITE = -4, /* NaN or Inf value                                                   */
@@ -114,7 +114,7 @@ void sacd_default_options(sacd_options *opt);
  * uniformly in [0,1) from `seed` (Alg 1 input; reading C12) and their Grams, and
  * capture the sweep graph.
  *   coords : host or device, nnz x 3 uint32 (q,p,s), 0-based.   vals : host or device, fp32.
- *   dims   : host, {Q, P, S}, each >= 1 and < 2^32.              rank : 1..256.
+ *   dims   : host, {Q, P, S}, each >= 1 and < 2^30.              rank : 1..256.
  * Errors: EINVAL, ERANGE, EDUP, ENONFINITE, ENOMEM, ECUDA.  nnz == 0 is legal.
  * The caller keeps ownership of coords/vals and may free them when the call returns. */
 int sacd_init(sacd_ctx **out, const uint32_t *coords, const float *vals, int64_t nnz, const int64_t dims[3],

@@ -149,6 +149,7 @@ static void destroy(sacd_ctx *c) {
     ModeData &m = c->m[n];
     cudaFree(m.idx_a);
     cudaFree(m.idx_b);
+    cudaFree(m.idx_n);
     cudaFree(m.val);
     cudaFree(m.row_ptr);
     cudaFree(m.items);
@@ -377,8 +378,8 @@ int sacd_init(sacd_ctx **out, const uint32_t *coords, const float *vals, int64_t
     return SACD_EINVAL;
   }
   for (int n = 0; n < 3; ++n)
-    if (dims[n] < 1 || dims[n] > 2147483647LL) {
-      set_error("sacd_init: dims must be in [1, 2^31)");
+    if (dims[n] < 1 || dims[n] >= (1LL << 30)) {
+      set_error("sacd_init: dims must be in [1, 2^30)");
       return SACD_EINVAL;
     }
   if ((double)dims[0] * (double)dims[1] * (double)dims[2] >= 1.8e19) {
@@ -523,6 +524,12 @@ int sacd_mttkrp(sacd_ctx *c, int32_t mode, double *out, int64_t ld) {
     set_error("sacd_mttkrp: bad mode/ld/out");
     return SACD_ESTATE;
   }
+  // empty slices are not written by the MTTKRP kernel: clear M first for this entry point
+  cudaError_t e = cudaMemsetAsync(c->M, 0, (size_t)c->m[mode].I * c->pitch * real_size(*c), c->stream);
+  if (e != cudaSuccess) {
+    set_error(std::string("sacd_mttkrp: ") + cudaGetErrorString(e));
+    return sticky(c, SACD_ECUDA);
+  }
   int rc = launch_mttkrp(*c, mode, c->M);
   if (rc == SACD_OK) rc = read_matrix(c, c->M, c->m[mode].I, out, ld);
   return sticky(c, rc);
@@ -612,7 +619,10 @@ int sacd_layout(sacd_ctx *c, int32_t mode, uint32_t *idx_a, uint32_t *idx_b, flo
   }
   ModeData &md = c->m[mode];
   int rc = SACD_OK;
-  if (rc == SACD_OK && idx_a && c->nnz) rc = dev_read(c, idx_a, md.idx_a, (size_t)c->nnz * 4);
+  if (rc == SACD_OK && idx_a && c->nnz) {
+    rc = dev_read(c, idx_a, md.idx_a, (size_t)c->nnz * 4);
+    for (long long e = 0; rc == SACD_OK && e < c->nnz; ++e) idx_a[e] &= kIdxMask;  // strip the flag bits
+  }
   if (rc == SACD_OK && idx_b && c->nnz) rc = dev_read(c, idx_b, md.idx_b, (size_t)c->nnz * 4);
   if (rc == SACD_OK && val && c->nnz) rc = dev_read(c, val, md.val, (size_t)c->nnz * 4);
   if (rc == SACD_OK && row_ptr) rc = dev_read(c, row_ptr, md.row_ptr, (size_t)(md.I + 1) * 8);

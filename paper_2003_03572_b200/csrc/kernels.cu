@@ -121,87 +121,6 @@ __global__ void __launch_bounds__(256) k_mttkrp(const WorkItem *__restrict__ ite
   const long long item = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (item >= n_items) return;
   const WorkItem it = items[item];
-  if constexpr (G == 1) {
-    // One nonzero at a time per warp, lanes across the R columns.
-    //  * The warp loads 32 nonzeros' (idx_a, idx_b, x) with coalesced streaming loads and
-    //    broadcasts them by shuffle.
-    //  * Fiber factoring: the layout is sorted by (i_n, i_a, i_b), so a
-    //    run of equal i_a inside a row is a fiber and
-    //        m_i = sum_fibers a_(i_a) * ( sum_{e in fiber} x_e b_(i_b(e)) ),
-    //    one a-row gather per fiber instead of per nonzero.  The a-row load is issued when
-    //    the fiber starts and consumed when it closes; the next b-row is prefetched.
-    //  * Rows are walked warp-uniformly and flushed when the nonzero index crosses
-    //    row_ptr[row+1] (empty rows get zeros).
-    int row = it.row0;
-    long long row_end = min(row_ptr[row + 1], it.nz1);
-    Real acc[VPL][VEC], facc[VPL][VEC], arow[VPL][VEC], bcur[VPL][VEC], bnext[VPL][VEC];
-#pragma unroll
-    for (int v = 0; v < VPL; ++v)
-#pragma unroll
-      for (int c = 0; c < VEC; ++c) acc[v][c] = facc[v][c] = arow[v][c] = Real(0);
-    uint32_t cur_a = 0xffffffffu;
-    auto close_fiber = [&]() {
-#pragma unroll
-      for (int v = 0; v < VPL; ++v)
-#pragma unroll
-        for (int c = 0; c < VEC; ++c) {
-          acc[v][c] = fma(arow[v][c], facc[v][c], acc[v][c]);
-          facc[v][c] = Real(0);
-        }
-      cur_a = 0xffffffffu;
-    };
-    auto flush = [&](int rr) {
-      close_fiber();
-      Real *dst = (it.slot >= 0) ? partial + it.slot * RT : M + (long long)rr * RT;
-      VT *dv = reinterpret_cast<VT *>(dst);
-#pragma unroll
-      for (int v = 0; v < VPL; ++v) {
-        dv[lane + v * 32] = VV::make(acc[v]);
-#pragma unroll
-        for (int c = 0; c < VEC; ++c) acc[v][c] = Real(0);
-      }
-    };
-    auto load_row = [&](const Real *F, uint32_t idx, Real (&out)[VPL][VEC]) {
-      const VT *p = reinterpret_cast<const VT *>(F + (long long)idx * RT);
-#pragma unroll
-      for (int v = 0; v < VPL; ++v) VV::get(__ldg(p + lane + v * 32), out[v]);
-    };
-    for (long long base = it.nz0; base < it.nz1; base += 32) {
-      const int cnt = (int)min(32LL, it.nz1 - base);
-      uint32_t my_a = 0, my_b = 0;
-      float my_x = 0.f;
-      if (lane < cnt) {
-        my_a = ld_stream_u32(ia + base + lane);
-        my_b = ld_stream_u32(ib + base + lane);
-        my_x = ld_stream_f32(val + base + lane);
-      }
-      load_row(B, __shfl_sync(0xffffffffu, my_b, 0), bcur);
-      for (int j = 0; j < cnt; ++j) {
-        if (j + 1 < cnt) load_row(B, __shfl_sync(0xffffffffu, my_b, j + 1), bnext);
-        while (base + j >= row_end) {
-          flush(row);
-          ++row;
-          row_end = min(row_ptr[row + 1], it.nz1);
-        }
-        const uint32_t ea = __shfl_sync(0xffffffffu, my_a, j);
-        const Real x = (Real)__shfl_sync(0xffffffffu, my_x, j);
-        if (ea != cur_a) {
-          close_fiber();
-          cur_a = ea;
-          load_row(A, ea, arow);
-        }
-#pragma unroll
-        for (int v = 0; v < VPL; ++v)
-#pragma unroll
-          for (int c = 0; c < VEC; ++c) {
-            facc[v][c] = fma(x, bcur[v][c], facc[v][c]);
-            bcur[v][c] = bnext[v][c];
-          }
-      }
-    }
-    for (; row < it.row1; ++row) flush(row);   // the last row(s), including empty ones
-    return;
-  }
   const int grp = lane / LPN, sub = lane % LPN;
   for (int row = it.row0; row < it.row1; ++row) {
     long long s = row_ptr[row], t = row_ptr[row + 1];
@@ -214,7 +133,7 @@ __global__ void __launch_bounds__(256) k_mttkrp(const WorkItem *__restrict__ ite
       for (int c = 0; c < VEC; ++c) acc[v][c] = Real(0);
     for (long long e = s + grp; e < t; e += G) {
       const Real x = (Real)ld_stream_f32(val + e);
-      const VT *ap = reinterpret_cast<const VT *>(A + (long long)ld_stream_u32(ia + e) * RT);
+      const VT *ap = reinterpret_cast<const VT *>(A + (long long)(ld_stream_u32(ia + e) & kIdxMask) * RT);
       const VT *bp = reinterpret_cast<const VT *>(B + (long long)ld_stream_u32(ib + e) * RT);
 #pragma unroll
       for (int v = 0; v < VPL; ++v) {
@@ -238,6 +157,127 @@ __global__ void __launch_bounds__(256) k_mttkrp(const WorkItem *__restrict__ ite
       for (int v = 0; v < VPL; ++v) dv[sub + v * LPN] = VV::make(acc[v]);
     }
   }
+}
+
+// Wide-row MTTKRP (R > 16): one warp per work item, lane l owns columns [l*E, l*E+E),
+// E = RT/32, so every factor-row gather is one coalesced RT*sizeof(Real)-byte warp access.
+//  * The warp loads 32 nonzeros' (idx_a|flags, idx_b, x, row) with coalesced streaming
+//    loads and broadcasts them by shuffle.
+//  * Fiber factoring: the layout is sorted by (i_n, i_a, i_b), so a run of
+//    equal i_a inside a row is a fiber, and m_i = sum_fibers a_(i_a) * (sum_e x_e b_(i_b(e))):
+//    one a-row gather per fiber.  Fiber / row starts are precomputed flag bits of idx_a
+//    (built with the layout), so the per-nonzero path is: 3 shuffles, one b-row gather
+//    (prefetched one nonzero ahead), E FMAs.
+//  * Rows are flushed to M[row] when a row starts; empty rows are never touched (the row
+//    update reads row_ptr and uses m = 0 for them).  Split items (slot >= 0) hold a segment
+//    of one heavy row and flush to their partial slot.
+template <typename Real, int E>
+struct LaneRow {
+  Real v[E];
+  __device__ __forceinline__ void load(const Real *p) {
+    if constexpr (E * sizeof(Real) >= 16) {
+      using VV = V16<Real>;
+#pragma unroll
+      for (int k = 0; k < (int)(E * sizeof(Real) / 16); ++k)
+        VV::get(__ldg(reinterpret_cast<const typename VV::T *>(p) + k), v + k * VV::N);
+    } else if constexpr (E * sizeof(Real) == 8) {
+      if constexpr (sizeof(Real) == 8) {
+        v[0] = __ldg(p);
+      } else {
+        const float2 t = __ldg(reinterpret_cast<const float2 *>(p));
+        v[0] = t.x;
+        v[1] = t.y;
+      }
+    } else {
+      v[0] = __ldg(p);
+    }
+  }
+  __device__ __forceinline__ void store(Real *p) const {
+    if constexpr (E * sizeof(Real) >= 16) {
+      using VV = V16<Real>;
+#pragma unroll
+      for (int k = 0; k < (int)(E * sizeof(Real) / 16); ++k)
+        reinterpret_cast<typename VV::T *>(p)[k] = VV::make(v + k * VV::N);
+    } else {
+#pragma unroll
+      for (int k = 0; k < E; ++k) p[k] = v[k];
+    }
+  }
+};
+
+template <typename Real, int RT>
+__global__ void __launch_bounds__(256) k_mttkrp_fiber(const WorkItem *__restrict__ items, long long n_items,
+                                                      const uint32_t *__restrict__ ia,
+                                                      const uint32_t *__restrict__ ib,
+                                                      const float *__restrict__ val,
+                                                      const uint32_t *__restrict__ in_,
+                                                      const Real *__restrict__ A, const Real *__restrict__ B,
+                                                      Real *__restrict__ M, Real *__restrict__ partial) {
+  constexpr int E = RT / 32;
+  const int lane = threadIdx.x & 31;
+  const long long item = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (item >= n_items) return;
+  const WorkItem it = items[item];
+  if (it.nz0 >= it.nz1) return;
+  const Real *Al = A + lane * E;
+  const Real *Bl = B + lane * E;
+  Real *Ml = M + lane * E;
+  LaneRow<Real, E> arow, bA, bB;
+  Real acc[E], facc[E];
+#pragma unroll
+  for (int k = 0; k < E; ++k) acc[k] = facc[k] = arow.v[k] = Real(0);
+  long long cur_row = -1;
+  auto flush = [&]() {
+    LaneRow<Real, E> o;
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+      o.v[k] = acc[k];
+      acc[k] = Real(0);
+    }
+    if (it.slot >= 0) o.store(partial + it.slot * RT + lane * E);
+    else if (cur_row >= 0) o.store(Ml + cur_row * RT);
+  };
+  auto step = [&](uint32_t fa, float xf, const LaneRow<Real, E> &b, uint32_t my_n, int j) {
+    if (fa & kFiberStart) {
+#pragma unroll
+      for (int k = 0; k < E; ++k) {            // close the previous fiber: acc += a * facc
+        acc[k] = fma(arow.v[k], facc[k], acc[k]);
+        facc[k] = Real(0);
+      }
+      if (fa & kRowStart) {
+        flush();
+        cur_row = __shfl_sync(0xffffffffu, my_n, j);
+      }
+      arow.load(Al + (long long)(fa & kIdxMask) * RT);
+    }
+    const Real x = (Real)xf;
+#pragma unroll
+    for (int k = 0; k < E; ++k) facc[k] = fma(x, b.v[k], facc[k]);
+  };
+  for (long long base = it.nz0; base < it.nz1; base += 32) {
+    const int cnt = (int)min(32LL, it.nz1 - base);
+    uint32_t my_a = 0, my_b = 0, my_n = 0;
+    float my_x = 0.f;
+    if (lane < cnt) {
+      my_a = ld_stream_u32(ia + base + lane);
+      my_b = ld_stream_u32(ib + base + lane);
+      my_x = ld_stream_f32(val + base + lane);
+      my_n = ld_stream_u32(in_ + base + lane);
+    }
+    if (base == it.nz0 && lane == 0) my_a |= kFiberStart | kRowStart;  // an item starts a row/fiber
+    bA.load(Bl + (long long)__shfl_sync(0xffffffffu, my_b, 0) * RT);
+    int j = 0;
+    for (; j + 1 < cnt; j += 2) {
+      bB.load(Bl + (long long)__shfl_sync(0xffffffffu, my_b, j + 1) * RT);
+      step(__shfl_sync(0xffffffffu, my_a, j), __shfl_sync(0xffffffffu, my_x, j), bA, my_n, j);
+      if (j + 2 < cnt) bA.load(Bl + (long long)__shfl_sync(0xffffffffu, my_b, j + 2) * RT);
+      step(__shfl_sync(0xffffffffu, my_a, j + 1), __shfl_sync(0xffffffffu, my_x, j + 1), bB, my_n, j + 1);
+    }
+    if (j < cnt) step(__shfl_sync(0xffffffffu, my_a, j), __shfl_sync(0xffffffffu, my_x, j), bA, my_n, j);
+  }
+#pragma unroll
+  for (int k = 0; k < E; ++k) acc[k] = fma(arow.v[k], facc[k], acc[k]);
+  flush();
 }
 
 // Heavy rows split across items: M_row = sum of the row's partials.  One block per split
@@ -318,7 +358,8 @@ __global__ void __launch_bounds__(256) k_prepare(int mode, int R, const double *
 // walk is bank-conflict free; H is staged in shared memory when it fits.
 template <typename Real, int RT>
 __global__ void __launch_bounds__(rows_per_block<RT>())
-    k_sacd_rows(long long I, int R, int mode, int l_mode, const Real *__restrict__ M, Real *__restrict__ F,
+    k_sacd_rows(long long I, int R, int mode, int l_mode, const long long *__restrict__ row_ptr,
+                const Real *__restrict__ M, Real *__restrict__ F,
                 Real *__restrict__ Z, const Real *__restrict__ Hr, const DevState *__restrict__ st,
                 uint8_t *__restrict__ dec, double *__restrict__ ti_part, double *__restrict__ md_part,
                 long long *__restrict__ e_part, long long *__restrict__ ech_part) {
@@ -354,6 +395,7 @@ __global__ void __launch_bounds__(rows_per_block<RT>())
     const long long row = row0 + tid;
     Real *u = Us + tid * US;
     const Real *m = M + row * RT;
+    const bool empty = row_ptr[row] == row_ptr[row + 1];  // M is not written for empty slices: m = 0
     Real *zp = Z + row * RT;
     for (int c0 = 0; c0 < R; c0 += C) {
       // (1) block gradient with the current row (columns < c0 already updated), Eq 14:
@@ -378,6 +420,10 @@ __global__ void __launch_bounds__(rows_per_block<RT>())
       for (int x = 0; x < C / VEC; ++x) {
         VV::get(reinterpret_cast<const VT *>(m + c0)[x], mv + x * VEC);
         VV::get(reinterpret_cast<const VT *>(zp + c0)[x], zv + x * VEC);
+      }
+      if (empty) {
+#pragma unroll
+        for (int q = 0; q < C; ++q) mv[q] = Real(0);
       }
       // (2) Gauss-Seidel inside the block (C9): column r sees the steps dl of columns
       //     c0..r-1 through the correction sum_q' h_(r, c0+q') dl_q'.
@@ -458,14 +504,15 @@ __global__ void __launch_bounds__(rows_per_block<RT>())
 
 // sum_r F_ir M_ir per row block (initial objective f^0)
 template <typename Real, int RT>
-__global__ void k_fm_dot(long long I, int R, const Real *__restrict__ F, const Real *__restrict__ M,
+__global__ void k_fm_dot(long long I, int R, const long long *__restrict__ row_ptr, const Real *__restrict__ F,
+                         const Real *__restrict__ M,
                          double *__restrict__ ti_part, double *__restrict__ md_part, long long *__restrict__ e_part,
                          long long *__restrict__ ech_part) {
   constexpr int TR = rows_per_block<RT>();
   __shared__ double red[TR];
   const long long row = (long long)blockIdx.x * TR + threadIdx.x;
   double s = 0.0;
-  if (row < I)
+  if (row < I && row_ptr[row] != row_ptr[row + 1])
     for (int r = 0; r < R; ++r) s += (double)F[row * RT + r] * (double)M[row * RT + r];
   red[threadIdx.x] = s;
   __syncthreads();
@@ -677,9 +724,14 @@ struct Impl {
     if (md.n_items > 0) {
       const int wpb = 8;
       const long long blocks = (md.n_items + wpb - 1) / wpb;
-      k_mttkrp<Real, RT><<<(unsigned)blocks, wpb * 32, 0, c.stream>>>(
-          md.items, md.n_items, md.row_ptr, md.idx_a, md.idx_b, md.val, A, B, out,
-          reinterpret_cast<Real *>(c.partial));
+      if constexpr (RT >= 32)
+        k_mttkrp_fiber<Real, RT><<<(unsigned)blocks, wpb * 32, 0, c.stream>>>(
+            md.items, md.n_items, md.idx_a, md.idx_b, md.val, md.idx_n, A, B, out,
+            reinterpret_cast<Real *>(c.partial));
+      else
+        k_mttkrp<Real, RT><<<(unsigned)blocks, wpb * 32, 0, c.stream>>>(
+            md.items, md.n_items, md.row_ptr, md.idx_a, md.idx_b, md.val, A, B, out,
+            reinterpret_cast<Real *>(c.partial));
     }
     SACD_CUDA_TRY(cudaGetLastError());
     SACD_TRY(prof_end(c, 0, pe));
@@ -729,7 +781,7 @@ struct Impl {
     long long *e_part = c.cnt_part, *ech_part = c.cnt_part + c.max_row_blocks;
     int pe = prof_begin(c, 3);
     k_sacd_rows<Real, RT><<<(unsigned)nblk, TR, smem, c.stream>>>(
-        md.I, c.R, mode, c.opt.l_mode, M, reinterpret_cast<Real *>(md.F), reinterpret_cast<Real *>(md.Z),
+        md.I, c.R, mode, c.opt.l_mode, md.row_ptr, M, reinterpret_cast<Real *>(md.F), reinterpret_cast<Real *>(md.Z),
         reinterpret_cast<const Real *>(c.Hr), c.st, dec, ti_part, md_part, e_part, ech_part);
     SACD_CUDA_TRY(cudaGetLastError());
     SACD_TRY(prof_end(c, 3, pe));
@@ -750,7 +802,7 @@ struct Impl {
     const long long nblk = (md.I + TR - 1) / TR;
     double *ti_part = c.row_part, *md_part = c.row_part + c.max_row_blocks;
     long long *e_part = c.cnt_part, *ech_part = c.cnt_part + c.max_row_blocks;
-    k_fm_dot<Real, RT><<<(unsigned)nblk, TR, 0, c.stream>>>(md.I, c.R, reinterpret_cast<const Real *>(md.F), M,
+    k_fm_dot<Real, RT><<<(unsigned)nblk, TR, 0, c.stream>>>(md.I, c.R, md.row_ptr, reinterpret_cast<const Real *>(md.F), M,
                                                             ti_part, md_part, e_part, ech_part);
     k_finalize<<<1, 1024, 0, c.stream>>>(2, nblk, ti_part, md_part, e_part, ech_part, c.m[0].G, c.m[1].G, c.m[2].G,
                                          c.R, c.st, 2);

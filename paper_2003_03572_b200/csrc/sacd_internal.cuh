@@ -51,6 +51,12 @@ struct SplitRow {
 
 constexpr int kRing = 4096;
 
+// idx_a carries two flag bits set by the layout builder (mode lengths are < 2^30):
+// bit 31 = first nonzero of a fiber (new (i_n, i_a)), bit 30 = first nonzero of a row.
+constexpr uint32_t kFiberStart = 1u << 31;
+constexpr uint32_t kRowStart = 1u << 30;
+constexpr uint32_t kIdxMask = (1u << 30) - 1u;
+
 // Device-resident control state: everything the sweep graph needs to decide on device.
 struct DevState {
   int k;                 // completed/started sweeps
@@ -70,7 +76,7 @@ struct DevState {
 struct ModeData {
   long long I = 0;
   int a = 0, b = 0;               // the other modes ("a" = shorter)
-  uint32_t *idx_a = nullptr, *idx_b = nullptr;
+  uint32_t *idx_a = nullptr, *idx_b = nullptr, *idx_n = nullptr;  // idx_a has flag bits
   float *val = nullptr;
   long long *row_ptr = nullptr;   // I+1
   WorkItem *items = nullptr;
