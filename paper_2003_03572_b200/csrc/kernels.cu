@@ -206,7 +206,7 @@ struct LaneRow {
 };
 
 template <typename Real, int RT>
-__global__ void __launch_bounds__(256) k_mttkrp_fiber(const WorkItem *__restrict__ items, long long n_items,
+__global__ void __launch_bounds__(256, 2) k_mttkrp_fiber(const WorkItem *__restrict__ items, long long n_items,
                                                       const uint32_t *__restrict__ ia,
                                                       const uint32_t *__restrict__ ib,
                                                       const float *__restrict__ val,
@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(256) k_mttkrp_fiber(const WorkItem *__restrict
   const Real *Al = A + lane * E;
   const Real *Bl = B + lane * E;
   Real *Ml = M + lane * E;
-  LaneRow<Real, E> arow, bA, bB;
+  LaneRow<Real, E> arow;
   Real acc[E], facc[E];
 #pragma unroll
   for (int k = 0; k < E; ++k) acc[k] = facc[k] = arow.v[k] = Real(0);
@@ -265,15 +265,23 @@ __global__ void __launch_bounds__(256) k_mttkrp_fiber(const WorkItem *__restrict
       my_n = ld_stream_u32(in_ + base + lane);
     }
     if (base == it.nz0 && lane == 0) my_a |= kFiberStart | kRowStart;  // an item starts a row/fiber
-    bA.load(Bl + (long long)__shfl_sync(0xffffffffu, my_b, 0) * RT);
-    int j = 0;
-    for (; j + 1 < cnt; j += 2) {
-      bB.load(Bl + (long long)__shfl_sync(0xffffffffu, my_b, j + 1) * RT);
-      step(__shfl_sync(0xffffffffu, my_a, j), __shfl_sync(0xffffffffu, my_x, j), bA, my_n, j);
-      if (j + 2 < cnt) bA.load(Bl + (long long)__shfl_sync(0xffffffffu, my_b, j + 2) * RT);
-      step(__shfl_sync(0xffffffffu, my_a, j + 1), __shfl_sync(0xffffffffu, my_x, j + 1), bB, my_n, j + 1);
+    // batches of NB b-row gathers in flight per warp, then consumed in order
+    constexpr int NB = (E * sizeof(Real) <= 16) ? 8 : ((E * sizeof(Real) <= 32) ? 4 : 2);
+    for (int jb = 0; jb < cnt; jb += NB) {
+      LaneRow<Real, E> bb[NB];
+#pragma unroll
+      for (int u = 0; u < NB; ++u) {
+        const uint32_t eb = __shfl_sync(0xffffffffu, my_b, (jb + u) & 31);
+        if (jb + u < cnt) bb[u].load(Bl + (long long)eb * RT);
+      }
+#pragma unroll
+      for (int u = 0; u < NB; ++u) {
+        const int j = (jb + u) & 31;
+        const uint32_t fa = __shfl_sync(0xffffffffu, my_a, j);
+        const float xf = __shfl_sync(0xffffffffu, my_x, j);
+        if (jb + u < cnt) step(fa, xf, bb[u], my_n, j);
+      }
     }
-    if (j < cnt) step(__shfl_sync(0xffffffffu, my_a, j), __shfl_sync(0xffffffffu, my_x, j), bA, my_n, j);
   }
 #pragma unroll
   for (int k = 0; k < E; ++k) acc[k] = fma(arow.v[k], facc[k], acc[k]);
@@ -398,13 +406,12 @@ __global__ void __launch_bounds__(rows_per_block<RT>())
     const bool empty = row_ptr[row] == row_ptr[row + 1];  // M is not written for empty slices: m = 0
     Real *zp = Z + row * RT;
     for (int c0 = 0; c0 < R; c0 += C) {
-      // (1) block gradient with the current row (columns < c0 already updated), Eq 14:
-      //     acc_q = sum_j u_j h_(j, c0+q)        (H symmetric)
+      // (1) out-of-block part of the gradient with the current row (columns < c0 already
+      //     updated), Eq 14:  acc_q = sum_{j not in block} u_j h_(j, c0+q)   (H symmetric)
       Real acc[C];
 #pragma unroll
       for (int q = 0; q < C; ++q) acc[q] = Real(0);
-#pragma unroll 4
-      for (int j = 0; j < R; ++j) {
+      auto accumulate = [&](int j) {
         const Real uj = u[j];
         const VT *hj = reinterpret_cast<const VT *>(H + j * RT + c0);
 #pragma unroll
@@ -414,23 +421,29 @@ __global__ void __launch_bounds__(rows_per_block<RT>())
 #pragma unroll
           for (int y = 0; y < VEC; ++y) acc[x * VEC + y] = fma(uj, hv[y], acc[x * VEC + y]);
         }
-      }
-      Real mv[C], zv[C], dl[C];
+      };
+#pragma unroll 4
+      for (int j = 0; j < c0; ++j) accumulate(j);
+#pragma unroll 4
+      for (int j = c0 + C; j < R; ++j) accumulate(j);
+      Real mv[C], zv[C], ub[C];
 #pragma unroll
       for (int x = 0; x < C / VEC; ++x) {
         VV::get(reinterpret_cast<const VT *>(m + c0)[x], mv + x * VEC);
         VV::get(reinterpret_cast<const VT *>(zp + c0)[x], zv + x * VEC);
       }
+#pragma unroll
+      for (int q = 0; q < C; ++q) ub[q] = u[c0 + q];
       if (empty) {
 #pragma unroll
         for (int q = 0; q < C; ++q) mv[q] = Real(0);
       }
-      // (2) Gauss-Seidel inside the block (C9): column r sees the steps dl of columns
-      //     c0..r-1 through the correction sum_q' h_(r, c0+q') dl_q'.
+      // (2) Gauss-Seidel inside the block (C9): column r adds the in-block terms from the
+      //     CURRENT block values ub (never by subtracting old ones, so a gradient whose
+      //     other terms are exactly zero is computed exactly, as in the oracle).
 #pragma unroll
       for (int q = 0; q < C; ++q) {
         const int r = c0 + q;
-        dl[q] = Real(0);
         if (r < R) {
           const Real *Hr_ = H + r * RT;
           const Real h = Hr_[r];
@@ -439,9 +452,9 @@ __global__ void __launch_bounds__(rows_per_block<RT>())
           if (h != Real(0)) {
             Real sg = acc[q];
 #pragma unroll
-            for (int qq = 0; qq < q; ++qq) sg = fma(Hr_[c0 + qq], dl[qq], sg);
+            for (int qq = 0; qq < C; ++qq) sg = fma(ub[qq], Hr_[c0 + qq], sg);
             const Real g = sg - mv[q];                     // Eq 14
-            const Real ur = u[r];
+            const Real ur = ub[q];
             const Real un = fmax(Real(0), ur - g / h);     // Eq 11-13
             const Real d = un - ur;                        // Eq 12
             const Real L = l_mode ? Lf : h;
@@ -450,18 +463,19 @@ __global__ void __launch_bounds__(rows_per_block<RT>())
             sel = (branch == SACD_BR_FIRST) ? (z > Real(0))
                                             : ((branch == SACD_BR_EQ24) ? (z - zpr > Real(0)) : (zpr - z > Real(0)));
             if (sel) {
-              u[r] = un;
-              dl[q] = d;
+              ub[q] = un;
               E += 1;
               if (d != Real(0)) Ech += 1;
             }
           }
           zv[q] = z;                                       // z_prev <- z always (C8)
           ti += (double)z;                                 // Eq 25
-          md += (double)u[r] * (double)mv[q];
+          md += (double)ub[q] * (double)mv[q];
           if (dec) dec[row * R + r] = (uint8_t)sel;
         }
       }
+#pragma unroll
+      for (int q = 0; q < C; ++q) u[c0 + q] = ub[q];
 #pragma unroll
       for (int x = 0; x < C / VEC; ++x) reinterpret_cast<VT *>(zp + c0)[x] = VV::make(zv + x * VEC);
     }
