@@ -189,6 +189,19 @@ int sacd_layout(sacd_ctx *ctx, int32_t mode, uint32_t *idx_a, uint32_t *idx_b, f
 int sacd_profile_read(sacd_ctx *ctx, double ms[SACD_NUM_KCLASS], int64_t launches[SACD_NUM_KCLASS]);
 int sacd_profile_reset(sacd_ctx *ctx);
 
+/* Slice-sharding plan of one mode for `world` ranks; a pure host function
+ * (no GPU).  row_ptr: host, I + 1 entries of the mode-sorted layout (sacd_layout).
+ * Output for `rank` (0 <= rank < world):
+ *   out[0], out[1] : its nonzero range [lo, hi), lo = floor(rank * nnz / world)
+ *   out[2], out[3] : its owned rows [rlo, rhi): the rows whose first nonzero index
+ *                    row_ptr[r] lies in [lo, hi); the last rank also owns the trailing
+ *                    empty rows (row_ptr[r] == nnz)
+ *   out[4]         : its head row, the row owned by a lower rank to which the nonzeros
+ *                    [lo, min(hi, row_ptr[rlo])) belong, or -1 if there are none
+ * Every row is owned by exactly one rank; a row's MTTKRP is its owner's local part plus
+ * the head partials of the higher ranks whose head row it is.  Errors: EINVAL. */
+int sacd_shard_plan(const int64_t *row_ptr, int64_t I, int32_t world, int32_t rank, int64_t out[5]);
+
 /* ABI self-description for bindings: out = {SACD_ABI_VERSION, sizeof(sacd_options),
  * sizeof(sacd_iter_stats), sizeof(sacd_info)}.  Needs no GPU. */
 int sacd_abi_sizes(int32_t out[4]);

@@ -58,6 +58,31 @@ int prof_end(Context &c, int kclass, int idx) {
   return SACD_OK;
 }
 
+// ------------------------------------------------------------------ slice sharding
+// lower_bound over row_ptr[0..I]: first r with row_ptr[r] >= x
+static long long lower_row(const long long *rp, long long I, long long x) {
+  long long lo = 0, hi = I + 1;
+  while (lo < hi) {
+    const long long mid = (lo + hi) >> 1;
+    if (rp[mid] < x) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+ShardPlan plan_shard(const long long *rp, long long I, int world, int rank) {
+  ShardPlan p;
+  const long long nnz = rp[I];
+  p.lo = (long long)((__int128)rank * nnz / world);
+  p.hi = (long long)((__int128)(rank + 1) * nnz / world);
+  p.rlo = std::min(lower_row(rp, I, p.lo), I);
+  p.rhi = (rank == world - 1) ? I : std::min(lower_row(rp, I, p.hi), I);
+  if (p.rhi < p.rlo) p.rhi = p.rlo;
+  p.head = -1;
+  if (p.lo < p.hi && (p.rlo >= I || rp[p.rlo] > p.lo)) p.head = p.rlo - 1;
+  return p;
+}
+
 // ------------------------------------------------------------------ MTTKRP work partition
 // Items hold whole rows with <= T nonzeros in total and <= maxrows rows; a row with more
 // than T nonzeros is cut into ceil(nnz/T) row-relative segments, each writing a partial
@@ -693,6 +718,20 @@ int sacd_profile_reset(sacd_ctx *c) {
     c->prof_n[i] = 0;
   }
   return sticky(c, rc);
+}
+
+int sacd_shard_plan(const int64_t *row_ptr, int64_t I, int32_t world, int32_t rank, int64_t out[5]) {
+  if (!row_ptr || !out || I < 1 || world < 1 || rank < 0 || rank >= world) {
+    set_error("sacd_shard_plan: bad arguments");
+    return SACD_EINVAL;
+  }
+  ShardPlan p = plan_shard(reinterpret_cast<const long long *>(row_ptr), I, world, rank);
+  out[0] = p.lo;
+  out[1] = p.hi;
+  out[2] = p.rlo;
+  out[3] = p.rhi;
+  out[4] = p.head;
+  return SACD_OK;
 }
 
 int sacd_abi_sizes(int32_t out[4]) {

@@ -205,8 +205,8 @@ struct LaneRow {
   }
 };
 
-template <typename Real, int RT>
-__global__ void __launch_bounds__(256, 2) k_mttkrp_fiber(const WorkItem *__restrict__ items, long long n_items,
+template <typename Real, int RT, int NB, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_mttkrp_fiber(const WorkItem *__restrict__ items, long long n_items,
                                                       const uint32_t *__restrict__ ia,
                                                       const uint32_t *__restrict__ ib,
                                                       const float *__restrict__ val,
@@ -266,7 +266,6 @@ __global__ void __launch_bounds__(256, 2) k_mttkrp_fiber(const WorkItem *__restr
     }
     if (base == it.nz0 && lane == 0) my_a |= kFiberStart | kRowStart;  // an item starts a row/fiber
     // batches of NB b-row gathers in flight per warp, then consumed in order
-    constexpr int NB = (E * sizeof(Real) <= 16) ? 8 : ((E * sizeof(Real) <= 32) ? 4 : 2);
     for (int jb = 0; jb < cnt; jb += NB) {
       LaneRow<Real, E> bb[NB];
 #pragma unroll
@@ -738,10 +737,23 @@ struct Impl {
     if (md.n_items > 0) {
       const int wpb = 8;
       const long long blocks = (md.n_items + wpb - 1) / wpb;
-      if constexpr (RT >= 32)
-        k_mttkrp_fiber<Real, RT><<<(unsigned)blocks, wpb * 32, 0, c.stream>>>(
-            md.items, md.n_items, md.idx_a, md.idx_b, md.val, md.idx_n, A, B, out,
-            reinterpret_cast<Real *>(c.partial));
+      if constexpr (RT >= 32) {
+        // (NB gathers in flight per warp, min blocks per SM); opt.reserved[0] selects a
+        // tuning variant (0 = default).
+        const int var = c.opt.reserved[0];
+        auto go = [&](auto kern) {
+          kern<<<(unsigned)blocks, wpb * 32, 0, c.stream>>>(md.items, md.n_items, md.idx_a, md.idx_b, md.val,
+                                                           md.idx_n, A, B, out, reinterpret_cast<Real *>(c.partial));
+        };
+        constexpr int NBD = (RT * sizeof(Real) <= 512) ? 2 : 1;
+        if (var == 1) go(k_mttkrp_fiber<Real, RT, 1, 4>);
+        else if (var == 2) go(k_mttkrp_fiber<Real, RT, 4, 3>);
+        else if (var == 3) go(k_mttkrp_fiber<Real, RT, 8, 2>);
+        else if (var == 4) go(k_mttkrp_fiber<Real, RT, 4, 4>);
+        else if (var == 5) go(k_mttkrp_fiber<Real, RT, 2, 5>);
+        else if (var == 6) go(k_mttkrp_fiber<Real, RT, 1, 6>);
+        else go(k_mttkrp_fiber<Real, RT, NBD, 4>);
+      }
       else
         k_mttkrp<Real, RT><<<(unsigned)blocks, wpb * 32, 0, c.stream>>>(
             md.items, md.n_items, md.row_ptr, md.idx_a, md.idx_b, md.val, A, B, out,

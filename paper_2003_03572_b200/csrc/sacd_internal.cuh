@@ -125,6 +125,12 @@ struct Context {
 
 size_t real_size(const Context &c);
 
+// slice sharding plan of one mode (capi.cu; see sacd_shard_plan in include/sacd.h)
+struct ShardPlan {
+  long long lo = 0, hi = 0, rlo = 0, rhi = 0, head = -1;
+};
+ShardPlan plan_shard(const long long *row_ptr, long long I, int world, int rank);
+
 // layout.cu
 int build_layouts(Context &c, const uint32_t *coords_dev, const float *vals_dev);
 

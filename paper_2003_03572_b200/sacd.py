@@ -29,7 +29,8 @@ KCLASS = ("mttkrp", "fixup", "prepare", "rows", "gram", "finalize")
 EXPORTS = ("sacd_default_options", "sacd_init", "sacd_iterate", "sacd_sync", "sacd_fit", "sacd_factors",
            "sacd_stats", "sacd_get_info", "sacd_free", "sacd_last_error", "sacd_set_factors", "sacd_get_zprev",
            "sacd_set_zprev", "sacd_mttkrp", "sacd_time_mttkrp", "sacd_gram", "sacd_hessian", "sacd_mode_update",
-           "sacd_layout", "sacd_profile_read", "sacd_profile_reset", "sacd_abi_sizes", "sacd_nccl_unique_id")
+           "sacd_layout", "sacd_profile_read", "sacd_profile_reset", "sacd_shard_plan", "sacd_abi_sizes",
+           "sacd_nccl_unique_id")
 
 
 class Options(C.Structure):
@@ -94,6 +95,7 @@ def load_library(path: str = LIB_PATH):
     L.sacd_profile_reset.argtypes = [P]
     L.sacd_nccl_unique_id.argtypes = [P]
     L.sacd_abi_sizes.argtypes = [P]
+    L.sacd_shard_plan.argtypes = [P, i64, i32, i32, P]
     sz = (C.c_int32 * 4)()
     L.sacd_abi_sizes(sz)
     if tuple(sz) != (1, C.sizeof(Options), C.sizeof(IterStats), C.sizeof(Info)):
@@ -119,11 +121,19 @@ def _np(a, dtype):
     return np.ascontiguousarray(a, dtype=dtype)
 
 
+def shard_plan(row_ptr, world, rank):
+    """sacd_shard_plan: (lo, hi, rlo, rhi, head) of `rank` for one mode's row_ptr."""
+    rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    out = np.zeros(5, np.int64)
+    _check(load_library().sacd_shard_plan(_ptr(rp), rp.shape[0] - 1, int(world), int(rank), _ptr(out)))
+    return tuple(int(x) for x in out)
+
+
 class Sacd:
     """One SaCD factorisation context on one GPU (see include/sacd.h)."""
 
     def __init__(self, coords, vals, dims, rank, seed, *, precision="f64", l_mode="diag", variant="gs",
-                 device=-1, stream=None, use_graph=True, profile=False, nnz_per_item=0):
+                 device=-1, stream=None, use_graph=True, profile=False, nnz_per_item=0, mttkrp_variant=0):
         L = load_library()
         o = Options()
         L.sacd_default_options(C.byref(o))
@@ -135,6 +145,7 @@ class Sacd:
         o.use_graph = int(bool(use_graph))
         o.profile = int(bool(profile))
         o.nnz_per_item = int(nnz_per_item)
+        o.reserved[0] = int(mttkrp_variant)
         if not hasattr(coords, "data_ptr"):
             coords = _np(np.asarray(coords).reshape(-1, 3), np.uint32)
         if not hasattr(vals, "data_ptr"):
