@@ -97,12 +97,13 @@ void ora_init_factors(const int64_t dims[3], int R, uint64_t seed, double *U, do
 
 /* ------------------------------------------------------------------ layout
  * Table 2: Omega^(n)_i = the nonzeros whose mode-n index is i.  Entries are
- * ordered by the key (i_n, i_a, i_b) with a = the other mode of smaller length (ties ->
- * lower mode id) and b = the remaining one; keys are unique so the order is unique. */
+ * ordered by the key (i_n, i_a, i_b) with a = the other mode of LARGER length (ties ->
+ * lower mode id) and b = the remaining one (reading L1); keys are unique so the
+ * order is unique. */
 void ora_other_modes(const int64_t dims[3], int n, int *a, int *b) {
   int o1 = (n + 1) % 3, o2 = (n + 2) % 3;
   int lo = o1 < o2 ? o1 : o2, hi = o1 < o2 ? o2 : o1;
-  if (dims[hi] < dims[lo]) { *a = hi; *b = lo; }
+  if (dims[hi] > dims[lo]) { *a = hi; *b = lo; }
   else { *a = lo; *b = hi; }
 }
 
@@ -307,15 +308,30 @@ int ora_objective_sparse(const int64_t dims[3], int64_t nnz, const uint32_t *coo
     if (!G[n]) return ORA_ENOMEM;
     ora_gram(F[n], dims[n], R, G[n]);
   }
+  /* sum over Omega in 64 fixed, contiguous chunks (each sequential), then the chunks in
+     order: the result does not depend on the thread count */
+  enum { NCH = 64 };
+  double cse[NCH], csx[NCH];
+#pragma omp parallel for schedule(static)
+  for (int ch = 0; ch < NCH; ch++) {
+    const int64_t e0 = nnz * ch / NCH, e1 = nnz * (ch + 1) / NCH;
+    double a = 0.0, b = 0.0;
+    for (int64_t e = e0; e < e1; e++) {
+      double xh = 0.0;
+      for (int r = 0; r < R; r++)
+        xh += U[(int64_t)coords[3 * e] * R + r] * V[(int64_t)coords[3 * e + 1] * R + r] *
+              W[(int64_t)coords[3 * e + 2] * R + r];
+      const double d = (double)vals[e] - xh;
+      a += d * d;
+      b += xh * xh;
+    }
+    cse[ch] = a;
+    csx[ch] = b;
+  }
   double se = 0.0, sx2 = 0.0;
-  for (int64_t e = 0; e < nnz; e++) {
-    double xh = 0.0;
-    for (int r = 0; r < R; r++)
-      xh += U[(int64_t)coords[3 * e] * R + r] * V[(int64_t)coords[3 * e + 1] * R + r] *
-            W[(int64_t)coords[3 * e + 2] * R + r];
-    const double d = (double)vals[e] - xh;
-    se += d * d;
-    sx2 += xh * xh;
+  for (int ch = 0; ch < NCH; ch++) {
+    se += cse[ch];
+    sx2 += csx[ch];
   }
   *f_out = se + (model_norm2(G[0], G[1], G[2], R) - sx2);
   for (int n = 0; n < 3; n++) free(G[n]);

@@ -196,10 +196,13 @@ static void destroy(sacd_ctx *c) {
   delete c;
 }
 
+// Layout key (i_n, i_a, i_b): a = the LONGER other mode (ties -> lower mode id), b = the
+// shorter one, so the per-nonzero gathers hit the smaller, cache-resident factor and the
+// per-fiber gathers the larger one (reading L1).
 static int other_modes(const long long dims[3], int n, int *a, int *b) {
   const int o1 = (n + 1) % 3, o2 = (n + 2) % 3;
   const int lo = std::min(o1, o2), hi = std::max(o1, o2);
-  if (dims[hi] < dims[lo]) {
+  if (dims[hi] > dims[lo]) {
     *a = hi;
     *b = lo;
   } else {

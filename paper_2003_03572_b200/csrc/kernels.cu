@@ -745,14 +745,13 @@ struct Impl {
           kern<<<(unsigned)blocks, wpb * 32, 0, c.stream>>>(md.items, md.n_items, md.idx_a, md.idx_b, md.val,
                                                            md.idx_n, A, B, out, reinterpret_cast<Real *>(c.partial));
         };
-        constexpr int NBD = (RT * sizeof(Real) <= 512) ? 2 : 1;
+        // measured on B200 (tools/mttkrp_tune.py): occupancy beats deeper per-warp batching
         if (var == 1) go(k_mttkrp_fiber<Real, RT, 1, 4>);
-        else if (var == 2) go(k_mttkrp_fiber<Real, RT, 4, 3>);
-        else if (var == 3) go(k_mttkrp_fiber<Real, RT, 8, 2>);
-        else if (var == 4) go(k_mttkrp_fiber<Real, RT, 4, 4>);
-        else if (var == 5) go(k_mttkrp_fiber<Real, RT, 2, 5>);
-        else if (var == 6) go(k_mttkrp_fiber<Real, RT, 1, 6>);
-        else go(k_mttkrp_fiber<Real, RT, NBD, 4>);
+        else if (var == 2) go(k_mttkrp_fiber<Real, RT, 2, 4>);
+        else if (var == 3) go(k_mttkrp_fiber<Real, RT, 1, 7>);
+        else if (var == 5) go(k_mttkrp_fiber<Real, RT, 2, 6>);
+        else if (var == 6 || (var == 0 && sizeof(Real) == 8)) go(k_mttkrp_fiber<Real, RT, 1, 6>);
+        else go(k_mttkrp_fiber<Real, RT, 1, 7>);  // fp32 default
       }
       else
         k_mttkrp<Real, RT><<<(unsigned)blocks, wpb * 32, 0, c.stream>>>(

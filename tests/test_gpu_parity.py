@@ -276,3 +276,82 @@ def test_profile_mode_counts_launches():
         g.iterate(4)
         p = g.profile_read()
         assert p["mttkrp"][1] == 12 and p["rows"][1] == 12 and p["mttkrp"][0] > 0
+
+
+# ----------------------------------------------------------------------------- the BASELINE configs
+def _config_tensor(name):
+    import torch
+    cfg = SI.CONFIGS[name]
+    c, v = SI.make_tensor(cfg, device="cuda")
+    return cfg, c.cpu().numpy().astype(np.uint32), v.cpu().numpy()
+
+
+def test_end_to_end_c3_10_sweeps():
+    cfg, c, v = _config_tensor("c3")
+    fg, Fg, Eg, brg, ora = run_pair(c, v, cfg.dims, cfg.rank, cfg.seed, 10)
+    check_pair(fg, Fg, Eg, brg, ora)
+
+
+@pytest.mark.parametrize("R", [8, 16, 32, 64, 128, 256])
+def test_end_to_end_c5_rank_sweep(R):
+    cfg, c, v = _config_tensor("c5")
+    fg, Fg, Eg, brg, ora = run_pair(c, v, cfg.dims, R, cfg.seed, 10)
+    check_pair(fg, Fg, Eg, brg, ora)
+
+
+def _rows_sample(rp, k, seed):
+    """k rows: the heaviest, some empty ones if any, and random others."""
+    I = len(rp) - 1
+    cnt = np.diff(rp)
+    rng = np.random.default_rng(seed)
+    pick = {int(np.argmax(cnt))}
+    empt = np.nonzero(cnt == 0)[0]
+    if len(empt):
+        pick.update(rng.choice(empt, size=min(5, len(empt)), replace=False).tolist())
+    pick.update(rng.choice(I, size=min(k, I), replace=False).tolist())
+    return np.array(sorted(pick))
+
+
+def test_c4_full_size_sampled_rows_and_properties():
+    """c4 at full size (1e8 nonzeros, R = 64) in the bench's configuration: after two GPU
+    sweeps, one mode update per mode is checked teacher-forced on sampled rows (the heaviest
+    slice, empty slices, random rows) against the oracle's row pass computed one row at a
+    time from the GPU's own state; the objective is checked against the oracle's
+    sparse-explicit form; f is non-increasing; factors are nonnegative; E <= I R."""
+    cfg, c, v = _config_tensor("c4")
+    dims, R = cfg.dims, cfg.rank
+    with S(c, v, dims, R, cfg.seed) as g:
+        g.iterate(2)
+        st = g.stats()
+        fs = [s["objective"] for s in st]
+        F = g.factors()
+        for n in range(3):
+            assert (F[n] >= 0).all()
+        assert all(s["E"][n] <= dims[n] * R for s in st for n in range(3))
+        f_sparse = O.objective_sparse(c, v, dims, F)
+        assert abs(fs[-1] - f_sparse) <= 1e-9 * f_sparse
+        for n in range(3):
+            a, b = O.other_modes(dims, n)
+            F = g.factors()
+            Z = g.get_zprev(n)
+            H = O.hadamard(O.gram(F[a]), O.gram(F[b]))
+            assert np.abs(g.hessian(n) - H).max() <= 1e-10 * np.abs(H).max()
+            # rows to check and their nonzeros (oracle layout of the sub-tensor)
+            rp_full = g.layout(n)[3]
+            rows = _rows_sample(rp_full, 2000, n)
+            mask = np.isin(c[:, n], rows)
+            cs, vs = c[mask].copy(), v[mask]
+            remap = np.full(dims[n], -1, np.int64)
+            remap[rows] = np.arange(len(rows))
+            cs[:, n] = remap[cs[:, n]]
+            d2 = list(dims)
+            d2[n] = len(rows)
+            ia, ib, vv, rp = O.layout(cs, vs, d2, n)
+            M = O.mttkrp_layout(rp, ia, ib, vv, F[a], F[b])
+            out = g.mode_update(n, decisions=True)     # device rule: the sweep-3 branch (C10)
+            branch = O.branch(3, [st[0]["ti"][n], st[1]["ti"][n]])
+            Fn, zp, ti, E, Ech, md, dec = O.mode_pass(M, H, F[n][rows], Z[rows], branch, decisions=True)
+            assert np.array_equal(out["decisions"][rows], dec)
+            assert factor_err(g.factors(n)[rows], Fn) <= 1e-9
+            Zg = g.get_zprev(n)[rows]
+            assert np.abs(Zg - zp).max() <= 1e-9 * max(1.0, np.abs(zp).max())

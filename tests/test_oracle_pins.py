@@ -104,11 +104,12 @@ def test_layout_sorted_unique_and_complete():
 
 
 def test_layout_other_mode_rule():
-    # a = the other mode with the smaller length, ties -> lower mode id
-    assert O.other_modes((10, 5, 3), 0) == (2, 1)
+    # reading L1: a = the other mode with the LARGER length, ties -> lower mode id
+    assert O.other_modes((10, 5, 3), 0) == (1, 2)
     assert O.other_modes((10, 5, 5), 0) == (1, 2)
-    assert O.other_modes((10, 5, 3), 2) == (1, 0)
-    assert O.other_modes((1_000_000, 500_000, 10_000), 1) == (2, 0)
+    assert O.other_modes((10, 5, 3), 2) == (0, 1)
+    assert O.other_modes((1_000_000, 500_000, 10_000), 1) == (0, 2)
+    assert O.other_modes((1_000_000, 500_000, 10_000), 0) == (1, 2)
 
 
 def test_layout_slice_example():
