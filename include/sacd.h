@@ -77,7 +77,11 @@ typedef struct {
   int32_t use_graph;          /* 1 (default): sacd_iterate replays a captured CUDA graph    */
   int32_t profile;            /* 1: time every kernel class with CUDA events (no graph)     */
   int32_t nnz_per_item;       /* MTTKRP work-item size in nonzeros (0 = default)            */
-  int32_t reserved[7];
+  int32_t mttkrp_variant;     /* MTTKRP tuning variant (0 = default; tools/mttkrp_tune.py)  */
+  int32_t force_sharded;      /* 1: run the sharded (NCCL) engine also when world_size == 1 */
+  int32_t emulate_ranks;      /* G >= 2 (with world_size 1): emulate the G ranks of the     */
+                              /* sharded engine on this GPU, exchanges as local copies      */
+  int32_t reserved[4];
 } sacd_options;
 
 /* Per-sweep statistics (device-side ring, read by sacd_stats). */
@@ -208,6 +212,16 @@ int sacd_abi_sizes(int32_t out[4]);
 
 /* Multi-GPU: a fresh 128-byte NCCL unique id (rank 0), to be broadcast by the caller. */
 int sacd_nccl_unique_id(void *out128);
+
+/* Sharded engine (world_size > 1, force_sharded or emulate_ranks): per mode, every rank
+ * computes the MTTKRP of its nnz-balanced range of the mode-sorted nonzeros (plan:
+ * sacd_shard_plan); head partials of rows cut by a range boundary are all-gathered and
+ * added by the row owner in rank order; owners run the SaCD row update on their rows; the
+ * updated rows are broadcast by their owners (NCCL all-gather-v over NVLink) into every
+ * rank's replicated factor; (ti, md, E, E_changed, Gram partial) are all-gathered and
+ * summed in rank order, so every rank holds the same state and takes the same branch.
+ * Every rank passes the same full COO to sacd_init.  sacd_factors returns the full
+ * replicated factor; sacd_get_zprev / sacd_mttkrp / decisions are valid on owned rows. */
 
 #ifdef __cplusplus
 }

@@ -12,8 +12,21 @@ SOURCES = ["capi.cu", "kernels.cu", "layout.cu"]
 OUT = os.path.join(HERE, "libsacd.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
+def _nccl_dir():
+    """NCCL shipped with the PyTorch wheel (nvidia-nccl): headers + libnccl.so.2."""
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia")
+    for base in (spec.submodule_search_locations if spec else []):
+        d = os.path.join(base, "nccl")
+        if os.path.exists(os.path.join(d, "include", "nccl.h")):
+            return d
+    raise RuntimeError("nccl.h not found (nvidia-nccl wheel)")
+
+
+NCCL = _nccl_dir()
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
-         "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v", f"-I{ROOT}/include"]
+         "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v", f"-I{ROOT}/include", f"-I{NCCL}/include"]
+LIBS = [f"-L{NCCL}/lib", "-l:libnccl.so.2", f"-Xlinker", f"-rpath={NCCL}/lib"]
 
 
 def _stale() -> bool:
@@ -27,7 +40,7 @@ def _stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return OUT
-    cmd = [NVCC, *FLAGS, "-o", OUT + ".tmp", *[os.path.join(CSRC, s) for s in SOURCES]]
+    cmd = [NVCC, *FLAGS, "-o", OUT + ".tmp", *[os.path.join(CSRC, s) for s in SOURCES], *LIBS]
     log = os.path.join(HERE, "build.log")
     with open(log, "w") as fh:
         r = subprocess.run(cmd, stdout=fh, stderr=subprocess.STDOUT)

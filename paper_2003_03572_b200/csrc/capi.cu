@@ -7,6 +7,8 @@
 #include <new>
 #include <vector>
 
+#include <nccl.h>
+
 #include "sacd_internal.cuh"
 
 struct sacd_ctx : public sacd::Context {};
@@ -84,54 +86,73 @@ ShardPlan plan_shard(const long long *rp, long long I, int world, int rank) {
 }
 
 // ------------------------------------------------------------------ MTTKRP work partition
-// Items hold whole rows with <= T nonzeros in total and <= maxrows rows; a row with more
-// than T nonzeros is cut into ceil(nnz/T) row-relative segments, each writing a partial
-// slot that k_fixup sums in slot order (deterministic).
-static void build_items(const std::vector<long long> &rp, long long I, long long T, long long maxrows,
-                        std::vector<WorkItem> &items, std::vector<SplitRow> &splits, long long &nslots) {
+// Work items over the nonzero range [lo, hi) of one mode: whole rows with <= T local
+// nonzeros in total and <= maxrows rows per item; a row with more than T local nonzeros,
+// or one cut by the range boundary (sharded engine), is split into row-relative segments
+// of T nonzeros, each writing a partial slot that k_fixup sums in slot order into M[row]
+// (deterministic).  Rows without local nonzeros get no item: the row update reads row_ptr
+// and uses m = 0 for empty slices.
+static void build_items(const std::vector<long long> &rp, long long I, long long lo, long long hi, long long T,
+                        long long maxrows, std::vector<WorkItem> &items, std::vector<SplitRow> &splits,
+                        long long &nslots) {
   items.clear();
   splits.clear();
   nslots = 0;
-  long long i = 0;
-  while (i < I) {
-    const long long li = rp[i + 1] - rp[i];
-    if (li > T) {
-      const long long nseg = (li + T - 1) / T;
+  if (lo >= hi) return;
+  // the row containing nonzero lo: rp[r] <= lo < rp[r+1]
+  long long r = (long long)(std::upper_bound(rp.begin(), rp.begin() + I + 1, lo) - rp.begin()) - 1;
+  while (r < I && rp[r] < hi) {
+    const long long s0 = std::max(rp[r], lo), e0 = std::min(rp[r + 1], hi);
+    const long long len = e0 - s0;
+    if (len <= 0) {
+      ++r;
+      continue;
+    }
+    const bool clipped = rp[r] < lo || rp[r + 1] > hi;
+    if (clipped || len > T) {
+      const long long nseg = (len + T - 1) / T;
       SplitRow sr;
       sr.slot0 = nslots;
       sr.nslots = nseg;
-      sr.row = (int)i;
+      sr.row = (int)r;
       sr.pad = 0;
-      for (long long s = 0; s < nseg; ++s) {
+      for (long long q = 0; q < nseg; ++q) {
         WorkItem w;
-        w.nz0 = rp[i] + s * T;
-        w.nz1 = std::min(rp[i] + (s + 1) * T, rp[i + 1]);
-        w.row0 = (int)i;
-        w.row1 = (int)(i + 1);
+        w.nz0 = s0 + q * T;
+        w.nz1 = std::min(s0 + (q + 1) * T, e0);
+        w.row0 = (int)r;
+        w.row1 = (int)(r + 1);
         w.slot = nslots++;
         items.push_back(w);
       }
       splits.push_back(sr);
-      ++i;
+      ++r;
       continue;
     }
-    long long j = i, tot = 0;
-    while (j < I && j - i < maxrows) {
+    long long j = r, tot = 0;
+    while (j < I && j - r < maxrows && rp[j] < hi) {
       const long long l = rp[j + 1] - rp[j];
-      if (l > T) break;
-      if (tot + l > T && j > i) break;
+      if (rp[j + 1] > hi || l > T) break;
+      if (tot + l > T && j > r) break;
       tot += l;
       ++j;
     }
     WorkItem w;
-    w.nz0 = rp[i];
+    w.nz0 = rp[r];
     w.nz1 = rp[j];
-    w.row0 = (int)i;
+    w.row0 = (int)r;
     w.row1 = (int)j;
     w.slot = -1;
     items.push_back(w);
-    i = j;
+    r = j;
   }
+}
+
+template <typename T>
+static int upload(T **dst, const std::vector<T> &v) {
+  SACD_CUDA_TRY(cudaMalloc(dst, std::max<size_t>(1, v.size()) * sizeof(T)));
+  if (!v.empty()) SACD_CUDA_TRY(cudaMemcpy(*dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return SACD_OK;
 }
 
 static int capture_graph(Context &c) {
@@ -146,7 +167,9 @@ static int capture_graph(Context &c) {
   if (!c.opt.use_graph || c.opt.profile) return SACD_OK;
   SACD_CUDA_TRY(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
   int rc = SACD_OK;
-  for (int n = 0; n < 3 && rc == SACD_OK; ++n) rc = launch_mode_update(c, n, SACD_BR_AUTO, n == 0, n == 2, nullptr);
+  for (int n = 0; n < 3 && rc == SACD_OK; ++n)
+    rc = c.sharded ? launch_sharded_mode_update(c, n, SACD_BR_AUTO, n == 0, n == 2, nullptr)
+                   : launch_mode_update(c, n, SACD_BR_AUTO, n == 0, n == 2, nullptr);
   cudaGraph_t g = nullptr;
   cudaError_t e = cudaStreamEndCapture(c.stream, &g);
   if (rc != SACD_OK) {
@@ -160,7 +183,9 @@ static int capture_graph(Context &c) {
 }
 
 static int sweep_eager(Context &c) {
-  for (int n = 0; n < 3; ++n) SACD_TRY(launch_mode_update(c, n, SACD_BR_AUTO, n == 0, n == 2, nullptr));
+  for (int n = 0; n < 3; ++n)
+    SACD_TRY(c.sharded ? launch_sharded_mode_update(c, n, SACD_BR_AUTO, n == 0, n == 2, nullptr)
+                       : launch_mode_update(c, n, SACD_BR_AUTO, n == 0, n == 2, nullptr));
   return SACD_OK;
 }
 
@@ -192,6 +217,21 @@ static void destroy(sacd_ctx *c) {
   cudaFree(c->cnt_part);
   cudaFree(c->gram_part);
   cudaFree(c->decisions);
+  for (Shard &sh : c->shards) {
+    for (int n = 0; n < 3; ++n) {
+      cudaFree(sh.items[n]);
+      cudaFree(sh.splits[n]);
+    }
+    cudaFree(sh.M);
+    cudaFree(sh.partial);
+    cudaFree(sh.row_part);
+    cudaFree(sh.cnt_part);
+    cudaFree(sh.gram_part);
+  }
+  cudaFree(c->xid);
+  cudaFree(c->xrow);
+  cudaFree(c->xstats);
+  if (c->comm) ncclCommDestroy(reinterpret_cast<ncclComm_t>(c->comm));
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -258,31 +298,87 @@ static int init_impl(Context *c, const uint32_t *coords, const float *vals, uint
   cudaFreeAsync(dv, s);
   SACD_TRY(rc);
 
-  // partitions
+  // partitions (host planning over row_ptr, once)
   const long long T = c->opt.nnz_per_item > 0 ? c->opt.nnz_per_item : 1024;
   long long max_slots = 1, maxI = 1;
+  std::vector<long long> rps[3];
   for (int n = 0; n < 3; ++n) {
     ModeData &md = c->m[n];
-    std::vector<long long> rp((size_t)md.I + 1);
-    SACD_CUDA_TRY(cudaMemcpyAsync(rp.data(), md.row_ptr, rp.size() * 8, cudaMemcpyDeviceToHost, s));
-    SACD_CUDA_TRY(cudaStreamSynchronize(s));
-    std::vector<WorkItem> items;
-    std::vector<SplitRow> splits;
-    long long nslots = 0;
-    build_items(rp, md.I, T, 32, items, splits, nslots);
-    md.n_items = (long long)items.size();
-    md.n_splits = (long long)splits.size();
-    md.n_slots = nslots;
-    SACD_CUDA_TRY(cudaMalloc(&md.items, std::max<size_t>(1, items.size()) * sizeof(WorkItem)));
-    SACD_CUDA_TRY(cudaMalloc(&md.splits, std::max<size_t>(1, splits.size()) * sizeof(SplitRow)));
-    if (!items.empty())
-      SACD_CUDA_TRY(cudaMemcpy(md.items, items.data(), items.size() * sizeof(WorkItem), cudaMemcpyHostToDevice));
-    if (!splits.empty())
-      SACD_CUDA_TRY(
-          cudaMemcpy(md.splits, splits.data(), splits.size() * sizeof(SplitRow), cudaMemcpyHostToDevice));
-    max_slots = std::max(max_slots, nslots);
+    rps[n].resize((size_t)md.I + 1);
+    SACD_CUDA_TRY(cudaMemcpyAsync(rps[n].data(), md.row_ptr, rps[n].size() * 8, cudaMemcpyDeviceToHost, s));
     maxI = std::max(maxI, md.I);
-    c->device_bytes += (long long)(items.size() * sizeof(WorkItem) + splits.size() * sizeof(SplitRow));
+  }
+  SACD_CUDA_TRY(cudaStreamSynchronize(s));
+  if (!c->sharded) {
+    for (int n = 0; n < 3; ++n) {
+      ModeData &md = c->m[n];
+      std::vector<WorkItem> items;
+      std::vector<SplitRow> splits;
+      long long nslots = 0;
+      build_items(rps[n], md.I, 0, c->nnz, T, 32, items, splits, nslots);
+      md.n_items = (long long)items.size();
+      md.n_splits = (long long)splits.size();
+      md.n_slots = nslots;
+      SACD_TRY(upload(&md.items, items));
+      SACD_TRY(upload(&md.splits, splits));
+      max_slots = std::max(max_slots, nslots);
+      c->device_bytes += (long long)(items.size() * sizeof(WorkItem) + splits.size() * sizeof(SplitRow));
+    }
+  } else {
+    // sharded engine: plans of every rank, items of the local shard(s)
+    for (int n = 0; n < 3; ++n) {
+      c->all_plans[n].resize(c->G);
+      for (int q = 0; q < c->G; ++q) c->all_plans[n][q] = plan_shard(rps[n].data(), c->m[n].I, c->G, q);
+    }
+    const int first = c->opt.emulate_ranks > 1 ? 0 : c->me;
+    const int count = c->opt.emulate_ranks > 1 ? c->G : 1;
+    c->shards.resize(count);
+    for (int k = 0; k < count; ++k) {
+      Shard &sh = c->shards[k];
+      sh.rank = first + k;
+      long long slots_k = 1;
+      for (int n = 0; n < 3; ++n) {
+        sh.plan[n] = c->all_plans[n][sh.rank];
+        std::vector<WorkItem> items;
+        std::vector<SplitRow> splits;
+        long long nslots = 0;
+        build_items(rps[n], c->m[n].I, sh.plan[n].lo, sh.plan[n].hi, T, 32, items, splits, nslots);
+        sh.n_items[n] = (long long)items.size();
+        sh.n_splits[n] = (long long)splits.size();
+        SACD_TRY(upload(&sh.items[n], items));
+        SACD_TRY(upload(&sh.splits[n], splits));
+        slots_k = std::max(slots_k, nslots);
+        c->m[n].n_items += sh.n_items[n];
+        c->m[n].n_splits += sh.n_splits[n];
+      }
+      SACD_CUDA_TRY(cudaMalloc(&sh.M, (size_t)maxI * c->pitch * rs));
+      SACD_CUDA_TRY(cudaMalloc(&sh.partial, (size_t)slots_k * c->pitch * rs));
+      c->device_bytes += (long long)((size_t)maxI * c->pitch * rs + (size_t)slots_k * c->pitch * rs);
+    }
+    // NCCL communicator (one rank per process; emulated ranks need none)
+    if (c->opt.emulate_ranks <= 1) {
+      ncclUniqueId id;
+      if (c->world > 1) {
+        if (!c->opt.nccl_unique_id) {
+          set_error("sacd_init: world_size > 1 needs opt.nccl_unique_id (sacd_nccl_unique_id on rank 0)");
+          return SACD_EINVAL;
+        }
+        memcpy(&id, c->opt.nccl_unique_id, sizeof(id));
+      } else {
+        const ncclResult_t r = ncclGetUniqueId(&id);
+        if (r != ncclSuccess) {
+          set_error(std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+          return SACD_ENCCL;
+        }
+      }
+      ncclComm_t comm;
+      const ncclResult_t r = ncclCommInitRank(&comm, c->world, id, c->me);
+      if (r != ncclSuccess) {
+        set_error(std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+        return SACD_ENCCL;
+      }
+      c->comm = comm;
+    }
   }
   // factors, z_prev, Grams, scratch
   const int P = c->pitch, R = c->R;
@@ -306,10 +402,20 @@ static int init_impl(Context *c, const uint32_t *coords, const float *vals, uint
   c->device_bytes += (long long)((size_t)maxI * P * rs + (size_t)max_slots * P * rs + (size_t)P * P * rs +
                                  (size_t)c->max_row_blocks * 32 + (size_t)c->gram_blocks * R * R * 8 +
                                  sizeof(DevState));
+  if (c->sharded) {
+    for (Shard &sh : c->shards) {
+      SACD_CUDA_TRY(cudaMalloc(&sh.row_part, (size_t)c->max_row_blocks * 2 * 8));
+      SACD_CUDA_TRY(cudaMalloc(&sh.cnt_part, (size_t)c->max_row_blocks * 2 * 8));
+      SACD_CUDA_TRY(cudaMalloc(&sh.gram_part, (size_t)c->gram_blocks * R * R * 8));
+    }
+    SACD_CUDA_TRY(cudaMalloc(&c->xid, (size_t)c->G * 8));
+    SACD_CUDA_TRY(cudaMalloc(&c->xrow, (size_t)c->G * P * rs));
+    SACD_CUDA_TRY(cudaMalloc(&c->xstats, (size_t)c->G * (4 + (size_t)R * R) * 8));
+  }
   SACD_TRY(launch_setup(*c));
   SACD_TRY(launch_init_factors(*c, seed));
   for (int n = 0; n < 3; ++n) SACD_TRY(launch_gram(*c, n));
-  SACD_TRY(launch_initial_fit(*c));
+  SACD_TRY(c->sharded ? launch_sharded_initial_fit(*c) : launch_initial_fit(*c));
   SACD_CUDA_TRY(cudaStreamSynchronize(s));
   SACD_TRY(capture_graph(*c));
   SACD_CUDA_TRY(cudaStreamSynchronize(s));
@@ -419,8 +525,9 @@ int sacd_init(sacd_ctx **out, const uint32_t *coords, const float *vals, int64_t
     set_error("sacd_init: bad option value");
     return SACD_EINVAL;
   }
-  if (o.world_size != 1 || o.rank != 0) {
-    set_error("sacd_init: world_size > 1 requires the NCCL build (not in this library)");
+  if (o.world_size < 1 || o.rank < 0 || o.rank >= o.world_size || o.emulate_ranks < 0 ||
+      (o.emulate_ranks > 1 && o.world_size != 1)) {
+    set_error("sacd_init: bad world_size / rank / emulate_ranks");
     return SACD_EINVAL;
   }
   sacd_ctx *c = new (std::nothrow) sacd_ctx();
@@ -443,6 +550,10 @@ int sacd_init(sacd_ctx **out, const uint32_t *coords, const float *vals, int64_t
   }
   for (int n = 0; n < 3; ++n) c->dims[n] = dims[n];
   c->nnz = nnz;
+  c->world = o.world_size;
+  c->me = o.rank;
+  c->sharded = o.world_size > 1 || o.force_sharded || o.emulate_ranks > 1;
+  c->G = o.emulate_ranks > 1 ? o.emulate_ranks : o.world_size;
   c->R = rank;
   int p = 8;
   while (p < rank) p <<= 1;
@@ -558,7 +669,7 @@ int sacd_mttkrp(sacd_ctx *c, int32_t mode, double *out, int64_t ld) {
     set_error(std::string("sacd_mttkrp: ") + cudaGetErrorString(e));
     return sticky(c, SACD_ECUDA);
   }
-  int rc = launch_mttkrp(*c, mode, c->M);
+  int rc = c->sharded ? launch_sharded_mttkrp(*c, mode) : launch_mttkrp(*c, mode, c->M);
   if (rc == SACD_OK) rc = read_matrix(c, c->M, c->m[mode].I, out, ld);
   return sticky(c, rc);
 }
@@ -574,9 +685,10 @@ int sacd_time_mttkrp(sacd_ctx *c, int32_t mode, int32_t reps, double *ms) {
   cudaEvent_t e0, e1;
   SACD_CUDA_TRY(cudaEventCreate(&e0));
   SACD_CUDA_TRY(cudaEventCreate(&e1));
-  int rc = launch_mttkrp(*c, mode, c->M);  // warm-up
+  auto one = [&]() { return c->sharded ? launch_sharded_mttkrp(*c, mode) : launch_mttkrp(*c, mode, c->M); };
+  int rc = one();  // warm-up
   SACD_CUDA_TRY(cudaEventRecord(e0, c->stream));
-  for (int i = 0; i < reps && rc == SACD_OK; ++i) rc = launch_mttkrp(*c, mode, c->M);
+  for (int i = 0; i < reps && rc == SACD_OK; ++i) rc = one();
   SACD_CUDA_TRY(cudaEventRecord(e1, c->stream));
   SACD_CUDA_TRY(cudaEventSynchronize(e1));
   float t = 0.f;
@@ -620,7 +732,9 @@ int sacd_mode_update(sacd_ctx *c, int32_t mode, int32_t branch, uint8_t *decisio
   if (decisions) {
     SACD_CUDA_TRY(cudaMallocAsync(&dd, std::max<size_t>(1, nd), c->stream));
   }
-  int rc = launch_mode_update(*c, mode, branch, false, false, dd);
+  if (dd) SACD_CUDA_TRY(cudaMemsetAsync(dd, 0, std::max<size_t>(1, nd), c->stream));
+  int rc = c->sharded ? launch_sharded_mode_update(*c, mode, branch, false, false, dd)
+                      : launch_mode_update(*c, mode, branch, false, false, dd);
   if (rc == SACD_OK && decisions) rc = dev_read(c, decisions, dd, nd);
   if (dd) cudaFreeAsync(dd, c->stream);
   if (rc == SACD_OK) {
@@ -747,9 +861,15 @@ int sacd_abi_sizes(int32_t out[4]) {
 }
 
 int sacd_nccl_unique_id(void *out128) {
-  (void)out128;
-  set_error("sacd_nccl_unique_id: this library was built without NCCL");
-  return SACD_ENCCL;
+  if (!out128) return SACD_EINVAL;
+  ncclUniqueId id;
+  const ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) {
+    set_error(std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+    return SACD_ENCCL;
+  }
+  memcpy(out128, &id, sizeof(id));
+  return SACD_OK;
 }
 
 void sacd_free(sacd_ctx *c) { destroy(c); }

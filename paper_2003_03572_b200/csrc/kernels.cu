@@ -16,6 +16,8 @@
 // reruns are bitwise identical (unchanged elements recompute the same z exactly).
 #include <math.h>
 
+#include <nccl.h>
+
 #include "sacd_internal.cuh"
 
 namespace sacd {
@@ -365,7 +367,8 @@ __global__ void __launch_bounds__(256) k_prepare(int mode, int R, const double *
 // walk is bank-conflict free; H is staged in shared memory when it fits.
 template <typename Real, int RT>
 __global__ void __launch_bounds__(rows_per_block<RT>())
-    k_sacd_rows(long long I, int R, int mode, int l_mode, const long long *__restrict__ row_ptr,
+    k_sacd_rows(long long row_begin, long long row_end, int R, int mode, int l_mode,
+                const long long *__restrict__ row_ptr,
                 const Real *__restrict__ M, Real *__restrict__ F,
                 Real *__restrict__ Z, const Real *__restrict__ Hr, const DevState *__restrict__ st,
                 uint8_t *__restrict__ dec, double *__restrict__ ti_part, double *__restrict__ md_part,
@@ -380,8 +383,8 @@ __global__ void __launch_bounds__(rows_per_block<RT>())
   __shared__ long long red_l[2][TR / 32];
 
   const int tid = threadIdx.x;
-  const long long row0 = (long long)blockIdx.x * TR;
-  const int nrows = (int)min((long long)TR, I - row0);
+  const long long row0 = row_begin + (long long)blockIdx.x * TR;
+  const int nrows = (int)min((long long)TR, row_end - row0);
   if (HS) {
     for (int x = tid; x < RT * RT; x += TR) Hs[x] = Hr[x];
   }
@@ -517,15 +520,16 @@ __global__ void __launch_bounds__(rows_per_block<RT>())
 
 // sum_r F_ir M_ir per row block (initial objective f^0)
 template <typename Real, int RT>
-__global__ void k_fm_dot(long long I, int R, const long long *__restrict__ row_ptr, const Real *__restrict__ F,
+__global__ void k_fm_dot(long long row_begin, long long row_end, int R, const long long *__restrict__ row_ptr,
+                         const Real *__restrict__ F,
                          const Real *__restrict__ M,
                          double *__restrict__ ti_part, double *__restrict__ md_part, long long *__restrict__ e_part,
                          long long *__restrict__ ech_part) {
   constexpr int TR = rows_per_block<RT>();
   __shared__ double red[TR];
-  const long long row = (long long)blockIdx.x * TR + threadIdx.x;
+  const long long row = row_begin + (long long)blockIdx.x * TR + threadIdx.x;
   double s = 0.0;
-  if (row < I && row_ptr[row] != row_ptr[row + 1])
+  if (row < row_end && row_ptr[row] != row_ptr[row + 1])
     for (int r = 0; r < R; ++r) s += (double)F[row * RT + r] * (double)M[row * RT + r];
   red[threadIdx.x] = s;
   __syncthreads();
@@ -550,7 +554,8 @@ __host__ __device__ constexpr int gram_gt() {
 
 template <typename Real, int RT>
 __global__ void __launch_bounds__(gram_tg<gram_gt<RT>()>() * gram_tg<gram_gt<RT>()>())
-    k_gram_partial(long long I, int R, const Real *__restrict__ F, double *__restrict__ part) {
+    k_gram_partial(long long row_begin, long long row_end, int R, const Real *__restrict__ F,
+                   double *__restrict__ part) {
   constexpr int GT = gram_gt<RT>();
   constexpr int TG = gram_tg<GT>();
   constexpr int T = GT / TG;
@@ -574,9 +579,9 @@ __global__ void __launch_bounds__(gram_tg<gram_gt<RT>()>() * gram_tg<gram_gt<RT>
   const int tid = threadIdx.x;
   const int ty = tid / TG, tx = tid % TG;
   const bool active = (bi != bj) || (ty <= tx);
-  const long long per = (I + gridDim.x - 1) / gridDim.x;
-  const long long i0 = (long long)blockIdx.x * per;
-  const long long i1 = min(I, i0 + per);
+  const long long per = (row_end - row_begin + gridDim.x - 1) / gridDim.x;
+  const long long i0 = row_begin + (long long)blockIdx.x * per;
+  const long long i1 = min(row_end, i0 + per);
   double acc[T][T];
 #pragma unroll
   for (int a = 0; a < T; ++a)
@@ -632,12 +637,47 @@ __global__ void k_gram_reduce(int R, int nblk, const double *__restrict__ part, 
 // ------------------------------------------------------------------ finalize a mode pass
 // flags: 1 = record the pass (ti/E/history), 2 = compute f (needs all three Grams),
 //        4 = push a stats-ring record (end of sweep)
+// Record a finished pass in the device state (thread 0 only).
+// flags: 1 = record the pass (ti/E/history), 2 = compute f, 4 = push a stats-ring record.
+__device__ void apply_pass(DevState *st, int mode, double ti, double md, long long E, long long Ech, double mn,
+                           int flags) {
+  if (flags & 1) {
+    st->ti_cur[mode] = ti;
+    st->E[mode] = E;
+    st->Ech[mode] = Ech;
+    st->ti2[mode] = st->ti1[mode];
+    st->ti1[mode] = ti;
+    st->nhist[mode] += 1;
+  }
+  if (mode == 2) st->mdot = md;
+  if (flags & 2) {
+    const double f = st->xnorm2 - 2.0 * md + mn;
+    st->f = f;
+    st->fit = st->xnorm2 > 0.0 ? 1.0 - sqrt(f > 0.0 ? f : 0.0) / sqrt(st->xnorm2) : 0.0;
+  }
+  if (flags & 4) {
+    sacd_iter_stats &rec = st->ring[st->ring_count % kRing];
+    rec.k = st->k;
+    rec.objective = st->f;
+    rec.fit = st->fit;
+    for (int n = 0; n < 3; ++n) {
+      rec.branch[n] = st->branch[n];
+      rec.ti[n] = st->ti_cur[n];
+      rec.E[n] = st->E[n];
+      rec.E_changed[n] = st->Ech[n];
+    }
+    st->ring_count += 1;
+  }
+}
+
+// Fixed-order reduction of the per-block partials of a pass.  flags as apply_pass, plus
+// 8 = local: write (ti, md, E, Ech) to local_out[0..3] and leave the state alone (sharded).
 __global__ void __launch_bounds__(1024) k_finalize(int mode, long long nblk, const double *__restrict__ ti_part,
                                                    const double *__restrict__ md_part,
                                                    const long long *__restrict__ e_part,
                                                    const long long *__restrict__ ech_part, const double *G0,
                                                    const double *G1, const double *G2, int R, DevState *st,
-                                                   int flags) {
+                                                   int flags, double *local_out) {
   __shared__ double sd[3][1024];
   __shared__ long long sl[2][1024];
   const int tid = threadIdx.x;
@@ -649,7 +689,7 @@ __global__ void __launch_bounds__(1024) k_finalize(int mode, long long nblk, con
     E += e_part[b];
     Ech += ech_part[b];
   }
-  if (flags & 2)
+  if ((flags & 2) && !(flags & 8))
     for (int x = tid; x < R * R; x += 1024) mn += G0[x] * G1[x] * G2[x];
   sd[0][tid] = ti;
   sd[1][tid] = md;
@@ -668,33 +708,73 @@ __global__ void __launch_bounds__(1024) k_finalize(int mode, long long nblk, con
     __syncthreads();
   }
   if (tid == 0) {
-    if (flags & 1) {
-      st->ti_cur[mode] = sd[0][0];
-      st->E[mode] = sl[0][0];
-      st->Ech[mode] = sl[1][0];
-      st->ti2[mode] = st->ti1[mode];
-      st->ti1[mode] = sd[0][0];
-      st->nhist[mode] += 1;
+    if (flags & 8) {
+      local_out[0] = sd[0][0];
+      local_out[1] = sd[1][0];
+      local_out[2] = (double)sl[0][0];
+      local_out[3] = (double)sl[1][0];
+    } else {
+      apply_pass(st, mode, sd[0][0], sd[1][0], sl[0][0], sl[1][0], sd[2][0], flags);
     }
-    if (mode == 2) st->mdot = sd[1][0];
-    if (flags & 2) {
-      const double f = st->xnorm2 - 2.0 * sd[1][0] + sd[2][0];
-      st->f = f;
-      st->fit = st->xnorm2 > 0.0 ? 1.0 - sqrt(f > 0.0 ? f : 0.0) / sqrt(st->xnorm2) : 0.0;
+  }
+}
+
+// ------------------------------------------------------------------ sharded-engine kernels
+// Every rank q writes its head row id / partial row into slot q of the exchange buffers
+// and its (ti, md, E, Ech, Gram partial) into slot q of the stats buffer; NCCL all-gathers
+// them in place (or, with emulated ranks on one GPU, they are already all local).
+template <typename Real, int RT>
+__global__ void k_pack_head(long long head, const Real *__restrict__ M, long long *__restrict__ id_slot,
+                            Real *__restrict__ row_slot) {
+  for (int c = threadIdx.x; c < RT; c += blockDim.x) row_slot[c] = head >= 0 ? M[head * RT + c] : Real(0);
+  if (threadIdx.x == 0) *id_slot = head;
+}
+
+// The owner adds the head partials of the other ranks to its rows, in rank order.
+template <typename Real, int RT>
+__global__ void k_merge_heads(int G, long long rlo, long long rhi, const long long *__restrict__ ids,
+                              const Real *__restrict__ rows, Real *__restrict__ M) {
+  for (int q = 0; q < G; ++q) {
+    const long long id = ids[q];
+    if (id >= rlo && id < rhi)
+      for (int c = threadIdx.x; c < RT; c += blockDim.x) M[id * RT + c] += rows[(long long)q * RT + c];
+  }
+}
+
+// Sum the G ranks' slots in rank order: Gram (if flags & 32) and (ti, md, E, Ech); then
+// apply the pass to the device state.  stats slot layout: [ti, md, E, Ech, Gram R x R].
+__global__ void __launch_bounds__(1024) k_finalize_global(int mode, int G, int R, const double *__restrict__ stats,
+                                                          double *Gout, const double *G0, const double *G1,
+                                                          const double *G2, DevState *st, int flags) {
+  __shared__ double red[1024];
+  const int tid = threadIdx.x;
+  const long long slot = 4 + (long long)R * R;
+  if (flags & 32) {
+    for (int x = tid; x < R * R; x += 1024) {
+      double s = 0.0;
+      for (int q = 0; q < G; ++q) s += stats[q * slot + 4 + x];
+      Gout[x] = s;
     }
-    if (flags & 4) {
-      sacd_iter_stats &rec = st->ring[st->ring_count % kRing];
-      rec.k = st->k;
-      rec.objective = st->f;
-      rec.fit = st->fit;
-      for (int n = 0; n < 3; ++n) {
-        rec.branch[n] = st->branch[n];
-        rec.ti[n] = st->ti_cur[n];
-        rec.E[n] = st->E[n];
-        rec.E_changed[n] = st->Ech[n];
-      }
-      st->ring_count += 1;
+    __syncthreads();
+  }
+  double mn = 0.0;
+  if (flags & 2)
+    for (int x = tid; x < R * R; x += 1024) mn += G0[x] * G1[x] * G2[x];
+  red[tid] = mn;
+  __syncthreads();
+  for (int o = 512; o > 0; o >>= 1) {
+    if (tid < o) red[tid] += red[tid + o];
+    __syncthreads();
+  }
+  if (tid == 0) {
+    double ti = 0.0, md = 0.0, E = 0.0, Ech = 0.0;
+    for (int q = 0; q < G; ++q) {
+      ti += stats[q * slot + 0];
+      md += stats[q * slot + 1];
+      E += stats[q * slot + 2];
+      Ech += stats[q * slot + 3];
     }
+    apply_pass(st, mode, ti, md, (long long)E, (long long)Ech, red[0], flags & 7);
   }
 }
 
@@ -729,43 +809,157 @@ inline int grid1d(long long n, int block = 256) {
 template <typename Real, int RT>
 struct Impl {
   static int mttkrp(Context &c, int mode, void *out_v) {
-    Real *out = reinterpret_cast<Real *>(out_v);
+    ModeData &md = c.m[mode];
+    return mttkrp_on(c, mode, md.items, md.n_items, md.splits, md.n_splits, reinterpret_cast<Real *>(out_v),
+                     reinterpret_cast<Real *>(c.partial));
+  }
+
+  static int mttkrp_on(Context &c, int mode, const WorkItem *items, long long n_items, const SplitRow *splits,
+                       long long n_splits, Real *out, Real *partial) {
     ModeData &md = c.m[mode];
     const Real *A = reinterpret_cast<const Real *>(c.m[md.a].F);
     const Real *B = reinterpret_cast<const Real *>(c.m[md.b].F);
     int pe = prof_begin(c, 0);
-    if (md.n_items > 0) {
+    if (n_items > 0) {
       const int wpb = 8;
-      const long long blocks = (md.n_items + wpb - 1) / wpb;
+      const long long blocks = (n_items + wpb - 1) / wpb;
       if constexpr (RT >= 32) {
-        // (NB gathers in flight per warp, min blocks per SM); opt.reserved[0] selects a
-        // tuning variant (0 = default).
-        const int var = c.opt.reserved[0];
+        // (NB gathers in flight per warp, min blocks per SM); opt.mttkrp_variant selects a
+        // tuning variant (0 = default, measured on B200 with tools/mttkrp_tune.py:
+        // occupancy beats deeper per-warp batching).
+        const int var = c.opt.mttkrp_variant;
         auto go = [&](auto kern) {
-          kern<<<(unsigned)blocks, wpb * 32, 0, c.stream>>>(md.items, md.n_items, md.idx_a, md.idx_b, md.val,
-                                                           md.idx_n, A, B, out, reinterpret_cast<Real *>(c.partial));
+          kern<<<(unsigned)blocks, wpb * 32, 0, c.stream>>>(items, n_items, md.idx_a, md.idx_b, md.val, md.idx_n, A,
+                                                           B, out, partial);
         };
-        // measured on B200 (tools/mttkrp_tune.py): occupancy beats deeper per-warp batching
         if (var == 1) go(k_mttkrp_fiber<Real, RT, 1, 4>);
         else if (var == 2) go(k_mttkrp_fiber<Real, RT, 2, 4>);
         else if (var == 3) go(k_mttkrp_fiber<Real, RT, 1, 7>);
         else if (var == 5) go(k_mttkrp_fiber<Real, RT, 2, 6>);
         else if (var == 6 || (var == 0 && sizeof(Real) == 8)) go(k_mttkrp_fiber<Real, RT, 1, 6>);
         else go(k_mttkrp_fiber<Real, RT, 1, 7>);  // fp32 default
+      } else {
+        k_mttkrp<Real, RT><<<(unsigned)blocks, wpb * 32, 0, c.stream>>>(items, n_items, md.row_ptr, md.idx_a,
+                                                                       md.idx_b, md.val, A, B, out, partial);
       }
-      else
-        k_mttkrp<Real, RT><<<(unsigned)blocks, wpb * 32, 0, c.stream>>>(
-            md.items, md.n_items, md.row_ptr, md.idx_a, md.idx_b, md.val, A, B, out,
-            reinterpret_cast<Real *>(c.partial));
     }
     SACD_CUDA_TRY(cudaGetLastError());
     SACD_TRY(prof_end(c, 0, pe));
-    if (md.n_splits > 0) {
+    if (n_splits > 0) {
       pe = prof_begin(c, 1);
-      k_fixup<Real, RT><<<(unsigned)md.n_splits, 256, 0, c.stream>>>(md.splits, md.n_splits,
-                                                                 reinterpret_cast<const Real *>(c.partial), out);
+      k_fixup<Real, RT><<<(unsigned)n_splits, 256, 0, c.stream>>>(splits, n_splits, partial, out);
       SACD_CUDA_TRY(cudaGetLastError());
       SACD_TRY(prof_end(c, 1, pe));
+    }
+    return SACD_OK;
+  }
+
+  // ---- sharded engine -------------------------------------------------
+  // Each rank computes the MTTKRP of its nonzero range; the head partials (rows whose
+  // first nonzero is on a lower rank) are exchanged and added by the owners in rank order.
+  static int sharded_mttkrp_merge(Context &c, int mode) {
+    for (Shard &sh : c.shards)
+      SACD_TRY(mttkrp_on(c, mode, sh.items[mode], sh.n_items[mode], sh.splits[mode], sh.n_splits[mode],
+                         reinterpret_cast<Real *>(sh.M), reinterpret_cast<Real *>(sh.partial)));
+    Real *xrow = reinterpret_cast<Real *>(c.xrow);
+    for (Shard &sh : c.shards)
+      k_pack_head<Real, RT><<<1, 256, 0, c.stream>>>(sh.plan[mode].head, reinterpret_cast<const Real *>(sh.M),
+                                                     c.xid + sh.rank, xrow + (long long)sh.rank * RT);
+    SACD_CUDA_TRY(cudaGetLastError());
+    if (c.comm) {
+      SACD_TRY(nccl_allgather_inplace(c, c.xid, 1, 2));
+      SACD_TRY(nccl_allgather_inplace(c, c.xrow, RT, sizeof(Real) == 8 ? 0 : 1));
+    }
+    for (Shard &sh : c.shards)
+      k_merge_heads<Real, RT><<<1, 256, 0, c.stream>>>(c.G, sh.plan[mode].rlo, sh.plan[mode].rhi, c.xid, xrow,
+                                                       reinterpret_cast<Real *>(sh.M));
+    SACD_CUDA_TRY(cudaGetLastError());
+    return SACD_OK;
+  }
+
+  static int sharded_mode_update(Context &c, int mode, int branch_override, bool begin_sweep, bool end_sweep,
+                                 uint8_t *dec) {
+    ModeData &md = c.m[mode];
+    SACD_TRY(sharded_mttkrp_merge(c, mode));
+    SACD_TRY(prepare(c, mode, branch_override, begin_sweep, 1));
+    constexpr int TR = rows_per_block<RT>();
+    constexpr size_t smem = rows_smem_bytes<Real, RT>();
+    constexpr int GT = gram_gt<RT>();
+    constexpr int TG = gram_tg<GT>();
+    constexpr int NBP = RT / GT;
+    const long long slot = 4 + (long long)c.R * c.R;
+    for (Shard &sh : c.shards) {
+      const long long rlo = sh.plan[mode].rlo, rhi = sh.plan[mode].rhi;
+      const long long nblk = (rhi - rlo + TR - 1) / TR;
+      double *ti_part = sh.row_part, *md_part = sh.row_part + c.max_row_blocks;
+      long long *e_part = sh.cnt_part, *ech_part = sh.cnt_part + c.max_row_blocks;
+      int pe = prof_begin(c, 3);
+      if (nblk > 0)
+        k_sacd_rows<Real, RT><<<(unsigned)nblk, TR, smem, c.stream>>>(
+            rlo, rhi, c.R, mode, c.opt.l_mode, md.row_ptr, reinterpret_cast<const Real *>(sh.M),
+            reinterpret_cast<Real *>(md.F), reinterpret_cast<Real *>(md.Z), reinterpret_cast<const Real *>(c.Hr),
+            c.st, dec, ti_part, md_part, e_part, ech_part);
+      SACD_CUDA_TRY(cudaGetLastError());
+      SACD_TRY(prof_end(c, 3, pe));
+      pe = prof_begin(c, 4);
+      double *sl = c.xstats + sh.rank * slot;
+      k_gram_partial<Real, RT><<<dim3(c.gram_blocks, NBP * (NBP + 1) / 2), TG * TG, 0, c.stream>>>(
+          rlo, rhi, c.R, reinterpret_cast<const Real *>(md.F), sh.gram_part);
+      k_gram_reduce<<<(c.R * c.R + 255) / 256, 256, 0, c.stream>>>(c.R, c.gram_blocks, sh.gram_part, sl + 4);
+      SACD_CUDA_TRY(cudaGetLastError());
+      SACD_TRY(prof_end(c, 4, pe));
+      k_finalize<<<1, 1024, 0, c.stream>>>(mode, nblk, ti_part, md_part, e_part, ech_part, nullptr, nullptr,
+                                           nullptr, c.R, c.st, 8, sl);
+      SACD_CUDA_TRY(cudaGetLastError());
+    }
+    if (c.comm) SACD_TRY(nccl_allgather_inplace(c, c.xstats, (size_t)slot, 0));
+    int pe = prof_begin(c, 5);
+    k_finalize_global<<<1, 1024, 0, c.stream>>>(mode, c.G, c.R, c.xstats, md.G, c.m[0].G, c.m[1].G, c.m[2].G, c.st,
+                                                32 | 1 | (end_sweep ? 6 : 0));
+    SACD_CUDA_TRY(cudaGetLastError());
+    SACD_TRY(prof_end(c, 5, pe));
+    if (c.comm) SACD_TRY(nccl_broadcast_rows(c, mode));
+    return SACD_OK;
+  }
+
+  static int sharded_initial_fit(Context &c) {
+    SACD_TRY(sharded_mttkrp_merge(c, 2));
+    ModeData &md = c.m[2];
+    constexpr int TR = rows_per_block<RT>();
+    const long long slot = 4 + (long long)c.R * c.R;
+    for (Shard &sh : c.shards) {
+      const long long rlo = sh.plan[2].rlo, rhi = sh.plan[2].rhi;
+      const long long nblk = (rhi - rlo + TR - 1) / TR;
+      double *ti_part = sh.row_part, *md_part = sh.row_part + c.max_row_blocks;
+      long long *e_part = sh.cnt_part, *ech_part = sh.cnt_part + c.max_row_blocks;
+      if (nblk > 0)
+        k_fm_dot<Real, RT><<<(unsigned)nblk, TR, 0, c.stream>>>(rlo, rhi, c.R, md.row_ptr,
+                                                                reinterpret_cast<const Real *>(md.F),
+                                                                reinterpret_cast<const Real *>(sh.M), ti_part,
+                                                                md_part, e_part, ech_part);
+      k_finalize<<<1, 1024, 0, c.stream>>>(2, nblk, ti_part, md_part, e_part, ech_part, nullptr, nullptr, nullptr,
+                                           c.R, c.st, 8, c.xstats + sh.rank * slot);
+    }
+    SACD_CUDA_TRY(cudaGetLastError());
+    if (c.comm) SACD_TRY(nccl_allgather_inplace(c, c.xstats, (size_t)slot, 0));
+    k_finalize_global<<<1, 1024, 0, c.stream>>>(2, c.G, c.R, c.xstats, nullptr, c.m[0].G, c.m[1].G, c.m[2].G, c.st,
+                                                2);
+    SACD_CUDA_TRY(cudaGetLastError());
+    return SACD_OK;
+  }
+
+  // merged MTTKRP of every shard's owned rows into c.M (entry point sacd_mttkrp)
+  static int sharded_mttkrp_api(Context &c, int mode) {
+    const size_t rs = sizeof(Real);
+    const size_t bytes = (size_t)c.m[mode].I * RT * rs;
+    for (Shard &sh : c.shards) SACD_CUDA_TRY(cudaMemsetAsync(sh.M, 0, bytes, c.stream));
+    SACD_TRY(sharded_mttkrp_merge(c, mode));
+    for (Shard &sh : c.shards) {
+      const long long rlo = sh.plan[mode].rlo, rhi = sh.plan[mode].rhi;
+      if (rhi > rlo)
+        SACD_CUDA_TRY(cudaMemcpyAsync(reinterpret_cast<char *>(c.M) + rlo * RT * rs,
+                                      reinterpret_cast<const char *>(sh.M) + rlo * RT * rs, (rhi - rlo) * RT * rs,
+                                      cudaMemcpyDeviceToDevice, c.stream));
     }
     return SACD_OK;
   }
@@ -776,8 +970,8 @@ struct Impl {
     constexpr int TG = gram_tg<GT>();
     constexpr int NB = RT / GT;
     int pe = prof_begin(c, 4);
-    k_gram_partial<Real, RT><<<dim3(c.gram_blocks, NB * (NB + 1) / 2), TG * TG, 0, c.stream>>>(md.I, c.R, reinterpret_cast<const Real *>(md.F),
-                                                                    c.gram_part);
+    k_gram_partial<Real, RT><<<dim3(c.gram_blocks, NB * (NB + 1) / 2), TG * TG, 0, c.stream>>>(
+        0, md.I, c.R, reinterpret_cast<const Real *>(md.F), c.gram_part);
     k_gram_reduce<<<(c.R * c.R + 255) / 256, 256, 0, c.stream>>>(c.R, c.gram_blocks, c.gram_part, md.G);
     SACD_CUDA_TRY(cudaGetLastError());
     return prof_end(c, 4, pe);
@@ -806,7 +1000,7 @@ struct Impl {
     long long *e_part = c.cnt_part, *ech_part = c.cnt_part + c.max_row_blocks;
     int pe = prof_begin(c, 3);
     k_sacd_rows<Real, RT><<<(unsigned)nblk, TR, smem, c.stream>>>(
-        md.I, c.R, mode, c.opt.l_mode, md.row_ptr, M, reinterpret_cast<Real *>(md.F), reinterpret_cast<Real *>(md.Z),
+        0, md.I, c.R, mode, c.opt.l_mode, md.row_ptr, M, reinterpret_cast<Real *>(md.F), reinterpret_cast<Real *>(md.Z),
         reinterpret_cast<const Real *>(c.Hr), c.st, dec, ti_part, md_part, e_part, ech_part);
     SACD_CUDA_TRY(cudaGetLastError());
     SACD_TRY(prof_end(c, 3, pe));
@@ -814,7 +1008,7 @@ struct Impl {
     pe = prof_begin(c, 5);
     const int flags = 1 | (end_sweep ? 6 : 0);
     k_finalize<<<1, 1024, 0, c.stream>>>(mode, nblk, ti_part, md_part, e_part, ech_part, c.m[0].G, c.m[1].G,
-                                         c.m[2].G, c.R, c.st, flags);
+                                         c.m[2].G, c.R, c.st, flags, nullptr);
     SACD_CUDA_TRY(cudaGetLastError());
     return prof_end(c, 5, pe);
   }
@@ -827,10 +1021,10 @@ struct Impl {
     const long long nblk = (md.I + TR - 1) / TR;
     double *ti_part = c.row_part, *md_part = c.row_part + c.max_row_blocks;
     long long *e_part = c.cnt_part, *ech_part = c.cnt_part + c.max_row_blocks;
-    k_fm_dot<Real, RT><<<(unsigned)nblk, TR, 0, c.stream>>>(md.I, c.R, md.row_ptr, reinterpret_cast<const Real *>(md.F), M,
+    k_fm_dot<Real, RT><<<(unsigned)nblk, TR, 0, c.stream>>>(0, md.I, c.R, md.row_ptr, reinterpret_cast<const Real *>(md.F), M,
                                                             ti_part, md_part, e_part, ech_part);
     k_finalize<<<1, 1024, 0, c.stream>>>(2, nblk, ti_part, md_part, e_part, ech_part, c.m[0].G, c.m[1].G, c.m[2].G,
-                                         c.R, c.st, 2);
+                                         c.R, c.st, 2, nullptr);
     SACD_CUDA_TRY(cudaGetLastError());
     return SACD_OK;
   }
@@ -912,6 +1106,49 @@ int launch_mode_update(Context &c, int mode, int branch_override, bool begin_swe
 }
 
 int launch_initial_fit(Context &c) { SACD_DISPATCH(c, I_::initial_fit(c)); }
+
+int launch_sharded_mode_update(Context &c, int mode, int branch_override, bool begin_sweep, bool end_sweep,
+                               uint8_t *decisions_dev) {
+  SACD_DISPATCH(c, I_::sharded_mode_update(c, mode, branch_override, begin_sweep, end_sweep, decisions_dev));
+}
+
+int launch_sharded_mttkrp(Context &c, int mode) { SACD_DISPATCH(c, I_::sharded_mttkrp_api(c, mode)); }
+
+int launch_sharded_initial_fit(Context &c) { SACD_DISPATCH(c, I_::sharded_initial_fit(c)); }
+
+// ------------------------------------------------------------------ NCCL transport
+int nccl_allgather_inplace(Context &c, void *buf, size_t count, int dtype) {
+  const ncclDataType_t t = dtype == 0 ? ncclFloat64 : (dtype == 1 ? ncclFloat32 : ncclInt64);
+  const size_t esz = dtype == 1 ? 4 : 8;
+  const ncclResult_t r = ncclAllGather(reinterpret_cast<char *>(buf) + (size_t)c.me * count * esz, buf, count, t,
+                                       reinterpret_cast<ncclComm_t>(c.comm), c.stream);
+  if (r != ncclSuccess) {
+    set_error(std::string("ncclAllGather: ") + ncclGetErrorString(r));
+    return SACD_ENCCL;
+  }
+  return SACD_OK;
+}
+
+// All-gather-v of the updated factor rows: one in-place broadcast per owner, grouped.
+int nccl_broadcast_rows(Context &c, int mode) {
+  const size_t rs = real_size(c);
+  const ncclDataType_t t = rs == 8 ? ncclFloat64 : ncclFloat32;
+  char *F = reinterpret_cast<char *>(c.m[mode].F);
+  ncclResult_t r = ncclGroupStart();
+  for (int q = 0; q < c.G && r == ncclSuccess; ++q) {
+    const ShardPlan &p = c.all_plans[mode][q];
+    const size_t cnt = (size_t)(p.rhi - p.rlo) * c.pitch;
+    if (cnt == 0) continue;
+    char *ptr = F + (size_t)p.rlo * c.pitch * rs;
+    r = ncclBroadcast(ptr, ptr, cnt, t, q, reinterpret_cast<ncclComm_t>(c.comm), c.stream);
+  }
+  const ncclResult_t r2 = ncclGroupEnd();
+  if (r != ncclSuccess || r2 != ncclSuccess) {
+    set_error(std::string("ncclBroadcast: ") + ncclGetErrorString(r != ncclSuccess ? r : r2));
+    return SACD_ENCCL;
+  }
+  return SACD_OK;
+}
 
 int launch_convert_in(Context &c, const double *src_dev, long long rows, void *dst) {
   if (c.opt.precision == SACD_F64)

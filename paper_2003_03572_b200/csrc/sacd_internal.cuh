@@ -88,6 +88,28 @@ struct ModeData {
   double *G = nullptr;            // fp64 R x R Gram of F
 };
 
+// slice sharding plan of one mode (capi.cu; see sacd_shard_plan in include/sacd.h)
+struct ShardPlan {
+  long long lo = 0, hi = 0, rlo = 0, rhi = 0, head = -1;
+};
+
+// One rank's share of the sharded engine: its nonzero ranges, MTTKRP work
+// items over them, and its private scratch.  A process holds one shard (NCCL) or all of
+// them (emulated ranks on one GPU).
+struct Shard {
+  int rank = 0;
+  ShardPlan plan[3];
+  WorkItem *items[3] = {nullptr, nullptr, nullptr};
+  long long n_items[3] = {0, 0, 0};
+  SplitRow *splits[3] = {nullptr, nullptr, nullptr};
+  long long n_splits[3] = {0, 0, 0};
+  void *M = nullptr;             // Real [maxI * pitch]
+  void *partial = nullptr;       // Real [slots * pitch]
+  double *row_part = nullptr;    // 2 * max row blocks
+  long long *cnt_part = nullptr; // 2 * max row blocks
+  double *gram_part = nullptr;   // gram blocks * R * R
+};
+
 struct Context {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -120,15 +142,20 @@ struct Context {
   size_t ev_next = 0;
   double prof_ms[SACD_NUM_KCLASS]{};
   long long prof_n[SACD_NUM_KCLASS]{};
-  bool world_multi = false;
+  // sharded engine (world > 1, forced, or emulated ranks)
+  bool sharded = false;
+  int G = 1;                      // total ranks
+  int world = 1, me = 0;          // NCCL process group
+  void *comm = nullptr;           // ncclComm_t
+  std::vector<ShardPlan> all_plans[3];
+  std::vector<Shard> shards;
+  long long *xid = nullptr;       // [G] head row ids
+  void *xrow = nullptr;           // [G * pitch] head partial rows (Real)
+  double *xstats = nullptr;       // [G * (4 + R*R)] (ti, md, E, Ech, Gram partial)
 };
 
 size_t real_size(const Context &c);
 
-// slice sharding plan of one mode (capi.cu; see sacd_shard_plan in include/sacd.h)
-struct ShardPlan {
-  long long lo = 0, hi = 0, rlo = 0, rhi = 0, head = -1;
-};
 ShardPlan plan_shard(const long long *row_ptr, long long I, int world, int rank);
 
 // layout.cu
@@ -145,6 +172,12 @@ int launch_convert_in(Context &c, const double *src_dev, long long rows, void *d
 int launch_convert_out(Context &c, const void *src, long long rows, double *dst_dev);
 int launch_hessian_only(Context &c, int mode);
 int launch_setup(Context &c);
+int launch_sharded_mode_update(Context &c, int mode, int branch_override, bool begin_sweep, bool end_sweep,
+                               uint8_t *decisions_dev);
+int launch_sharded_mttkrp(Context &c, int mode);   // merged M of the owned rows -> c.M
+int launch_sharded_initial_fit(Context &c);
+int nccl_allgather_inplace(Context &c, void *buf, size_t count_per_rank, int dtype);  // dtype 0 f64, 1 f32, 2 i64
+int nccl_broadcast_rows(Context &c, int mode);
 long long rows_block_for(const Context &c);
 
 // profiling helpers (kernels.cu uses them around launches)

@@ -37,7 +37,8 @@ class Options(C.Structure):
     _fields_ = [("struct_size", C.c_uint32), ("precision", C.c_int32), ("l_mode", C.c_int32),
                 ("variant", C.c_int32), ("device", C.c_int32), ("world_size", C.c_int32), ("rank", C.c_int32),
                 ("nccl_unique_id", C.c_void_p), ("stream", C.c_void_p), ("use_graph", C.c_int32),
-                ("profile", C.c_int32), ("nnz_per_item", C.c_int32), ("reserved", C.c_int32 * 7)]
+                ("profile", C.c_int32), ("nnz_per_item", C.c_int32), ("mttkrp_variant", C.c_int32),
+                ("force_sharded", C.c_int32), ("emulate_ranks", C.c_int32), ("reserved", C.c_int32 * 4)]
 
 
 class IterStats(C.Structure):
@@ -121,6 +122,13 @@ def _np(a, dtype):
     return np.ascontiguousarray(a, dtype=dtype)
 
 
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id (call on rank 0, broadcast to the others)."""
+    buf = C.create_string_buffer(128)
+    _check(load_library().sacd_nccl_unique_id(buf))
+    return buf.raw
+
+
 def shard_plan(row_ptr, world, rank):
     """sacd_shard_plan: (lo, hi, rlo, rhi, head) of `rank` for one mode's row_ptr."""
     rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
@@ -133,7 +141,8 @@ class Sacd:
     """One SaCD factorisation context on one GPU (see include/sacd.h)."""
 
     def __init__(self, coords, vals, dims, rank, seed, *, precision="f64", l_mode="diag", variant="gs",
-                 device=-1, stream=None, use_graph=True, profile=False, nnz_per_item=0, mttkrp_variant=0):
+                 device=-1, stream=None, use_graph=True, profile=False, nnz_per_item=0, mttkrp_variant=0,
+                 world_size=1, world_rank=0, nccl_id=None, force_sharded=False, emulate_ranks=0):
         L = load_library()
         o = Options()
         L.sacd_default_options(C.byref(o))
@@ -145,7 +154,15 @@ class Sacd:
         o.use_graph = int(bool(use_graph))
         o.profile = int(bool(profile))
         o.nnz_per_item = int(nnz_per_item)
-        o.reserved[0] = int(mttkrp_variant)
+        o.mttkrp_variant = int(mttkrp_variant)
+        o.world_size = int(world_size)
+        o.rank = int(world_rank)
+        o.force_sharded = int(bool(force_sharded))
+        o.emulate_ranks = int(emulate_ranks)
+        self._nccl_id = None
+        if nccl_id is not None:
+            self._nccl_id = C.create_string_buffer(bytes(nccl_id), 128)
+            o.nccl_unique_id = C.cast(self._nccl_id, C.c_void_p)
         if not hasattr(coords, "data_ptr"):
             coords = _np(np.asarray(coords).reshape(-1, 3), np.uint32)
         if not hasattr(vals, "data_ptr"):

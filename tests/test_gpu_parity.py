@@ -355,3 +355,55 @@ def test_c4_full_size_sampled_rows_and_properties():
             assert factor_err(g.factors(n)[rows], Fn) <= 1e-9
             Zg = g.get_zprev(n)[rows]
             assert np.abs(Zg - zp).max() <= 1e-9 * max(1.0, np.abs(zp).max())
+
+
+# ----------------------------------------------------------------------------- sharded engine
+@pytest.mark.parametrize("G", [2, 3, 8])
+@pytest.mark.parametrize("R", [5, 64])
+def test_sharded_emulated_ranks_end_to_end(G, R):
+    """SURVEY 8(e) on one GPU: G ranks of the sharded engine emulated in one context (the
+    exchanges become local), with heavy slices cut by the rank boundaries: same decisions,
+    branch and E as the oracle, f and factors within the north-star tolerances."""
+    dims = (300, 200, 50)
+    c, v = ragged_tensor(dims, 20000, 8, heavy_rows=((2, 1, 3000), (0, 5, 900), (1, 199, 1500)))
+    fg, Fg, Eg, brg, ora = run_pair(c, v, dims, R, 17, 10, nnz_per_item=256, emulate_ranks=G)
+    check_pair(fg, Fg, Eg, brg, ora)
+    assert np.array_equal(Eg, ora["E"])
+
+
+@pytest.mark.parametrize("G", [2, 5])
+def test_sharded_emulated_teacher_forced(G):
+    dims, R = (60, 45, 33), 16
+    c, v = ragged_tensor(dims, 5000, 21, heavy_rows=((1, 4, 1500), (0, 59, 800)))
+    F = O.init_factors(dims, R, 9)
+    with S(c, v, dims, R, 9, nnz_per_item=64, emulate_ranks=G) as g:
+        for n in range(3):
+            assert np.abs(g.mttkrp(n) - O.mttkrp(c, v, dims, n, F)).max() <= 1e-12 * max(
+                1.0, np.abs(O.mttkrp(c, v, dims, n, F)).max())
+            out = g.mode_update(n, branch=0, decisions=True)
+            M = O.mttkrp(c, v, dims, n, F)
+            H = O.mode_hessian(F, dims, n)
+            Fn, zp, ti, E, Ech, md, dec = O.mode_pass(M, H, F[n], np.zeros_like(F[n]), 0, decisions=True)
+            assert np.array_equal(out["decisions"], dec) and out["E"] == E
+            assert factor_err(g.factors(n), Fn) <= 1e-9
+            assert abs(out["ti"] - ti) <= 1e-9 * max(1.0, abs(ti))
+            F[n] = Fn
+            g.set_factors(n, Fn)
+
+
+def test_sharded_nccl_world1_matches_unsharded():
+    """The real NCCL transport (all-gathers, grouped broadcasts) with a one-rank
+    communicator: identical decisions and E to the unsharded engine, f to 1e-12."""
+    cfg = SI.CONFIGS["c1"]
+    c, v = SI.make_tensor(cfg)
+    c, v = c.numpy(), v.numpy()
+    out = []
+    for forced in (False, True):
+        with S(c, v, cfg.dims, cfg.rank, cfg.seed, force_sharded=forced) as g:
+            g.iterate(6)
+            st = g.stats()
+            out.append((np.array([s["objective"] for s in st]), np.array([s["E"] for s in st]), g.factors()))
+    np.testing.assert_allclose(out[1][0], out[0][0], rtol=1e-12)
+    assert np.array_equal(out[1][1], out[0][1])
+    for n in range(3):
+        assert factor_err(out[1][2][n], out[0][2][n]) <= 1e-10
