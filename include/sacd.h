@@ -108,6 +108,8 @@ typedef struct {
   int64_t items[3]; /* MTTKRP work items per mode                                            */
   int64_t split_rows[3];
   int64_t device_bytes;
+  int32_t kernels_per_sweep; /* libsacd kernels launched per sweep (from the captured graph)   */
+  int32_t world_size, world_rank, sharded_ranks; /* sharded engine: G ranks (1 = unsharded)    */
 } sacd_info;
 
 void sacd_default_options(sacd_options *opt);

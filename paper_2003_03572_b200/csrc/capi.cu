@@ -155,6 +155,8 @@ static int upload(T **dst, const std::vector<T> &v) {
   return SACD_OK;
 }
 
+// Capture one sweep as a CUDA graph (replayed by sacd_iterate unless profiling), and count
+// the libsacd kernels it launches (NCCL's own kernels excluded).
 static int capture_graph(Context &c) {
   if (c.graph_exec) {
     cudaGraphExecDestroy(c.graph_exec);
@@ -164,12 +166,14 @@ static int capture_graph(Context &c) {
     cudaGraphDestroy(c.graph);
     c.graph = nullptr;
   }
-  if (!c.opt.use_graph || c.opt.profile) return SACD_OK;
+  const int saved_profile = c.opt.profile;
+  c.opt.profile = 0;
   SACD_CUDA_TRY(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
   int rc = SACD_OK;
   for (int n = 0; n < 3 && rc == SACD_OK; ++n)
     rc = c.sharded ? launch_sharded_mode_update(c, n, SACD_BR_AUTO, n == 0, n == 2, nullptr)
                    : launch_mode_update(c, n, SACD_BR_AUTO, n == 0, n == 2, nullptr);
+  c.opt.profile = saved_profile;
   cudaGraph_t g = nullptr;
   cudaError_t e = cudaStreamEndCapture(c.stream, &g);
   if (rc != SACD_OK) {
@@ -177,6 +181,25 @@ static int capture_graph(Context &c) {
     return rc;
   }
   SACD_CUDA_TRY(e);
+  size_t nn = 0;
+  SACD_CUDA_TRY(cudaGraphGetNodes(g, nullptr, &nn));
+  std::vector<cudaGraphNode_t> nodes(nn);
+  if (nn) SACD_CUDA_TRY(cudaGraphGetNodes(g, nodes.data(), &nn));
+  c.kernels_per_sweep = 0;
+  for (auto nd : nodes) {
+    cudaGraphNodeType t;
+    if (cudaGraphNodeGetType(nd, &t) != cudaSuccess || t != cudaGraphNodeTypeKernel) continue;
+    cudaKernelNodeParams kp;
+    const char *name = nullptr;
+    if (cudaGraphKernelNodeGetParams(nd, &kp) == cudaSuccess && cudaFuncGetName(&name, kp.func) == cudaSuccess &&
+        name && strstr(name, "sacd"))
+      c.kernels_per_sweep += 1;
+  }
+  cudaGetLastError();
+  if (!c.opt.use_graph || c.opt.profile) {
+    cudaGraphDestroy(g);
+    return SACD_OK;
+  }
   c.graph = g;
   SACD_CUDA_TRY(cudaGraphInstantiate(&c.graph_exec, c.graph, 0));
   return SACD_OK;
@@ -808,6 +831,10 @@ int sacd_get_info(sacd_ctx *c, sacd_info *o) {
   o->l_mode = c->opt.l_mode;
   o->variant = c->opt.variant;
   o->device_bytes = c->device_bytes;
+  o->kernels_per_sweep = c->kernels_per_sweep;
+  o->world_size = c->world;
+  o->world_rank = c->me;
+  o->sharded_ranks = c->sharded ? c->G : 1;
   int k = 0;
   int rc = dev_read(c, &k, reinterpret_cast<const char *>(c->st) + offsetof(DevState, k), sizeof(int));
   if (rc == SACD_OK)

@@ -136,6 +136,7 @@ struct Context {
   // graph
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t graph_exec = nullptr;
+  int kernels_per_sweep = 0;
   // profiling
   std::vector<cudaEvent_t> ev_pool;
   std::vector<std::pair<int, int>> ev_pending;  // (class, pool index of start)

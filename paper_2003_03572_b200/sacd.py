@@ -50,7 +50,9 @@ class Info(C.Structure):
     _fields_ = [("dims", C.c_int64 * 3), ("nnz", C.c_int64), ("rank", C.c_int32), ("pitch", C.c_int32),
                 ("precision", C.c_int32), ("l_mode", C.c_int32), ("variant", C.c_int32), ("k", C.c_int32),
                 ("mode_a", C.c_int32 * 3), ("mode_b", C.c_int32 * 3), ("xnorm2", C.c_double),
-                ("items", C.c_int64 * 3), ("split_rows", C.c_int64 * 3), ("device_bytes", C.c_int64)]
+                ("items", C.c_int64 * 3), ("split_rows", C.c_int64 * 3), ("device_bytes", C.c_int64),
+                ("kernels_per_sweep", C.c_int32), ("world_size", C.c_int32), ("world_rank", C.c_int32),
+                ("sharded_ranks", C.c_int32)]
 
 
 class SacdError(RuntimeError):
@@ -233,7 +235,8 @@ class Sacd:
         return dict(dims=list(i.dims), nnz=i.nnz, rank=i.rank, pitch=i.pitch, precision=i.precision,
                     l_mode=i.l_mode, variant=i.variant, k=i.k, mode_a=list(i.mode_a), mode_b=list(i.mode_b),
                     xnorm2=i.xnorm2, items=list(i.items), split_rows=list(i.split_rows),
-                    device_bytes=i.device_bytes)
+                    device_bytes=i.device_bytes, kernels_per_sweep=i.kernels_per_sweep,
+                    world_size=i.world_size, world_rank=i.world_rank, sharded_ranks=i.sharded_ranks)
 
     # -- component entry points
     def set_factors(self, mode, F):
