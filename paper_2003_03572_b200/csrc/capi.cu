@@ -374,7 +374,7 @@ static int init_impl(Context *c, const uint32_t *coords, const float *vals, uint
         c->m[n].n_items += sh.n_items[n];
         c->m[n].n_splits += sh.n_splits[n];
       }
-      SACD_CUDA_TRY(cudaMalloc(&sh.M, (size_t)maxI * c->pitch * rs));
+      SACD_CUDA_TRY(cudaMalloc(&sh.M, (size_t)((maxI + 31) / 32 * 32) * c->pitch * rs));
       SACD_CUDA_TRY(cudaMalloc(&sh.partial, (size_t)slots_k * c->pitch * rs));
       c->device_bytes += (long long)((size_t)maxI * c->pitch * rs + (size_t)slots_k * c->pitch * rs);
     }
@@ -408,14 +408,15 @@ static int init_impl(Context *c, const uint32_t *coords, const float *vals, uint
   for (int n = 0; n < 3; ++n) {
     ModeData &md = c->m[n];
     SACD_CUDA_TRY(cudaMalloc(&md.F, (size_t)md.I * P * rs));
-    SACD_CUDA_TRY(cudaMalloc(&md.Z, (size_t)md.I * P * rs));
-    SACD_CUDA_TRY(cudaMemsetAsync(md.Z, 0, (size_t)md.I * P * rs, s));
+    const size_t zrows = (size_t)((md.I + 31) / 32 * 32);
+    SACD_CUDA_TRY(cudaMalloc(&md.Z, zrows * P * rs));
+    SACD_CUDA_TRY(cudaMemsetAsync(md.Z, 0, zrows * P * rs, s));
     SACD_CUDA_TRY(cudaMalloc(&md.G, (size_t)R * R * 8));
     c->device_bytes += (long long)(2 * (size_t)md.I * P * rs + (size_t)R * R * 8);
   }
   c->max_row_blocks = (maxI + 31) / 32 + 1;  // >= ceil(I / rows_per_block) for every pitch
   c->gram_blocks = (int)std::min<long long>(296, std::max<long long>(1, (maxI + 63) / 64));
-  SACD_CUDA_TRY(cudaMalloc(&c->M, (size_t)maxI * P * rs));
+  SACD_CUDA_TRY(cudaMalloc(&c->M, (size_t)((maxI + 31) / 32 * 32) * P * rs));
   SACD_CUDA_TRY(cudaMalloc(&c->partial, (size_t)max_slots * P * rs));
   SACD_CUDA_TRY(cudaMalloc(&c->Hr, (size_t)P * P * rs));
   SACD_CUDA_TRY(cudaMalloc(&c->Hd, (size_t)R * R * 8));
@@ -453,11 +454,11 @@ static int dev_read(Context *c, T *dst, const void *src, size_t bytes) {
 }
 
 // factor-like matrix (Real, pitch) -> host fp64 with leading dimension ld
-static int read_matrix(Context *c, const void *src, long long rows, double *out, long long ld) {
+static int read_matrix(Context *c, const void *src, long long rows, double *out, long long ld, bool ttl = false) {
   double *tmp = nullptr;
   cudaStream_t s = c->stream;
   SACD_CUDA_TRY(cudaMallocAsync(&tmp, (size_t)std::max(1LL, rows) * c->R * 8, s));
-  int rc = launch_convert_out(*c, src, rows, tmp);
+  int rc = launch_convert_out(*c, src, rows, tmp, ttl);
   if (rc == SACD_OK) {
     cudaError_t e = cudaMemcpy2DAsync(out, (size_t)ld * 8, tmp, (size_t)c->R * 8, (size_t)c->R * 8, (size_t)rows,
                                       cudaMemcpyDeviceToHost, s);
@@ -471,7 +472,7 @@ static int read_matrix(Context *c, const void *src, long long rows, double *out,
   return rc;
 }
 
-static int write_matrix(Context *c, void *dst, long long rows, const double *in, long long ld) {
+static int write_matrix(Context *c, void *dst, long long rows, const double *in, long long ld, bool ttl = false) {
   double *tmp = nullptr;
   cudaStream_t s = c->stream;
   SACD_CUDA_TRY(cudaMallocAsync(&tmp, (size_t)std::max(1LL, rows) * c->R * 8, s));
@@ -481,7 +482,7 @@ static int write_matrix(Context *c, void *dst, long long rows, const double *in,
     set_error(std::string("write_matrix: ") + cudaGetErrorString(e));
     return SACD_ECUDA;
   }
-  int rc = launch_convert_in(*c, tmp, rows, dst);
+  int rc = launch_convert_in(*c, tmp, rows, dst, ttl);
   cudaFreeAsync(tmp, s);
   if (rc == SACD_OK) {
     e = cudaStreamSynchronize(s);
@@ -656,7 +657,7 @@ int sacd_get_zprev(sacd_ctx *c, int32_t mode, double *out, int64_t ld) {
     set_error("sacd_get_zprev: bad mode/ld/out");
     return SACD_ESTATE;
   }
-  return sticky(c, read_matrix(c, c->m[mode].Z, c->m[mode].I, out, ld));
+  return sticky(c, read_matrix(c, c->m[mode].Z, c->m[mode].I, out, ld, true));
 }
 
 int sacd_set_zprev(sacd_ctx *c, int32_t mode, const double *in, int64_t ld) {
@@ -665,7 +666,7 @@ int sacd_set_zprev(sacd_ctx *c, int32_t mode, const double *in, int64_t ld) {
     set_error("sacd_set_zprev: bad mode/ld/in");
     return SACD_ESTATE;
   }
-  return sticky(c, write_matrix(c, c->m[mode].Z, c->m[mode].I, in, ld));
+  return sticky(c, write_matrix(c, c->m[mode].Z, c->m[mode].I, in, ld, true));
 }
 
 int sacd_set_factors(sacd_ctx *c, int32_t mode, const double *in, int64_t ld) {
@@ -687,13 +688,14 @@ int sacd_mttkrp(sacd_ctx *c, int32_t mode, double *out, int64_t ld) {
     return SACD_ESTATE;
   }
   // empty slices are not written by the MTTKRP kernel: clear M first for this entry point
-  cudaError_t e = cudaMemsetAsync(c->M, 0, (size_t)c->m[mode].I * c->pitch * real_size(*c), c->stream);
+  cudaError_t e =
+      cudaMemsetAsync(c->M, 0, (size_t)((c->m[mode].I + 31) / 32 * 32) * c->pitch * real_size(*c), c->stream);
   if (e != cudaSuccess) {
     set_error(std::string("sacd_mttkrp: ") + cudaGetErrorString(e));
     return sticky(c, SACD_ECUDA);
   }
   int rc = c->sharded ? launch_sharded_mttkrp(*c, mode) : launch_mttkrp(*c, mode, c->M);
-  if (rc == SACD_OK) rc = read_matrix(c, c->M, c->m[mode].I, out, ld);
+  if (rc == SACD_OK) rc = read_matrix(c, c->M, c->m[mode].I, out, ld, true);
   return sticky(c, rc);
 }
 

@@ -25,6 +25,13 @@ namespace sacd {
 namespace {
 
 // ------------------------------------------------------------------ small helpers
+inline int grid1d(long long n, int block = 256) {
+  long long g = (n + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > 148 * 32) g = 148 * 32;
+  return (int)g;
+}
+
 template <typename Real>
 struct V16;
 template <>
@@ -59,6 +66,14 @@ __device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
   z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
   return z ^ (z >> 31);
+}
+
+// M (the MTTKRP result) and Z (z_prev) are stored "TT": 32-row tiles, column-major inside a
+// tile, so the thread-per-row update reads and writes them as contiguous 256-byte warp
+// accesses.  Element (i, c) of a matrix with row pitch RT lives at tt(i, c).
+template <int RT>
+__host__ __device__ __forceinline__ long long tt(long long i, int c) {
+  return (i >> 5) * (32LL * RT) + (long long)c * 32 + (i & 31);
 }
 
 template <int RT>
@@ -153,10 +168,16 @@ __global__ void __launch_bounds__(256) k_mttkrp(const WorkItem *__restrict__ ite
 #pragma unroll
         for (int c = 0; c < VEC; ++c) acc[v][c] += __shfl_xor_sync(0xffffffffu, acc[v][c], off);
     if (grp == 0) {
-      Real *dst = (it.slot >= 0) ? partial + it.slot * RT : M + (long long)row * RT;
-      VT *dv = reinterpret_cast<VT *>(dst);
+      if (it.slot >= 0) {
+        VT *dv = reinterpret_cast<VT *>(partial + it.slot * RT);
 #pragma unroll
-      for (int v = 0; v < VPL; ++v) dv[sub + v * LPN] = VV::make(acc[v]);
+        for (int v = 0; v < VPL; ++v) dv[sub + v * LPN] = VV::make(acc[v]);
+      } else {
+#pragma unroll
+        for (int v = 0; v < VPL; ++v)
+#pragma unroll
+          for (int c = 0; c < VEC; ++c) M[tt<RT>(row, (sub + v * LPN) * VEC + c)] = acc[v][c];
+      }
     }
   }
 }
@@ -173,6 +194,13 @@ __global__ void __launch_bounds__(256) k_mttkrp(const WorkItem *__restrict__ ite
 //  * Rows are flushed to M[row] when a row starts; empty rows are never touched (the row
 //    update reads row_ptr and uses m = 0 for them).  Split items (slot >= 0) hold a segment
 //    of one heavy row and flush to their partial slot.
+// Default occupancy target of k_mttkrp_fiber (measured on B200 with tools/mttkrp_tune.py:
+// the kernel is latency-bound, so the most resident warps that fit without spilling win).
+template <typename Real, int RT>
+__host__ __device__ constexpr int fiber_min_blocks() {
+  return (RT / 32) * sizeof(Real) <= 8 ? 7 : ((RT / 32) * sizeof(Real) <= 16 ? 6 : ((RT / 32) * sizeof(Real) <= 32 ? 4 : 2));
+}
+
 template <typename Real, int E>
 struct LaneRow {
   Real v[E];
@@ -223,21 +251,24 @@ __global__ void __launch_bounds__(256, MINB) k_mttkrp_fiber(const WorkItem *__re
   if (it.nz0 >= it.nz1) return;
   const Real *Al = A + lane * E;
   const Real *Bl = B + lane * E;
-  Real *Ml = M + lane * E;
   LaneRow<Real, E> arow;
   Real acc[E], facc[E];
 #pragma unroll
   for (int k = 0; k < E; ++k) acc[k] = facc[k] = arow.v[k] = Real(0);
   long long cur_row = -1;
   auto flush = [&]() {
-    LaneRow<Real, E> o;
+    if (it.slot >= 0) {
+      LaneRow<Real, E> o;
 #pragma unroll
-    for (int k = 0; k < E; ++k) {
-      o.v[k] = acc[k];
-      acc[k] = Real(0);
+      for (int k = 0; k < E; ++k) o.v[k] = acc[k];
+      o.store(partial + it.slot * RT + lane * E);
+    } else if (cur_row >= 0) {
+      Real *dst = M + (cur_row >> 5) * (32LL * RT) + (cur_row & 31) + lane * (E * 32);  // TT layout
+#pragma unroll
+      for (int k = 0; k < E; ++k) dst[k * 32] = acc[k];
     }
-    if (it.slot >= 0) o.store(partial + it.slot * RT + lane * E);
-    else if (cur_row >= 0) o.store(Ml + cur_row * RT);
+#pragma unroll
+    for (int k = 0; k < E; ++k) acc[k] = Real(0);
   };
   auto step = [&](uint32_t fa, float xf, const LaneRow<Real, E> &b, uint32_t my_n, int j) {
     if (fa & kFiberStart) {
@@ -320,7 +351,7 @@ __global__ void __launch_bounds__(256) k_fixup(const SplitRow *__restrict__ spli
     Real s = red[0][c];
 #pragma unroll
     for (int k = 1; k < 8; ++k) s += red[k][c];
-    M[(long long)sr.row * RT + c] = s;
+    M[tt<RT>(sr.row, c)] = s;
   }
 }
 
@@ -404,9 +435,9 @@ __global__ void __launch_bounds__(rows_per_block<RT>())
   if (tid < nrows) {
     const long long row = row0 + tid;
     Real *u = Us + tid * US;
-    const Real *m = M + row * RT;
+    const Real *m = M + tt<RT>(row, 0);                    // TT layout: column c at m[32 c]
     const bool empty = row_ptr[row] == row_ptr[row + 1];  // M is not written for empty slices: m = 0
-    Real *zp = Z + row * RT;
+    Real *zp = Z + tt<RT>(row, 0);
     for (int c0 = 0; c0 < R; c0 += C) {
       // (1) out-of-block part of the gradient with the current row (columns < c0 already
       //     updated), Eq 14:  acc_q = sum_{j not in block} u_j h_(j, c0+q)   (H symmetric)
@@ -430,9 +461,9 @@ __global__ void __launch_bounds__(rows_per_block<RT>())
       for (int j = c0 + C; j < R; ++j) accumulate(j);
       Real mv[C], zv[C], ub[C];
 #pragma unroll
-      for (int x = 0; x < C / VEC; ++x) {
-        VV::get(reinterpret_cast<const VT *>(m + c0)[x], mv + x * VEC);
-        VV::get(reinterpret_cast<const VT *>(zp + c0)[x], zv + x * VEC);
+      for (int q = 0; q < C; ++q) {
+        mv[q] = m[32 * (c0 + q)];
+        zv[q] = zp[32 * (c0 + q)];
       }
 #pragma unroll
       for (int q = 0; q < C; ++q) ub[q] = u[c0 + q];
@@ -479,7 +510,7 @@ __global__ void __launch_bounds__(rows_per_block<RT>())
 #pragma unroll
       for (int q = 0; q < C; ++q) u[c0 + q] = ub[q];
 #pragma unroll
-      for (int x = 0; x < C / VEC; ++x) reinterpret_cast<VT *>(zp + c0)[x] = VV::make(zv + x * VEC);
+      for (int q = 0; q < C; ++q) zp[32 * (c0 + q)] = zv[q];
     }
   }
   __syncthreads();
@@ -530,7 +561,7 @@ __global__ void k_fm_dot(long long row_begin, long long row_end, int R, const lo
   const long long row = row_begin + (long long)blockIdx.x * TR + threadIdx.x;
   double s = 0.0;
   if (row < row_end && row_ptr[row] != row_ptr[row + 1])
-    for (int r = 0; r < R; ++r) s += (double)F[row * RT + r] * (double)M[row * RT + r];
+    for (int r = 0; r < R; ++r) s += (double)F[row * RT + r] * (double)M[tt<RT>(row, r)];
   red[threadIdx.x] = s;
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -556,13 +587,16 @@ template <typename Real, int RT>
 __global__ void __launch_bounds__(gram_tg<gram_gt<RT>()>() * gram_tg<gram_gt<RT>()>())
     k_gram_partial(long long row_begin, long long row_end, int R, const Real *__restrict__ F,
                    double *__restrict__ part) {
+  // Thread (ty, tx) of a TG x TG grid owns entries (bi*GT + ty + TG*a, bj*GT + tx + TG*b),
+  // a, b < T: for a fixed staged row the warp reads TG consecutive values (conflict-free)
+  // and a few broadcast ones.  A diagonal panel pair also computes its lower half
+  // (redundant); the reduce reads the (min, max) entry.
   constexpr int GT = gram_gt<RT>();
   constexpr int TG = gram_tg<GT>();
   constexpr int T = GT / TG;
   constexpr int CH = GT >= 128 ? 16 : 32;
   __shared__ double Fa[CH][GT + 1];
   __shared__ double Fb[CH][GT + 1];
-  // panel pair from blockIdx.y (row-major over the upper triangle of NB x NB panels)
   constexpr int NB = RT / GT;
   int bi = 0, bj = 0;
   {
@@ -578,7 +612,6 @@ __global__ void __launch_bounds__(gram_tg<gram_gt<RT>()>() * gram_tg<gram_gt<RT>
   }
   const int tid = threadIdx.x;
   const int ty = tid / TG, tx = tid % TG;
-  const bool active = (bi != bj) || (ty <= tx);
   const long long per = (row_end - row_begin + gridDim.x - 1) / gridDim.x;
   const long long i0 = row_begin + (long long)blockIdx.x * per;
   const long long i1 = min(row_end, i0 + per);
@@ -596,30 +629,26 @@ __global__ void __launch_bounds__(gram_tg<gram_gt<RT>()>() * gram_tg<gram_gt<RT>
       Fb[k][col] = (double)F[(c0 + k) * RT + bj * GT + col];
     }
     __syncthreads();
-    if (active) {
-      for (int k = 0; k < nr; ++k) {
-        double av[T], bv[T];
+    for (int k = 0; k < nr; ++k) {
+      double av[T], bv[T];
 #pragma unroll
-        for (int a = 0; a < T; ++a) av[a] = Fa[k][ty * T + a];
+      for (int a = 0; a < T; ++a) av[a] = Fa[k][ty + TG * a];
 #pragma unroll
-        for (int b = 0; b < T; ++b) bv[b] = Fb[k][tx * T + b];
+      for (int b = 0; b < T; ++b) bv[b] = Fb[k][tx + TG * b];
 #pragma unroll
-        for (int a = 0; a < T; ++a)
+      for (int a = 0; a < T; ++a)
 #pragma unroll
-          for (int b = 0; b < T; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
-      }
+        for (int b = 0; b < T; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
     }
   }
-  if (active) {
-    double *p = part + (long long)blockIdx.x * R * R;
+  double *p = part + (long long)blockIdx.x * R * R;
 #pragma unroll
-    for (int a = 0; a < T; ++a)
+  for (int a = 0; a < T; ++a)
 #pragma unroll
-      for (int b = 0; b < T; ++b) {
-        const int r = bi * GT + ty * T + a, t = bj * GT + tx * T + b;
-        if (r < R && t < R) p[r * R + t] = acc[a][b];
-      }
-  }
+    for (int b = 0; b < T; ++b) {
+      const int r = bi * GT + ty + TG * a, t = bj * GT + tx + TG * b;
+      if (r < R && t < R) p[r * R + t] = acc[a][b];
+    }
 }
 
 // G[r][t] = sum over blocks (in order) of the upper-triangle partial; mirrored exactly.
@@ -628,7 +657,7 @@ __global__ void k_gram_reduce(int R, int nblk, const double *__restrict__ part, 
   if (x >= R * R) return;
   const int r = x / R, t = x % R;
   const int src = (r <= t) ? (r * R + t) : (t * R + r);
-  // (an entry with r <= t lies in tile (r/T, t/T), which has ty <= tx, so it was written)
+  // (an entry with r <= t lies in panel pair (r/GT, t/GT) with bi <= bj, which wrote it)
   double s = 0.0;
   for (int b = 0; b < nblk; ++b) s += part[(long long)b * R * R + src];
   G[x] = s;
@@ -726,8 +755,18 @@ __global__ void __launch_bounds__(1024) k_finalize(int mode, long long nblk, con
 template <typename Real, int RT>
 __global__ void k_pack_head(long long head, const Real *__restrict__ M, long long *__restrict__ id_slot,
                             Real *__restrict__ row_slot) {
-  for (int c = threadIdx.x; c < RT; c += blockDim.x) row_slot[c] = head >= 0 ? M[head * RT + c] : Real(0);
+  for (int c = threadIdx.x; c < RT; c += blockDim.x) row_slot[c] = head >= 0 ? M[tt<RT>(head, c)] : Real(0);
   if (threadIdx.x == 0) *id_slot = head;
+}
+
+template <typename Real, int RT>
+__global__ void k_copy_rows_tt(long long rlo, long long rhi, const Real *__restrict__ src, Real *__restrict__ dst) {
+  for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < (rhi - rlo) * RT;
+       x += (long long)gridDim.x * blockDim.x) {
+    const long long i = rlo + x / RT;
+    const int c = (int)(x % RT);
+    dst[tt<RT>(i, c)] = src[tt<RT>(i, c)];
+  }
 }
 
 // The owner adds the head partials of the other ranks to its rows, in rank order.
@@ -737,7 +776,7 @@ __global__ void k_merge_heads(int G, long long rlo, long long rhi, const long lo
   for (int q = 0; q < G; ++q) {
     const long long id = ids[q];
     if (id >= rlo && id < rhi)
-      for (int c = threadIdx.x; c < RT; c += blockDim.x) M[id * RT + c] += rows[(long long)q * RT + c];
+      for (int c = threadIdx.x; c < RT; c += blockDim.x) M[tt<RT>(id, c)] += rows[(long long)q * RT + c];
   }
 }
 
@@ -778,32 +817,33 @@ __global__ void __launch_bounds__(1024) k_finalize_global(int mode, int G, int R
   }
 }
 
+// host-order fp64 (rows x R) <-> device Real (row-major with pitch RT, or TT tiles)
+__device__ __forceinline__ long long dev_index(long long i, int r, int RT, bool ttl) {
+  return ttl ? (i >> 5) * (32LL * RT) + (long long)r * 32 + (i & 31) : i * RT + r;
+}
+
 template <typename Real>
-__global__ void k_convert_in(const double *__restrict__ src, long long rows, int R, int RT, Real *__restrict__ dst) {
+__global__ void k_convert_in(const double *__restrict__ src, long long rows, int R, int RT, Real *__restrict__ dst,
+                             bool ttl) {
   for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < rows * RT;
        x += (long long)gridDim.x * blockDim.x) {
     const long long i = x / RT;
     const int r = (int)(x - i * RT);
-    dst[x] = r < R ? (Real)src[i * R + r] : Real(0);
+    dst[dev_index(i, r, RT, ttl)] = r < R ? (Real)src[i * R + r] : Real(0);
   }
 }
 
 template <typename Real>
-__global__ void k_convert_out(const Real *__restrict__ src, long long rows, int R, int RT, double *__restrict__ dst) {
+__global__ void k_convert_out(const Real *__restrict__ src, long long rows, int R, int RT, double *__restrict__ dst,
+                              bool ttl) {
   for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < rows * R;
        x += (long long)gridDim.x * blockDim.x) {
     const long long i = x / R;
     const int r = (int)(x - i * R);
-    dst[x] = (double)src[i * RT + r];
+    dst[x] = (double)src[dev_index(i, r, RT, ttl)];
   }
 }
 
-inline int grid1d(long long n, int block = 256) {
-  long long g = (n + block - 1) / block;
-  if (g < 1) g = 1;
-  if (g > 148 * 32) g = 148 * 32;
-  return (int)g;
-}
 
 // ------------------------------------------------------------------ launch implementations
 template <typename Real, int RT>
@@ -836,8 +876,8 @@ struct Impl {
         else if (var == 2) go(k_mttkrp_fiber<Real, RT, 2, 4>);
         else if (var == 3) go(k_mttkrp_fiber<Real, RT, 1, 7>);
         else if (var == 5) go(k_mttkrp_fiber<Real, RT, 2, 6>);
-        else if (var == 6 || (var == 0 && sizeof(Real) == 8)) go(k_mttkrp_fiber<Real, RT, 1, 6>);
-        else go(k_mttkrp_fiber<Real, RT, 1, 7>);  // fp32 default
+        else if (var == 6) go(k_mttkrp_fiber<Real, RT, 1, 6>);
+        else go(k_mttkrp_fiber<Real, RT, 1, fiber_min_blocks<Real, RT>()>);  // default
       } else {
         k_mttkrp<Real, RT><<<(unsigned)blocks, wpb * 32, 0, c.stream>>>(items, n_items, md.row_ptr, md.idx_a,
                                                                        md.idx_b, md.val, A, B, out, partial);
@@ -950,17 +990,16 @@ struct Impl {
 
   // merged MTTKRP of every shard's owned rows into c.M (entry point sacd_mttkrp)
   static int sharded_mttkrp_api(Context &c, int mode) {
-    const size_t rs = sizeof(Real);
-    const size_t bytes = (size_t)c.m[mode].I * RT * rs;
+    const size_t bytes = (size_t)((c.m[mode].I + 31) / 32 * 32) * RT * sizeof(Real);
     for (Shard &sh : c.shards) SACD_CUDA_TRY(cudaMemsetAsync(sh.M, 0, bytes, c.stream));
     SACD_TRY(sharded_mttkrp_merge(c, mode));
     for (Shard &sh : c.shards) {
       const long long rlo = sh.plan[mode].rlo, rhi = sh.plan[mode].rhi;
       if (rhi > rlo)
-        SACD_CUDA_TRY(cudaMemcpyAsync(reinterpret_cast<char *>(c.M) + rlo * RT * rs,
-                                      reinterpret_cast<const char *>(sh.M) + rlo * RT * rs, (rhi - rlo) * RT * rs,
-                                      cudaMemcpyDeviceToDevice, c.stream));
+        k_copy_rows_tt<Real, RT><<<grid1d((rhi - rlo) * RT), 256, 0, c.stream>>>(
+            rlo, rhi, reinterpret_cast<const Real *>(sh.M), reinterpret_cast<Real *>(c.M));
     }
+    SACD_CUDA_TRY(cudaGetLastError());
     return SACD_OK;
   }
 
@@ -1150,24 +1189,24 @@ int nccl_broadcast_rows(Context &c, int mode) {
   return SACD_OK;
 }
 
-int launch_convert_in(Context &c, const double *src_dev, long long rows, void *dst) {
+int launch_convert_in(Context &c, const double *src_dev, long long rows, void *dst, bool ttl) {
   if (c.opt.precision == SACD_F64)
     k_convert_in<double><<<grid1d(rows * c.pitch), 256, 0, c.stream>>>(src_dev, rows, c.R, c.pitch,
-                                                                        reinterpret_cast<double *>(dst));
+                                                                        reinterpret_cast<double *>(dst), ttl);
   else
     k_convert_in<float><<<grid1d(rows * c.pitch), 256, 0, c.stream>>>(src_dev, rows, c.R, c.pitch,
-                                                                       reinterpret_cast<float *>(dst));
+                                                                       reinterpret_cast<float *>(dst), ttl);
   SACD_CUDA_TRY(cudaGetLastError());
   return SACD_OK;
 }
 
-int launch_convert_out(Context &c, const void *src, long long rows, double *dst_dev) {
+int launch_convert_out(Context &c, const void *src, long long rows, double *dst_dev, bool ttl) {
   if (c.opt.precision == SACD_F64)
     k_convert_out<double><<<grid1d(rows * c.R), 256, 0, c.stream>>>(reinterpret_cast<const double *>(src), rows, c.R,
-                                                                     c.pitch, dst_dev);
+                                                                     c.pitch, dst_dev, ttl);
   else
     k_convert_out<float><<<grid1d(rows * c.R), 256, 0, c.stream>>>(reinterpret_cast<const float *>(src), rows, c.R,
-                                                                    c.pitch, dst_dev);
+                                                                    c.pitch, dst_dev, ttl);
   SACD_CUDA_TRY(cudaGetLastError());
   return SACD_OK;
 }

@@ -84,7 +84,7 @@ struct ModeData {
   SplitRow *splits = nullptr;
   long long n_splits = 0, n_slots = 0;
   void *F = nullptr;              // Real[I * pitch]
-  void *Z = nullptr;              // Real[I * pitch]  (z_prev)
+  void *Z = nullptr;              // Real[ceil32(I) * pitch]  (z_prev, TT layout)
   double *G = nullptr;            // fp64 R x R Gram of F
 };
 
@@ -122,7 +122,7 @@ struct Context {
   ModeData m[3];
   DevState *st = nullptr;         // device
   // scratch
-  void *M = nullptr;              // Real[maxI * pitch]
+  void *M = nullptr;              // Real[ceil32(maxI) * pitch] (TT layout)
   void *partial = nullptr;        // Real[max slots * pitch]
   void *Hr = nullptr;             // Real[pitch * pitch]
   double *Hd = nullptr;           // R x R
@@ -169,8 +169,8 @@ int launch_mode_update(Context &c, int mode, int branch_override, bool begin_swe
                        uint8_t *decisions_dev);
 int launch_gram(Context &c, int mode);
 int launch_initial_fit(Context &c);
-int launch_convert_in(Context &c, const double *src_dev, long long rows, void *dst);
-int launch_convert_out(Context &c, const void *src, long long rows, double *dst_dev);
+int launch_convert_in(Context &c, const double *src_dev, long long rows, void *dst, bool tt_layout);
+int launch_convert_out(Context &c, const void *src, long long rows, double *dst_dev, bool tt_layout);
 int launch_hessian_only(Context &c, int mode);
 int launch_setup(Context &c);
 int launch_sharded_mode_update(Context &c, int mode, int branch_override, bool begin_sweep, bool end_sweep,
