@@ -695,7 +695,7 @@ int sacd_mttkrp(sacd_ctx *c, int32_t mode, double *out, int64_t ld) {
     return sticky(c, SACD_ECUDA);
   }
   int rc = c->sharded ? launch_sharded_mttkrp(*c, mode) : launch_mttkrp(*c, mode, c->M);
-  if (rc == SACD_OK) rc = read_matrix(c, c->M, c->m[mode].I, out, ld, true);
+  if (rc == SACD_OK) rc = read_matrix(c, c->M, c->m[mode].I, out, ld, false);
   return sticky(c, rc);
 }
 

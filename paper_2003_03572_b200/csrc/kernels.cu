@@ -173,10 +173,9 @@ __global__ void __launch_bounds__(256) k_mttkrp(const WorkItem *__restrict__ ite
 #pragma unroll
         for (int v = 0; v < VPL; ++v) dv[sub + v * LPN] = VV::make(acc[v]);
       } else {
+        VT *dv = reinterpret_cast<VT *>(M + (long long)row * RT);
 #pragma unroll
-        for (int v = 0; v < VPL; ++v)
-#pragma unroll
-          for (int c = 0; c < VEC; ++c) M[tt<RT>(row, (sub + v * LPN) * VEC + c)] = acc[v][c];
+        for (int v = 0; v < VPL; ++v) dv[sub + v * LPN] = VV::make(acc[v]);
       }
     }
   }
@@ -256,19 +255,16 @@ __global__ void __launch_bounds__(256, MINB) k_mttkrp_fiber(const WorkItem *__re
 #pragma unroll
   for (int k = 0; k < E; ++k) acc[k] = facc[k] = arow.v[k] = Real(0);
   long long cur_row = -1;
+  Real *Ml = M + lane * E;
   auto flush = [&]() {
-    if (it.slot >= 0) {
-      LaneRow<Real, E> o;
+    LaneRow<Real, E> o;
 #pragma unroll
-      for (int k = 0; k < E; ++k) o.v[k] = acc[k];
-      o.store(partial + it.slot * RT + lane * E);
-    } else if (cur_row >= 0) {
-      Real *dst = M + (cur_row >> 5) * (32LL * RT) + (cur_row & 31) + lane * (E * 32);  // TT layout
-#pragma unroll
-      for (int k = 0; k < E; ++k) dst[k * 32] = acc[k];
+    for (int k = 0; k < E; ++k) {
+      o.v[k] = acc[k];
+      acc[k] = Real(0);
     }
-#pragma unroll
-    for (int k = 0; k < E; ++k) acc[k] = Real(0);
+    if (it.slot >= 0) o.store(partial + it.slot * RT + lane * E);
+    else if (cur_row >= 0) o.store(Ml + cur_row * RT);
   };
   auto step = [&](uint32_t fa, float xf, const LaneRow<Real, E> &b, uint32_t my_n, int j) {
     if (fa & kFiberStart) {
@@ -351,7 +347,7 @@ __global__ void __launch_bounds__(256) k_fixup(const SplitRow *__restrict__ spli
     Real s = red[0][c];
 #pragma unroll
     for (int k = 1; k < 8; ++k) s += red[k][c];
-    M[tt<RT>(sr.row, c)] = s;
+    M[(long long)sr.row * RT + c] = s;
   }
 }
 
@@ -432,13 +428,26 @@ __global__ void __launch_bounds__(rows_per_block<RT>())
   constexpr int C = 8;  // column block: each u_j read from shared memory feeds C FMAs
   double ti = 0.0, md = 0.0;
   long long E = 0, Ech = 0;
-  if (tid < nrows) {
+  // M is row-major (written by the MTTKRP as whole rows): each warp transposes the 32 x C
+  // block of its rows through a small shared tile, so global reads stay coalesced.
+  __shared__ Real Mst[TR / 32][32][C + 1];
+  const int lane = tid & 31, wp = tid >> 5;
+  const bool active = tid < nrows;
+  {
     const long long row = row0 + tid;
     Real *u = Us + tid * US;
-    const Real *m = M + tt<RT>(row, 0);                    // TT layout: column c at m[32 c]
-    const bool empty = row_ptr[row] == row_ptr[row + 1];  // M is not written for empty slices: m = 0
-    Real *zp = Z + tt<RT>(row, 0);
+    const bool empty = active ? row_ptr[row] == row_ptr[row + 1] : true;  // empty slice: m = 0
+    Real *zp = Z + tt<RT>(active ? row : row0, 0);         // z_prev in the TT layout
     for (int c0 = 0; c0 < R; c0 += C) {
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < C; ++k) {
+        const int x = lane + 32 * k, rl = x / C, cl = x % C;
+        const long long rg = row0 + wp * 32 + rl;
+        Mst[wp][rl][cl] = (rg < row_end) ? M[rg * RT + c0 + cl] : Real(0);
+      }
+      __syncwarp();
+      if (!active) continue;
       // (1) out-of-block part of the gradient with the current row (columns < c0 already
       //     updated), Eq 14:  acc_q = sum_{j not in block} u_j h_(j, c0+q)   (H symmetric)
       Real acc[C];
@@ -462,7 +471,7 @@ __global__ void __launch_bounds__(rows_per_block<RT>())
       Real mv[C], zv[C], ub[C];
 #pragma unroll
       for (int q = 0; q < C; ++q) {
-        mv[q] = m[32 * (c0 + q)];
+        mv[q] = Mst[wp][lane][q];
         zv[q] = zp[32 * (c0 + q)];
       }
 #pragma unroll
@@ -561,7 +570,7 @@ __global__ void k_fm_dot(long long row_begin, long long row_end, int R, const lo
   const long long row = row_begin + (long long)blockIdx.x * TR + threadIdx.x;
   double s = 0.0;
   if (row < row_end && row_ptr[row] != row_ptr[row + 1])
-    for (int r = 0; r < R; ++r) s += (double)F[row * RT + r] * (double)M[tt<RT>(row, r)];
+    for (int r = 0; r < R; ++r) s += (double)F[row * RT + r] * (double)M[row * RT + r];
   red[threadIdx.x] = s;
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -755,7 +764,7 @@ __global__ void __launch_bounds__(1024) k_finalize(int mode, long long nblk, con
 template <typename Real, int RT>
 __global__ void k_pack_head(long long head, const Real *__restrict__ M, long long *__restrict__ id_slot,
                             Real *__restrict__ row_slot) {
-  for (int c = threadIdx.x; c < RT; c += blockDim.x) row_slot[c] = head >= 0 ? M[tt<RT>(head, c)] : Real(0);
+  for (int c = threadIdx.x; c < RT; c += blockDim.x) row_slot[c] = head >= 0 ? M[head * RT + c] : Real(0);
   if (threadIdx.x == 0) *id_slot = head;
 }
 
@@ -765,7 +774,7 @@ __global__ void k_copy_rows_tt(long long rlo, long long rhi, const Real *__restr
        x += (long long)gridDim.x * blockDim.x) {
     const long long i = rlo + x / RT;
     const int c = (int)(x % RT);
-    dst[tt<RT>(i, c)] = src[tt<RT>(i, c)];
+    dst[i * RT + c] = src[i * RT + c];
   }
 }
 
@@ -776,7 +785,7 @@ __global__ void k_merge_heads(int G, long long rlo, long long rhi, const long lo
   for (int q = 0; q < G; ++q) {
     const long long id = ids[q];
     if (id >= rlo && id < rhi)
-      for (int c = threadIdx.x; c < RT; c += blockDim.x) M[tt<RT>(id, c)] += rows[(long long)q * RT + c];
+      for (int c = threadIdx.x; c < RT; c += blockDim.x) M[id * RT + c] += rows[(long long)q * RT + c];
   }
 }
 
