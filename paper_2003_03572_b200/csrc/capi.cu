@@ -224,6 +224,7 @@ static void destroy(sacd_ctx *c) {
     cudaFree(m.idx_b);
     cudaFree(m.idx_n);
     cudaFree(m.val);
+    cudaFree(m.nzm);
     cudaFree(m.row_ptr);
     cudaFree(m.items);
     cudaFree(m.splits);
@@ -790,7 +791,10 @@ int sacd_layout(sacd_ctx *c, int32_t mode, uint32_t *idx_a, uint32_t *idx_b, flo
     rc = dev_read(c, idx_a, md.idx_a, (size_t)c->nnz * 4);
     for (long long e = 0; rc == SACD_OK && e < c->nnz; ++e) idx_a[e] &= kIdxMask;  // strip the flag bits
   }
-  if (rc == SACD_OK && idx_b && c->nnz) rc = dev_read(c, idx_b, md.idx_b, (size_t)c->nnz * 4);
+  if (rc == SACD_OK && idx_b && c->nnz) {
+    rc = dev_read(c, idx_b, md.idx_b, (size_t)c->nnz * 4);
+    for (long long e = 0; rc == SACD_OK && e < c->nnz; ++e) idx_b[e] &= kIdxMask;
+  }
   if (rc == SACD_OK && val && c->nnz) rc = dev_read(c, val, md.val, (size_t)c->nnz * 4);
   if (rc == SACD_OK && row_ptr) rc = dev_read(c, row_ptr, md.row_ptr, (size_t)(md.I + 1) * 8);
   return sticky(c, rc);

@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(256) k_mttkrp(const WorkItem *__restrict__ ite
     for (long long e = s + grp; e < t; e += G) {
       const Real x = (Real)ld_stream_f32(val + e);
       const VT *ap = reinterpret_cast<const VT *>(A + (long long)(ld_stream_u32(ia + e) & kIdxMask) * RT);
-      const VT *bp = reinterpret_cast<const VT *>(B + (long long)ld_stream_u32(ib + e) * RT);
+      const VT *bp = reinterpret_cast<const VT *>(B + (long long)(ld_stream_u32(ib + e) & kIdxMask) * RT);
 #pragma unroll
       for (int v = 0; v < VPL; ++v) {
         Real av[VEC], bv[VEC];
@@ -300,7 +300,7 @@ __global__ void __launch_bounds__(256, MINB) k_mttkrp_fiber(const WorkItem *__re
 #pragma unroll
       for (int u = 0; u < NB; ++u) {
         const uint32_t eb = __shfl_sync(0xffffffffu, my_b, (jb + u) & 31);
-        if (jb + u < cnt) bb[u].load(Bl + (long long)eb * RT);
+        if (jb + u < cnt) bb[u].load(Bl + (long long)(eb & kIdxMask) * RT);
       }
 #pragma unroll
       for (int u = 0; u < NB; ++u) {
@@ -314,6 +314,223 @@ __global__ void __launch_bounds__(256, MINB) k_mttkrp_fiber(const WorkItem *__re
 #pragma unroll
   for (int k = 0; k < E; ++k) acc[k] = fma(arow.v[k], facc[k], acc[k]);
   flush();
+}
+
+// Sub-warp fiber MTTKRP (R > 16): a worker of SW lanes (8, 16 or 32) per work item, so one
+// warp runs 32/SW items at once and every shuffle instruction serves all of them.
+//  * Lane l of a worker owns the 16-byte column chunks k*SW + l (k < NV), so each chunk
+//    load of a factor row is one contiguous SW*16-byte access (full sectors).
+//  * The fiber / row flag bits ride on idx_b (layout.cu), so a nonzero costs two shuffles
+//    (b index + flags, value); the a index and the row id are fetched only at fiber / row
+//    starts.  The next batch's metadata is prefetched one batch ahead.
+//  * NB b-rows (and, with PA, the a-rows of fibers starting among them) are issued before
+//    any is consumed, so a worker keeps NB gathers in flight.
+// Same arithmetic and order as k_mttkrp_fiber: m_i = sum_fibers a (.) (sum_e x_e b_e).
+template <typename Real, int RT>
+__host__ __device__ constexpr int sub_warp_lanes() {  // 16 bytes of a row per lane, at most 32 lanes
+  return RT * (int)sizeof(Real) / 16 > 32 ? 32 : RT * (int)sizeof(Real) / 16;
+}
+
+template <typename Real, int RT, int SW>
+struct SubRow {
+  using VV = V16<Real>;
+  using VT = typename VV::T;
+  static constexpr int NV = RT / VV::N / SW;  // 16-byte chunks per lane
+  static constexpr int E = NV * VV::N;
+  Real v[E];
+  // p = row base + lane * VEC
+  __device__ __forceinline__ void load(const Real *p) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) VV::get(__ldg(reinterpret_cast<const VT *>(p) + k * SW), v + k * VV::N);
+  }
+  __device__ __forceinline__ void store(Real *p) const { store_from(p, v); }
+  __device__ static __forceinline__ void store_from(Real *p, const Real (&x)[E]) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      Real t[VV::N];
+#pragma unroll
+      for (int c = 0; c < VV::N; ++c) t[c] = x[k * VV::N + c];
+      reinterpret_cast<VT *>(p)[k * SW] = VV::make(t);
+    }
+  }
+};
+
+__device__ __forceinline__ uint4 ld_stream_u4(const uint4 *p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
+template <typename Real, int RT, int SW, int NB, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_mttkrp_sw(const WorkItem *__restrict__ items, long long n_items,
+                                                        const uint4 *__restrict__ nzm,
+                                                        const Real *__restrict__ A, const Real *__restrict__ B,
+                                                        Real *__restrict__ M, Real *__restrict__ partial) {
+  using SR = SubRow<Real, RT, SW>;
+  constexpr int E = SR::E;
+  constexpr int VEC = V16<Real>::N;
+  static_assert(SR::NV >= 1, "row narrower than a sub-warp of 16-byte chunks");
+  const int lane = threadIdx.x & (SW - 1);
+  const unsigned mask = SW == 32 ? 0xffffffffu : (((1u << SW) - 1u) << (threadIdx.x & 31 & ~(SW - 1)));
+  const int shift = threadIdx.x & 31 & ~(SW - 1);  // this worker's lanes in a ballot
+  const long long item = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / SW;
+  if (item >= n_items) return;
+  const long long nz0 = items[item].nz0, nz1 = items[item].nz1;
+  const int slot = (int)items[item].slot;
+  if (nz0 >= nz1) return;
+  const Real *Al = A + lane * VEC;
+  const Real *Bl = B + lane * VEC;
+  SR arow, anext;
+  Real acc[E], facc[E];
+#pragma unroll
+  for (int k = 0; k < E; ++k) acc[k] = facc[k] = arow.v[k] = anext.v[k] = Real(0);
+  int cur_row = -1;
+  bool need_next = true;  // the a-row of the next fiber start is not in flight yet
+  for (long long base = nz0; base < nz1; base += SW) {
+    const int cnt = (int)min((long long)SW, nz1 - base);
+    // this batch's metadata: lane l holds nonzero base + l as {a|flags, b|flags, x, row}
+    uint4 my = make_uint4(0u, 0u, 0u, 0u);
+    if (lane < cnt) my = __ldg(nzm + base + lane);
+    if (base + SW + lane < nz1) asm volatile("prefetch.global.L1 [%0];" ::"l"(nzm + base + SW + lane));
+    if (base == nz0 && lane == 0) my.y |= kFiberStart | kRowStart;  // an item starts a row and a fiber
+    // fiber starts of this batch (bit j = nonzero base + j)
+    const unsigned fmask = (__ballot_sync(mask, (my.y & kFiberStart) != 0) >> shift) &
+                           (SW == 32 ? 0xffffffffu : ((1u << SW) - 1u));
+    if (need_next && fmask) {
+      const int j0 = __ffs(fmask) - 1;
+      anext.load(Al + (long long)(__shfl_sync(mask, my.x, j0, SW) & kIdxMask) * RT);
+      need_next = false;
+    }
+    for (int jb = 0; jb < cnt; jb += NB) {
+      SR bb[NB];
+      uint32_t fb[NB];
+      float xf[NB];
+#pragma unroll
+      for (int u = 0; u < NB; ++u) {  // NB gathers in flight (rows past cnt read row 0: harmless)
+        const int j = (jb + u) & (SW - 1);
+        fb[u] = __shfl_sync(mask, my.y, j, SW);
+        xf[u] = __uint_as_float(__shfl_sync(mask, my.z, j, SW));
+        bb[u].load(Bl + (long long)(fb[u] & kIdxMask) * RT);
+      }
+#pragma unroll
+      for (int u = 0; u < NB; ++u) {
+        if (jb + u < cnt) {
+          const int j = jb + u;
+          if (fb[u] & kFiberStart) {
+#pragma unroll
+            for (int k = 0; k < E; ++k) {  // close the previous fiber: acc += a * facc
+              acc[k] = fma(arow.v[k], facc[k], acc[k]);
+              facc[k] = Real(0);
+            }
+            if (fb[u] & kRowStart) {
+              const int nrow = (int)__shfl_sync(mask, my.w, j, SW);
+              if (slot >= 0) SR::store_from(partial + (long long)slot * RT + lane * VEC, acc);
+              else if (cur_row >= 0) SR::store_from(M + (long long)cur_row * RT + lane * VEC, acc);
+#pragma unroll
+              for (int k = 0; k < E; ++k) acc[k] = Real(0);
+              cur_row = nrow;
+            }
+#pragma unroll
+            for (int k = 0; k < E; ++k) arow.v[k] = anext.v[k];
+            // issue the a-row of the next fiber start (in this batch, else at the next batch)
+            const unsigned rest = j + 1 < 32 ? (fmask & ~((2u << j) - 1u)) : 0u;
+            if (rest) {
+              const int jn = __ffs(rest) - 1;
+              anext.load(Al + (long long)(__shfl_sync(mask, my.x, jn, SW) & kIdxMask) * RT);
+            } else {
+              need_next = true;
+            }
+          }
+          const Real x = (Real)xf[u];
+#pragma unroll
+          for (int k = 0; k < E; ++k) facc[k] = fma(x, bb[u].v[k], facc[k]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < E; ++k) acc[k] = fma(arow.v[k], facc[k], acc[k]);
+  if (slot >= 0) SR::store_from(partial + (long long)slot * RT + lane * VEC, acc);
+  else if (cur_row >= 0) SR::store_from(M + (long long)cur_row * RT + lane * VEC, acc);
+}
+
+// Lean sub-warp fiber MTTKRP.  The MTTKRP is issue-bound (ncu: ~34 warp instructions per
+// nonzero in the warp-per-item kernel), so this kernel minimises instructions per nonzero:
+//  * SW lanes per worker (32/SW workers per warp), each lane holding E = RT/SW columns, so
+//    every shuffle / address / branch instruction serves 32/SW nonzeros at once;
+//  * the batch loop is fully unrolled over SW nonzeros; entries past the end carry x = 0,
+//    b = 0 and no flags, so they add exact zeros instead of needing predicates;
+//  * b-rows are prefetched D nonzeros ahead (registers renamed by the unroll), and the
+//    next batch's 16-byte metadata is in flight while the current batch is consumed.
+// Same arithmetic and order as k_mttkrp_fiber (bitwise-equal results).
+template <typename Real, int RT, int SW, int D, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_mttkrp_lean(const WorkItem *__restrict__ items, long long n_items,
+                                                          const uint4 *__restrict__ nzm,
+                                                          const Real *__restrict__ A, const Real *__restrict__ B,
+                                                          Real *__restrict__ M, Real *__restrict__ partial) {
+  using SR = SubRow<Real, RT, SW>;
+  constexpr int E = SR::E;
+  constexpr int VEC = V16<Real>::N;
+  static_assert(SR::NV >= 1, "row narrower than a sub-warp of 16-byte chunks");
+  const int lane = threadIdx.x & (SW - 1);
+  const unsigned mask = SW == 32 ? 0xffffffffu : (((1u << SW) - 1u) << (threadIdx.x & 31 & ~(SW - 1)));
+  const long long item = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / SW;
+  if (item >= n_items) return;
+  const long long nz0 = items[item].nz0, nz1 = items[item].nz1;
+  const int slot = (int)items[item].slot;
+  const Real *Al = A + lane * VEC;
+  const Real *Bl = B + lane * VEC;
+  SR arow;
+  Real acc[E], facc[E];
+#pragma unroll
+  for (int k = 0; k < E; ++k) acc[k] = facc[k] = arow.v[k] = Real(0);
+  int cur_row = -1;
+  uint4 my = make_uint4(0u, 0u, 0u, 0u);
+  if (nz0 + lane < nz1) my = ld_stream_u4(nzm + nz0 + lane);
+  if (lane == 0) my.y |= kFiberStart | kRowStart;  // an item starts a row and a fiber
+  for (long long base = nz0; base < nz1; base += SW) {
+    uint4 nx = make_uint4(0u, 0u, 0u, 0u);
+    if (base + SW + lane < nz1) nx = ld_stream_u4(nzm + base + SW + lane);
+    uint32_t fb[SW];
+    SR bb[D + 1];
+#pragma unroll
+    for (int j = 0; j < D && j < SW; ++j) {
+      fb[j] = __shfl_sync(mask, my.y, j, SW);
+      bb[j % (D + 1)].load(Bl + (long long)(fb[j] & kIdxMask) * RT);
+    }
+#pragma unroll
+    for (int j = 0; j < SW; ++j) {
+      if (j + D < SW) {
+        fb[j + D] = __shfl_sync(mask, my.y, j + D, SW);
+        bb[(j + D) % (D + 1)].load(Bl + (long long)(fb[j + D] & kIdxMask) * RT);
+      }
+      const Real x = (Real)__uint_as_float(__shfl_sync(mask, my.z, j, SW));
+      if (fb[j] & kFiberStart) {
+#pragma unroll
+        for (int k = 0; k < E; ++k) {  // close the previous fiber: acc += a * facc
+          acc[k] = fma(arow.v[k], facc[k], acc[k]);
+          facc[k] = Real(0);
+        }
+        if (fb[j] & kRowStart) {
+          if (slot >= 0) SR::store_from(partial + (long long)slot * RT + lane * VEC, acc);
+          else if (cur_row >= 0) SR::store_from(M + (long long)cur_row * RT + lane * VEC, acc);
+#pragma unroll
+          for (int k = 0; k < E; ++k) acc[k] = Real(0);
+          cur_row = (int)__shfl_sync(mask, my.w, j, SW);
+        }
+        arow.load(Al + (long long)(__shfl_sync(mask, my.x, j, SW) & kIdxMask) * RT);
+      }
+#pragma unroll
+      for (int k = 0; k < E; ++k) facc[k] = fma(x, bb[j % (D + 1)].v[k], facc[k]);
+    }
+    my = nx;
+  }
+#pragma unroll
+  for (int k = 0; k < E; ++k) acc[k] = fma(arow.v[k], facc[k], acc[k]);
+  if (slot >= 0) SR::store_from(partial + (long long)slot * RT + lane * VEC, acc);
+  else if (cur_row >= 0) SR::store_from(M + (long long)cur_row * RT + lane * VEC, acc);
 }
 
 // Heavy rows split across items: M_row = sum of the row's partials.  One block per split
@@ -881,12 +1098,49 @@ struct Impl {
           kern<<<(unsigned)blocks, wpb * 32, 0, c.stream>>>(items, n_items, md.idx_a, md.idx_b, md.val, md.idx_n, A,
                                                            B, out, partial);
         };
-        if (var == 1) go(k_mttkrp_fiber<Real, RT, 1, 4>);
-        else if (var == 2) go(k_mttkrp_fiber<Real, RT, 2, 4>);
-        else if (var == 3) go(k_mttkrp_fiber<Real, RT, 1, 7>);
-        else if (var == 5) go(k_mttkrp_fiber<Real, RT, 2, 6>);
-        else if (var == 6) go(k_mttkrp_fiber<Real, RT, 1, 6>);
-        else go(k_mttkrp_fiber<Real, RT, 1, fiber_min_blocks<Real, RT>()>);  // default
+        constexpr int SW = sub_warp_lanes<Real, RT>();
+        const long long sblocks = (n_items * SW + 255) / 256;
+        auto gos = [&](auto kern) {
+          kern<<<(unsigned)sblocks, 256, 0, c.stream>>>(items, n_items, md.nzm, A, B, out, partial);
+        };
+        if (var == 1) go(k_mttkrp_fiber<Real, RT, 1, fiber_min_blocks<Real, RT>()>);
+        else if (var == 10) gos(k_mttkrp_sw<Real, RT, SW, 1, 4>);
+        else if (var == 11) gos(k_mttkrp_sw<Real, RT, SW, 2, 4>);
+        else if (var == 12) gos(k_mttkrp_sw<Real, RT, SW, 4, 4>);
+        else if (var == 13) gos(k_mttkrp_sw<Real, RT, SW, 4, 3>);
+        else if (var == 14) gos(k_mttkrp_sw<Real, RT, SW, 8, 2>);
+        else if (var == 15) gos(k_mttkrp_sw<Real, RT, SW, 2, 6>);
+        else if (var >= 20 && var < 30) {
+          // lean kernel: E elements per lane -> SW = RT / E lanes per worker
+          constexpr int VEC = V16<Real>::N;
+          constexpr int E8 = 8 < VEC ? VEC : 8;
+          constexpr int SW8 = RT / E8 > 32 ? 32 : (RT / E8 < 1 ? 1 : RT / E8);
+          constexpr int E4 = 4 < VEC ? VEC : 4;
+          constexpr int SW4 = RT / E4 > 32 ? 32 : (RT / E4 < 1 ? 1 : RT / E4);
+          auto gol = [&](auto kern, int sw) {
+            const long long lb = (n_items * sw + 255) / 256;
+            kern<<<(unsigned)lb, 256, 0, c.stream>>>(items, n_items, md.nzm, A, B, out, partial);
+          };
+          if (var == 20) gol(k_mttkrp_lean<Real, RT, SW4, 1, 4>, SW4);
+          else if (var == 21) gol(k_mttkrp_lean<Real, RT, SW4, 2, 3>, SW4);
+          else if (var == 22) gol(k_mttkrp_lean<Real, RT, SW8, 1, 2>, SW8);
+          else if (var == 23) gol(k_mttkrp_lean<Real, RT, SW8, 1, 3>, SW8);
+          else if (var == 24) gol(k_mttkrp_lean<Real, RT, SW4, 1, 3>, SW4);
+          else gol(k_mttkrp_lean<Real, RT, SW8, 2, 2>, SW8);
+        }
+        else if (sizeof(Real) == 8 && RT >= 256) {
+          go(k_mttkrp_fiber<Real, RT, 1, fiber_min_blocks<Real, RT>()>);  // default, fp64, R > 128
+        } else {
+          // default (measured on B200, tools/mttkrp_tune.py): the lean sub-warp kernel with
+          // 4 fp64 / 8 fp32 columns per lane
+          constexpr int VEC = V16<Real>::N;
+          constexpr int EL = sizeof(Real) == 8 ? (4 < VEC ? VEC : 4) : (8 < VEC ? VEC : 8);
+          constexpr int SWL = RT / EL > 32 ? 32 : (RT / EL < 1 ? 1 : RT / EL);
+          constexpr int MB = sizeof(Real) == 8 ? 3 : 2;
+          const long long lb = (n_items * SWL + 255) / 256;
+          k_mttkrp_lean<Real, RT, SWL, 1, MB><<<(unsigned)lb, 256, 0, c.stream>>>(items, n_items, md.nzm, A, B, out,
+                                                                                 partial);
+        }
       } else {
         k_mttkrp<Real, RT><<<(unsigned)blocks, wpb * 32, 0, c.stream>>>(items, n_items, md.row_ptr, md.idx_a,
                                                                        md.idx_b, md.val, A, B, out, partial);

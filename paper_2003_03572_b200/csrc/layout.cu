@@ -44,13 +44,13 @@ __global__ void k_check_dup(const unsigned long long *__restrict__ keys, long lo
     if (keys[e] == keys[e - 1]) atomicOr(flags, 4);
 }
 
-// Gather the sorted entries; idx_a gets the fiber-start / row-start flag bits and idx_n
+// Gather the sorted entries; idx_a and idx_b get the fiber-start / row-start flag bits and idx_n
 // the row index (both derived from the sorted keys).
 __global__ void k_gather(const uint32_t *__restrict__ coords, const float *__restrict__ vals,
                          const uint32_t *__restrict__ pos, const unsigned long long *__restrict__ keys,
                          long long nnz, int a, int b, unsigned long long Ib, unsigned long long IaIb,
                          uint32_t *__restrict__ ia, uint32_t *__restrict__ ib, uint32_t *__restrict__ in_,
-                         float *__restrict__ v) {
+                         float *__restrict__ v, uint4 *__restrict__ nzm) {
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nnz;
        e += (long long)gridDim.x * blockDim.x) {
     const long long p = pos[e];
@@ -62,10 +62,14 @@ __global__ void k_gather(const uint32_t *__restrict__ coords, const float *__res
       row_start = (kp / IaIb) != row;
       fiber_start = (kp / Ib) != (k / Ib);
     }
-    ia[e] = coords[3 * p + a] | (fiber_start ? kFiberStart : 0u) | (row_start ? kRowStart : 0u);
-    ib[e] = coords[3 * p + b];
+    const uint32_t fl = (fiber_start ? kFiberStart : 0u) | (row_start ? kRowStart : 0u);
+    const uint32_t xa = coords[3 * p + a] | fl, xb = coords[3 * p + b] | fl;
+    const float x = vals[p];
+    ia[e] = xa;
+    ib[e] = xb;
     in_[e] = (uint32_t)row;
-    v[e] = vals[p];
+    v[e] = x;
+    nzm[e] = make_uint4(xa, xb, __float_as_uint(x), (uint32_t)row);
   }
 }
 
@@ -168,8 +172,9 @@ int build_layouts(Context &c, const uint32_t *coords, const float *vals) {
     SACD_CUDA_TRY(cudaMallocAsync(&md.idx_b, ne * 4, s));
     SACD_CUDA_TRY(cudaMallocAsync(&md.idx_n, ne * 4, s));
     SACD_CUDA_TRY(cudaMallocAsync(&md.val, ne * 4, s));
+    SACD_CUDA_TRY(cudaMallocAsync(&md.nzm, ne * 16, s));
     SACD_CUDA_TRY(cudaMallocAsync(&md.row_ptr, (size_t)(md.I + 1) * 8, s));
-    c.device_bytes += (long long)ne * 16 + (md.I + 1) * 8;
+    c.device_bytes += (long long)ne * 32 + (md.I + 1) * 8;
     if (nnz > 0) {
       k_make_keys<<<grid_for(nnz), 256, 0, s>>>(coords, nnz, n, a, b, Ia, Ib, keys, pos);
       const int end_bit = bits_for((unsigned long long)c.dims[n] * Ia * Ib - 1ULL);
@@ -177,7 +182,7 @@ int build_layouts(Context &c, const uint32_t *coords, const float *vals) {
           cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys, keys2, pos, pos2, (int)nnz, 0, end_bit, s));
       k_check_dup<<<grid_for(nnz), 256, 0, s>>>(keys2, nnz, flags);
       k_gather<<<grid_for(nnz), 256, 0, s>>>(coords, vals, pos2, keys2, nnz, a, b, Ib, Ia * Ib, md.idx_a, md.idx_b,
-                                             md.idx_n, md.val);
+                                             md.idx_n, md.val, md.nzm);
     }
     k_row_ptr<<<grid_for(md.I + 1), 256, 0, s>>>(keys2, nnz, md.I, Ia * Ib, md.row_ptr);
     SACD_CUDA_TRY(cudaGetLastError());

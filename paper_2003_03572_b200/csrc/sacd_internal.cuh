@@ -78,6 +78,7 @@ struct ModeData {
   int a = 0, b = 0;               // the other modes ("a" = shorter)
   uint32_t *idx_a = nullptr, *idx_b = nullptr, *idx_n = nullptr;  // idx_a has flag bits
   float *val = nullptr;
+  uint4 *nzm = nullptr;           // per nonzero {idx_a|flags, idx_b|flags, bits(val), row}: one 16-byte load
   long long *row_ptr = nullptr;   // I+1
   WorkItem *items = nullptr;
   long long n_items = 0;

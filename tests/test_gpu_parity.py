@@ -120,6 +120,32 @@ def test_mttkrp_gram_hessian(R, precision):
             assert np.abs(g.hessian(n) - Ho).max() <= tol * np.abs(Ho).max()
 
 
+@pytest.mark.parametrize("R", [33, 64, 128, 256])
+@pytest.mark.parametrize("precision", ["f64", "f32"])
+def test_mttkrp_variants_bitwise(R, precision):
+    """Every MTTKRP kernel variant (old warp fiber kernel = 1, sub-warp kernels 10..15,
+    default 0) performs the same fiber-factored sums in the same order, so their M are
+    bitwise equal; and each equals the oracle's MTTKRP within rounding.  Heavy rows and a
+    small work-item size force split rows (partial slots + fix-up)."""
+    dims = (53, 31, 67)
+    c, v = ragged_tensor(dims, 5000, 17, heavy_rows=((0, 1, 900), (1, 4, 500), (2, 7, 800)))
+    F = O.init_factors(dims, R, 5)
+    Mo = [O.mttkrp(c, v, dims, n, F) for n in range(3)]
+    ref = None
+    for var in (1, 10, 11, 12, 13, 14, 15, 0):
+        with S(c, v, dims, R, 5, precision=precision, nnz_per_item=48, mttkrp_variant=var) as g:
+            Ms = [g.mttkrp(n) for n in range(3)]
+        tol = 1e-12 if precision == "f64" else 1e-5
+        for n in range(3):
+            scale = np.maximum(np.abs(Mo[n]).max(axis=0, keepdims=True), 1e-30)
+            assert (np.abs(Ms[n] - Mo[n]) / scale).max() <= tol, (var, n)
+        if ref is None:
+            ref = Ms
+        else:
+            for n in range(3):
+                assert np.array_equal(Ms[n], ref[n]), (var, n)
+
+
 @pytest.mark.parametrize("R", [3, 16, 64, 128])
 @pytest.mark.parametrize("branch", [0, 1, 2])
 @pytest.mark.parametrize("l_mode", ["diag", "frob"])

@@ -15,7 +15,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c4")
 ap.add_argument("--precision", default="f64")
 ap.add_argument("--rank", type=int, default=None)
-ap.add_argument("--variants", default="0,1,2,3,4,5,6")
+ap.add_argument("--variants", default="1,10,11,12,13,14,15,0")
 ap.add_argument("--nnz-per-item", type=int, default=0)
 ap.add_argument("--reps", type=int, default=5)
 a = ap.parse_args()
