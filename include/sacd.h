@@ -81,7 +81,8 @@ typedef struct {
   int32_t force_sharded;      /* 1: run the sharded (NCCL) engine also when world_size == 1 */
   int32_t emulate_ranks;      /* G >= 2 (with world_size 1): emulate the G ranks of the     */
                               /* sharded engine on this GPU, exchanges as local copies      */
-  int32_t reserved[4];
+  int32_t reserved[4];        /* [0]: row-update tuning variant (0 = default, 1 = H read from  */
+                              /* global/L1 instead of shared memory); others must be 0       */
 } sacd_options;
 
 /* Per-sweep statistics (device-side ring, read by sacd_stats). */
@@ -151,6 +152,24 @@ void sacd_free(sacd_ctx *ctx);
 const char *sacd_last_error(void);
 
 /* --------------------------------------------------------------------------------------
+ * Held-out evaluation (the paper's 80/20 protocol).
+ * ------------------------------------------------------------------------------------ */
+
+/* Predictions of the current CP model at n coordinates (Eq 8):
+ *   out[e] = sum_{r<R} u_(q_e, r) v_(p_e, r) w_(s_e, r)
+ *   coords : host or device, n x 3 uint32 (q,p,s), each index < dims[mode].
+ *   out    : host or device, n fp64 (written).  n == 0 is legal.
+ * Errors: EINVAL (n < 0 or null pointers with n > 0), ERANGE (index out of range; nothing
+ * written), ENOMEM, ECUDA.  Synchronous; the caller owns both buffers. */
+int sacd_predict(sacd_ctx *ctx, const uint32_t *coords, int64_t n, double *out);
+
+/* Root mean squared error of the current model on n held-out entries (Eq 30,
+ * P:886-890): sqrt( sum_e (x_e - xhat_e)^2 / n ), the squared errors summed in fp64 in a
+ * fixed order (deterministic).  coords as sacd_predict; vals: host or device, n fp32.
+ * n == 0 gives *rmse = 0.  Errors as sacd_predict.  Synchronous. */
+int sacd_rmse(sacd_ctx *ctx, const uint32_t *coords, const float *vals, int64_t n, double *rmse);
+
+/* --------------------------------------------------------------------------------------
  * Component entry points (teacher forcing, parity tests and kernel timing).  Each runs the
  * same kernels the sweep runs.
  * ------------------------------------------------------------------------------------ */
@@ -194,6 +213,10 @@ int sacd_layout(sacd_ctx *ctx, int32_t mode, uint32_t *idx_a, uint32_t *idx_b, f
 #define SACD_NUM_KCLASS 6
 int sacd_profile_read(sacd_ctx *ctx, double ms[SACD_NUM_KCLASS], int64_t launches[SACD_NUM_KCLASS]);
 int sacd_profile_reset(sacd_ctx *ctx);
+/* Switch profiling on (sacd_iterate launches eagerly with per-class CUDA events) or off
+ * (sacd_iterate replays the captured sweep graph, if opt.use_graph).  Never fails on a
+ * live context. */
+int sacd_set_profile(sacd_ctx *ctx, int32_t on);
 
 /* Slice-sharding plan of one mode for `world` ranks; a pure host function
  * (no GPU).  row_ptr: host, I + 1 entries of the mode-sorted layout (sacd_layout).

@@ -8,7 +8,7 @@ module only compiles it with gcc and marshals numpy arrays through ctypes.
 
 Parity status per function (pins in tests/test_oracle_pins.py):
   layout, init, gram/hadamard/frobenius, mttkrp, mode_pass (step, importance,
-  selection), objective (dense, sparse, Gram trick)  -- pinned.
+  selection), objective (dense, sparse, Gram trick), predict / rmse  -- pinned.
   Selection dynamics end to end (trajectories of E / ti)  -- parity unpinned (the paper
   prints no trace); they are only checked for internal consistency.
 """
@@ -64,6 +64,8 @@ def lib():
         L.ora_objective_dense.argtypes = [P, i64, P, P, P, P, P, i32, P]
         L.ora_objective_sparse.argtypes = [P, i64, P, P, P, P, P, i32, P]
         L.ora_sacd_run.argtypes = [i64, P, P, P, i32, u64, i32, i32, i32, P, P, P, P, P, P, P, P, P, P, P]
+        L.ora_predict.argtypes = [i64, P, P, P, P, P, i32, P]
+        L.ora_rmse.argtypes = [i64, P, P, P, P, P, P, i32, P]
         _lib = L
     return _lib
 
@@ -246,3 +248,24 @@ def sacd_run(coords, vals, dims, R, seed, K, l_mode=L_DIAG, variant=VAR_GS_LAGGE
 def fit_from_f(f, xnorm2):
     """Reading C16: fit = 1 - sqrt(f)/||X||."""
     return 1.0 - np.sqrt(np.maximum(f, 0.0)) / np.sqrt(xnorm2) if xnorm2 > 0 else 0.0
+
+
+def predict(coords, dims, F):
+    """Eq 8 at the given coordinates (u32 [n][3])."""
+    c = np.ascontiguousarray(np.asarray(coords, dtype=np.uint32).reshape(-1, 3))
+    d = _dims(dims)
+    F = [np.ascontiguousarray(x, dtype=np.float64) for x in F]
+    out = np.zeros(c.shape[0], np.float64)
+    _check(lib().ora_predict(c.shape[0], _p(c), _p(d), _p(F[0]), _p(F[1]), _p(F[2]), F[0].shape[1], _p(out)))
+    return out
+
+
+def rmse(coords, vals, dims, F):
+    """Eq 30: held-out RMSE of the CP model F = [U, V, W]."""
+    c, v = _coo(coords, vals)
+    d = _dims(dims)
+    F = [np.ascontiguousarray(x, dtype=np.float64) for x in F]
+    r = C.c_double()
+    _check(lib().ora_rmse(v.shape[0], _p(c), _p(v), _p(d), _p(F[0]), _p(F[1]), _p(F[2]), F[0].shape[1],
+                          C.byref(r)))
+    return r.value

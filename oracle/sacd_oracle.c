@@ -22,6 +22,7 @@
  *                   or Eq 27 chosen by total importance Eq 25-26,
  *                   lagged by one sweep (C10)
  *   objective       Eq 6-7 over all cells (C1), via the Gram identity
+ *   predict / RMSE  Eq 8 at held-out coordinates; Eq 30
  *
  * Parity status: pinned by tests/test_oracle_pins.py (P1-P12 in DESIGN.md section 3).
  * The selection dynamics end to end (E, ti trajectories) are "parity unpinned": the paper
@@ -335,6 +336,46 @@ int ora_objective_sparse(const int64_t dims[3], int64_t nnz, const uint32_t *coo
   }
   *f_out = se + (model_norm2(G[0], G[1], G[2], R) - sx2);
   for (int n = 0; n < 3; n++) free(G[n]);
+  return ORA_OK;
+}
+
+/* ------------------------------------------------------------------ held-out evaluation
+ * Eq 8: xhat_qps = sum_{r=1}^R u_qr v_pr w_sr, summed over r in order.
+ * out[e] for the n test coordinates (u32 [n][3]); each index must be in range. */
+int ora_predict(int64_t n, const uint32_t *coords, const int64_t dims[3], const double *U, const double *V,
+                const double *W, int R, double *out) {
+  for (int64_t e = 0; e < n; e++)
+    for (int m = 0; m < 3; m++)
+      if ((int64_t)coords[3 * e + m] >= dims[m]) return ORA_ERANGE;
+#pragma omp parallel for schedule(static)
+  for (int64_t e = 0; e < n; e++) {
+    double xh = 0.0;
+    for (int r = 0; r < R; r++)
+      xh += U[(int64_t)coords[3 * e] * R + r] * V[(int64_t)coords[3 * e + 1] * R + r] *
+            W[(int64_t)coords[3 * e + 2] * R + r];
+    out[e] = xh;
+  }
+  return ORA_OK;
+}
+
+/* Eq 30: RMSE = sqrt( sum (x_test - xhat_test)^2 / n ), the squared errors summed
+ * sequentially in test-entry order.  n = 0 gives 0. */
+int ora_rmse(int64_t n, const uint32_t *coords, const float *vals, const int64_t dims[3], const double *U,
+             const double *V, const double *W, int R, double *rmse_out) {
+  double *xh = (double *)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+  if (!xh) return ORA_ENOMEM;
+  int rc = ora_predict(n, coords, dims, U, V, W, R, xh);
+  if (rc != ORA_OK) {
+    free(xh);
+    return rc;
+  }
+  double se = 0.0;
+  for (int64_t e = 0; e < n; e++) {
+    const double d = (double)vals[e] - xh[e];
+    se += d * d;
+  }
+  *rmse_out = n > 0 ? sqrt(se / (double)n) : 0.0;
+  free(xh);
   return ORA_OK;
 }
 

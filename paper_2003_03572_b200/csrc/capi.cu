@@ -1,6 +1,7 @@
 // capi.cu -- the C ABI of libsacd (include/sacd.h): context lifetime, the MTTKRP work
 // partition (host-side planning over row_ptr, done once at init), the sweep CUDA graph,
 // teacher-forcing entry points and profiling.
+#include <math.h>
 #include <string.h>
 
 #include <algorithm>
@@ -115,7 +116,7 @@ static void build_items(const std::vector<long long> &rp, long long I, long long
       sr.slot0 = nslots;
       sr.nslots = nseg;
       sr.row = (int)r;
-      sr.pad = 0;
+      sr.chunk0 = 0;
       for (long long q = 0; q < nseg; ++q) {
         WorkItem w;
         w.nz0 = s0 + q * T;
@@ -145,6 +146,22 @@ static void build_items(const std::vector<long long> &rp, long long I, long long
     w.slot = -1;
     items.push_back(w);
     r = j;
+  }
+}
+
+// two-level fix-up plan of a split-row list (sets SplitRow::chunk0)
+static void plan_fixup(std::vector<SplitRow> &splits, std::vector<FixChunk> &chunks) {
+  chunks.clear();
+  for (SplitRow &sr : splits) {
+    const long long nch = (sr.nslots + kFixChunk - 1) / kFixChunk;
+    sr.chunk0 = (int)chunks.size();
+    for (long long q = 0; q < nch; ++q) {
+      FixChunk fc;
+      fc.slot0 = sr.slot0 + q * kFixChunk;
+      fc.nslots = (int)std::min<long long>(kFixChunk, sr.nslots - q * kFixChunk);
+      fc.out = nch == 1 ? -(sr.row + 1) : (int)chunks.size();
+      chunks.push_back(fc);
+    }
   }
 }
 
@@ -196,7 +213,7 @@ static int capture_graph(Context &c) {
       c.kernels_per_sweep += 1;
   }
   cudaGetLastError();
-  if (!c.opt.use_graph || c.opt.profile) {
+  if (!c.opt.use_graph) {
     cudaGraphDestroy(g);
     return SACD_OK;
   }
@@ -228,13 +245,16 @@ static void destroy(sacd_ctx *c) {
     cudaFree(m.row_ptr);
     cudaFree(m.items);
     cudaFree(m.splits);
+    cudaFree(m.chunks);
     cudaFree(m.F);
     cudaFree(m.Z);
     cudaFree(m.G);
+    cudaFree(m.cmask);
   }
   cudaFree(c->st);
   cudaFree(c->M);
   cudaFree(c->partial);
+  cudaFree(c->fixbuf);
   cudaFree(c->Hr);
   cudaFree(c->Hd);
   cudaFree(c->row_part);
@@ -245,6 +265,7 @@ static void destroy(sacd_ctx *c) {
     for (int n = 0; n < 3; ++n) {
       cudaFree(sh.items[n]);
       cudaFree(sh.splits[n]);
+      cudaFree(sh.chunks[n]);
     }
     cudaFree(sh.M);
     cudaFree(sh.partial);
@@ -324,7 +345,7 @@ static int init_impl(Context *c, const uint32_t *coords, const float *vals, uint
 
   // partitions (host planning over row_ptr, once)
   const long long T = c->opt.nnz_per_item > 0 ? c->opt.nnz_per_item : 1024;
-  long long max_slots = 1, maxI = 1;
+  long long max_slots = 1, maxI = 1, max_chunks = 1;
   std::vector<long long> rps[3];
   for (int n = 0; n < 3; ++n) {
     ModeData &md = c->m[n];
@@ -343,8 +364,13 @@ static int init_impl(Context *c, const uint32_t *coords, const float *vals, uint
       md.n_items = (long long)items.size();
       md.n_splits = (long long)splits.size();
       md.n_slots = nslots;
+      std::vector<FixChunk> chunks;
+      plan_fixup(splits, chunks);
+      md.n_chunks = (long long)chunks.size();
+      max_chunks = std::max(max_chunks, md.n_chunks);
       SACD_TRY(upload(&md.items, items));
       SACD_TRY(upload(&md.splits, splits));
+      SACD_TRY(upload(&md.chunks, chunks));
       max_slots = std::max(max_slots, nslots);
       c->device_bytes += (long long)(items.size() * sizeof(WorkItem) + splits.size() * sizeof(SplitRow));
     }
@@ -369,8 +395,13 @@ static int init_impl(Context *c, const uint32_t *coords, const float *vals, uint
         build_items(rps[n], c->m[n].I, sh.plan[n].lo, sh.plan[n].hi, T, 32, items, splits, nslots);
         sh.n_items[n] = (long long)items.size();
         sh.n_splits[n] = (long long)splits.size();
+        std::vector<FixChunk> chunks;
+        plan_fixup(splits, chunks);
+        sh.n_chunks[n] = (long long)chunks.size();
+        max_chunks = std::max(max_chunks, sh.n_chunks[n]);
         SACD_TRY(upload(&sh.items[n], items));
         SACD_TRY(upload(&sh.splits[n], splits));
+        SACD_TRY(upload(&sh.chunks[n], chunks));
         slots_k = std::max(slots_k, nslots);
         c->m[n].n_items += sh.n_items[n];
         c->m[n].n_splits += sh.n_splits[n];
@@ -413,12 +444,16 @@ static int init_impl(Context *c, const uint32_t *coords, const float *vals, uint
     SACD_CUDA_TRY(cudaMalloc(&md.Z, zrows * P * rs));
     SACD_CUDA_TRY(cudaMemsetAsync(md.Z, 0, zrows * P * rs, s));
     SACD_CUDA_TRY(cudaMalloc(&md.G, (size_t)R * R * 8));
+    SACD_CUDA_TRY(cudaMalloc(&md.cmask, (size_t)std::max(1LL, md.I) * 4));
+    SACD_CUDA_TRY(cudaMemsetAsync(md.cmask, 0, (size_t)std::max(1LL, md.I) * 4, s));
     c->device_bytes += (long long)(2 * (size_t)md.I * P * rs + (size_t)R * R * 8);
   }
   c->max_row_blocks = (maxI + 31) / 32 + 1;  // >= ceil(I / rows_per_block) for every pitch
   c->gram_blocks = (int)std::min<long long>(296, std::max<long long>(1, (maxI + 63) / 64));
   SACD_CUDA_TRY(cudaMalloc(&c->M, (size_t)((maxI + 31) / 32 * 32) * P * rs));
   SACD_CUDA_TRY(cudaMalloc(&c->partial, (size_t)max_slots * P * rs));
+  SACD_CUDA_TRY(cudaMalloc(&c->fixbuf, (size_t)max_chunks * P * rs));
+  c->device_bytes += (long long)((size_t)max_chunks * P * rs);
   SACD_CUDA_TRY(cudaMalloc(&c->Hr, (size_t)P * P * rs));
   SACD_CUDA_TRY(cudaMalloc(&c->Hd, (size_t)R * R * 8));
   SACD_CUDA_TRY(cudaMalloc(&c->row_part, (size_t)c->max_row_blocks * 2 * 8));
@@ -609,7 +644,7 @@ int sacd_iterate(sacd_ctx *c, int32_t n) {
     return SACD_EINVAL;
   }
   for (int i = 0; i < n; ++i) {
-    if (c->graph_exec) {
+    if (c->graph_exec && !c->opt.profile) {
       cudaError_t e = cudaGraphLaunch(c->graph_exec, c->stream);
       if (e != cudaSuccess) {
         set_error(std::string("cudaGraphLaunch: ") + cudaGetErrorString(e));
@@ -680,6 +715,74 @@ int sacd_set_factors(sacd_ctx *c, int32_t mode, const double *in, int64_t ld) {
   if (rc == SACD_OK) rc = launch_gram(*c, mode);
   if (rc == SACD_OK && cudaStreamSynchronize(c->stream) != cudaSuccess) rc = SACD_ECUDA;
   return sticky(c, rc);
+}
+
+// held-out evaluation: predictions (out) and / or RMSE at n coordinates (host or device)
+static int eval_impl(Context *c, const uint32_t *coords, const float *vals, long long n, double *out,
+                     double *rmse) {
+  cudaStream_t s = c->stream;
+  const size_t nn = (size_t)std::max(1LL, n), nb = (size_t)std::max(1LL, (n + 7) / 8);
+  uint32_t *dc = nullptr;
+  float *dv = nullptr;
+  double *dout = nullptr, *part = nullptr, *sse = nullptr;
+  int *flag = nullptr;
+  int rc = SACD_OK, hflag = 0;
+  double hsse = 0.0;
+  auto ck = [&](cudaError_t e) {
+    if (e != cudaSuccess && rc == SACD_OK) {
+      set_error(std::string("sacd_predict/rmse: ") + cudaGetErrorString(e));
+      rc = e == cudaErrorMemoryAllocation ? SACD_ENOMEM : SACD_ECUDA;
+    }
+    return rc == SACD_OK;
+  };
+  if (ck(cudaMallocAsync(&dc, nn * 12, s)) && ck(cudaMallocAsync(&dout, nn * 8, s)) &&
+      ck(cudaMallocAsync(&part, nb * 8, s)) && ck(cudaMallocAsync(&sse, 8, s)) && ck(cudaMallocAsync(&flag, 4, s)) &&
+      (!vals || ck(cudaMallocAsync(&dv, nn * 4, s))) && ck(cudaMemsetAsync(flag, 0, 4, s)) &&
+      (n == 0 || ck(cudaMemcpyAsync(dc, coords, (size_t)n * 12, cudaMemcpyDefault, s))) &&
+      (!vals || n == 0 || ck(cudaMemcpyAsync(dv, vals, (size_t)n * 4, cudaMemcpyDefault, s)))) {
+    rc = launch_range_check(*c, dc, n, flag);
+    if (rc == SACD_OK && ck(cudaMemcpyAsync(&hflag, flag, 4, cudaMemcpyDeviceToHost, s)) &&
+        ck(cudaStreamSynchronize(s))) {
+      if (hflag) {
+        set_error("sacd_predict/rmse: coordinate index out of range");
+        rc = SACD_ERANGE;
+      } else {
+        rc = launch_predict(*c, dc, n, dv, out ? dout : nullptr, part, rmse ? sse : nullptr);
+        if (rc == SACD_OK && out && n > 0) ck(cudaMemcpyAsync(out, dout, (size_t)n * 8, cudaMemcpyDefault, s));
+        if (rc == SACD_OK && rmse) ck(cudaMemcpyAsync(&hsse, sse, 8, cudaMemcpyDeviceToHost, s));
+        if (rc == SACD_OK) ck(cudaStreamSynchronize(s));
+        if (rc == SACD_OK && rmse) *rmse = n > 0 ? sqrt(hsse / (double)n) : 0.0;
+      }
+    }
+  }
+  cudaFreeAsync(dc, s);
+  cudaFreeAsync(dv, s);
+  cudaFreeAsync(dout, s);
+  cudaFreeAsync(part, s);
+  cudaFreeAsync(sse, s);
+  cudaFreeAsync(flag, s);
+  cudaStreamSynchronize(s);
+  return rc;
+}
+
+int sacd_predict(sacd_ctx *c, const uint32_t *coords, int64_t n, double *out) {
+  CTX_CHECK(c);
+  if (n < 0 || (n > 0 && (!coords || !out))) {
+    set_error("sacd_predict: bad n / null pointer");
+    return SACD_EINVAL;
+  }
+  const int rc = eval_impl(c, coords, nullptr, n, out, nullptr);
+  return rc == SACD_ERANGE ? rc : sticky(c, rc);
+}
+
+int sacd_rmse(sacd_ctx *c, const uint32_t *coords, const float *vals, int64_t n, double *rmse) {
+  CTX_CHECK(c);
+  if (n < 0 || !rmse || (n > 0 && (!coords || !vals))) {
+    set_error("sacd_rmse: bad n / null pointer");
+    return SACD_EINVAL;
+  }
+  const int rc = eval_impl(c, coords, vals, n, nullptr, rmse);
+  return rc == SACD_ERANGE ? rc : sticky(c, rc);
 }
 
 int sacd_mttkrp(sacd_ctx *c, int32_t mode, double *out, int64_t ld) {
@@ -857,6 +960,12 @@ int sacd_profile_read(sacd_ctx *c, double ms[SACD_NUM_KCLASS], int64_t launches[
     if (ms) ms[i] = c->prof_ms[i];
     if (launches) launches[i] = c->prof_n[i];
   }
+  return SACD_OK;
+}
+
+int sacd_set_profile(sacd_ctx *c, int32_t on) {
+  CTX_CHECK(c);
+  c->opt.profile = on ? 1 : 0;
   return SACD_OK;
 }
 

@@ -86,10 +86,9 @@ __host__ __device__ constexpr bool h_in_smem() {
   return (size_t)RT * RT * sizeof(Real) <= 64 * 1024;
 }
 
-template <typename Real, int RT>
+template <typename Real, int RT, bool HS = h_in_smem<Real, RT>()>
 __host__ __device__ constexpr size_t rows_smem_bytes() {
-  return (h_in_smem<Real, RT>() ? (size_t)RT * RT * sizeof(Real) : 0) +
-         (size_t)rows_per_block<RT>() * (RT + 1) * sizeof(Real);
+  return (HS ? (size_t)RT * RT * sizeof(Real) : 0) + (size_t)rows_per_block<RT>() * (RT + 1) * sizeof(Real);
 }
 
 template <int RT>
@@ -363,6 +362,33 @@ __device__ __forceinline__ uint4 ld_stream_u4(const uint4 *p) {
   return v;
 }
 
+// Chunk support mask of each factor row: bit k = 16-byte chunk k (elements
+// [k*VEC, (k+1)*VEC)) holds a nonzero.  One warp per row (lane k tests chunk k); rows of at
+// most 32 chunks (RT * sizeof(Real) <= 512).  SaCD's projection leaves most factor entries
+// exactly zero (tools/factor_stats.py: ~80% on c4), and the skipping MTTKRP uses these masks
+// to gather only chunks where both the a-row and the b-row are nonzero.
+template <typename Real, int RT>
+__global__ void __launch_bounds__(256) k_chunk_mask(const Real *__restrict__ F, long long I,
+                                                   uint32_t *__restrict__ cmask) {
+  using VV = V16<Real>;
+  constexpr int NCH = RT / VV::N;
+  static_assert(NCH <= 32, "chunk masks hold at most 32 chunks");
+  const int lane = threadIdx.x & 31;
+  const long long w0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long row = w0; row < I; row += nw) {
+    bool nz = false;
+    if (lane < NCH) {
+      Real v[VV::N];
+      VV::get(__ldg(reinterpret_cast<const typename VV::T *>(F + row * RT) + lane), v);
+#pragma unroll
+      for (int c = 0; c < VV::N; ++c) nz |= (v[c] != Real(0));
+    }
+    const uint32_t m = __ballot_sync(0xffffffffu, nz);
+    if (lane == 0) cmask[row] = m;
+  }
+}
+
 template <typename Real, int RT, int SW, int NB, int MINB>
 __global__ void __launch_bounds__(256, MINB) k_mttkrp_sw(const WorkItem *__restrict__ items, long long n_items,
                                                         const uint4 *__restrict__ nzm,
@@ -533,39 +559,183 @@ __global__ void __launch_bounds__(256, MINB) k_mttkrp_lean(const WorkItem *__res
   else if (cur_row >= 0) SR::store_from(M + (long long)cur_row * RT + lane * VEC, acc);
 }
 
-// Heavy rows split across items: M_row = sum of the row's partials.  One block per split
-// row; warp w sums slots w, w+8, ... and the 8 warp sums are combined in warp order, so the
-// result is deterministic.
+// Support-skipping lean MTTKRP (exact).  Per nonzero, only the 16-byte chunks where both the
+// fiber's a-row and the nonzero's b-row are nonzero (chunk masks, k_chunk_mask) are gathered
+// and accumulated; a-rows are gathered only on their nonzero chunks.  Bitwise equal to the
+// dense kernels: a skipped b chunk is zero (x*0 adds an exact zero), and a column whose a
+// entry is zero only ever enters M as fma(0, facc, acc) = acc.  Lane l of a worker owns the
+// chunks k*SW + l, i.e. bit k*SW + l of a mask.  The masks of a batch's nonzeros are
+// gathered one batch ahead (lane l: masks of its nonzero's a- and b-rows).
+template <typename Real, int RT, int SW, int D, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_mttkrp_skip(const WorkItem *__restrict__ items, long long n_items,
+                                                          const uint4 *__restrict__ nzm,
+                                                          const Real *__restrict__ A, const Real *__restrict__ B,
+                                                          const uint32_t *__restrict__ cmA,
+                                                          const uint32_t *__restrict__ cmB,
+                                                          Real *__restrict__ M, Real *__restrict__ partial) {
+  using SR = SubRow<Real, RT, SW>;
+  using VV = V16<Real>;
+  using VT = typename VV::T;
+  constexpr int E = SR::E;
+  constexpr int NV = SR::NV;
+  constexpr int VEC = VV::N;
+  static_assert(NV >= 1, "row narrower than a sub-warp of 16-byte chunks");
+  static_assert(RT / VEC <= 32, "chunk masks hold at most 32 chunks");
+  const int lane = threadIdx.x & (SW - 1);
+  const unsigned mask = SW == 32 ? 0xffffffffu : (((1u << SW) - 1u) << (threadIdx.x & 31 & ~(SW - 1)));
+  const long long item = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / SW;
+  if (item >= n_items) return;
+  const long long nz0 = items[item].nz0, nz1 = items[item].nz1;
+  const int slot = (int)items[item].slot;
+  const Real *Al = A + lane * VEC;
+  const Real *Bl = B + lane * VEC;
+  Real arow[E], acc[E], facc[E];
+#pragma unroll
+  for (int k = 0; k < E; ++k) acc[k] = facc[k] = arow[k] = Real(0);
+  uint32_t am_cur = 0;  // chunk mask of the current fiber's a-row
+  int cur_row = -1;
+  // batch t: metadata `my` and the combined / a masks of its nonzeros; batch t+1: `nx`
+  // (metadata) whose masks are gathered at the start of batch t; batch t+2: `nx2`.
+  uint4 my = make_uint4(0u, 0u, 0u, 0u), nx = make_uint4(0u, 0u, 0u, 0u);
+  if (nz0 + lane < nz1) my = ld_stream_u4(nzm + nz0 + lane);
+  if (nz0 + SW + lane < nz1) nx = ld_stream_u4(nzm + nz0 + SW + lane);
+  if (lane == 0) my.y |= kFiberStart | kRowStart;  // an item starts a row and a fiber
+  uint32_t my_am = 0, my_m = 0;
+  if (nz0 + lane < nz1) {
+    my_am = __ldg(cmA + (my.x & kIdxMask));
+    my_m = my_am & __ldg(cmB + (my.y & kIdxMask));
+  }
+  for (long long base = nz0; base < nz1; base += SW) {
+    uint4 nx2 = make_uint4(0u, 0u, 0u, 0u);
+    if (base + 2 * SW + lane < nz1) nx2 = ld_stream_u4(nzm + base + 2 * SW + lane);
+    uint32_t nx_am = 0, nx_m = 0;
+    if (base + SW + lane < nz1) {
+      nx_am = __ldg(cmA + (nx.x & kIdxMask));
+      nx_m = nx_am & __ldg(cmB + (nx.y & kIdxMask));
+    }
+    uint32_t fb[SW], mb[SW];
+    Real bb[D + 1][E];
+    auto issue = [&](int j) {
+      fb[j] = __shfl_sync(mask, my.y, j, SW);
+      mb[j] = __shfl_sync(mask, my_m, j, SW);
+      const VT *p = reinterpret_cast<const VT *>(Bl + (long long)(fb[j] & kIdxMask) * RT);
+#pragma unroll
+      for (int k = 0; k < NV; ++k)
+        if ((mb[j] >> (k * SW + lane)) & 1u) VV::get(__ldg(p + k * SW), &bb[j % (D + 1)][k * VEC]);
+    };
+#pragma unroll
+    for (int j = 0; j < D && j < SW; ++j) issue(j);
+#pragma unroll
+    for (int j = 0; j < SW; ++j) {
+      if (j + D < SW) issue(j + D);
+      const Real x = (Real)__uint_as_float(__shfl_sync(mask, my.z, j, SW));
+      if (fb[j] & kFiberStart) {
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {  // close the previous fiber on its a-row's nonzero chunks
+          const bool on = (am_cur >> (k * SW + lane)) & 1u;
+#pragma unroll
+          for (int cc = 0; cc < VEC; ++cc) {
+            if (on) acc[k * VEC + cc] = fma(arow[k * VEC + cc], facc[k * VEC + cc], acc[k * VEC + cc]);
+            facc[k * VEC + cc] = Real(0);
+          }
+        }
+        if (fb[j] & kRowStart) {
+          if (slot >= 0) SR::store_from(partial + (long long)slot * RT + lane * VEC, acc);
+          else if (cur_row >= 0) SR::store_from(M + (long long)cur_row * RT + lane * VEC, acc);
+#pragma unroll
+          for (int k = 0; k < E; ++k) acc[k] = Real(0);
+          cur_row = (int)__shfl_sync(mask, my.w, j, SW);
+        }
+        am_cur = __shfl_sync(mask, my_am, j, SW);
+        const VT *p = reinterpret_cast<const VT *>(Al + (long long)(__shfl_sync(mask, my.x, j, SW) & kIdxMask) * RT);
+#pragma unroll
+        for (int k = 0; k < NV; ++k)
+          if ((am_cur >> (k * SW + lane)) & 1u) VV::get(__ldg(p + k * SW), &arow[k * VEC]);
+      }
+#pragma unroll
+      for (int k = 0; k < NV; ++k) {
+        if ((mb[j] >> (k * SW + lane)) & 1u) {
+#pragma unroll
+          for (int cc = 0; cc < VEC; ++cc)
+            facc[k * VEC + cc] = fma(x, bb[j % (D + 1)][k * VEC + cc], facc[k * VEC + cc]);
+        }
+      }
+    }
+    my = nx;
+    nx = nx2;
+    my_am = nx_am;
+    my_m = nx_m;
+  }
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const bool on = (am_cur >> (k * SW + lane)) & 1u;
+#pragma unroll
+    for (int cc = 0; cc < VEC; ++cc)
+      if (on) acc[k * VEC + cc] = fma(arow[k * VEC + cc], facc[k * VEC + cc], acc[k * VEC + cc]);
+  }
+  if (slot >= 0) SR::store_from(partial + (long long)slot * RT + lane * VEC, acc);
+  else if (cur_row >= 0) SR::store_from(M + (long long)cur_row * RT + lane * VEC, acc);
+}
+
+// Heavy rows split across items: M_row = sum of the row's partial slots, in two levels so
+// that a row with thousands of slots (a 10%-of-nnz slice) is summed in parallel:
+//   level 1: one warp per FixChunk sums its <= kFixChunk slots (4 independent running sums
+//            over slots j = u mod 4, combined in u order) -> M[row] or a level-2 row;
+//   level 2: one warp per split row with several chunks sums its chunk rows in order.
+// Fixed orders throughout: deterministic.
 template <typename Real, int RT>
-__global__ void __launch_bounds__(256) k_fixup(const SplitRow *__restrict__ splits, long long n,
-                                               const Real *__restrict__ partial, Real *__restrict__ M) {
-  constexpr int CPL = RT >= 32 ? RT / 32 : 1;  // columns per lane
-  __shared__ Real red[8][RT];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const SplitRow sr = splits[blockIdx.x];
+__global__ void __launch_bounds__(256) k_fix1(const FixChunk *__restrict__ chunks, long long n,
+                                              const Real *__restrict__ partial, Real *__restrict__ buf,
+                                              Real *__restrict__ M) {
+  constexpr int CPL = RT >= 32 ? RT / 32 : 1;  // columns per lane: c = lane + 32 q
+  const int lane = threadIdx.x & 31;
+  const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (w >= n) return;
+  const FixChunk fc = chunks[w];
+  Real acc[4][CPL];
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int q = 0; q < CPL; ++q) acc[u][q] = Real(0);
+  for (int j0 = 0; j0 < fc.nslots; j0 += 4) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (j0 + u < fc.nslots) {
+        const Real *p = partial + (fc.slot0 + j0 + u) * RT;
+#pragma unroll
+        for (int q = 0; q < CPL; ++q)
+          if (lane + 32 * q < RT) acc[u][q] += p[lane + 32 * q];
+      }
+    }
+  }
+  Real *dst = fc.out < 0 ? M + (long long)(-fc.out - 1) * RT : buf + (long long)fc.out * RT;
+#pragma unroll
+  for (int q = 0; q < CPL; ++q)
+    if (lane + 32 * q < RT) dst[lane + 32 * q] = (acc[0][q] + acc[1][q]) + (acc[2][q] + acc[3][q]);
+}
+
+template <typename Real, int RT>
+__global__ void __launch_bounds__(256) k_fix2(const SplitRow *__restrict__ splits, long long n,
+                                              const Real *__restrict__ buf, Real *__restrict__ M) {
+  constexpr int CPL = RT >= 32 ? RT / 32 : 1;
+  const int lane = threadIdx.x & 31;
+  const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (w >= n) return;
+  const SplitRow sr = splits[w];
+  const long long nch = (sr.nslots + kFixChunk - 1) / kFixChunk;
+  if (nch <= 1) return;  // written by level 1
   Real acc[CPL];
 #pragma unroll
   for (int q = 0; q < CPL; ++q) acc[q] = Real(0);
-  for (long long k = w; k < sr.nslots; k += 8) {
-    const Real *p = partial + (sr.slot0 + k) * RT;
+  for (long long k = 0; k < nch; ++k) {
+    const Real *p = buf + (sr.chunk0 + k) * RT;
 #pragma unroll
-    for (int q = 0; q < CPL; ++q) {
-      const int c = lane + 32 * q;
-      if (c < RT) acc[q] += p[c];
-    }
+    for (int q = 0; q < CPL; ++q)
+      if (lane + 32 * q < RT) acc[q] += p[lane + 32 * q];
   }
 #pragma unroll
-  for (int q = 0; q < CPL; ++q) {
-    const int c = lane + 32 * q;
-    if (c < RT) red[w][c] = acc[q];
-  }
-  __syncthreads();
-  for (int c = threadIdx.x; c < RT; c += 256) {
-    Real s = red[0][c];
-#pragma unroll
-    for (int k = 1; k < 8; ++k) s += red[k][c];
-    M[(long long)sr.row * RT + c] = s;
-  }
+  for (int q = 0; q < CPL; ++q)
+    if (lane + 32 * q < RT) M[(long long)sr.row * RT + lane + 32 * q] = acc[q];
 }
 
 // ------------------------------------------------------------------ H, L and the branch
@@ -609,7 +779,7 @@ __global__ void __launch_bounds__(256) k_prepare(int mode, int R, const double *
 // One thread per row (rows are independent given A and B: Eq ucap).  The block's
 // rows are staged in shared memory with an odd stride (RT+1) so the per-thread column
 // walk is bank-conflict free; H is staged in shared memory when it fits.
-template <typename Real, int RT>
+template <typename Real, int RT, bool HS>
 __global__ void __launch_bounds__(rows_per_block<RT>())
     k_sacd_rows(long long row_begin, long long row_end, int R, int mode, int l_mode,
                 const long long *__restrict__ row_ptr,
@@ -619,7 +789,6 @@ __global__ void __launch_bounds__(rows_per_block<RT>())
                 long long *__restrict__ e_part, long long *__restrict__ ech_part) {
   constexpr int TR = rows_per_block<RT>();
   constexpr int US = RT + 1;
-  constexpr bool HS = h_in_smem<Real, RT>();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Real *Hs = reinterpret_cast<Real *>(smem_raw);
   Real *Us = reinterpret_cast<Real *>(smem_raw + (HS ? (size_t)RT * RT * sizeof(Real) : 0));
@@ -1071,17 +1240,82 @@ __global__ void k_convert_out(const Real *__restrict__ src, long long rows, int 
 }
 
 
+// ------------------------------------------------------------------ held-out evaluation
+// Eq 8 at test coordinates: one warp per entry, lane l multiplies columns
+// l, l+32, ... and the warp sums them by a fixed xor tree.  With vals != nullptr also the
+// squared error (Eq 30), reduced per block in a fixed order into part[block].
+template <typename Real, int RT>
+__global__ void __launch_bounds__(256) k_predict(const uint32_t *__restrict__ coords, long long n,
+                                                 const Real *__restrict__ U, const Real *__restrict__ V,
+                                                 const Real *__restrict__ W, const float *__restrict__ vals,
+                                                 double *__restrict__ out, double *__restrict__ part) {
+  constexpr int CPL = RT >= 32 ? RT / 32 : 1;
+  __shared__ double red[8];
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  const long long e = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  double se = 0.0;
+  if (e < n) {
+    const long long q = coords[3 * e], p = coords[3 * e + 1], s = coords[3 * e + 2];
+    double xh = 0.0;
+#pragma unroll
+    for (int k = 0; k < CPL; ++k) {
+      const int c = lane + 32 * k;
+      if (c < RT) xh += (double)U[q * RT + c] * (double)V[p * RT + c] * (double)W[s * RT + c];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) xh += __shfl_xor_sync(0xffffffffu, xh, o);
+    if (lane == 0) {
+      if (out) out[e] = xh;
+      if (vals) {
+        const double d = (double)vals[e] - xh;
+        se = d * d;
+      }
+    }
+  }
+  if (part) {
+    if (lane == 0) red[wp] = se;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int k = 0; k < 8; ++k) t += red[k];
+      part[blockIdx.x] = t;
+    }
+  }
+}
+
+__global__ void k_range_check(const uint32_t *__restrict__ coords, long long n, long long d0, long long d1,
+                              long long d2, int *__restrict__ flag) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x)
+    if (coords[3 * e] >= d0 || coords[3 * e + 1] >= d1 || coords[3 * e + 2] >= d2) atomicOr(flag, 1);
+}
+
+// fixed-order sum of the block partials (one block)
+__global__ void __launch_bounds__(1024) k_sum_parts(const double *__restrict__ part, long long nb,
+                                                    double *__restrict__ out) {
+  __shared__ double sd[1024];
+  double t = 0.0;
+  for (long long b = threadIdx.x; b < nb; b += 1024) t += part[b];
+  sd[threadIdx.x] = t;
+  __syncthreads();
+  for (int o = 512; o > 0; o >>= 1) {
+    if (threadIdx.x < o) sd[threadIdx.x] += sd[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = sd[0];
+}
+
 // ------------------------------------------------------------------ launch implementations
 template <typename Real, int RT>
 struct Impl {
   static int mttkrp(Context &c, int mode, void *out_v) {
     ModeData &md = c.m[mode];
-    return mttkrp_on(c, mode, md.items, md.n_items, md.splits, md.n_splits, reinterpret_cast<Real *>(out_v),
+    return mttkrp_on(c, mode, md.items, md.n_items, md.splits, md.n_splits, md.chunks, md.n_chunks,
+                     reinterpret_cast<Real *>(out_v),
                      reinterpret_cast<Real *>(c.partial));
   }
 
   static int mttkrp_on(Context &c, int mode, const WorkItem *items, long long n_items, const SplitRow *splits,
-                       long long n_splits, Real *out, Real *partial) {
+                       long long n_splits, const FixChunk *chunks, long long n_chunks, Real *out, Real *partial) {
     ModeData &md = c.m[mode];
     const Real *A = reinterpret_cast<const Real *>(c.m[md.a].F);
     const Real *B = reinterpret_cast<const Real *>(c.m[md.b].F);
@@ -1110,7 +1344,7 @@ struct Impl {
         else if (var == 13) gos(k_mttkrp_sw<Real, RT, SW, 4, 3>);
         else if (var == 14) gos(k_mttkrp_sw<Real, RT, SW, 8, 2>);
         else if (var == 15) gos(k_mttkrp_sw<Real, RT, SW, 2, 6>);
-        else if (var >= 20 && var < 30) {
+        else if (var >= 20 && var < 50) {
           // lean kernel: E elements per lane -> SW = RT / E lanes per worker
           constexpr int VEC = V16<Real>::N;
           constexpr int E8 = 8 < VEC ? VEC : 8;
@@ -1121,11 +1355,34 @@ struct Impl {
             const long long lb = (n_items * sw + 255) / 256;
             kern<<<(unsigned)lb, 256, 0, c.stream>>>(items, n_items, md.nzm, A, B, out, partial);
           };
+          if constexpr (RT / VEC <= 32) {
+            if (var == 26 || var == 27 || var == 28) {
+              constexpr int EL = sizeof(Real) == 8 ? E4 : E8;
+              constexpr int SWL = sizeof(Real) == 8 ? SW4 : SW8;
+              const uint32_t *cmA = c.m[md.a].cmask, *cmB = c.m[md.b].cmask;
+              (void)EL;
+              auto gok = [&](auto kern) {
+                const long long lb = (n_items * SWL + 255) / 256;
+                kern<<<(unsigned)lb, 256, 0, c.stream>>>(items, n_items, md.nzm, A, B, cmA, cmB, out, partial);
+              };
+              if (var == 26) gok(k_mttkrp_skip<Real, RT, SWL, 1, sizeof(Real) == 8 ? 3 : 2>);
+              else if (var == 27) gok(k_mttkrp_skip<Real, RT, SWL, 2, 2>);
+              else gok(k_mttkrp_skip<Real, RT, SWL, 1, 2>);
+              SACD_CUDA_TRY(cudaGetLastError());
+              SACD_TRY(prof_end(c, 0, pe));
+              goto fixup;
+            }
+          }
           if (var == 20) gol(k_mttkrp_lean<Real, RT, SW4, 1, 4>, SW4);
           else if (var == 21) gol(k_mttkrp_lean<Real, RT, SW4, 2, 3>, SW4);
           else if (var == 22) gol(k_mttkrp_lean<Real, RT, SW8, 1, 2>, SW8);
           else if (var == 23) gol(k_mttkrp_lean<Real, RT, SW8, 1, 3>, SW8);
           else if (var == 24) gol(k_mttkrp_lean<Real, RT, SW4, 1, 3>, SW4);
+          else if (var == 40) gol(k_mttkrp_lean<Real, RT, sub_warp_lanes<Real, RT>(), 1, 6>, sub_warp_lanes<Real, RT>());
+          else if (var == 41) gol(k_mttkrp_lean<Real, RT, sub_warp_lanes<Real, RT>(), 1, 5>, sub_warp_lanes<Real, RT>());
+          else if (var == 42) gol(k_mttkrp_lean<Real, RT, sub_warp_lanes<Real, RT>(), 2, 5>, sub_warp_lanes<Real, RT>());
+          else if (var == 43) gol(k_mttkrp_lean<Real, RT, sub_warp_lanes<Real, RT>(), 2, 4>, sub_warp_lanes<Real, RT>());
+          else if (var == 44) gol(k_mttkrp_lean<Real, RT, sub_warp_lanes<Real, RT>(), 1, 8>, sub_warp_lanes<Real, RT>());
           else gol(k_mttkrp_lean<Real, RT, SW8, 2, 2>, SW8);
         }
         else if (sizeof(Real) == 8 && RT >= 256) {
@@ -1148,9 +1405,12 @@ struct Impl {
     }
     SACD_CUDA_TRY(cudaGetLastError());
     SACD_TRY(prof_end(c, 0, pe));
+  fixup:
     if (n_splits > 0) {
       pe = prof_begin(c, 1);
-      k_fixup<Real, RT><<<(unsigned)n_splits, 256, 0, c.stream>>>(splits, n_splits, partial, out);
+      Real *buf = reinterpret_cast<Real *>(c.fixbuf);
+      k_fix1<Real, RT><<<(unsigned)((n_chunks + 7) / 8), 256, 0, c.stream>>>(chunks, n_chunks, partial, buf, out);
+      k_fix2<Real, RT><<<(unsigned)((n_splits + 7) / 8), 256, 0, c.stream>>>(splits, n_splits, buf, out);
       SACD_CUDA_TRY(cudaGetLastError());
       SACD_TRY(prof_end(c, 1, pe));
     }
@@ -1163,6 +1423,7 @@ struct Impl {
   static int sharded_mttkrp_merge(Context &c, int mode) {
     for (Shard &sh : c.shards)
       SACD_TRY(mttkrp_on(c, mode, sh.items[mode], sh.n_items[mode], sh.splits[mode], sh.n_splits[mode],
+                         sh.chunks[mode], sh.n_chunks[mode],
                          reinterpret_cast<Real *>(sh.M), reinterpret_cast<Real *>(sh.partial)));
     Real *xrow = reinterpret_cast<Real *>(c.xrow);
     for (Shard &sh : c.shards)
@@ -1198,10 +1459,8 @@ struct Impl {
       long long *e_part = sh.cnt_part, *ech_part = sh.cnt_part + c.max_row_blocks;
       int pe = prof_begin(c, 3);
       if (nblk > 0)
-        k_sacd_rows<Real, RT><<<(unsigned)nblk, TR, smem, c.stream>>>(
-            rlo, rhi, c.R, mode, c.opt.l_mode, md.row_ptr, reinterpret_cast<const Real *>(sh.M),
-            reinterpret_cast<Real *>(md.F), reinterpret_cast<Real *>(md.Z), reinterpret_cast<const Real *>(c.Hr),
-            c.st, dec, ti_part, md_part, e_part, ech_part);
+        SACD_TRY(rows(c, nblk, rlo, rhi, mode, reinterpret_cast<const Real *>(sh.M), dec, ti_part, md_part, e_part,
+                      ech_part));
       SACD_CUDA_TRY(cudaGetLastError());
       SACD_TRY(prof_end(c, 3, pe));
       pe = prof_begin(c, 4);
@@ -1222,6 +1481,7 @@ struct Impl {
     SACD_CUDA_TRY(cudaGetLastError());
     SACD_TRY(prof_end(c, 5, pe));
     if (c.comm) SACD_TRY(nccl_broadcast_rows(c, mode));
+    SACD_TRY(chunk_mask(c, mode));
     return SACD_OK;
   }
 
@@ -1276,7 +1536,20 @@ struct Impl {
         0, md.I, c.R, reinterpret_cast<const Real *>(md.F), c.gram_part);
     k_gram_reduce<<<(c.R * c.R + 255) / 256, 256, 0, c.stream>>>(c.R, c.gram_blocks, c.gram_part, md.G);
     SACD_CUDA_TRY(cudaGetLastError());
+    SACD_TRY(chunk_mask(c, mode));
     return prof_end(c, 4, pe);
+  }
+
+  // chunk support masks of F_mode (used by the skipping MTTKRP of the other modes)
+  static int chunk_mask(Context &c, int mode) {
+    if constexpr (RT / V16<Real>::N <= 32) {
+      ModeData &md = c.m[mode];
+      if (md.I > 0)
+        k_chunk_mask<Real, RT><<<grid1d(md.I * 32), 256, 0, c.stream>>>(reinterpret_cast<const Real *>(md.F), md.I,
+                                                                         md.cmask);
+      SACD_CUDA_TRY(cudaGetLastError());
+    }
+    return SACD_OK;
   }
 
   static int prepare(Context &c, int mode, int branch_override, bool begin_sweep, int write_state) {
@@ -1301,9 +1574,7 @@ struct Impl {
     double *ti_part = c.row_part, *md_part = c.row_part + c.max_row_blocks;
     long long *e_part = c.cnt_part, *ech_part = c.cnt_part + c.max_row_blocks;
     int pe = prof_begin(c, 3);
-    k_sacd_rows<Real, RT><<<(unsigned)nblk, TR, smem, c.stream>>>(
-        0, md.I, c.R, mode, c.opt.l_mode, md.row_ptr, M, reinterpret_cast<Real *>(md.F), reinterpret_cast<Real *>(md.Z),
-        reinterpret_cast<const Real *>(c.Hr), c.st, dec, ti_part, md_part, e_part, ech_part);
+    SACD_TRY(rows(c, nblk, 0, md.I, mode, M, dec, ti_part, md_part, e_part, ech_part));
     SACD_CUDA_TRY(cudaGetLastError());
     SACD_TRY(prof_end(c, 3, pe));
     SACD_TRY(gram(c, mode));
@@ -1331,9 +1602,43 @@ struct Impl {
     return SACD_OK;
   }
 
+  // predictions (out) and / or the squared-error sum (sse) at n device coordinates
+  static int predict(Context &c, const uint32_t *coords, long long n, const float *vals, double *out, double *part,
+                     double *sse) {
+    const long long nb = (n + 7) / 8;
+    if (n > 0)
+      k_predict<Real, RT><<<(unsigned)nb, 256, 0, c.stream>>>(
+          coords, n, reinterpret_cast<const Real *>(c.m[0].F), reinterpret_cast<const Real *>(c.m[1].F),
+          reinterpret_cast<const Real *>(c.m[2].F), vals, out, part);
+    if (sse) k_sum_parts<<<1, 1024, 0, c.stream>>>(part, n > 0 ? nb : 0, sse);
+    SACD_CUDA_TRY(cudaGetLastError());
+    return SACD_OK;
+  }
+
+  // the fused row update over rows [rlo, rhi) (nblk blocks); opt.reserved[0] = 1 reads H
+  // from global memory (L1) instead of staging it in shared memory
+  static int rows(Context &c, long long nblk, long long rlo, long long rhi, int mode, const Real *M, uint8_t *dec,
+                  double *ti_part, double *md_part, long long *e_part, long long *ech_part) {
+    constexpr int TR = rows_per_block<RT>();
+    ModeData &md = c.m[mode];
+    auto go = [&](auto kern, size_t smem) {
+      if (nblk > 0)
+        kern<<<(unsigned)nblk, TR, smem, c.stream>>>(rlo, rhi, c.R, mode, c.opt.l_mode, md.row_ptr, M,
+                                                      reinterpret_cast<Real *>(md.F), reinterpret_cast<Real *>(md.Z),
+                                                      reinterpret_cast<const Real *>(c.Hr), c.st, dec, ti_part,
+                                                      md_part, e_part, ech_part);
+    };
+    if (c.opt.reserved[0] == 1) go(k_sacd_rows<Real, RT, false>, rows_smem_bytes<Real, RT, false>());
+    else go(k_sacd_rows<Real, RT, h_in_smem<Real, RT>()>, rows_smem_bytes<Real, RT>());
+    SACD_CUDA_TRY(cudaGetLastError());
+    return SACD_OK;
+  }
+
   static int setup(Context &c) {
-    constexpr size_t smem = rows_smem_bytes<Real, RT>();
-    SACD_CUDA_TRY(cudaFuncSetAttribute(k_sacd_rows<Real, RT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    SACD_CUDA_TRY(cudaFuncSetAttribute(k_sacd_rows<Real, RT, h_in_smem<Real, RT>()>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rows_smem_bytes<Real, RT>()));
+    SACD_CUDA_TRY(cudaFuncSetAttribute(k_sacd_rows<Real, RT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)rows_smem_bytes<Real, RT, false>()));
     return SACD_OK;
   }
 };
@@ -1408,6 +1713,17 @@ int launch_mode_update(Context &c, int mode, int branch_override, bool begin_swe
 }
 
 int launch_initial_fit(Context &c) { SACD_DISPATCH(c, I_::initial_fit(c)); }
+
+int launch_range_check(Context &c, const uint32_t *coords, long long n, int *flag) {
+  if (n > 0) k_range_check<<<grid1d(n), 256, 0, c.stream>>>(coords, n, c.dims[0], c.dims[1], c.dims[2], flag);
+  SACD_CUDA_TRY(cudaGetLastError());
+  return SACD_OK;
+}
+
+int launch_predict(Context &c, const uint32_t *coords, long long n, const float *vals, double *out, double *part,
+                   double *sse) {
+  SACD_DISPATCH(c, I_::predict(c, coords, n, vals, out, part, sse));
+}
 
 int launch_sharded_mode_update(Context &c, int mode, int branch_override, bool begin_sweep, bool end_sweep,
                                uint8_t *decisions_dev) {

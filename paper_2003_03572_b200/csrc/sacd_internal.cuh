@@ -46,7 +46,16 @@ struct WorkItem {
 
 struct SplitRow {
   long long slot0, nslots;
-  int row, pad;
+  int row, chunk0;  // chunk0: first FixChunk of this row (ceil(nslots / kFixChunk) chunks)
+};
+
+// Fix-up of split rows in two levels: chunk c sums slots [slot0, slot0 + nslots) (at most
+// kFixChunk) in slot order into M[row] directly (out < 0: row = -out - 1, single-chunk
+// rows) or into the level-2 buffer row `out`; level 2 sums a row's chunk rows in order.
+constexpr int kFixChunk = 64;
+struct FixChunk {
+  long long slot0;
+  int nslots, out;
 };
 
 constexpr int kRing = 4096;
@@ -84,9 +93,12 @@ struct ModeData {
   long long n_items = 0;
   SplitRow *splits = nullptr;
   long long n_splits = 0, n_slots = 0;
+  FixChunk *chunks = nullptr;
+  long long n_chunks = 0;
   void *F = nullptr;              // Real[I * pitch]
   void *Z = nullptr;              // Real[ceil32(I) * pitch]  (z_prev, TT layout)
   double *G = nullptr;            // fp64 R x R Gram of F
+  uint32_t *cmask = nullptr;      // [I] 16-byte chunk support mask of each row of F (k_chunk_mask)
 };
 
 // slice sharding plan of one mode (capi.cu; see sacd_shard_plan in include/sacd.h)
@@ -104,6 +116,8 @@ struct Shard {
   long long n_items[3] = {0, 0, 0};
   SplitRow *splits[3] = {nullptr, nullptr, nullptr};
   long long n_splits[3] = {0, 0, 0};
+  FixChunk *chunks[3] = {nullptr, nullptr, nullptr};
+  long long n_chunks[3] = {0, 0, 0};
   void *M = nullptr;             // Real [maxI * pitch]
   void *partial = nullptr;       // Real [slots * pitch]
   double *row_part = nullptr;    // 2 * max row blocks
@@ -125,6 +139,7 @@ struct Context {
   // scratch
   void *M = nullptr;              // Real[ceil32(maxI) * pitch] (TT layout)
   void *partial = nullptr;        // Real[max slots * pitch]
+  void *fixbuf = nullptr;         // Real[max chunks * pitch] (level-2 fix-up rows)
   void *Hr = nullptr;             // Real[pitch * pitch]
   double *Hd = nullptr;           // R x R
   double *row_part = nullptr;     // 4 * max row blocks (ti, mdot) as doubles
@@ -170,6 +185,9 @@ int launch_mode_update(Context &c, int mode, int branch_override, bool begin_swe
                        uint8_t *decisions_dev);
 int launch_gram(Context &c, int mode);
 int launch_initial_fit(Context &c);
+int launch_range_check(Context &c, const uint32_t *coords_dev, long long n, int *flag_dev);
+int launch_predict(Context &c, const uint32_t *coords_dev, long long n, const float *vals_dev, double *out_dev,
+                   double *part_dev, double *sse_dev);  // vals/out/sse may be null
 int launch_convert_in(Context &c, const double *src_dev, long long rows, void *dst, bool tt_layout);
 int launch_convert_out(Context &c, const void *src, long long rows, double *dst_dev, bool tt_layout);
 int launch_hessian_only(Context &c, int mode);

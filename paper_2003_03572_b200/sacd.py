@@ -30,7 +30,7 @@ EXPORTS = ("sacd_default_options", "sacd_init", "sacd_iterate", "sacd_sync", "sa
            "sacd_stats", "sacd_get_info", "sacd_free", "sacd_last_error", "sacd_set_factors", "sacd_get_zprev",
            "sacd_set_zprev", "sacd_mttkrp", "sacd_time_mttkrp", "sacd_gram", "sacd_hessian", "sacd_mode_update",
            "sacd_layout", "sacd_profile_read", "sacd_profile_reset", "sacd_shard_plan", "sacd_abi_sizes",
-           "sacd_nccl_unique_id")
+           "sacd_nccl_unique_id", "sacd_predict", "sacd_rmse", "sacd_set_profile")
 
 
 class Options(C.Structure):
@@ -99,6 +99,9 @@ def load_library(path: str = LIB_PATH):
     L.sacd_nccl_unique_id.argtypes = [P]
     L.sacd_abi_sizes.argtypes = [P]
     L.sacd_shard_plan.argtypes = [P, i64, i32, i32, P]
+    L.sacd_predict.argtypes = [P, P, i64, P]
+    L.sacd_set_profile.argtypes = [P, i32]
+    L.sacd_rmse.argtypes = [P, P, P, i64, C.POINTER(d)]
     sz = (C.c_int32 * 4)()
     L.sacd_abi_sizes(sz)
     if tuple(sz) != (1, C.sizeof(Options), C.sizeof(IterStats), C.sizeof(Info)):
@@ -144,7 +147,7 @@ class Sacd:
 
     def __init__(self, coords, vals, dims, rank, seed, *, precision="f64", l_mode="diag", variant="gs",
                  device=-1, stream=None, use_graph=True, profile=False, nnz_per_item=0, mttkrp_variant=0,
-                 world_size=1, world_rank=0, nccl_id=None, force_sharded=False, emulate_ranks=0):
+                 world_size=1, world_rank=0, nccl_id=None, force_sharded=False, emulate_ranks=0, rows_variant=0):
         L = load_library()
         o = Options()
         L.sacd_default_options(C.byref(o))
@@ -161,6 +164,7 @@ class Sacd:
         o.rank = int(world_rank)
         o.force_sharded = int(bool(force_sharded))
         o.emulate_ranks = int(emulate_ranks)
+        o.reserved[0] = int(rows_variant)
         self._nccl_id = None
         if nccl_id is not None:
             self._nccl_id = C.create_string_buffer(bytes(nccl_id), 128)
@@ -297,5 +301,25 @@ class Sacd:
         _check(load_library().sacd_profile_read(self._h, _ptr(ms), _ptr(n)))
         return {k: (float(ms[i]), int(n[i])) for i, k in enumerate(KCLASS)}
 
+    def set_profile(self, on):
+        _check(load_library().sacd_set_profile(self._h, int(bool(on))))
+
     def profile_reset(self):
         _check(load_library().sacd_profile_reset(self._h))
+
+    # ---- held-out evaluation
+    def predict(self, coords):
+        """Eq 8 at the given (n, 3) coordinates (host numpy or device torch); fp64 numpy."""
+        c = coords if hasattr(coords, "data_ptr") else _np(np.asarray(coords).reshape(-1, 3), np.uint32)
+        n = int(c.shape[0])
+        out = np.zeros(n, np.float64)
+        _check(load_library().sacd_predict(self._h, _ptr(c), n, _ptr(out)))
+        return out
+
+    def rmse(self, coords, vals):
+        """Eq 30 on held-out entries (coords (n, 3) u32, vals fp32; host or device)."""
+        c = coords if hasattr(coords, "data_ptr") else _np(np.asarray(coords).reshape(-1, 3), np.uint32)
+        v = vals if hasattr(vals, "data_ptr") else _np(vals, np.float32)
+        r = C.c_double()
+        _check(load_library().sacd_rmse(self._h, _ptr(c), _ptr(v), int(c.shape[0]), C.byref(r)))
+        return r.value

@@ -9,7 +9,7 @@ selection or objective).  It only defines:
       rand(seed, tag, ctr) = mix64(mix64(seed ^ tag) + (ctr + 1) * 0x9E3779B97F4A7C15)   (mod 2^64)
       unit24(x) = (x >> 40) * 2^-24      unit53(x) = (x >> 11) * 2^-53
   Tags: INIT=1 (factor init; implemented independently by the CUDA path and by oracle/),
-  COORD=2, VALUE=3, PLANT=4, NOISE=5.
+  COORD=2, VALUE=3, PLANT=4, NOISE=5, SPLIT=6 (held-out split).
 * the five BASELINE.json workloads c1..c5 (SURVEY.md section 8(d) "Synthetic inputs"):
   coordinates are "the first nnz distinct (q,p,s) in draw order", draw j using
   ctr = 3j + mode; values are keyed by the linear key q*P*S + p*S + s.
@@ -31,7 +31,7 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
-TAG_INIT, TAG_COORD, TAG_VALUE, TAG_PLANT, TAG_NOISE = 1, 2, 3, 4, 5
+TAG_INIT, TAG_COORD, TAG_VALUE, TAG_PLANT, TAG_NOISE, TAG_SPLIT = 1, 2, 3, 4, 5, 6
 SEED_BASE = 2003035720
 
 _M64 = (1 << 64)
@@ -259,3 +259,15 @@ def tiny_tensor(dims, density, seed, *, values="unit", device="cpu"):
     else:
         raise ValueError(values)
     return c.to(torch.int32).contiguous(), v.contiguous()
+
+
+def split_train_test(coords: torch.Tensor, vals: torch.Tensor, dims, seed: int, test_frac: float = 0.2):
+    """Seeded held-out split (the paper's 80/20 protocol): an entry is a test
+    entry iff unit53(rand(seed, SPLIT, linear key)) < test_frac.  Keyed by the coordinate,
+    so the split does not depend on entry order.  Use the tensor's own seed: rand() streams
+    collide when seed ^ tag collide (reading C12), e.g. seed 3 / COORD=2 and seed 7 / SPLIT=6.
+    Returns (train_c, train_v, test_c, test_v)."""
+    c = coords.long()
+    key = (c[:, 0] * dims[1] + c[:, 1]) * dims[2] + c[:, 2]
+    test = unit53_t(rand_t(seed, TAG_SPLIT, key)) < test_frac
+    return coords[~test], vals[~test], coords[test], vals[test]

@@ -123,7 +123,8 @@ def test_mttkrp_gram_hessian(R, precision):
 @pytest.mark.parametrize("R", [33, 64, 128, 256])
 @pytest.mark.parametrize("precision", ["f64", "f32"])
 def test_mttkrp_variants_bitwise(R, precision):
-    """Every MTTKRP kernel variant (old warp fiber kernel = 1, sub-warp kernels 10..15,
+    """Every MTTKRP kernel variant (old warp fiber kernel = 1, sub-warp kernels 10.., lean 20..,
+    support-skipping 26-28,
     default 0) performs the same fiber-factored sums in the same order, so their M are
     bitwise equal; and each equals the oracle's MTTKRP within rounding.  Heavy rows and a
     small work-item size force split rows (partial slots + fix-up)."""
@@ -132,7 +133,7 @@ def test_mttkrp_variants_bitwise(R, precision):
     F = O.init_factors(dims, R, 5)
     Mo = [O.mttkrp(c, v, dims, n, F) for n in range(3)]
     ref = None
-    for var in (1, 10, 11, 12, 13, 14, 15, 0):
+    for var in (1, 10, 13, 20, 22, 24, 26, 27, 40, 43, 0):
         with S(c, v, dims, R, 5, precision=precision, nnz_per_item=48, mttkrp_variant=var) as g:
             Ms = [g.mttkrp(n) for n in range(3)]
         tol = 1e-12 if precision == "f64" else 1e-5
@@ -433,3 +434,55 @@ def test_sharded_nccl_world1_matches_unsharded():
     assert np.array_equal(out[1][1], out[0][1])
     for n in range(3):
         assert factor_err(out[1][2][n], out[0][2][n]) <= 1e-10
+
+
+# ----------------------------------------------------------------------------- held-out evaluation (f3)
+@pytest.mark.parametrize("precision", ["f64", "f32"])
+@pytest.mark.parametrize("R", [5, 64, 200])
+def test_predict_rmse_parity(precision, R):
+    """sacd_predict / sacd_rmse (Eq 8, Eq 30) against the oracle after a few sweeps on the
+    80% training split, evaluated on the 20% held-out entries (host and device inputs)."""
+    import torch
+    cfg = SI.custom_config((300, 200, 150), 60000, R, cid=31)
+    c, v = SI.make_tensor(cfg)
+    trc, trv, tec, tev = SI.split_train_test(c, v, cfg.dims, cfg.seed)
+    with S(trc.numpy(), trv.numpy(), cfg.dims, R, cfg.seed, precision=precision) as g:
+        g.iterate(4)
+        F = g.factors()
+        xo = O.predict(tec.numpy(), cfg.dims, F)
+        xg = g.predict(tec.numpy())
+        tol = 1e-12 if precision == "f64" else 1e-5
+        assert np.abs(xg - xo).max() <= tol * max(np.abs(xo).max(), 1e-30)
+        ro = O.rmse(tec.numpy(), tev.numpy(), cfg.dims, F)
+        rg = g.rmse(tec.numpy(), tev.numpy())
+        assert abs(rg - ro) <= 1e-12 * ro
+        rd = g.rmse(tec.cuda().to(torch.int32).contiguous(), tev.cuda())  # device pointers
+        assert rd == rg
+
+
+def test_predict_errors_and_empty():
+    from paper_2003_03572_b200.sacd import SacdError, SACD_ERANGE
+    dims = (20, 10, 5)
+    c, v = SI.tiny_tensor(dims, 0.2, 2)
+    with S(c.numpy(), v.numpy(), dims, 3, 2) as g:
+        with pytest.raises(SacdError) as e:
+            g.predict(np.array([[0, 10, 0]], np.uint32))
+        assert e.value.code == SACD_ERANGE
+        assert g.rmse(np.zeros((0, 3), np.uint32), np.zeros(0, np.float32)) == 0.0
+        assert g.predict(np.zeros((0, 3), np.uint32)).shape == (0,)
+        g.iterate(1)   # the context is still usable after ERANGE
+
+
+def test_heldout_rmse_end_to_end_c2():
+    """80/20 split of c2 (10 sweeps): GPU and oracle held-out RMSE agree to 1e-6 relative
+    (the trajectories agree per the end-to-end tolerances)."""
+    cfg = SI.CONFIGS["c2"]
+    c, v = SI.make_tensor(cfg)
+    trc, trv, tec, tev = SI.split_train_test(c, v, cfg.dims, cfg.seed)
+    K = 10
+    with S(trc.numpy(), trv.numpy(), cfg.dims, cfg.rank, cfg.seed) as g:
+        g.iterate(K)
+        rg = g.rmse(tec.numpy(), tev.numpy())
+    out = O.sacd_run(trc.numpy(), trv.numpy(), cfg.dims, cfg.rank, cfg.seed, K)
+    ro = O.rmse(tec.numpy(), tev.numpy(), cfg.dims, out["F"])
+    assert abs(rg - ro) <= 1e-6 * ro, (rg, ro)

@@ -469,3 +469,59 @@ def test_jacobi_literal_increases_f():
     assert (np.diff(out["f"]) > 0).any()
     gs = O.sacd_run(c.numpy(), v.numpy(), dims, R, 5, 15)
     assert (np.diff(gs["f"]) <= 1e-12 * gs["f"][0]).all()
+
+
+# ----------------------------------------------------------------------------- held-out evaluation (f3)
+def test_predict_sum_of_squares_is_gram_identity():
+    """Eq 8 over every cell of a small box: sum xhat^2 = 1^T (G_U * G_V * G_W) 1 (the Gram
+    identity behind Eq 7's model term), a different route than the per-cell products."""
+    dims = (7, 5, 6)
+    F = O.init_factors(dims, 4, 21)
+    cells = np.stack(np.meshgrid(*[np.arange(d) for d in dims], indexing="ij"), -1).reshape(-1, 3)
+    xh = O.predict(cells.astype(np.uint32), dims, F)
+    G = [O.gram(f) for f in F]
+    assert abs((xh ** 2).sum() - (G[0] * G[1] * G[2]).sum()) <= 1e-12 * (xh ** 2).sum()
+    # and the CP model entry itself against the dense Kruskal tensor of f_dense (Eq 8)
+    Xh = np.einsum("qr,pr,sr->qps", *F)
+    assert np.allclose(xh, Xh.reshape(-1), rtol=1e-14, atol=0)
+
+
+def test_rmse_against_dense_objective():
+    """Eq 30 on the TRAINING entries: n * rmse^2 = sum_Omega (x - xhat)^2
+    = f_dense - sum_{cells not in Omega} xhat^2 (Eq 7 over all cells, C1)."""
+    dims = (6, 7, 5)
+    c, v, F = rand_inst(dims, 0.3, 3, 8)
+    X = dense_tensor(c, v, dims)
+    r = O.rmse(c, v, dims, F)
+    mask = np.ones(dims, bool)
+    mask[c[:, 0], c[:, 1], c[:, 2]] = False
+    Xh = np.einsum("qr,pr,sr->qps", *F)
+    lhs = len(v) * r * r
+    rhs = f_dense(X, F) - (Xh[mask] ** 2).sum()
+    assert abs(lhs - rhs) <= 1e-10 * abs(rhs)
+
+
+def test_predict_errors_and_empty():
+    dims = (4, 4, 4)
+    F = O.init_factors(dims, 2, 1)
+    with pytest.raises(O.OracleError):
+        O.predict(np.array([[0, 4, 0]], np.uint32), dims, F)
+    assert O.rmse(np.zeros((0, 3), np.uint32), np.zeros(0, np.float32), dims, F) == 0.0
+
+
+def test_rmse_paper_synthetic_band(golden):
+    """P13: the paper's held-out RMSE on its synthetic tensors
+    (Fig rmsesyn, tests/golden/rmse_synthetic_fig_rmsesyn.json): 80/20 split of a 2048^3
+    tensor, density 1e-5, values uniform (0,1], R = 10, 30 sweeps -> RMSE in the band."""
+    g = golden["rmse_synthetic_fig_rmsesyn"]
+    lo, hi = g["band_for_large_modes"]
+    assert all(lo <= x <= hi for x in g["sacd_rmse"][3:])
+    dims = (2048, 2048, 2048)
+    nnz = int(1e-5 * 2048 ** 3)
+    cfg = SI.custom_config(dims, nnz, 10, cid=1411)
+    c, v = SI.make_tensor(cfg)
+    trc, trv, tec, tev = SI.split_train_test(c, v, dims, cfg.seed)
+    out = O.sacd_run(trc.numpy(), trv.numpy(), dims, 10, cfg.seed, 30)
+    assert np.all(np.diff(out["f"]) <= 1e-9 * out["f"][0])     # monotone (Lemma 3)
+    r = O.rmse(tec.numpy(), tev.numpy(), dims, out["F"])
+    assert lo <= r <= hi, r
