@@ -82,7 +82,9 @@ typedef struct {
   int32_t emulate_ranks;      /* G >= 2 (with world_size 1): emulate the G ranks of the     */
                               /* sharded engine on this GPU, exchanges as local copies      */
   int32_t reserved[4];        /* [0]: row-update tuning variant (0 = default, 1 = H read from  */
-                              /* global/L1 instead of shared memory); others must be 0       */
+                              /* global/L1 instead of shared memory);                        */
+                              /* [1]: MTTKRP a-blocked order: > 0 = blocks of that many      */
+                              /* a-rows, <= 0 = canonical order (default); [2], [3] must be 0 */
 } sacd_options;
 
 /* Per-sweep statistics (device-side ring, read by sacd_stats). */

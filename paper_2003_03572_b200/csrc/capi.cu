@@ -149,6 +149,58 @@ static void build_items(const std::vector<long long> &rp, long long I, long long
   }
 }
 
+// Work items over the segments of an a-blocked execution order (layout.cu,
+// build_blocked_order): every (blk, row) segment is cut into T-nonzero items, each writing
+// a partial slot; a row's slots are contiguous and ordered by block, then by position, so
+// the split-row fix-up sums the row in execution order (deterministic).
+static void build_items_segments(const std::vector<long long> &seg_start, const std::vector<int> &seg_row,
+                                 long long nnz, long long I, long long T, std::vector<WorkItem> &items,
+                                 std::vector<SplitRow> &splits, long long &nslots) {
+  items.clear();
+  splits.clear();
+  const size_t ns = seg_start.size();
+  std::vector<long long> cnt((size_t)I, 0), slot0((size_t)I, 0), next((size_t)I, 0);
+  for (size_t k = 0; k < ns; ++k) {
+    const long long len = (k + 1 < ns ? seg_start[k + 1] : nnz) - seg_start[k];
+    cnt[(size_t)seg_row[k]] += (len + T - 1) / T;
+  }
+  nslots = 0;
+  for (long long r = 0; r < I; ++r) {
+    slot0[(size_t)r] = nslots;
+    if (cnt[(size_t)r] > 0) {
+      SplitRow sr;
+      sr.slot0 = nslots;
+      sr.nslots = cnt[(size_t)r];
+      sr.row = (int)r;
+      sr.chunk0 = 0;
+      splits.push_back(sr);
+    }
+    nslots += cnt[(size_t)r];
+  }
+  for (size_t k = 0; k < ns; ++k) {
+    const long long e0 = seg_start[k], e1 = k + 1 < ns ? seg_start[k + 1] : nnz;
+    const int r = seg_row[k];
+    for (long long z = e0; z < e1; z += T) {
+      WorkItem w;
+      w.nz0 = z;
+      w.nz1 = std::min(z + T, e1);
+      w.row0 = r;
+      w.row1 = r + 1;
+      w.slot = slot0[(size_t)r] + next[(size_t)r]++;
+      items.push_back(w);
+    }
+  }
+}
+
+// Does the selected MTTKRP kernel read the 16-byte nonzero records (nzm)?  Only those
+// kernels can run an a-blocked execution order (the warp fiber kernel and the R <= 16
+// kernel read the canonical SoA arrays).
+static bool mttkrp_reads_nzm(const Context &c) {
+  if (c.pitch < 32 || c.opt.mttkrp_variant == 1) return false;
+  if (c.opt.precision == SACD_F64 && c.pitch >= 256 && c.opt.mttkrp_variant == 0) return false;
+  return true;
+}
+
 // two-level fix-up plan of a split-row list (sets SplitRow::chunk0)
 static void plan_fixup(std::vector<SplitRow> &splits, std::vector<FixChunk> &chunks) {
   chunks.clear();
@@ -360,7 +412,21 @@ static int init_impl(Context *c, const uint32_t *coords, const float *vals, uint
       std::vector<WorkItem> items;
       std::vector<SplitRow> splits;
       long long nslots = 0;
-      build_items(rps[n], md.I, 0, c->nnz, T, 32, items, splits, nslots);
+      // a-blocked execution order (opt.reserved[1] > 0: blocks of that many a-rows).  Off by
+      // default: on c4's W mode (F_a = 512 MB, 1e4-nnz slices) it cut the launch's DRAM
+      // reads from 13.7 to 10.8 GB but not its time (5.38 vs 5.40 ms): the per-nonzero
+      // b-row gathers dominate there.
+      long long ablk = 0;
+      if (c->opt.reserved[1] > 0) ablk = c->opt.reserved[1];
+      if (ablk > 0 && ablk < c->dims[md.a] && c->nnz > 0 && mttkrp_reads_nzm(*c)) {
+        std::vector<long long> seg_start;
+        std::vector<int> seg_row;
+        SACD_TRY(build_blocked_order(*c, n, ablk, seg_start, seg_row));
+        build_items_segments(seg_start, seg_row, c->nnz, md.I, T, items, splits, nslots);
+        md.ablk_rows = ablk;
+      } else {
+        build_items(rps[n], md.I, 0, c->nnz, T, 32, items, splits, nslots);
+      }
       md.n_items = (long long)items.size();
       md.n_splits = (long long)splits.size();
       md.n_slots = nslots;

@@ -491,7 +491,29 @@ __global__ void __launch_bounds__(256, MINB) k_mttkrp_sw(const WorkItem *__restr
 //  * b-rows are prefetched D nonzeros ahead (registers renamed by the unroll), and the
 //    next batch's 16-byte metadata is in flight while the current batch is consumed.
 // Same arithmetic and order as k_mttkrp_fiber (bitwise-equal results).
-template <typename Real, int RT, int SW, int D, int MINB>
+// Prefetch of a batch's factor rows into L2 (PF = 1: a-rows of fiber starts; 3: also the
+// b-rows) or L1 (PF = 2: a-rows): the per-fiber a-row gathers miss L2 on big factors and
+// their latency is otherwise exposed at the next fiber close, ~2.7 nonzeros later.
+template <typename Real, int RT, int PF>
+__device__ __forceinline__ void prefetch_rows(const uint4 &m, bool valid, const Real *A, const Real *B) {
+  constexpr int LINES = (RT * (int)sizeof(Real) + 127) / 128;
+  if (!valid) return;
+  if (m.y & kFiberStart) {
+    const char *pa = reinterpret_cast<const char *>(A + (long long)(m.x & kIdxMask) * RT);
+#pragma unroll
+    for (int k = 0; k < LINES; ++k) {
+      if (PF == 2) asm volatile("prefetch.global.L1 [%0];" ::"l"(pa + 128 * k));
+      else asm volatile("prefetch.global.L2 [%0];" ::"l"(pa + 128 * k));
+    }
+  }
+  if (PF == 3) {
+    const char *pb = reinterpret_cast<const char *>(B + (long long)(m.y & kIdxMask) * RT);
+#pragma unroll
+    for (int k = 0; k < LINES; ++k) asm volatile("prefetch.global.L2 [%0];" ::"l"(pb + 128 * k));
+  }
+}
+
+template <typename Real, int RT, int SW, int D, int MINB, int PF = 0>
 __global__ void __launch_bounds__(256, MINB) k_mttkrp_lean(const WorkItem *__restrict__ items, long long n_items,
                                                           const uint4 *__restrict__ nzm,
                                                           const Real *__restrict__ A, const Real *__restrict__ B,
@@ -515,10 +537,24 @@ __global__ void __launch_bounds__(256, MINB) k_mttkrp_lean(const WorkItem *__res
   int cur_row = -1;
   uint4 my = make_uint4(0u, 0u, 0u, 0u);
   if (nz0 + lane < nz1) my = ld_stream_u4(nzm + nz0 + lane);
+  uint4 nx = make_uint4(0u, 0u, 0u, 0u);  // PF: metadata one batch ahead, rows prefetched
+  if constexpr (PF > 0) {
+    if (nz0 + SW + lane < nz1) nx = ld_stream_u4(nzm + nz0 + SW + lane);
+    prefetch_rows<Real, RT, PF>(my, nz0 + lane < nz1, A, B);
+  }
   if (lane == 0) my.y |= kFiberStart | kRowStart;  // an item starts a row and a fiber
   for (long long base = nz0; base < nz1; base += SW) {
-    uint4 nx = make_uint4(0u, 0u, 0u, 0u);
-    if (base + SW + lane < nz1) nx = ld_stream_u4(nzm + base + SW + lane);
+    uint4 nx2 = make_uint4(0u, 0u, 0u, 0u);
+    if constexpr (PF > 0) {
+      if (base + 2 * SW + lane < nz1) nx2 = ld_stream_u4(nzm + base + 2 * SW + lane);
+      prefetch_rows<Real, RT, PF>(nx, base + SW + lane < nz1, A, B);
+    } else {
+      nx = make_uint4(0u, 0u, 0u, 0u);  // lanes past the end must carry x = 0 and no flags
+      if (base + SW + lane < nz1) nx = ld_stream_u4(nzm + base + SW + lane);
+    }
+    // x of this lane's nonzero, converted once per batch (F2F runs on the narrow XU pipe:
+    // converting per nonzero in every lane of the worker made the fp64 kernel XU-bound)
+    const Real xl = (Real)__uint_as_float(my.z);
     uint32_t fb[SW];
     SR bb[D + 1];
 #pragma unroll
@@ -532,7 +568,7 @@ __global__ void __launch_bounds__(256, MINB) k_mttkrp_lean(const WorkItem *__res
         fb[j + D] = __shfl_sync(mask, my.y, j + D, SW);
         bb[(j + D) % (D + 1)].load(Bl + (long long)(fb[j + D] & kIdxMask) * RT);
       }
-      const Real x = (Real)__uint_as_float(__shfl_sync(mask, my.z, j, SW));
+      const Real x = __shfl_sync(mask, xl, j, SW);
       if (fb[j] & kFiberStart) {
 #pragma unroll
         for (int k = 0; k < E; ++k) {  // close the previous fiber: acc += a * facc
@@ -552,6 +588,7 @@ __global__ void __launch_bounds__(256, MINB) k_mttkrp_lean(const WorkItem *__res
       for (int k = 0; k < E; ++k) facc[k] = fma(x, bb[j % (D + 1)].v[k], facc[k]);
     }
     my = nx;
+    if constexpr (PF > 0) nx = nx2;
   }
 #pragma unroll
   for (int k = 0; k < E; ++k) acc[k] = fma(arow.v[k], facc[k], acc[k]);
@@ -613,6 +650,7 @@ __global__ void __launch_bounds__(256, MINB) k_mttkrp_skip(const WorkItem *__res
       nx_am = __ldg(cmA + (nx.x & kIdxMask));
       nx_m = nx_am & __ldg(cmB + (nx.y & kIdxMask));
     }
+    const Real xl = (Real)__uint_as_float(my.z);  // one XU conversion per lane per batch
     uint32_t fb[SW], mb[SW];
     Real bb[D + 1][E];
     auto issue = [&](int j) {
@@ -628,7 +666,7 @@ __global__ void __launch_bounds__(256, MINB) k_mttkrp_skip(const WorkItem *__res
 #pragma unroll
     for (int j = 0; j < SW; ++j) {
       if (j + D < SW) issue(j + D);
-      const Real x = (Real)__uint_as_float(__shfl_sync(mask, my.z, j, SW));
+      const Real x = __shfl_sync(mask, xl, j, SW);
       if (fb[j] & kFiberStart) {
 #pragma unroll
         for (int k = 0; k < NV; ++k) {  // close the previous fiber on its a-row's nonzero chunks
@@ -1378,6 +1416,11 @@ struct Impl {
           else if (var == 22) gol(k_mttkrp_lean<Real, RT, SW8, 1, 2>, SW8);
           else if (var == 23) gol(k_mttkrp_lean<Real, RT, SW8, 1, 3>, SW8);
           else if (var == 24) gol(k_mttkrp_lean<Real, RT, SW4, 1, 3>, SW4);
+          else if (var == 45) gol(k_mttkrp_lean<Real, RT, SW4, 1, 3, 1>, SW4);
+          else if (var == 46) gol(k_mttkrp_lean<Real, RT, SW4, 1, 3, 2>, SW4);
+          else if (var == 47) gol(k_mttkrp_lean<Real, RT, SW4, 1, 3, 3>, SW4);
+          else if (var == 48) gol(k_mttkrp_lean<Real, RT, SW8, 1, 2, 1>, SW8);
+          else if (var == 49) gol(k_mttkrp_lean<Real, RT, SW8, 1, 2, 3>, SW8);
           else if (var == 40) gol(k_mttkrp_lean<Real, RT, sub_warp_lanes<Real, RT>(), 1, 6>, sub_warp_lanes<Real, RT>());
           else if (var == 41) gol(k_mttkrp_lean<Real, RT, sub_warp_lanes<Real, RT>(), 1, 5>, sub_warp_lanes<Real, RT>());
           else if (var == 42) gol(k_mttkrp_lean<Real, RT, sub_warp_lanes<Real, RT>(), 2, 5>, sub_warp_lanes<Real, RT>());
@@ -1542,6 +1585,8 @@ struct Impl {
 
   // chunk support masks of F_mode (used by the skipping MTTKRP of the other modes)
   static int chunk_mask(Context &c, int mode) {
+    const int var = c.opt.mttkrp_variant;
+    if (var < 26 || var > 28) return SACD_OK;  // only the support-skipping variants read them
     if constexpr (RT / V16<Real>::N <= 32) {
       ModeData &md = c.m[mode];
       if (md.I > 0)

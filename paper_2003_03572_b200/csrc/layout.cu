@@ -10,6 +10,7 @@
 // Steps (all on device): validate -> 64-bit keys -> cub radix sort of (key, position) ->
 // duplicate check -> gather idx_a, idx_b, val -> row_ptr by binary search -> ||X||^2.
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 
 #include "sacd_internal.cuh"
 
@@ -121,6 +122,11 @@ inline int grid_for(long long n) {
   return (int)g;
 }
 
+__global__ void k_widen(const uint32_t *__restrict__ a, long long n, unsigned long long *__restrict__ b) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x)
+    b[e] = a[e];
+}
+
 int bits_for(unsigned long long maxkey) {
   int b = 1;
   while (b < 64 && (maxkey >> b) != 0) b++;
@@ -128,6 +134,114 @@ int bits_for(unsigned long long maxkey) {
 }
 
 }  // namespace
+
+// ---- a-blocked execution order (MTTKRP locality for modes with long slices) ----------
+// The MTTKRP of mode n gathers one a-row per fiber.  When F_a is much larger than L2 and
+// the slices are long (few rows), consecutive work items touch a-rows spread over all of
+// F_a.  Regrouping the nonzeros by a-block (i_a / ablk_rows) keeps one block of F_a
+// (<= ~40 MB) hot in L2 while every slice is swept: the order becomes (blk, i_n, i_a, i_b),
+// a stable regrouping of the canonical order, and every (blk, row) run is a row segment
+// whose partial the split-row fix-up sums in block order (deterministic).
+__global__ void k_block_keys(const uint32_t *__restrict__ ia, long long nnz, long long ablk_rows,
+                             uint32_t *__restrict__ keys, uint32_t *__restrict__ pos) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nnz;
+       e += (long long)gridDim.x * blockDim.x) {
+    keys[e] = (uint32_t)((long long)(ia[e] & kIdxMask) / ablk_rows);
+    pos[e] = (uint32_t)e;
+  }
+}
+
+// blocked nzm + segment-start flags: segment = maximal run of equal (blk, row)
+__global__ void k_block_gather(const uint32_t *__restrict__ perm, const uint32_t *__restrict__ blk,
+                               const uint32_t *__restrict__ ia, const uint32_t *__restrict__ ib,
+                               const uint32_t *__restrict__ in_, const float *__restrict__ v, long long nnz,
+                               uint4 *__restrict__ nzm, uint32_t *__restrict__ seg_flag) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nnz;
+       e += (long long)gridDim.x * blockDim.x) {
+    const uint32_t p = perm[e];
+    const uint32_t a = ia[p] & kIdxMask, b = ib[p] & kIdxMask, row = in_[p];
+    bool seg = true, fib = true;
+    if (e > 0) {
+      const uint32_t q = perm[e - 1];
+      seg = blk[e] != blk[e - 1] || in_[q] != row;
+      fib = seg || (ia[q] & kIdxMask) != a;
+    }
+    const uint32_t fl = (fib ? kFiberStart : 0u) | (seg ? kRowStart : 0u);
+    nzm[e] = make_uint4(a | fl, b | fl, __float_as_uint(v[p]), row);
+    seg_flag[e] = seg ? 1u : 0u;
+  }
+}
+
+__global__ void k_seg_list(const uint32_t *__restrict__ seg_flag, const unsigned long long *__restrict__ seg_idx,
+                           const uint32_t *__restrict__ nzm_row, long long nnz, long long *__restrict__ seg_start,
+                           int *__restrict__ seg_row) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nnz;
+       e += (long long)gridDim.x * blockDim.x)
+    if (seg_flag[e]) {
+      const unsigned long long k = seg_idx[e];  // exclusive prefix count of segment starts
+      seg_start[k] = e;
+      seg_row[k] = (int)nzm_row[4 * e + 3];
+    }
+}
+
+int build_blocked_order(Context &c, int n, long long ablk_rows, std::vector<long long> &seg_start,
+                        std::vector<int> &seg_row) {
+  ModeData &md = c.m[n];
+  const long long nnz = c.nnz;
+  cudaStream_t s = c.stream;
+  uint32_t *keys = nullptr, *keys2 = nullptr, *pos = nullptr, *perm = nullptr, *flag = nullptr;
+  unsigned long long *idx = nullptr, *flag64 = nullptr;
+  long long *d_start = nullptr;
+  int *d_row = nullptr;
+  void *temp = nullptr;
+  size_t tb = 0, tb2 = 0;
+  const size_t ne = (size_t)nnz;
+  SACD_CUDA_TRY(cudaMallocAsync(&keys, ne * 4, s));
+  SACD_CUDA_TRY(cudaMallocAsync(&keys2, ne * 4, s));
+  SACD_CUDA_TRY(cudaMallocAsync(&pos, ne * 4, s));
+  SACD_CUDA_TRY(cudaMallocAsync(&perm, ne * 4, s));
+  SACD_CUDA_TRY(cudaMallocAsync(&flag, ne * 4, s));
+  SACD_CUDA_TRY(cudaMallocAsync(&flag64, ne * 8, s));
+  SACD_CUDA_TRY(cudaMallocAsync(&idx, ne * 8, s));
+  const long long nblk = (md.I > 0 ? (c.dims[md.a] + ablk_rows - 1) / ablk_rows : 1);
+  const int end_bit = bits_for((unsigned long long)std::max(1LL, nblk - 1));
+  k_block_keys<<<grid_for(nnz), 256, 0, s>>>(md.idx_a, nnz, ablk_rows, keys, pos);
+  SACD_CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, keys2, pos, perm, (int)nnz, 0, end_bit, s));
+  SACD_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tb2, flag64, idx, (int)nnz, s));
+  SACD_CUDA_TRY(cudaMallocAsync(&temp, std::max(tb, tb2), s));
+  SACD_CUDA_TRY(cub::DeviceRadixSort::SortPairs(temp, tb, keys, keys2, pos, perm, (int)nnz, 0, end_bit, s));
+  k_block_gather<<<grid_for(nnz), 256, 0, s>>>(perm, keys2, md.idx_a, md.idx_b, md.idx_n, md.val, nnz, md.nzm, flag);
+  k_widen<<<grid_for(nnz), 256, 0, s>>>(flag, nnz, flag64);
+  SACD_CUDA_TRY(cub::DeviceScan::ExclusiveSum(temp, tb2, flag64, idx, (int)nnz, s));
+  unsigned long long nseg = 0, last = 0;
+  uint32_t lastf = 0;
+  SACD_CUDA_TRY(cudaMemcpyAsync(&last, idx + nnz - 1, 8, cudaMemcpyDeviceToHost, s));
+  SACD_CUDA_TRY(cudaMemcpyAsync(&lastf, flag + nnz - 1, 4, cudaMemcpyDeviceToHost, s));
+  SACD_CUDA_TRY(cudaStreamSynchronize(s));
+  nseg = last + lastf;
+  SACD_CUDA_TRY(cudaMallocAsync(&d_start, (size_t)nseg * 8, s));
+  SACD_CUDA_TRY(cudaMallocAsync(&d_row, (size_t)nseg * 4, s));
+  k_seg_list<<<grid_for(nnz), 256, 0, s>>>(flag, idx, reinterpret_cast<const uint32_t *>(md.nzm), nnz, d_start,
+                                           d_row);
+  SACD_CUDA_TRY(cudaGetLastError());
+  seg_start.resize(nseg);
+  seg_row.resize(nseg);
+  SACD_CUDA_TRY(cudaMemcpyAsync(seg_start.data(), d_start, (size_t)nseg * 8, cudaMemcpyDeviceToHost, s));
+  SACD_CUDA_TRY(cudaMemcpyAsync(seg_row.data(), d_row, (size_t)nseg * 4, cudaMemcpyDeviceToHost, s));
+  SACD_CUDA_TRY(cudaStreamSynchronize(s));
+  cudaFreeAsync(keys, s);
+  cudaFreeAsync(keys2, s);
+  cudaFreeAsync(pos, s);
+  cudaFreeAsync(perm, s);
+  cudaFreeAsync(flag, s);
+  cudaFreeAsync(flag64, s);
+  cudaFreeAsync(idx, s);
+  cudaFreeAsync(d_start, s);
+  cudaFreeAsync(d_row, s);
+  cudaFreeAsync(temp, s);
+  SACD_CUDA_TRY(cudaStreamSynchronize(s));
+  return SACD_OK;
+}
 
 int build_layouts(Context &c, const uint32_t *coords, const float *vals) {
   const long long nnz = c.nnz;

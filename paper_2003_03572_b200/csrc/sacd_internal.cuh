@@ -95,6 +95,7 @@ struct ModeData {
   long long n_splits = 0, n_slots = 0;
   FixChunk *chunks = nullptr;
   long long n_chunks = 0;
+  long long ablk_rows = 0;        // > 0: nzm / items follow the a-blocked execution order
   void *F = nullptr;              // Real[I * pitch]
   void *Z = nullptr;              // Real[ceil32(I) * pitch]  (z_prev, TT layout)
   double *G = nullptr;            // fp64 R x R Gram of F
@@ -177,6 +178,10 @@ ShardPlan plan_shard(const long long *row_ptr, long long I, int world, int rank)
 
 // layout.cu
 int build_layouts(Context &c, const uint32_t *coords_dev, const float *vals_dev);
+// rewrite md.nzm of mode n in the a-blocked order (block = i_a / ablk_rows); returns the
+// (blk, row) segments in execution order: start offsets and row ids
+int build_blocked_order(Context &c, int n, long long ablk_rows, std::vector<long long> &seg_start,
+                        std::vector<int> &seg_row);
 
 // kernels.cu
 int launch_init_factors(Context &c, uint64_t seed);

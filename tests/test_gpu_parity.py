@@ -486,3 +486,35 @@ def test_heldout_rmse_end_to_end_c2():
     out = O.sacd_run(trc.numpy(), trv.numpy(), cfg.dims, cfg.rank, cfg.seed, K)
     ro = O.rmse(tec.numpy(), tev.numpy(), cfg.dims, out["F"])
     assert abs(rg - ro) <= 1e-6 * ro, (rg, ro)
+
+
+# ----------------------------------------------------------------------------- a-blocked execution order
+@pytest.mark.parametrize("precision", ["f64", "f32"])
+@pytest.mark.parametrize("R", [33, 64])
+def test_ablocked_order_mttkrp_and_sweeps(precision, R):
+    """The a-blocked MTTKRP order (forced here with small blocks) gives the oracle's MTTKRP
+    within rounding, the same layout readback, and sweeps that match the unblocked run to
+    the end-to-end tolerances."""
+    dims = (61, 47, 9)
+    c, v = ragged_tensor(dims, 6000, 23, heavy_rows=((2, 3, 900), (0, 5, 400)))
+    F = O.init_factors(dims, R, 4)
+    Mo = [O.mttkrp(c, v, dims, n, F) for n in range(3)]
+    tol = 1e-12 if precision == "f64" else 1e-5
+    with S(c, v, dims, R, 4, precision=precision, nnz_per_item=40, ablk_rows=7) as g:
+        for n in range(3):
+            scale = np.maximum(np.abs(Mo[n]).max(axis=0, keepdims=True), 1e-30)
+            assert (np.abs(g.mttkrp(n) - Mo[n]) / scale).max() <= tol, n
+            ia, ib, vv, rp = g.layout(n)
+            oa, ob, ov, orp = O.layout(c, v, dims, n)
+            assert np.array_equal(ia, oa) and np.array_equal(ib, ob) and np.array_equal(rp, orp)
+        g.iterate(6)
+        fb = [s["objective"] for s in g.stats()]
+        Fb = g.factors()
+    with S(c, v, dims, R, 4, precision=precision, nnz_per_item=40, ablk_rows=-1) as g:
+        g.iterate(6)
+        fu = [s["objective"] for s in g.stats()]
+    assert np.max(np.abs(np.array(fb) - np.array(fu)) / np.array(fu)) <= F_TOL
+    if precision == "f64":
+        out = O.sacd_run(c, v, dims, R, 4, 6)
+        for n in range(3):
+            assert factor_err(Fb[n], out["F"][n]) <= FACTOR_TOL

@@ -18,10 +18,11 @@ ap.add_argument("--variant", type=int, default=0)
 ap.add_argument("--mode", type=int, default=0)
 ap.add_argument("--rank", type=int, default=None)
 ap.add_argument("--sweeps", type=int, default=0)
+ap.add_argument("--ablk", type=int, default=0)
 a = ap.parse_args()
 cfg = SI.CONFIGS[a.config]
 c, v = SI.make_tensor(cfg, device="cuda")
-g = Sacd(c, v, cfg.dims, a.rank or cfg.rank, cfg.seed, precision=a.precision, mttkrp_variant=a.variant)
+g = Sacd(c, v, cfg.dims, a.rank or cfg.rank, cfg.seed, precision=a.precision, mttkrp_variant=a.variant, ablk_rows=a.ablk)
 if a.sweeps:
     g.iterate(a.sweeps)
 g.mttkrp(a.mode)
