@@ -84,7 +84,9 @@ typedef struct {
   int32_t reserved[4];        /* [0]: row-update tuning variant (0 = default, 1 = H read from  */
                               /* global/L1 instead of shared memory);                        */
                               /* [1]: MTTKRP a-blocked order: > 0 = blocks of that many      */
-                              /* a-rows, <= 0 = canonical order (default); [2], [3] must be 0 */
+                              /* a-rows, <= 0 = canonical order (default);                  */
+                              /* [2]: Gram kernel (0 = default: fp64 tensor cores (DMMA) for  */
+                              /* the fp64 build with pitch >= 32, 1 = the FMA kernel); [3] = 0 */
 } sacd_options;
 
 /* Per-sweep statistics (device-side ring, read by sacd_stats). */

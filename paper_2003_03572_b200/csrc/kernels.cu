@@ -1084,6 +1084,94 @@ __global__ void __launch_bounds__(gram_tg<gram_gt<RT>()>() * gram_tg<gram_gt<RT>
     }
 }
 
+// fp64 Gram on the tensor cores (DMMA, mma.sync m8n8k4 f64): G = F^T F as a GEMM with
+// M = N = RT (columns) and K = rows.  blockIdx.x = a contiguous row range (as
+// k_gram_partial), blockIdx.y = an upper-triangle pair (qi <= qj) of 32-column panels; the
+// 4 warps of a block take 4 contiguous sub-ranges of the rows (multiples of 4), each lane
+// holding a 32 x 32 quadrant as 4 x 4 m8n8 tiles, and the warps' quadrants are summed in
+// warp order through shared memory.  Fragments (PTX m8n8k4 .f64): A[m][k] = F[i0+k][r0+m]
+// is held by lane (g = lane >> 2, t = lane & 3) as F[i0+t][r0+g]; B[k][n] = F[i0+k][c0+n]
+// as F[i0+t][c0+g]; C[g][2t + {0,1}].  Same partial contract as k_gram_partial (entries
+// r <= t of every panel pair are written; the reduce reads those).
+template <int RT>
+__global__ void __launch_bounds__(128) k_gram_dmma(long long row_begin, long long row_end, int R,
+                                                   const double *__restrict__ F, double *__restrict__ part) {
+  constexpr int NP = RT / 32;
+  int qi = 0, qj = 0;
+  {
+    int y = blockIdx.y;
+    for (int a = 0; a < NP; ++a) {
+      if (y < NP - a) {
+        qi = a;
+        qj = a + y;
+        break;
+      }
+      y -= NP - a;
+    }
+  }
+  __shared__ double red[3][32 * 32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const long long per = (row_end - row_begin + gridDim.x - 1) / gridDim.x;
+  const long long b0 = row_begin + (long long)blockIdx.x * per;
+  const long long b1 = min(row_end, b0 + per);
+  const long long wper = ((b1 - b0 + 3) / 4 + 3) / 4 * 4;  // rows per warp, multiple of 4
+  const long long i0 = min(b1, b0 + w * wper), i1 = min(b1, i0 + wper);
+  double acc[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  const double *Fa = F + qi * 32 + g;
+  const double *Fb = F + qj * 32 + g;
+  for (long long r0 = i0; r0 < i1; r0 += 8) {
+    double av[2][4], bv[2][4];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const long long row = r0 + 4 * h + t;
+      const bool ok = row < i1;
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        av[h][m] = ok ? __ldg(Fa + row * RT + 8 * m) : 0.0;
+        bv[h][m] = ok ? __ldg(Fb + row * RT + 8 * m) : 0.0;
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                       : "+d"(acc[a][b][0]), "+d"(acc[a][b][1])
+                       : "d"(av[h][a]), "d"(bv[h][b]));
+  }
+  // fixed-order sum of the 4 warps' quadrants
+  if (w > 0) {
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) red[w - 1][(8 * a + g) * 32 + 8 * b + 2 * t + e] = acc[a][b][e];
+  }
+  __syncthreads();
+  if (w == 0) {
+    double *p = part + (long long)blockIdx.x * R * R;
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int x = (8 * a + g) * 32 + 8 * b + 2 * t + e;
+          const double v = ((acc[a][b][e] + red[0][x]) + red[1][x]) + red[2][x];
+          const int r = qi * 32 + 8 * a + g, c = qj * 32 + 8 * b + 2 * t + e;
+          if (r < R && c < R && (qi < qj || r <= c)) p[r * R + c] = v;
+        }
+  }
+}
+
 // G[r][t] = sum over blocks (in order) of the upper-triangle partial; mirrored exactly.
 __global__ void k_gram_reduce(int R, int nblk, const double *__restrict__ part, double *__restrict__ G) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1430,6 +1518,15 @@ struct Impl {
         }
         else if (sizeof(Real) == 8 && RT >= 256) {
           go(k_mttkrp_fiber<Real, RT, 1, fiber_min_blocks<Real, RT>()>);  // default, fp64, R > 128
+        } else if (sizeof(Real) == 8 && RT <= 64 && md.n_fibers > 0 && c.nnz >= 2 * md.n_fibers) {
+          // fp64, R <= 64, mean fiber length >= 2 (the Zipf configs c3, c4): one warp per item
+          // (2 fp64 columns per lane at R = 64) at 48 registers / 40 warps per SM.  Measured on
+          // B200 (tools/mttkrp_tune.py, variant 41): c4 13.65 vs 15.17 ms per sweep, c3 1.22 vs
+          // 1.28; on the uniform c5 (fibers of length ~1) it loses, so those keep the default.
+          constexpr int SWF = sub_warp_lanes<Real, RT>();
+          const long long lb = (n_items * SWF + 255) / 256;
+          k_mttkrp_lean<Real, RT, SWF, 1, 5><<<(unsigned)lb, 256, 0, c.stream>>>(items, n_items, md.nzm, A, B, out,
+                                                                                partial);
         } else {
           // default (measured on B200, tools/mttkrp_tune.py): the lean sub-warp kernel with
           // 4 fp64 / 8 fp32 columns per lane
@@ -1508,8 +1605,7 @@ struct Impl {
       SACD_TRY(prof_end(c, 3, pe));
       pe = prof_begin(c, 4);
       double *sl = c.xstats + sh.rank * slot;
-      k_gram_partial<Real, RT><<<dim3(c.gram_blocks, NBP * (NBP + 1) / 2), TG * TG, 0, c.stream>>>(
-          rlo, rhi, c.R, reinterpret_cast<const Real *>(md.F), sh.gram_part);
+      gram_partial(c, rlo, rhi, reinterpret_cast<const Real *>(md.F), sh.gram_part);
       k_gram_reduce<<<(c.R * c.R + 255) / 256, 256, 0, c.stream>>>(c.R, c.gram_blocks, sh.gram_part, sl + 4);
       SACD_CUDA_TRY(cudaGetLastError());
       SACD_TRY(prof_end(c, 4, pe));
@@ -1569,14 +1665,28 @@ struct Impl {
     return SACD_OK;
   }
 
-  static int gram(Context &c, int mode) {
-    ModeData &md = c.m[mode];
+  // Gram partials of rows [rlo, rhi) of F: DMMA (fp64 tensor cores) for fp64 with RT >= 32
+  // (opt.reserved[2] = 1 selects the FMA kernel), else the shared-memory FMA kernel
+  static void gram_partial(Context &c, long long rlo, long long rhi, const Real *F, double *part) {
+    if constexpr (sizeof(Real) == 8 && RT >= 32) {
+      if (c.opt.reserved[2] != 1) {
+        constexpr int NP = RT / 32;
+        k_gram_dmma<RT><<<dim3(c.gram_blocks, NP * (NP + 1) / 2), 128, 0, c.stream>>>(
+            rlo, rhi, c.R, reinterpret_cast<const double *>(F), part);
+        return;
+      }
+    }
     constexpr int GT = gram_gt<RT>();
     constexpr int TG = gram_tg<GT>();
     constexpr int NB = RT / GT;
+    k_gram_partial<Real, RT><<<dim3(c.gram_blocks, NB * (NB + 1) / 2), TG * TG, 0, c.stream>>>(rlo, rhi, c.R, F,
+                                                                                              part);
+  }
+
+  static int gram(Context &c, int mode) {
+    ModeData &md = c.m[mode];
     int pe = prof_begin(c, 4);
-    k_gram_partial<Real, RT><<<dim3(c.gram_blocks, NB * (NB + 1) / 2), TG * TG, 0, c.stream>>>(
-        0, md.I, c.R, reinterpret_cast<const Real *>(md.F), c.gram_part);
+    gram_partial(c, 0, md.I, reinterpret_cast<const Real *>(md.F), c.gram_part);
     k_gram_reduce<<<(c.R * c.R + 255) / 256, 256, 0, c.stream>>>(c.R, c.gram_blocks, c.gram_part, md.G);
     SACD_CUDA_TRY(cudaGetLastError());
     SACD_TRY(chunk_mask(c, mode));

@@ -51,9 +51,11 @@ __global__ void k_gather(const uint32_t *__restrict__ coords, const float *__res
                          const uint32_t *__restrict__ pos, const unsigned long long *__restrict__ keys,
                          long long nnz, int a, int b, unsigned long long Ib, unsigned long long IaIb,
                          uint32_t *__restrict__ ia, uint32_t *__restrict__ ib, uint32_t *__restrict__ in_,
-                         float *__restrict__ v, uint4 *__restrict__ nzm) {
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nnz;
-       e += (long long)gridDim.x * blockDim.x) {
+                         float *__restrict__ v, uint4 *__restrict__ nzm, unsigned long long *__restrict__ nfib) {
+  for (long long e0 = blockIdx.x * (long long)blockDim.x; e0 < nnz; e0 += (long long)gridDim.x * blockDim.x) {
+    const long long e = e0 + threadIdx.x;  // warp-uniform loop: the fiber count uses a ballot
+    bool fs = false;
+    if (e < nnz) {
     const long long p = pos[e];
     const unsigned long long k = keys[e];
     const unsigned long long row = k / IaIb;
@@ -71,6 +73,10 @@ __global__ void k_gather(const uint32_t *__restrict__ coords, const float *__res
     in_[e] = (uint32_t)row;
     v[e] = x;
     nzm[e] = make_uint4(xa, xb, __float_as_uint(x), (uint32_t)row);
+    fs = fiber_start;
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, fs);
+    if ((threadIdx.x & 31) == 0 && bal) atomicAdd(nfib, (unsigned long long)__popc(bal));
   }
 }
 
@@ -247,8 +253,9 @@ int build_layouts(Context &c, const uint32_t *coords, const float *vals) {
   const long long nnz = c.nnz;
   cudaStream_t s = c.stream;
   int *flags = nullptr;
-  SACD_CUDA_TRY(cudaMallocAsync(&flags, sizeof(int), s));
-  SACD_CUDA_TRY(cudaMemsetAsync(flags, 0, sizeof(int), s));
+  SACD_CUDA_TRY(cudaMallocAsync(&flags, 4 * sizeof(unsigned long long), s));  // flags | fiber counts [3]
+  SACD_CUDA_TRY(cudaMemsetAsync(flags, 0, 4 * sizeof(unsigned long long), s));
+  unsigned long long *nfib = reinterpret_cast<unsigned long long *>(flags) + 1;
   if (nnz > 0)
     k_validate<<<grid_for(nnz), 256, 0, s>>>(coords, vals, nnz, c.dims[0], c.dims[1], c.dims[2], flags);
   int hflags = 0;
@@ -296,12 +303,14 @@ int build_layouts(Context &c, const uint32_t *coords, const float *vals) {
           cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys, keys2, pos, pos2, (int)nnz, 0, end_bit, s));
       k_check_dup<<<grid_for(nnz), 256, 0, s>>>(keys2, nnz, flags);
       k_gather<<<grid_for(nnz), 256, 0, s>>>(coords, vals, pos2, keys2, nnz, a, b, Ib, Ia * Ib, md.idx_a, md.idx_b,
-                                             md.idx_n, md.val, md.nzm);
+                                             md.idx_n, md.val, md.nzm, nfib + n);
     }
     k_row_ptr<<<grid_for(md.I + 1), 256, 0, s>>>(keys2, nnz, md.I, Ia * Ib, md.row_ptr);
     SACD_CUDA_TRY(cudaGetLastError());
   }
   SACD_CUDA_TRY(cudaMemcpyAsync(&hflags, flags, sizeof(int), cudaMemcpyDeviceToHost, s));
+  unsigned long long hfib[3] = {0, 0, 0};
+  SACD_CUDA_TRY(cudaMemcpyAsync(hfib, nfib, sizeof(hfib), cudaMemcpyDeviceToHost, s));
   // ||X||^2 in mode-0 layout order
   double *part = nullptr;
   SACD_CUDA_TRY(cudaMallocAsync(&part, kNormBlocks * sizeof(double), s));
@@ -321,6 +330,7 @@ int build_layouts(Context &c, const uint32_t *coords, const float *vals) {
     set_error("sacd_init: duplicate coordinate");
     return SACD_EDUP;
   }
+  for (int n = 0; n < 3; ++n) c.m[n].n_fibers = (long long)hfib[n];
   return SACD_OK;
 }
 

@@ -96,6 +96,7 @@ struct ModeData {
   FixChunk *chunks = nullptr;
   long long n_chunks = 0;
   long long ablk_rows = 0;        // > 0: nzm / items follow the a-blocked execution order
+  long long n_fibers = 0;         // distinct (i_n, i_a) in the layout (MTTKRP kernel choice)
   void *F = nullptr;              // Real[I * pitch]
   void *Z = nullptr;              // Real[ceil32(I) * pitch]  (z_prev, TT layout)
   double *G = nullptr;            // fp64 R x R Gram of F

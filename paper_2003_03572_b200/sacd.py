@@ -147,7 +147,8 @@ class Sacd:
 
     def __init__(self, coords, vals, dims, rank, seed, *, precision="f64", l_mode="diag", variant="gs",
                  device=-1, stream=None, use_graph=True, profile=False, nnz_per_item=0, mttkrp_variant=0,
-                 world_size=1, world_rank=0, nccl_id=None, force_sharded=False, emulate_ranks=0, rows_variant=0, ablk_rows=0):
+                 world_size=1, world_rank=0, nccl_id=None, force_sharded=False, emulate_ranks=0, rows_variant=0, ablk_rows=0,
+                 gram_variant=0):
         L = load_library()
         o = Options()
         L.sacd_default_options(C.byref(o))
@@ -166,6 +167,7 @@ class Sacd:
         o.emulate_ranks = int(emulate_ranks)
         o.reserved[0] = int(rows_variant)
         o.reserved[1] = int(ablk_rows)
+        o.reserved[2] = int(gram_variant)
         self._nccl_id = None
         if nccl_id is not None:
             self._nccl_id = C.create_string_buffer(bytes(nccl_id), 128)
