@@ -61,6 +61,18 @@ __device__ __forceinline__ float ld_stream_f32(const float *p) {
   return v;
 }
 
+// Asynchronous global -> shared copies (LDGSTS): the row-block staging of the row-update
+// kernels keeps every load in flight at once instead of one register round trip per element.
+template <int BYTES>
+__device__ __forceinline__ void cp_async(void *smem, const void *gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  if constexpr (BYTES == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem));
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(sa), "l"(gmem), "n"(BYTES));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 // Reading C12: rand(seed, tag, ctr) = mix64(mix64(seed ^ tag) + (ctr + 1) * golden)
 __device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
@@ -837,10 +849,12 @@ __global__ void __launch_bounds__(rows_per_block<RT>())
   const long long row0 = row_begin + (long long)blockIdx.x * TR;
   const int nrows = (int)min((long long)TR, row_end - row0);
   if (HS) {
-    for (int x = tid; x < RT * RT; x += TR) Hs[x] = Hr[x];
+    constexpr int PER = 16 / (int)sizeof(Real);
+    for (int x = tid; x < RT * RT / PER; x += TR) cp_async<16>(Hs + PER * x, Hr + PER * x);
   }
   const Real *Fg = F + row0 * RT;
-  for (int x = tid; x < nrows * RT; x += TR) Us[(x / RT) * US + (x % RT)] = Fg[x];
+  for (int x = tid; x < nrows * RT; x += TR) cp_async<(int)sizeof(Real)>(Us + (x / RT) * US + (x % RT), Fg + x);
+  cp_async_wait_all();
   __syncthreads();
   const Real *H = HS ? Hs : Hr;
   const int branch = st->branch[mode];
@@ -980,6 +994,215 @@ __global__ void __launch_bounds__(rows_per_block<RT>())
     e_part[blockIdx.x] = c;
     ech_part[blockIdx.x] = d;
   }
+}
+
+// Fused row update with the out-of-block gradient on the fp64 tensor cores (Real = double,
+// RT <= 64).  Same semantics and per-row order of operations as k_sacd_rows: for column block
+// [c0, c0+8) the out-of-block part acc_q = sum_{j not in block} u_j h_(j,c0+q) of every row
+// of a warp (32 rows) is one (32 x RT) x (RT x 8) product of the CURRENT rows (columns < c0
+// already updated this pass, Gauss-Seidel C9) with H, issued as DMMA m8n8k4 (4 row tiles x
+// the k-steps outside the block, in ascending k); the in-block Gauss-Seidel step then runs
+// one thread per row exactly as in k_sacd_rows.  Fragments: A[m][k] = u[8mt+m][4kk+k] held
+// by lane (g = lane >> 2, t = lane & 3) as Us[8mt+g][4kk+t]; B[k][n] = H[4kk+k][c0+n] as
+// H[4kk+t][c0+g] (from L1: H is read-only and shared by every block); C[g][2t + {0,1}].
+// The accumulator tile and the block's M tile are transposed to one-row-per-thread through
+// a per-warp shared tile.  Shared memory: Us (rows x (RT+2), conflict-free for both the
+// fragment reads and the 16-byte row walks) + 32 x 18 doubles per warp.
+template <int RT, int WPB>
+__global__ void __launch_bounds__(WPB * 32)
+    k_sacd_rows_mma(long long row_begin, long long row_end, int R, int mode, int l_mode,
+                    const long long *__restrict__ row_ptr, const double *__restrict__ M, double *__restrict__ F,
+                    double *__restrict__ Z, const double *__restrict__ H, const DevState *__restrict__ st,
+                    uint8_t *__restrict__ dec, double *__restrict__ ti_part, double *__restrict__ md_part,
+                    long long *__restrict__ e_part, long long *__restrict__ ech_part) {
+  constexpr int TR = WPB * 32;
+  constexpr int US = RT + 2;
+  constexpr int C = 8;
+  constexpr int TS = 2 * C + 2;
+  constexpr int NKS = RT / 4;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double *Us = reinterpret_cast<double *>(smem_raw);
+  double *Hd = Us + TR * US + WPB * 32 * TS;  // the 8 x 8 diagonal blocks of H: [RT/8][8][8]
+  __shared__ double red_d[2][WPB];
+  __shared__ long long red_l[2][WPB];
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, wp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  double *Tw = Us + TR * US + wp * 32 * TS;
+  const long long row0 = row_begin + (long long)blockIdx.x * TR;
+  const int nrows = (int)min((long long)TR, row_end - row0);
+  const double *Fg = F + row0 * RT;
+  static_assert(((RT + 2) * 8) % 16 == 0, "row stride must keep 16-byte chunks aligned");
+  for (int x = tid; x < TR * RT / 2; x += TR) {  // 16-byte chunks
+    const int r = (2 * x) / RT, col = (2 * x) % RT;
+    if (r < nrows) cp_async<16>(Us + r * US + col, Fg + 2 * x);
+    else *reinterpret_cast<double2 *>(Us + r * US + col) = make_double2(0.0, 0.0);
+  }
+  cp_async_wait_all();
+  for (int x = tid; x < RT * C; x += TR) {
+    const int b = x / (C * C), q = (x / C) % C, qq = x % C;
+    Hd[x] = H[(b * C + q) * RT + b * C + qq];
+  }
+  __syncthreads();
+  const int branch = st->branch[mode];
+  const double Lf = st->Lfrob[mode];
+  const int kmax = (R + 3) / 4;  // k-steps past R multiply zero padding
+
+  double ti = 0.0, md = 0.0;
+  long long E = 0, Ech = 0;
+  const bool active = tid < nrows;
+  const long long row = row0 + tid;
+  double *u = Us + tid * US;
+  const bool empty = active ? row_ptr[row] == row_ptr[row + 1] : true;  // empty slice: m = 0
+  double *zp = Z + tt<RT>(active ? row : row0, 0);
+  const double *Uw = Us + (wp * 32 + g) * US + t;
+
+  // software pipeline over column blocks: the B fragments, the M tile and this thread's
+  // z_prev of block c0 + 8 are loaded while block c0 is processed (all read-only here)
+  double bf[NKS], mt[C], zv[C];
+  auto load_block = [&](int c, double (&b)[NKS], double (&mm)[C], double (&zz)[C]) {
+    const int kb = c / 4;
+#pragma unroll
+    for (int kk = 0; kk < NKS; ++kk)
+      b[kk] = (kk == kb || kk == kb + 1 || kk >= kmax) ? 0.0 : __ldg(H + (4 * kk + t) * RT + c + g);
+#pragma unroll
+    for (int k = 0; k < C; ++k) {
+      const int x = lane + 32 * k, rl = x / C, cl = x % C;
+      const long long rg = row0 + wp * 32 + rl;
+      mm[k] = (rg < row_end) ? __ldg(M + rg * RT + c + cl) : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < C; ++q) zz[q] = (active && c + q < RT) ? zp[32 * (c + q)] : 0.0;
+  };
+  load_block(0, bf, mt, zv);
+  for (int c0 = 0; c0 < R; c0 += C) {
+    double bfn[NKS], mtn[C], zvn[C];
+    if (c0 + C < R) load_block(c0 + C, bfn, mtn, zvn);
+    // (1) out-of-block gradient of the warp's 32 rows on the tensor cores: all k-steps
+    //     unrolled, the block's own k-steps (and those past R) with a zero B fragment (adding
+    //     0 * a leaves an accumulator unchanged); even / odd k-steps in two sets of tiles
+    double cacc[2][4][2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int m = 0; m < 4; ++m) cacc[h][m][0] = cacc[h][m][1] = 0.0;
+#pragma unroll
+    for (int kk = 0; kk < NKS; ++kk) {
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const double a = Uw[8 * m * US + 4 * kk];
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                     : "+d"(cacc[kk & 1][m][0]), "+d"(cacc[kk & 1][m][1])
+                     : "d"(a), "d"(bf[kk]));
+      }
+    }
+    // (2) accumulators and the block's M tile to one row per thread
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      Tw[(8 * m + g) * TS + 2 * t] = cacc[0][m][0] + cacc[1][m][0];
+      Tw[(8 * m + g) * TS + 2 * t + 1] = cacc[0][m][1] + cacc[1][m][1];
+    }
+#pragma unroll
+    for (int k = 0; k < C; ++k) {
+      const int x = lane + 32 * k, rl = x / C, cl = x % C;
+      Tw[rl * TS + C + cl] = mt[k];
+    }
+    __syncwarp();
+    if (active) {
+      double acc[C], mv[C], ub[C];
+#pragma unroll
+      for (int q = 0; q < C; ++q) {
+        acc[q] = Tw[lane * TS + q];
+        mv[q] = empty ? 0.0 : Tw[lane * TS + C + q];
+        ub[q] = u[c0 + q];
+      }
+      const double *Hb = Hd + (c0 / C) * C * C;
+      // (3) in-block Gauss-Seidel (C9), as k_sacd_rows
+#pragma unroll
+      for (int q = 0; q < C; ++q) {
+        const int r = c0 + q;
+        if (r < R) {
+          const double h = Hb[q * C + q];
+          double z = 0.0;
+          bool sel = false;
+          if (h != 0.0) {
+            double sg = acc[q];
+#pragma unroll
+            for (int qq = 0; qq < C; ++qq) sg = fma(ub[qq], Hb[q * C + qq], sg);
+            const double gr = sg - mv[q];                  // Eq 14
+            const double ur = ub[q];
+            const double un = fmax(0.0, ur - gr / h);      // Eq 11-13
+            const double d = un - ur;                      // Eq 12
+            const double L = l_mode ? Lf : h;
+            z = -gr * d - (L * 0.5) * d * d;               // Eq 20
+            const double zpr = zv[q];
+            sel = (branch == SACD_BR_FIRST) ? (z > 0.0)
+                                            : ((branch == SACD_BR_EQ24) ? (z - zpr > 0.0) : (zpr - z > 0.0));
+            if (sel) {
+              ub[q] = un;
+              E += 1;
+              if (d != 0.0) Ech += 1;
+            }
+          }
+          zv[q] = z;                                       // z_prev <- z always (C8)
+          ti += z;                                         // Eq 25
+          md += ub[q] * mv[q];
+          if (dec) dec[row * R + r] = (uint8_t)sel;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < C; ++q) u[c0 + q] = ub[q];
+#pragma unroll
+      for (int q = 0; q < C; ++q) zp[32 * (c0 + q)] = zv[q];
+    }
+    __syncwarp();  // the updated block columns feed the next block's fragments; Tw is reused
+#pragma unroll
+    for (int kk = 0; kk < NKS; ++kk) bf[kk] = bfn[kk];
+#pragma unroll
+    for (int q = 0; q < C; ++q) {
+      mt[q] = mtn[q];
+      zv[q] = zvn[q];
+    }
+  }
+  __syncthreads();
+  double *Fo = F + row0 * RT;
+  for (int x = tid; x < nrows * RT; x += TR) Fo[x] = Us[(x / RT) * US + (x % RT)];
+
+  // fixed-order block reduction of (ti, md, E, Ech)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ti += __shfl_xor_sync(0xffffffffu, ti, o);
+    md += __shfl_xor_sync(0xffffffffu, md, o);
+    E += __shfl_xor_sync(0xffffffffu, E, o);
+    Ech += __shfl_xor_sync(0xffffffffu, Ech, o);
+  }
+  if (lane == 0) {
+    red_d[0][wp] = ti;
+    red_d[1][wp] = md;
+    red_l[0][wp] = E;
+    red_l[1][wp] = Ech;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double a = 0.0, b = 0.0;
+    long long c = 0, d = 0;
+    for (int k = 0; k < WPB; ++k) {
+      a += red_d[0][k];
+      b += red_d[1][k];
+      c += red_l[0][k];
+      d += red_l[1][k];
+    }
+    ti_part[blockIdx.x] = a;
+    md_part[blockIdx.x] = b;
+    e_part[blockIdx.x] = c;
+    ech_part[blockIdx.x] = d;
+  }
+}
+
+template <int RT, int WPB>
+__host__ __device__ constexpr size_t rows_mma_smem_bytes() {
+  return (size_t)WPB * 32 * (RT + 2) * 8 + (size_t)WPB * 32 * 18 * 8 + (size_t)RT * 8 * 8;
 }
 
 // sum_r F_ir M_ir per row block (initial objective f^0)
@@ -1783,6 +2006,19 @@ struct Impl {
                                                       reinterpret_cast<const Real *>(c.Hr), c.st, dec, ti_part,
                                                       md_part, e_part, ech_part);
     };
+    if constexpr (sizeof(Real) == 8 && RT <= 64 && rows_per_block<RT>() == 128) {
+      if (c.opt.reserved[0] == 0) {  // default for fp64, R <= 64: out-of-block gradient on DMMA
+        if (nblk > 0)
+          k_sacd_rows_mma<RT, 4><<<(unsigned)nblk, 128, rows_mma_smem_bytes<RT, 4>(), c.stream>>>(
+              rlo, rhi, c.R, mode, c.opt.l_mode, md.row_ptr, reinterpret_cast<const double *>(M),
+              reinterpret_cast<double *>(md.F), reinterpret_cast<double *>(md.Z),
+              reinterpret_cast<const double *>(c.Hr), c.st, dec, ti_part, md_part, e_part, ech_part);
+        SACD_CUDA_TRY(cudaGetLastError());
+        return SACD_OK;
+      }
+    }
+    // reserved[0]: 1 = the FMA kernel with H read from global memory (L1), else (0 for the
+    // other pitches / precisions, 2) the FMA kernel with H staged in shared memory
     if (c.opt.reserved[0] == 1) go(k_sacd_rows<Real, RT, false>, rows_smem_bytes<Real, RT, false>());
     else go(k_sacd_rows<Real, RT, h_in_smem<Real, RT>()>, rows_smem_bytes<Real, RT>());
     SACD_CUDA_TRY(cudaGetLastError());
@@ -1794,6 +2030,9 @@ struct Impl {
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rows_smem_bytes<Real, RT>()));
     SACD_CUDA_TRY(cudaFuncSetAttribute(k_sacd_rows<Real, RT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)rows_smem_bytes<Real, RT, false>()));
+    if constexpr (sizeof(Real) == 8 && RT <= 64 && rows_per_block<RT>() == 128)
+      SACD_CUDA_TRY(cudaFuncSetAttribute(k_sacd_rows_mma<RT, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)rows_mma_smem_bytes<RT, 4>()));
     return SACD_OK;
   }
 };
