@@ -129,7 +129,9 @@ void sacd_default_options(sacd_options *opt);
  *   coords : host or device, nnz x 3 uint32 (q,p,s), 0-based.   vals : host or device, fp32.
  *   dims   : host, {Q, P, S}, each >= 1 and < 2^30.              rank : 1..256.
  * Errors: EINVAL, ERANGE, EDUP, ENONFINITE, ENOMEM, ECUDA.  nnz == 0 is legal.
- * The caller keeps ownership of coords/vals and may free them when the call returns. */
+ * The caller keeps ownership of coords/vals and may free them when the call returns.
+ * Device inputs may come from any stream: the call synchronises the device before reading
+ * them (so e.g. tensors just produced on PyTorch's current stream are complete). */
 int sacd_init(sacd_ctx **out, const uint32_t *coords, const float *vals, int64_t nnz, const int64_t dims[3],
               int32_t rank, uint64_t seed, const sacd_options *opt);
 
@@ -166,7 +168,8 @@ const char *sacd_last_error(void);
  *   coords : host or device, n x 3 uint32 (q,p,s), each index < dims[mode].
  *   out    : host or device, n fp64 (written).  n == 0 is legal.
  * Errors: EINVAL (n < 0 or null pointers with n > 0), ERANGE (index out of range; nothing
- * written), ENOMEM, ECUDA.  Synchronous; the caller owns both buffers. */
+ * written), ENOMEM, ECUDA.  Synchronous; the caller owns both buffers.  Device inputs are
+ * read after a device synchronisation, as in sacd_init. */
 int sacd_predict(sacd_ctx *ctx, const uint32_t *coords, int64_t n, double *out);
 
 /* Root mean squared error of the current model on n held-out entries (Eq 30,

@@ -371,9 +371,30 @@ static int sticky(Context *c, int rc) {
   return rc;
 }
 
+// Device-resident inputs may have been produced on any stream (e.g. PyTorch's current
+// stream), which the context's non-blocking stream does not order against: synchronise the
+// device before reading them.  Host inputs need nothing (the copies are from pageable or
+// pinned memory the caller owns).
+static int sync_if_device(const void *a, const void *b) {
+  for (const void *p : {a, b}) {
+    if (!p) continue;
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+      cudaGetLastError();  // unregistered host memory on older drivers
+      continue;
+    }
+    if (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) {
+      SACD_CUDA_TRY(cudaDeviceSynchronize());
+      return SACD_OK;
+    }
+  }
+  return SACD_OK;
+}
+
 static int init_impl(Context *c, const uint32_t *coords, const float *vals, uint64_t seed) {
   const size_t rs = real_size(*c);
   cudaStream_t s = c->stream;
+  SACD_TRY(sync_if_device(coords, vals));
   SACD_CUDA_TRY(cudaMalloc(&c->st, sizeof(DevState)));
   SACD_CUDA_TRY(cudaMemsetAsync(c->st, 0, sizeof(DevState), s));
   for (int n = 0; n < 3; ++n) {
@@ -792,7 +813,8 @@ static int eval_impl(Context *c, const uint32_t *coords, const float *vals, long
   float *dv = nullptr;
   double *dout = nullptr, *part = nullptr, *sse = nullptr;
   int *flag = nullptr;
-  int rc = SACD_OK, hflag = 0;
+  int rc = sync_if_device(coords, vals), hflag = 0;
+  if (rc != SACD_OK) return rc;
   double hsse = 0.0;
   auto ck = [&](cudaError_t e) {
     if (e != cudaSuccess && rc == SACD_OK) {

@@ -295,6 +295,27 @@ def test_device_pointer_inputs():
         assert np.array_equal(g1.factors(0), g2.factors(0))
 
 
+def test_device_inputs_from_torch_stream_are_complete():
+    """sacd_init / sacd_rmse read device inputs after a device synchronisation, so tensors
+    produced on PyTorch's stream right before the call are complete (the library stream is
+    non-blocking).  c3 (1e7 nonzeros) is generated on the GPU and handed over at once; its
+    layout must equal the one built from the same tensor copied to the host."""
+    import torch
+    cfg = SI.CONFIGS["c3"]
+    c, v = SI.make_tensor(cfg, device="cuda")  # queued on torch's stream, not synchronised
+    with S(c, v, cfg.dims, 4, cfg.seed) as g1:
+        ch, vh = c.cpu().numpy(), v.cpu().numpy()
+        with S(ch, vh, cfg.dims, 4, cfg.seed) as g2:
+            for n in range(3):
+                la, lb = g1.layout(n), g2.layout(n)
+                for x, y in zip(la, lb):
+                    assert np.array_equal(x, y)
+        c2, v2 = SI.make_tensor(cfg, device="cuda")
+        r_dev = g1.rmse(c2[:100000], v2[:100000])
+        r_host = g1.rmse(c2[:100000].cpu().numpy(), v2[:100000].cpu().numpy())
+        assert r_dev == r_host
+
+
 def test_profile_mode_counts_launches():
     cfg = SI.CONFIGS["c1"]
     c, v = SI.make_tensor(cfg)
