@@ -25,7 +25,7 @@ SRC = os.path.join(HERE, "sacd_oracle.c")
 LIB = os.path.join(HERE, "liboracle.so")
 
 BR_FIRST, BR_EQ24, BR_EQ27 = 0, 1, 2
-VAR_GS_LAGGED, VAR_SELECT_OFF, VAR_JACOBI = 0, 1, 2
+VAR_GS_LAGGED, VAR_SELECT_OFF, VAR_JACOBI, VAR_SNAPSHOT = 0, 1, 2, 3
 L_DIAG, L_FROB = 0, 1
 
 
@@ -61,6 +61,7 @@ def lib():
         L.ora_mttkrp.argtypes = [i64, i32, P, P, P, P, P, P, P]
         L.ora_mode_pass.argtypes = [i64, i32, P, P, P, P, i32, i32, i32, P, P, P, P, P]
         L.ora_branch.argtypes = [i32, P, i32]
+        L.ora_mode_pass_snapshot.argtypes = [i64, i32, P, P, P, P, i32, f64, i32, i32, P, P, P, P, P, P]
         L.ora_objective_dense.argtypes = [P, i64, P, P, P, P, P, i32, P]
         L.ora_objective_sparse.argtypes = [P, i64, P, P, P, P, P, i32, P]
         L.ora_sacd_run.argtypes = [i64, P, P, P, i32, u64, i32, i32, i32, P, P, P, P, P, P, P, P, P, P, P]
@@ -193,6 +194,23 @@ def mode_pass(M, H, F, zprev, branch, l_mode=L_DIAG, jacobi=False, decisions=Fal
                                _p(dec) if dec is not None else None, C.byref(ti), C.byref(E), C.byref(Ech),
                                C.byref(md)))
     return F, zp, ti.value, E.value, Ech.value, md.value, (dec.reshape(I, R) if dec is not None else None)
+
+
+def mode_pass_snapshot(M, H, F, zprev, first, ti_prev, l_mode=L_DIAG, decisions=False, branch=-1):
+    """Snapshot-scored pass (reading C10'); returns
+    (F_new, zprev_new, ti, E, E_changed, mdot, decisions|None, branch)."""
+    F = np.array(F, dtype=np.float64, copy=True, order="C")
+    zp = np.array(zprev, dtype=np.float64, copy=True, order="C")
+    M = np.ascontiguousarray(M, dtype=np.float64)
+    H = np.ascontiguousarray(H, dtype=np.float64)
+    I, R = F.shape
+    dec = np.zeros(I * R, np.uint8) if decisions else None
+    ti, E, Ech, md, br = C.c_double(), C.c_int64(), C.c_int64(), C.c_double(), C.c_int32()
+    _check(lib().ora_mode_pass_snapshot(I, R, _p(M), _p(H), _p(F), _p(zp), int(bool(first)), float(ti_prev),
+                                        int(branch), l_mode, _p(dec) if dec is not None else None, C.byref(ti),
+                                        C.byref(E), C.byref(Ech), C.byref(md), C.byref(br)))
+    return (F, zp, ti.value, E.value, Ech.value, md.value, (dec.reshape(I, R) if dec is not None else None),
+            br.value)
 
 
 def branch(k, ti_hist, variant=VAR_GS_LAGGED):

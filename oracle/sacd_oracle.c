@@ -50,6 +50,8 @@
 #define VAR_GS_LAGGED 0  /* default reading (C9, C10)                          */
 #define VAR_SELECT_OFF 1 /* the k==1 rule every sweep: plain projected GS CD   */
 #define VAR_JACOBI 2     /* Lemma 2 literal: g from the row at pass start (C9) */
+#define VAR_SNAPSHOT 3   /* exact-timing ti: Alg 1's z from G at pass start, */
+                         /* ti^k from those z, updates Gauss-Seidel (reading C10')        */
 
 void ora_set_threads(int n) {
 #ifdef _OPENMP
@@ -261,6 +263,90 @@ int ora_mode_pass(int64_t I, int R, const double *M, const double *H, double *F,
   return ORA_OK;
 }
 
+/* ------------------------------------------------------------------ snapshot-scored pass
+ * SURVEY 8(f) f4 / DESIGN.md reading C10': the exact-timing alternative to the lagged ti.
+ * Alg 1 computes G (hence every gradient) once per mode pass, so every z^k_qr of
+ * Eq 20 is known before any selection and ti^k (Eq 25) can gate the same pass
+ * (Eq 27 if ti^k > ti^{k-1}; else Eq 24; k == 1: z > 0):
+ *   (1) snapshot  zs_qr = -g0*d0 - (L/2)*d0^2 with g0 = -m_qr + sum_j u0_qj h_jr from the
+ *       rows at pass start (u0) and d0 = max(0, u0_qr - g0/h_rr) - u0_qr; zs = 0 if h_rr == 0;
+ *   (2) ti^k = sum of zs in row-major order; branch from (first, ti^k, ti_prev);
+ *   (3) for each row, r = 0..R-1 in order: sel by the branch on (zs_qr, zprev_qr); a
+ *       selected element takes the Gauss-Seidel step of the CURRENT row (Eq 14 with
+ *       columns < r updated, Eq 11-13), so each applied update is an exact coordinate
+ *       minimisation and f stays non-increasing; zprev_qr <- zs_qr.
+ * Outputs as ora_mode_pass, plus the branch it chose. */
+int ora_mode_pass_snapshot(int64_t I, int R, const double *M, const double *H, double *F, double *zprev,
+                           int first, double ti_prev, int branch_override, int l_mode, uint8_t *decisions,
+                           double *ti_out, int64_t *E_out, int64_t *Ech_out, double *mdot_out, int *branch_out) {
+  if (R < 1) return ORA_EINVAL;
+  const double Lfrob = ora_frobenius(H, R);
+  double *zs = (double *)malloc(sizeof(double) * (size_t)(I > 0 ? I * R : 1));
+  if (!zs) return ORA_ENOMEM;
+  /* (1) snapshot importance from the rows at pass start (no update in this loop) */
+#pragma omp parallel for schedule(dynamic, 64)
+  for (int64_t i = 0; i < I; i++) {
+    const double *u = F + i * R;
+    const double *m = M + i * R;
+    for (int r = 0; r < R; r++) {
+      const double h = H[r * R + r];
+      double z = 0.0;
+      if (h != 0.0) {
+        double s = 0.0;
+        for (int j = 0; j < R; j++) s += u[j] * H[j * R + r];
+        const double g = -m[r] + s;
+        const double uhat = fmax(0.0, u[r] - g / h) - u[r];
+        const double L = (l_mode == 0) ? h : Lfrob;
+        z = -g * uhat - (L / 2.0) * uhat * uhat;
+      }
+      zs[i * R + r] = z;
+    }
+  }
+  /* (2) exact-timing total importance and branch */
+  double ti = 0.0;
+  for (int64_t x = 0; x < I * R; x++) ti += zs[x];
+  const int branch = branch_override >= 0 ? branch_override : (first ? BR_FIRST : (ti > ti_prev ? BR_EQ27 : BR_EQ24));
+  if (branch < 0 || branch > 2) { free(zs); return ORA_EINVAL; }
+  /* (3) Gauss-Seidel pass gated by the snapshot */
+  int64_t E = 0, Ech = 0;
+#pragma omp parallel for schedule(dynamic, 64) reduction(+ : E, Ech)
+  for (int64_t i = 0; i < I; i++) {
+    double *u = F + i * R;
+    double *zp = zprev + i * R;
+    const double *m = M + i * R;
+    for (int r = 0; r < R; r++) {
+      const double h = H[r * R + r];
+      const double z = zs[i * R + r];
+      int sel = 0;
+      if (h != 0.0) {
+        if (branch == BR_FIRST) sel = z > 0.0;
+        else if (branch == BR_EQ24) sel = (z - zp[r]) > 0.0;
+        else sel = (zp[r] - z) > 0.0;
+        if (sel) {
+          double s = 0.0;
+          for (int j = 0; j < R; j++) s += u[j] * H[j * R + r];
+          const double g = -m[r] + s;
+          const double unew = fmax(0.0, u[r] - g / h);
+          E += 1;
+          if (unew != u[r]) Ech += 1;
+          u[r] = unew;
+        }
+      }
+      zp[r] = z;
+      if (decisions) decisions[i * R + r] = (uint8_t)sel;
+    }
+  }
+  double mdot = 0.0;
+  for (int64_t x = 0; x < I * R; x++) mdot += F[x] * M[x];
+  free(zs);
+  *ti_out = ti;
+  *E_out = E;
+  *Ech_out = Ech;
+  if (mdot_out) *mdot_out = mdot;
+  if (branch_out) *branch_out = branch;
+  return ORA_OK;
+}
+
 /* Reading C10: branch at sweep k (1-based) for a mode whose total-importance history is
  * ti_hist[0..k-2] (ti^1 .. ti^{k-1}). */
 int ora_branch(int k, const double *ti_hist, int variant) {
@@ -446,11 +532,17 @@ int ora_sacd_run(int64_t nnz, const uint32_t *coords, const float *vals, const i
       ora_gram(F[b], dims[b], R, G[b]);
       ora_hadamard(G[a], G[b], (int64_t)R * R, H);
       ora_mttkrp(dims[n], R, rp[n], ia[n], ib[n], vv[n], F[a], F[b], M[n]);
-      const int br = ora_branch(k, tih + n * (K + 1), variant);
+      int br;
       double tk;
       int64_t e1, e2;
-      rc = ora_mode_pass(dims[n], R, M[n], H, F[n], zp[n], br, l_mode, variant == VAR_JACOBI, NULL, &tk, &e1,
-                         &e2, &mdot);
+      if (variant == VAR_SNAPSHOT) {
+        rc = ora_mode_pass_snapshot(dims[n], R, M[n], H, F[n], zp[n], k == 1, k > 1 ? tih[n * (K + 1) + (k - 2)] : 0.0,
+                                    -1, l_mode, NULL, &tk, &e1, &e2, &mdot, &br);
+      } else {
+        br = ora_branch(k, tih + n * (K + 1), variant);
+        rc = ora_mode_pass(dims[n], R, M[n], H, F[n], zp[n], br, l_mode, variant == VAR_JACOBI, NULL, &tk, &e1,
+                           &e2, &mdot);
+      }
       if (rc) goto done;
       tih[n * (K + 1) + (k - 1)] = tk;
       ti[(k - 1) * 3 + n] = tk;

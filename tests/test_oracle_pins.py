@@ -471,6 +471,98 @@ def test_jacobi_literal_increases_f():
     assert (np.diff(gs["f"]) <= 1e-12 * gs["f"][0]).all()
 
 
+# ----------------------------------------------------------------------------- snapshot-scored exact ti (f4)
+@pytest.mark.parametrize("n", [0, 1, 2])
+def test_snapshot_scores_are_pass_start_half_decreases(n):
+    """Reading C10': the snapshot z of every element is Alg 1's Eq 20 with G
+    from the pass start, i.e. (L_r = h_rr, P6) half the exact decrease of the dense
+    objective when that ONE coordinate takes its projected step from the pass-start
+    factors; ti^k is their sum (Eq 25).  Brute force on every (i, r)."""
+    dims, R = (4, 5, 3), 3
+    c, v, F = rand_inst(dims, 0.7, R, 41 + n)
+    X = dense_tensor(c, v, dims)
+    M = O.mttkrp(c, v, dims, n, F)
+    H = O.mode_hessian(F, dims, n)
+    _, zs, ti, *_ = O.mode_pass_snapshot(M, H, F[n], np.zeros_like(F[n]), True, 0.0)
+    base = f_dense(X, F)
+    for i in range(dims[n]):
+        for r in range(R):
+            # exact 1-D minimiser over t >= -u of the parabola through 3 points
+            vals = []
+            for t in (0.0, 0.5, 1.0):
+                tmp = [x.copy() for x in F]
+                tmp[n][i, r] += t
+                vals.append(f_dense(X, tmp))
+            f0, f1, f2 = vals
+            a2, b1 = 4 * (f2 - 2 * f1 + f0), 4 * f1 - 3 * f0 - f2
+            tstar = max(-b1 / a2, -F[n][i, r])
+            tmp = [x.copy() for x in F]
+            tmp[n][i, r] += tstar
+            assert abs(2 * zs[i, r] - (base - f_dense(X, tmp))) <= 1e-8 * base
+    assert abs(ti - zs.sum()) <= 1e-12 * max(1.0, abs(ti))
+
+
+def test_snapshot_branch_is_exact_timing_and_run_is_monotone():
+    """Reading C10': the branch of sweep k >= 2 is Eq 27 iff ti^k > ti^{k-1} with the CURRENT
+    pass's ti, k = 1 is the z > 0 rule; every applied update is a
+    Gauss-Seidel coordinate minimisation, so f is non-increasing (Lemma 3), factors
+    stay >= 0 and E <= I_n R (Lemma 4).  The run's f equals the dense objective (P9)."""
+    dims, R, K = (6, 5, 7), 4, 12
+    c, v = SI.tiny_tensor(dims, 0.3, 19)
+    c, v = c.numpy(), v.numpy()
+    out = O.sacd_run(c, v, dims, R, 77, K, variant=O.VAR_SNAPSHOT)
+    f, ti, br = out["f"], out["ti"], out["branch"]
+    assert (br[0] == O.BR_FIRST).all()
+    for k in range(1, K):
+        for n in range(3):
+            assert br[k, n] == (O.BR_EQ27 if ti[k, n] > ti[k - 1, n] else O.BR_EQ24)
+    assert (np.diff(f) <= 1e-12 * f[0]).all()
+    X = dense_tensor(c, v, dims)
+    assert abs(f[-1] - f_dense(X, out["F"])) <= 1e-10 * f[0]
+    for n in range(3):
+        assert (out["F"][n] >= 0).all()
+        assert (out["E"][:, n] <= dims[n] * R).all() and (out["Ech"][:, n] <= out["E"][:, n]).all()
+        assert abs(ti[-1, n] - out["zprev"][n].sum()) <= 1e-12 * max(1, abs(ti[-1, n]))
+
+
+def test_snapshot_gate_and_gauss_seidel_steps():
+    """Reading C10': element (i, r) is updated iff its snapshot score passes the gate
+    (Eq 24: z - z_prev > 0; Eq 27: z_prev - z > 0; z > 0 at k = 1), and an
+    updated element lands on the exact minimiser of the CURRENT row (columns < r already
+    updated): checked coordinate by coordinate against the dense objective."""
+    dims, R = (5, 4, 3), 3
+    c, v, F = rand_inst(dims, 0.6, R, 57)
+    X = dense_tensor(c, v, dims)
+    n = 0
+    M = O.mttkrp(c, v, dims, n, F)
+    H = O.mode_hessian(F, dims, n)
+    rng = np.random.default_rng(5)
+    zp0 = rng.random(F[n].shape) * 0.05
+    for br in (O.BR_FIRST, O.BR_EQ24, O.BR_EQ27):
+        Fn, zs, ti, E, Ech, md, dec, b = O.mode_pass_snapshot(M, H, F[n], zp0, False, 0.0, decisions=True,
+                                                              branch=br)
+        assert b == br
+        gate = {O.BR_FIRST: zs > 0, O.BR_EQ24: zs - zp0 > 0, O.BR_EQ27: zp0 - zs > 0}[br]
+        np.testing.assert_array_equal(dec.astype(bool), gate & (np.diag(H) != 0)[None, :])
+        assert E == dec.sum()
+        cur = [x.copy() for x in F]
+        for i in range(dims[n]):
+            for r in range(R):
+                if not dec[i, r]:
+                    assert Fn[i, r] == cur[n][i, r]
+                    continue
+                vals = []
+                for t in (0.0, 0.5, 1.0):
+                    tmp = [x.copy() for x in cur]
+                    tmp[n][i, r] += t
+                    vals.append(f_dense(X, tmp))
+                f0, f1, f2 = vals
+                a2, b1 = 4 * (f2 - 2 * f1 + f0), 4 * f1 - 3 * f0 - f2
+                tstar = max(-b1 / a2, -cur[n][i, r])
+                assert abs(Fn[i, r] - (cur[n][i, r] + tstar)) <= 1e-9 * max(1.0, abs(Fn[i, r]))
+                cur[n][i, r] = Fn[i, r]
+
+
 # ----------------------------------------------------------------------------- held-out evaluation (f3)
 def test_predict_sum_of_squares_is_gram_identity():
     """Eq 8 over every cell of a small box: sum xhat^2 = 1^T (G_U * G_V * G_W) 1 (the Gram
