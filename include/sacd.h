@@ -55,7 +55,13 @@ enum {
 /* Element selection. */
 enum {
   SACD_VARIANT_GS_LAGGED = 0, /* Alg 1 selection with the lagged ti branch (C10) */
-  SACD_VARIANT_SELECT_OFF = 1 /* the k==1 rule (z > 0) every sweep: projected GS CD            */
+  SACD_VARIANT_SELECT_OFF = 1, /* the k==1 rule (z > 0) every sweep: projected GS CD           */
+  SACD_VARIANT_JACOBI = 2,     /* Lemma 2 literally: every gradient of a pass from   */
+                               /* the rows at pass start (not monotone: reading C9, pin P12)     */
+  SACD_VARIANT_SNAPSHOT = 3    /* exact-timing ti (reading C10'): Alg 1's z from G at */
+                               /* pass start give ti^k, which picks Eq 24 / Eq 27 for   */
+                               /* the SAME pass; those z gate Gauss-Seidel updates; */
+                               /* z_prev <- them.  Costs one extra read of M, F, z_prev per mode */
 };
 
 /* Arithmetic precision of factors, z_prev, MTTKRP and the row update (Grams, H and all
@@ -69,7 +75,8 @@ typedef struct {
   uint32_t struct_size;       /* = sizeof(sacd_options) (ABI versioning)                    */
   int32_t precision;          /* SACD_F64 (default) | SACD_F32                              */
   int32_t l_mode;             /* SACD_L_DIAG (default) | SACD_L_FROB                        */
-  int32_t variant;            /* SACD_VARIANT_GS_LAGGED (default) | SACD_VARIANT_SELECT_OFF */
+  int32_t variant;            /* SACD_VARIANT_* (default GS_LAGGED); JACOBI and SNAPSHOT run  */
+                              /* unsharded only (EINVAL with world_size > 1 / emulate_ranks)  */
   int32_t device;             /* CUDA ordinal; -1 = the calling thread's current device      */
   int32_t world_size, rank;   /* slice sharding across GPUs (1, 0 = single GPU)             */
   const void *nccl_unique_id; /* 128 bytes from sacd_nccl_unique_id() on rank 0 (G > 1)     */

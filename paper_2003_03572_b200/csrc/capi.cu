@@ -305,6 +305,7 @@ static void destroy(sacd_ctx *c) {
   }
   cudaFree(c->st);
   cudaFree(c->M);
+  cudaFree(c->Zs);
   cudaFree(c->partial);
   cudaFree(c->fixbuf);
   cudaFree(c->Hr);
@@ -538,6 +539,10 @@ static int init_impl(Context *c, const uint32_t *coords, const float *vals, uint
   c->max_row_blocks = (maxI + 31) / 32 + 1;  // >= ceil(I / rows_per_block) for every pitch
   c->gram_blocks = (int)std::min<long long>(296, std::max<long long>(1, (maxI + 63) / 64));
   SACD_CUDA_TRY(cudaMalloc(&c->M, (size_t)((maxI + 31) / 32 * 32) * P * rs));
+  if (c->opt.variant == SACD_VARIANT_SNAPSHOT) {  // snapshot importances of one pass (TT layout)
+    SACD_CUDA_TRY(cudaMalloc(&c->Zs, (size_t)((maxI + 31) / 32 * 32) * P * rs));
+    c->device_bytes += (long long)((size_t)((maxI + 31) / 32 * 32) * P * rs);
+  }
   SACD_CUDA_TRY(cudaMalloc(&c->partial, (size_t)max_slots * P * rs));
   SACD_CUDA_TRY(cudaMalloc(&c->fixbuf, (size_t)max_chunks * P * rs));
   c->device_bytes += (long long)((size_t)max_chunks * P * rs);
@@ -668,8 +673,12 @@ int sacd_init(sacd_ctx **out, const uint32_t *coords, const float *vals, int64_t
     return SACD_EINVAL;
   }
   if ((o.precision != SACD_F64 && o.precision != SACD_F32) || (o.l_mode != SACD_L_DIAG && o.l_mode != SACD_L_FROB) ||
-      (o.variant != SACD_VARIANT_GS_LAGGED && o.variant != SACD_VARIANT_SELECT_OFF)) {
+      o.variant < SACD_VARIANT_GS_LAGGED || o.variant > SACD_VARIANT_SNAPSHOT) {
     set_error("sacd_init: bad option value");
+    return SACD_EINVAL;
+  }
+  if (o.variant >= SACD_VARIANT_JACOBI && (o.world_size > 1 || o.emulate_ranks > 1 || o.force_sharded)) {
+    set_error("sacd_init: the JACOBI / SNAPSHOT variants run unsharded only");
     return SACD_EINVAL;
   }
   if (o.world_size < 1 || o.rank < 0 || o.rank >= o.world_size || o.emulate_ranks < 0 ||

@@ -836,7 +836,12 @@ __global__ void __launch_bounds__(rows_per_block<RT>())
                 const Real *__restrict__ M, Real *__restrict__ F,
                 Real *__restrict__ Z, const Real *__restrict__ Hr, const DevState *__restrict__ st,
                 uint8_t *__restrict__ dec, double *__restrict__ ti_part, double *__restrict__ md_part,
-                long long *__restrict__ e_part, long long *__restrict__ ech_part) {
+                long long *__restrict__ e_part, long long *__restrict__ ech_part, int vflags = 0,
+                Real *__restrict__ Zs = nullptr) {
+  // vflags (reading variants): 1 = JACOBI gradients from the rows at pass start
+  // (Lemma 2 literal); 2 = SCORE only (with 1: the snapshot z of every element into Zs, ti,
+  // no update); 4 = SNAP (Gauss-Seidel updates gated by the snapshot Zs, z_prev <- Zs)
+  const bool jac = vflags & 1, score = vflags & 2, snap = vflags & 4;
   constexpr int TR = rows_per_block<RT>();
   constexpr int US = RT + 1;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -876,6 +881,7 @@ __global__ void __launch_bounds__(rows_per_block<RT>())
     Real *u = Us + tid * US;
     const bool empty = active ? row_ptr[row] == row_ptr[row + 1] : true;  // empty slice: m = 0
     Real *zp = Z + tt<RT>(active ? row : row0, 0);         // z_prev in the TT layout
+    Real *zsp = (score || snap) ? Zs + tt<RT>(active ? row : row0, 0) : nullptr;
     for (int c0 = 0; c0 < R; c0 += C) {
       __syncwarp();
 #pragma unroll
@@ -906,11 +912,12 @@ __global__ void __launch_bounds__(rows_per_block<RT>())
       for (int j = 0; j < c0; ++j) accumulate(j);
 #pragma unroll 4
       for (int j = c0 + C; j < R; ++j) accumulate(j);
-      Real mv[C], zv[C], ub[C];
+      Real mv[C], zv[C], ub[C], zs[C];
 #pragma unroll
       for (int q = 0; q < C; ++q) {
         mv[q] = Mst[wp][lane][q];
-        zv[q] = zp[32 * (c0 + q)];
+        zv[q] = score ? Real(0) : zp[32 * (c0 + q)];
+        zs[q] = snap ? zsp[32 * (c0 + q)] : Real(0);
       }
 #pragma unroll
       for (int q = 0; q < C; ++q) ub[q] = u[c0 + q];
@@ -932,7 +939,7 @@ __global__ void __launch_bounds__(rows_per_block<RT>())
           if (h != Real(0)) {
             Real sg = acc[q];
 #pragma unroll
-            for (int qq = 0; qq < C; ++qq) sg = fma(ub[qq], Hr_[c0 + qq], sg);
+            for (int qq = 0; qq < C; ++qq) sg = fma(jac ? u[c0 + qq] : ub[qq], Hr_[c0 + qq], sg);
             const Real g = sg - mv[q];                     // Eq 14
             const Real ur = ub[q];
             const Real un = fmax(Real(0), ur - g / h);     // Eq 11-13
@@ -940,29 +947,44 @@ __global__ void __launch_bounds__(rows_per_block<RT>())
             const Real L = l_mode ? Lf : h;
             z = -g * d - (L * Real(0.5)) * d * d;          // Eq 20
             const Real zpr = zv[q];
-            sel = (branch == SACD_BR_FIRST) ? (z > Real(0))
-                                            : ((branch == SACD_BR_EQ24) ? (z - zpr > Real(0)) : (zpr - z > Real(0)));
+            const Real zg = snap ? zs[q] : z;  // the score the gate sees
+            sel = !score && ((branch == SACD_BR_FIRST) ? (zg > Real(0))
+                                                       : ((branch == SACD_BR_EQ24) ? (zg - zpr > Real(0))
+                                                                                   : (zpr - zg > Real(0))));
             if (sel) {
               ub[q] = un;
               E += 1;
               if (d != Real(0)) Ech += 1;
             }
           }
+          if (snap) z = zs[q];
           zv[q] = z;                                       // z_prev <- z always (C8)
           ti += (double)z;                                 // Eq 25
           md += (double)ub[q] * (double)mv[q];
-          if (dec) dec[row * R + r] = (uint8_t)sel;
+          if (dec && !score) dec[row * R + r] = (uint8_t)sel;
         }
       }
+      if (score) {
 #pragma unroll
-      for (int q = 0; q < C; ++q) u[c0 + q] = ub[q];
+        for (int q = 0; q < C; ++q) zsp[32 * (c0 + q)] = zv[q];
+        continue;
+      }
+      if (jac) {  // the staged rows keep the pass-start values; updates go straight to F
+#pragma unroll
+        for (int q = 0; q < C; ++q)
+          if (c0 + q < R) F[row * RT + c0 + q] = ub[q];
+      } else {
+#pragma unroll
+        for (int q = 0; q < C; ++q) u[c0 + q] = ub[q];
+      }
 #pragma unroll
       for (int q = 0; q < C; ++q) zp[32 * (c0 + q)] = zv[q];
     }
   }
   __syncthreads();
   Real *Fo = F + row0 * RT;
-  for (int x = tid; x < nrows * RT; x += TR) Fo[x] = Us[(x / RT) * US + (x % RT)];
+  if (!jac && !score)
+    for (int x = tid; x < nrows * RT; x += TR) Fo[x] = Us[(x / RT) * US + (x % RT)];
 
   // fixed-order block reduction of (ti, md, E, Ech)
 #pragma unroll
@@ -1492,6 +1514,30 @@ __global__ void __launch_bounds__(1024) k_finalize(int mode, long long nblk, con
   }
 }
 
+// Snapshot variant (reading C10'): ti^k = fixed-order sum of the score pass's block partials
+// (the same tree as k_finalize, so the recorded ti equals it bitwise); the branch of THIS
+// pass: k == 1 (no history) the z > 0 rule, else Eq 27 iff ti^k > ti^{k-1}.
+__global__ void __launch_bounds__(1024) k_snapshot_branch(int mode, long long nblk, const double *__restrict__ ti_part,
+                                                          DevState *st, int branch_override) {
+  __shared__ double sd[1024];
+  const int tid = threadIdx.x;
+  double ti = 0.0;
+  for (long long b = tid; b < nblk; b += 1024) ti += ti_part[b];
+  sd[tid] = ti;
+  __syncthreads();
+  for (int o = 512; o > 0; o >>= 1) {
+    if (tid < o) sd[tid] += sd[tid + o];
+    __syncthreads();
+  }
+  if (tid == 0) {
+    int br;
+    if (branch_override >= 0) br = branch_override;
+    else if (st->nhist[mode] == 0) br = SACD_BR_FIRST;
+    else br = (sd[0] > st->ti1[mode]) ? SACD_BR_EQ27 : SACD_BR_EQ24;
+    st->branch[mode] = br;
+  }
+}
+
 // ------------------------------------------------------------------ sharded-engine kernels
 // Every rank q writes its head row id / partial row into slot q of the exchange buffers
 // and its (ti, md, E, Ech, Gram partial) into slot q of the stats buffer; NCCL all-gathers
@@ -1952,7 +1998,16 @@ struct Impl {
     double *ti_part = c.row_part, *md_part = c.row_part + c.max_row_blocks;
     long long *e_part = c.cnt_part, *ech_part = c.cnt_part + c.max_row_blocks;
     int pe = prof_begin(c, 3);
-    SACD_TRY(rows(c, nblk, 0, md.I, mode, M, dec, ti_part, md_part, e_part, ech_part));
+    if (c.opt.variant == SACD_VARIANT_SNAPSHOT) {
+      // (1) snapshot scores from the rows at pass start, (2) ti^k and this pass's branch,
+      // (3) the Gauss-Seidel pass gated by the snapshot (reading C10')
+      SACD_TRY(rows(c, nblk, 0, md.I, mode, M, nullptr, ti_part, md_part, e_part, ech_part, 1 | 2));
+      k_snapshot_branch<<<1, 1024, 0, c.stream>>>(mode, nblk, ti_part, c.st, branch_override);
+      SACD_TRY(rows(c, nblk, 0, md.I, mode, M, dec, ti_part, md_part, e_part, ech_part, 4));
+    } else {
+      SACD_TRY(rows(c, nblk, 0, md.I, mode, M, dec, ti_part, md_part, e_part, ech_part,
+                    c.opt.variant == SACD_VARIANT_JACOBI ? 1 : 0));
+    }
     SACD_CUDA_TRY(cudaGetLastError());
     SACD_TRY(prof_end(c, 3, pe));
     SACD_TRY(gram(c, mode));
@@ -1996,7 +2051,7 @@ struct Impl {
   // the fused row update over rows [rlo, rhi) (nblk blocks); opt.reserved[0] = 1 reads H
   // from global memory (L1) instead of staging it in shared memory
   static int rows(Context &c, long long nblk, long long rlo, long long rhi, int mode, const Real *M, uint8_t *dec,
-                  double *ti_part, double *md_part, long long *e_part, long long *ech_part) {
+                  double *ti_part, double *md_part, long long *e_part, long long *ech_part, int vflags = 0) {
     constexpr int TR = rows_per_block<RT>();
     ModeData &md = c.m[mode];
     auto go = [&](auto kern, size_t smem) {
@@ -2004,10 +2059,11 @@ struct Impl {
         kern<<<(unsigned)nblk, TR, smem, c.stream>>>(rlo, rhi, c.R, mode, c.opt.l_mode, md.row_ptr, M,
                                                       reinterpret_cast<Real *>(md.F), reinterpret_cast<Real *>(md.Z),
                                                       reinterpret_cast<const Real *>(c.Hr), c.st, dec, ti_part,
-                                                      md_part, e_part, ech_part);
+                                                      md_part, e_part, ech_part, vflags,
+                                                      reinterpret_cast<Real *>(c.Zs));
     };
     if constexpr (sizeof(Real) == 8 && RT <= 64 && rows_per_block<RT>() == 128) {
-      if (c.opt.reserved[0] == 0) {  // default for fp64, R <= 64: out-of-block gradient on DMMA
+      if (c.opt.reserved[0] == 0 && vflags == 0) {  // default for fp64, R <= 64: out-of-block gradient on DMMA
         if (nblk > 0)
           k_sacd_rows_mma<RT, 4><<<(unsigned)nblk, 128, rows_mma_smem_bytes<RT, 4>(), c.stream>>>(
               rlo, rhi, c.R, mode, c.opt.l_mode, md.row_ptr, reinterpret_cast<const double *>(M),

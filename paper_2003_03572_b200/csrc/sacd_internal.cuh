@@ -140,6 +140,7 @@ struct Context {
   DevState *st = nullptr;         // device
   // scratch
   void *M = nullptr;              // Real[ceil32(maxI) * pitch] (TT layout)
+  void *Zs = nullptr;             // Real[ceil32(maxI) * pitch] snapshot z of a pass (SNAPSHOT variant)
   void *partial = nullptr;        // Real[max slots * pitch]
   void *fixbuf = nullptr;         // Real[max chunks * pitch] (level-2 fix-up rows)
   void *Hr = nullptr;             // Real[pitch * pitch]

@@ -19,7 +19,7 @@ SACD_OK, SACD_EINVAL, SACD_ERANGE, SACD_EDUP, SACD_ENONFINITE, SACD_ENOMEM, SACD
 STATUS = {0: "OK", -1: "EINVAL", -2: "ERANGE", -3: "EDUP", -4: "ENONFINITE", -5: "ENOMEM", -6: "ECUDA",
           -7: "ENCCL", -8: "ESTATE"}
 L_DIAG, L_FROB = 0, 1
-VARIANT_GS_LAGGED, VARIANT_SELECT_OFF = 0, 1
+VARIANT_GS_LAGGED, VARIANT_SELECT_OFF, VARIANT_JACOBI, VARIANT_SNAPSHOT = 0, 1, 2, 3
 F64, F32 = 0, 1
 BR_AUTO, BR_FIRST, BR_EQ24, BR_EQ27 = -1, 0, 1, 2
 NUM_KCLASS = 6
@@ -154,7 +154,8 @@ class Sacd:
         L.sacd_default_options(C.byref(o))
         o.precision = {"f64": F64, "f32": F32}[precision]
         o.l_mode = {"diag": L_DIAG, "frob": L_FROB}[l_mode]
-        o.variant = {"gs": VARIANT_GS_LAGGED, "select_off": VARIANT_SELECT_OFF}[variant]
+        o.variant = {"gs": VARIANT_GS_LAGGED, "select_off": VARIANT_SELECT_OFF, "jacobi": VARIANT_JACOBI,
+                     "snapshot": VARIANT_SNAPSHOT}[variant]
         o.device = int(device)
         o.stream = stream
         o.use_graph = int(bool(use_graph))

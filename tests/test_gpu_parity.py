@@ -207,7 +207,8 @@ def run_pair(c, v, dims, R, seed, K, **kw):
         Eg = np.array([s["E"] for s in st])
         brg = np.array([s["branch"] for s in st])
     l_mode = {"diag": O.L_DIAG, "frob": O.L_FROB}[kw.get("l_mode", "diag")]
-    variant = {"gs": O.VAR_GS_LAGGED, "select_off": O.VAR_SELECT_OFF}[kw.get("variant", "gs")]
+    variant = {"gs": O.VAR_GS_LAGGED, "select_off": O.VAR_SELECT_OFF, "jacobi": O.VAR_JACOBI,
+               "snapshot": O.VAR_SNAPSHOT}[kw.get("variant", "gs")]
     ora = O.sacd_run(c, v, dims, R, seed, K, l_mode=l_mode, variant=variant)
     return fg, Fg, Eg, brg, ora
 
@@ -237,6 +238,64 @@ def test_end_to_end_c1(variant, l_mode):
     fg, Fg, Eg, brg, ora = run_pair(c, v, cfg.dims, cfg.rank, cfg.seed, cfg.iters, variant=variant, l_mode=l_mode)
     check_pair(fg, Fg, Eg, brg, ora)
     assert np.array_equal(Eg, ora["E"])
+
+
+@pytest.mark.parametrize("variant", ["jacobi", "snapshot"])
+@pytest.mark.parametrize("l_mode", ["diag", "frob"])
+def test_end_to_end_reading_variants_c1(variant, l_mode):
+    """the Lemma-2-literal Jacobi variant and the snapshot-scored exact-ti
+    variant (reading C10') run in the same row kernels and match their oracles: f per sweep,
+    factors, branch and E."""
+    cfg = SI.CONFIGS["c1"]
+    c, v = SI.make_tensor(cfg)
+    c, v = c.numpy(), v.numpy()
+    fg, Fg, Eg, brg, ora = run_pair(c, v, cfg.dims, cfg.rank, cfg.seed, cfg.iters, variant=variant, l_mode=l_mode)
+    check_pair(fg, Fg, Eg, brg, ora)
+    assert np.array_equal(Eg, ora["E"])
+
+
+@pytest.mark.parametrize("variant", ["jacobi", "snapshot"])
+def test_end_to_end_reading_variants_ragged(variant):
+    dims = (300, 200, 50)
+    c, v = ragged_tensor(dims, 20000, 8, heavy_rows=((2, 1, 3000), (0, 5, 900)))
+    fg, Fg, Eg, brg, ora = run_pair(c, v, dims, 24, 17, 10, nnz_per_item=256, variant=variant)
+    check_pair(fg, Fg, Eg, brg, ora)
+    assert np.array_equal(Eg, ora["E"])
+
+
+@pytest.mark.parametrize("branch", [0, 1, 2, -1])
+def test_snapshot_one_pass_teacher_forced(branch):
+    """Snapshot variant, one pass from identical state (forced branch, or the device's own
+    exact-timing choice with -1): decisions, E, factors, z_prev and ti as the oracle."""
+    dims, R = (60, 45, 33), 16
+    c, v = ragged_tensor(dims, 5000, 21, heavy_rows=((1, 4, 500),))
+    F = O.init_factors(dims, R, 9)
+    rng = np.random.default_rng(7 + branch)
+    with S(c, v, dims, R, 9, variant="snapshot", nnz_per_item=128) as g:
+        for n in range(3):
+            Z0 = rng.random((dims[n], R)) * 0.1
+            g.set_zprev(n, Z0)
+            out = g.mode_update(n, branch=branch, decisions=True)
+            M = O.mttkrp(c, v, dims, n, F)
+            H = O.mode_hessian(F, dims, n)
+            Fn, zp, ti, E, Ech, md, dec, br = O.mode_pass_snapshot(M, H, F[n], Z0, True, 0.0, decisions=True,
+                                                                   branch=branch)
+            assert np.array_equal(out["decisions"], dec)
+            assert out["E"] == E and out["E_changed"] == Ech
+            assert factor_err(g.factors(n), Fn) <= 1e-9
+            assert np.abs(g.get_zprev(n) - zp).max() <= 1e-9 * max(1.0, np.abs(zp).max())
+            assert abs(out["ti"] - ti) <= 1e-9 * max(1.0, abs(ti))
+            F[n] = Fn
+            g.set_factors(n, Fn)
+
+
+def test_reading_variants_rejected_by_sharded_engine():
+    from paper_2003_03572_b200.sacd import SacdError
+    cfg = SI.CONFIGS["c1"]
+    c, v = SI.make_tensor(cfg)
+    for variant in ("jacobi", "snapshot"):
+        with pytest.raises(SacdError):
+            S(c.numpy(), v.numpy(), cfg.dims, cfg.rank, cfg.seed, variant=variant, emulate_ranks=2)
 
 
 def test_end_to_end_c2_10_sweeps():
