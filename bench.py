@@ -43,6 +43,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--nnz-per-item", type=int, default=0)
+    p.add_argument("--exchange", default="delta", choices=["full", "delta"],
+                   help="N > 1: factor-row exchange of the sharded engine (SURVEY f2 delta lists, or full rows)")
     return p.parse_args()
 
 
@@ -245,7 +247,7 @@ def main():
     if world > 1:
         obj = [nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
-        shard_kw = dict(world_size=world, world_rank=rank, nccl_id=obj[0])
+        shard_kw = dict(world_size=world, world_rank=rank, nccl_id=obj[0], exchange=args.exchange)
 
     K = args.steps if args.steps is not None else cfg.iters
     W = args.warmup
@@ -289,6 +291,7 @@ def main():
     prof = g.profile_read()
     g.set_profile(False)
     f_final, fit_final = g.fit()
+    info_end = g.info()
     ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
@@ -373,8 +376,13 @@ def main():
                 "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
                 "dtype": args.precision, "data": "synthetic",
                 "config": {"workload": cfg.name, "dims": list(cfg.dims), "nnz": nnz, "rank": R,
-                           "parallelism": f"slice-sharded x{world} (NCCL all-gather-v of factor rows)" if world > 1
-                           else "single GPU",
+                           "parallelism": (f"slice-sharded x{world} (NCCL; factor exchange: "
+                                           + ("changed elements as (index, value) lists, rows when smaller)"
+                                              if args.exchange == "delta" else "all-gather-v of owned rows)"))
+                           if world > 1 else "single GPU",
+                           **({"exchange_elems_sent": info_end["delta_elems_sent"],
+                               "exchange_elems_full_equiv": info_end["full_elems_equiv"]}
+                              if world > 1 and info_end.get("delta_exchange") else {}),
                            "l2": "inputs larger than L2 (mode layouts %.2f GB > 126 MB), no flush" % (36 * nnz / 1e9),
                            "b_comp_bytes_per_sweep": bcomp, "gen_seconds": t_gen,
                            "mttkrp_items": info["items"], "split_rows": info["split_rows"],

@@ -95,7 +95,11 @@ typedef struct {
                               /* [1]: MTTKRP a-blocked order: > 0 = blocks of that many      */
                               /* a-rows, <= 0 = canonical order (default);                  */
                               /* [2]: Gram kernel (0 = default: fp64 tensor cores (DMMA) for  */
-                              /* the fp64 build with pitch >= 32, 1 = the FMA kernel); [3] = 0 */
+                              /* the fp64 build with pitch >= 32, 1 = the FMA kernel);        */
+                              /* [3]: sharded exchange (0 = full owned rows, graph-captured;   */
+                              /* 1 = delta: only the changed elements as (index, value) lists, */
+                              /* full rows when those are smaller; NCCL sweeps then run eagerly */
+                              /* because the list lengths are read on the host)               */
 } sacd_options;
 
 /* Per-sweep statistics (device-side ring, read by sacd_stats). */
@@ -124,6 +128,9 @@ typedef struct {
   int64_t device_bytes;
   int32_t kernels_per_sweep; /* libsacd kernels launched per sweep (from the captured graph)   */
   int32_t world_size, world_rank, sharded_ranks; /* sharded engine: G ranks (1 = unsharded)    */
+  int32_t delta_exchange;   /* 1: sharded passes exchange changed elements          */
+  int64_t delta_elems_sent; /* NCCL delta exchange so far: elements sent as (index, value) ...  */
+  int64_t full_elems_equiv; /* ... and the elements the full-row exchange would have sent       */
 } sacd_info;
 
 void sacd_default_options(sacd_options *opt);

@@ -239,9 +239,11 @@ static int capture_graph(Context &c) {
   c.opt.profile = 0;
   SACD_CUDA_TRY(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
   int rc = SACD_OK;
+  c.capturing = true;
   for (int n = 0; n < 3 && rc == SACD_OK; ++n)
     rc = c.sharded ? launch_sharded_mode_update(c, n, SACD_BR_AUTO, n == 0, n == 2, nullptr)
                    : launch_mode_update(c, n, SACD_BR_AUTO, n == 0, n == 2, nullptr);
+  c.capturing = false;
   c.opt.profile = saved_profile;
   cudaGraph_t g = nullptr;
   cudaError_t e = cudaStreamEndCapture(c.stream, &g);
@@ -265,7 +267,8 @@ static int capture_graph(Context &c) {
       c.kernels_per_sweep += 1;
   }
   cudaGetLastError();
-  if (!c.opt.use_graph) {
+  // the NCCL delta exchange reads the list lengths on the host: its sweeps run eagerly
+  if (!c.opt.use_graph || (c.delta && c.comm)) {
     cudaGraphDestroy(g);
     return SACD_OK;
   }
@@ -306,6 +309,11 @@ static void destroy(sacd_ctx *c) {
   cudaFree(c->st);
   cudaFree(c->M);
   cudaFree(c->Zs);
+  cudaFree(c->Fold);
+  cudaFree(c->didx);
+  cudaFree(c->dval);
+  cudaFree(c->dcnt);
+  cudaFree(c->dblk);
   cudaFree(c->partial);
   cudaFree(c->fixbuf);
   cudaFree(c->Hr);
@@ -537,6 +545,28 @@ static int init_impl(Context *c, const uint32_t *coords, const float *vals, uint
     c->device_bytes += (long long)(2 * (size_t)md.I * P * rs + (size_t)R * R * 8);
   }
   c->max_row_blocks = (maxI + 31) / 32 + 1;  // >= ceil(I / rows_per_block) for every pitch
+  // delta exchange buffers: list slot q holds up to rank q's owned elements
+  c->delta = c->sharded && c->opt.reserved[3] == 1 && (double)maxI * P < 4294967295.0;
+  if (c->delta) {
+    c->doff.assign(c->G, 0);
+    c->dcap.assign(c->G, 0);
+    long long tot = 0;
+    for (int q = 0; q < c->G; ++q) {
+      long long cap = 1;
+      for (int n = 0; n < 3; ++n)
+        cap = std::max(cap, (c->all_plans[n][q].rhi - c->all_plans[n][q].rlo) * (long long)P);
+      c->doff[q] = tot;
+      c->dcap[q] = cap;
+      tot += cap;
+    }
+    SACD_CUDA_TRY(cudaMalloc(&c->Fold, (size_t)maxI * P * rs));
+    SACD_CUDA_TRY(cudaMalloc(&c->didx, (size_t)tot * 4));
+    SACD_CUDA_TRY(cudaMalloc(&c->dval, (size_t)tot * rs));
+    SACD_CUDA_TRY(cudaMalloc(&c->dcnt, (size_t)c->G * 8));
+    SACD_CUDA_TRY(cudaMalloc(&c->dblk, (size_t)kDeltaBlocks * 4));
+    SACD_CUDA_TRY(cudaMemset(c->dcnt, 0, (size_t)c->G * 8));
+    c->device_bytes += (long long)((size_t)maxI * P * rs + (size_t)tot * (4 + rs));
+  }
   c->gram_blocks = (int)std::min<long long>(296, std::max<long long>(1, (maxI + 63) / 64));
   SACD_CUDA_TRY(cudaMalloc(&c->M, (size_t)((maxI + 31) / 32 * 32) * P * rs));
   if (c->opt.variant == SACD_VARIANT_SNAPSHOT) {  // snapshot importances of one pass (TT layout)
@@ -1041,6 +1071,9 @@ int sacd_get_info(sacd_ctx *c, sacd_info *o) {
   o->world_size = c->world;
   o->world_rank = c->me;
   o->sharded_ranks = c->sharded ? c->G : 1;
+  o->delta_exchange = c->delta ? 1 : 0;
+  o->delta_elems_sent = c->delta_sent;
+  o->full_elems_equiv = c->full_equiv;
   int k = 0;
   int rc = dev_read(c, &k, reinterpret_cast<const char *>(c->st) + offsetof(DevState, k), sizeof(int));
   if (rc == SACD_OK)

@@ -1514,6 +1514,84 @@ __global__ void __launch_bounds__(1024) k_finalize(int mode, long long nblk, con
   }
 }
 
+// ------------------------------------------------------------------ delta exchange
+// Changed elements of F over [lo, hi) (element indices of the padded row-major factor),
+// compared bit for bit against Fold (so a +0 / -0 flip is sent too and every replica stays
+// bitwise identical).  Two passes over a fixed grid of kDeltaBlocks contiguous chunks: count,
+// then write in index order (warp ballots + block prefix), so the lists are deterministic.
+template <typename Real>
+__device__ __forceinline__ bool elem_changed(const Real *F, const Real *Fo, long long i) {
+  if constexpr (sizeof(Real) == 8)
+    return __double_as_longlong(F[i]) != __double_as_longlong(Fo[i]);
+  else
+    return __float_as_uint(F[i]) != __float_as_uint(Fo[i]);
+}
+
+template <typename Real>
+__global__ void __launch_bounds__(256) k_delta_count(long long lo, long long hi, const Real *__restrict__ F,
+                                                     const Real *__restrict__ Fo, int *__restrict__ blk) {
+  __shared__ int red[8];
+  const long long per = (hi - lo + gridDim.x - 1) / gridDim.x;
+  const long long b0 = lo + (long long)blockIdx.x * per, b1 = min(hi, b0 + per);
+  int n = 0;
+  for (long long i = b0 + threadIdx.x; i < b1; i += blockDim.x) n += elem_changed(F, Fo, i);
+  for (int o = 16; o > 0; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = n;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int w = 0; w < 8; ++w) t += red[w];
+    blk[blockIdx.x] = t;
+  }
+}
+
+template <typename Real>
+__global__ void __launch_bounds__(256) k_delta_write(long long lo, long long hi, const Real *__restrict__ F,
+                                                     const Real *__restrict__ Fo, const int *__restrict__ blk,
+                                                     uint32_t *__restrict__ idx, Real *__restrict__ val,
+                                                     long long *__restrict__ count) {
+  __shared__ int wcnt[8];
+  __shared__ long long base_s;
+  const long long per = (hi - lo + gridDim.x - 1) / gridDim.x;
+  const long long b0 = lo + (long long)blockIdx.x * per, b1 = min(hi, b0 + per);
+  if (threadIdx.x == 0) {
+    long long b = 0;
+    for (int k = 0; k < (int)blockIdx.x; ++k) b += blk[k];
+    base_s = b;
+    if (blockIdx.x == gridDim.x - 1) *count = b + blk[blockIdx.x];
+  }
+  __syncthreads();
+  long long base = base_s;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (long long t0 = b0; t0 < b1; t0 += blockDim.x) {
+    const long long i = t0 + threadIdx.x;
+    const bool ch = i < b1 && elem_changed(F, Fo, i);
+    const unsigned bal = __ballot_sync(0xffffffffu, ch);
+    if (lane == 0) wcnt[w] = __popc(bal);
+    __syncthreads();
+    int before = 0, tot = 0;
+    for (int k = 0; k < 8; ++k) {
+      before += k < w ? wcnt[k] : 0;
+      tot += wcnt[k];
+    }
+    if (ch) {
+      const long long o = base + before + __popc(bal & ((1u << lane) - 1u));
+      idx[o] = (uint32_t)i;
+      val[o] = F[i];
+    }
+    base += tot;
+    __syncthreads();
+  }
+}
+
+template <typename Real>
+__global__ void k_delta_apply(const uint32_t *__restrict__ idx, const Real *__restrict__ val,
+                              const long long *__restrict__ count, Real *__restrict__ F) {
+  const long long n = *count;
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x)
+    F[idx[k]] = val[k];
+}
+
 // Snapshot variant (reading C10'): ti^k = fixed-order sum of the score pass's block partials
 // (the same tree as k_finalize, so the recorded ti equals it bitwise); the branch of THIS
 // pass: k == 1 (no history) the z > 0 rule, else Eq 27 iff ti^k > ti^{k-1}.
@@ -1855,6 +1933,7 @@ struct Impl {
     ModeData &md = c.m[mode];
     SACD_TRY(sharded_mttkrp_merge(c, mode));
     SACD_TRY(prepare(c, mode, branch_override, begin_sweep, 1));
+    if (c.delta) SACD_TRY(delta_snapshot(c, mode));
     constexpr int TR = rows_per_block<RT>();
     constexpr size_t smem = rows_smem_bytes<Real, RT>();
     constexpr int GT = gram_gt<RT>();
@@ -1888,8 +1967,89 @@ struct Impl {
                                                 32 | 1 | (end_sweep ? 6 : 0));
     SACD_CUDA_TRY(cudaGetLastError());
     SACD_TRY(prof_end(c, 5, pe));
-    if (c.comm) SACD_TRY(nccl_broadcast_rows(c, mode));
+    if (c.delta) SACD_TRY(delta_exchange(c, mode));
+    else if (c.comm) SACD_TRY(nccl_broadcast_rows(c, mode));
     SACD_TRY(chunk_mask(c, mode));
+    return SACD_OK;
+  }
+
+  // snapshot of the local shards' owned rows before the pass (delta exchange)
+  static int delta_snapshot(Context &c, int mode) {
+    const size_t rb = (size_t)c.pitch * sizeof(Real);
+    for (Shard &sh : c.shards) {
+      const long long rlo = sh.plan[mode].rlo, rhi = sh.plan[mode].rhi;
+      if (rhi > rlo)
+        SACD_CUDA_TRY(cudaMemcpyAsync(reinterpret_cast<char *>(c.Fold) + rlo * rb,
+                                      reinterpret_cast<const char *>(c.m[mode].F) + rlo * rb, (rhi - rlo) * rb,
+                                      cudaMemcpyDeviceToDevice, c.stream));
+    }
+    return SACD_OK;
+  }
+
+  // every owner compacts the changed elements of its rows into its list slot; the
+  // lists travel instead of the rows (NCCL: list lengths all-gathered, then one grouped
+  // broadcast per owner of the index and value arrays; full rows when that is smaller, as in
+  // the first sweeps).  Emulated ranks exercise the same lists on one replica: the owned
+  // rows are reset to the snapshot and every list is applied, so a compaction or apply error
+  // changes the factors.
+  static int delta_exchange(Context &c, int mode) {
+    Real *F = reinterpret_cast<Real *>(c.m[mode].F);
+    Real *Fo = reinterpret_cast<Real *>(c.Fold);
+    Real *V = reinterpret_cast<Real *>(c.dval);
+    for (Shard &sh : c.shards) {
+      const int q = sh.rank;
+      const long long lo = sh.plan[mode].rlo * c.pitch, hi = sh.plan[mode].rhi * c.pitch;
+      k_delta_count<Real><<<kDeltaBlocks, 256, 0, c.stream>>>(lo, hi, F, Fo, c.dblk);
+      k_delta_write<Real><<<kDeltaBlocks, 256, 0, c.stream>>>(lo, hi, F, Fo, c.dblk, c.didx + c.doff[q], V + c.doff[q],
+                                                              c.dcnt + q);
+    }
+    SACD_CUDA_TRY(cudaGetLastError());
+    const size_t rb = (size_t)c.pitch * sizeof(Real);
+    if (!c.comm) {  // emulated ranks: reset the owned rows, apply every list in rank order
+      for (Shard &sh : c.shards) {
+        const long long rlo = sh.plan[mode].rlo, rhi = sh.plan[mode].rhi;
+        if (rhi > rlo)
+          SACD_CUDA_TRY(cudaMemcpyAsync(reinterpret_cast<char *>(F) + rlo * rb,
+                                        reinterpret_cast<const char *>(Fo) + rlo * rb, (rhi - rlo) * rb,
+                                        cudaMemcpyDeviceToDevice, c.stream));
+      }
+      for (int q = 0; q < c.G; ++q)
+        k_delta_apply<Real><<<kDeltaBlocks, 256, 0, c.stream>>>(c.didx + c.doff[q], V + c.doff[q], c.dcnt + q, F);
+      SACD_CUDA_TRY(cudaGetLastError());
+      return SACD_OK;
+    }
+    if (c.capturing) return nccl_broadcast_rows(c, mode);  // kernel count only; never replayed
+    SACD_TRY(nccl_allgather_inplace(c, c.dcnt, 1, 2));
+    std::vector<long long> h(c.G);
+    SACD_CUDA_TRY(cudaMemcpyAsync(h.data(), c.dcnt, (size_t)c.G * 8, cudaMemcpyDeviceToHost, c.stream));
+    SACD_CUDA_TRY(cudaStreamSynchronize(c.stream));
+    long long nd = 0, nf = 0;
+    for (int q = 0; q < c.G; ++q) {
+      nd += h[q];
+      nf += (c.all_plans[mode][q].rhi - c.all_plans[mode][q].rlo) * c.pitch;
+    }
+    c.full_equiv += nf;
+    if (nd * (long long)(4 + sizeof(Real)) >= nf * (long long)sizeof(Real)) return nccl_broadcast_rows(c, mode);
+    c.delta_sent += nd;
+    const ncclDataType_t t = sizeof(Real) == 8 ? ncclFloat64 : ncclFloat32;
+    ncclResult_t r = ncclGroupStart();
+    for (int q = 0; q < c.G && r == ncclSuccess; ++q) {
+      if (h[q] == 0) continue;
+      r = ncclBroadcast(c.didx + c.doff[q], c.didx + c.doff[q], (size_t)h[q], ncclUint32, q,
+                        reinterpret_cast<ncclComm_t>(c.comm), c.stream);
+      if (r == ncclSuccess)
+        r = ncclBroadcast(V + c.doff[q], V + c.doff[q], (size_t)h[q], t, q, reinterpret_cast<ncclComm_t>(c.comm),
+                          c.stream);
+    }
+    const ncclResult_t r2 = ncclGroupEnd();
+    if (r != ncclSuccess || r2 != ncclSuccess) {
+      set_error(std::string("ncclBroadcast (delta): ") + ncclGetErrorString(r != ncclSuccess ? r : r2));
+      return SACD_ENCCL;
+    }
+    for (int q = 0; q < c.G; ++q)
+      if (q != c.me && h[q] > 0)
+        k_delta_apply<Real><<<kDeltaBlocks, 256, 0, c.stream>>>(c.didx + c.doff[q], V + c.doff[q], c.dcnt + q, F);
+    SACD_CUDA_TRY(cudaGetLastError());
     return SACD_OK;
   }
 

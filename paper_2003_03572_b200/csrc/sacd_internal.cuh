@@ -172,7 +172,20 @@ struct Context {
   long long *xid = nullptr;       // [G] head row ids
   void *xrow = nullptr;           // [G * pitch] head partial rows (Real)
   double *xstats = nullptr;       // [G * (4 + R*R)] (ti, md, E, Ech, Gram partial)
+  // delta exchange (opt.reserved[3] = 1): per mode pass each owner sends only the
+  // elements of its rows that changed, as (element index, value) lists
+  bool delta = false;
+  bool capturing = false;         // inside capture_graph (no host synchronisation allowed)
+  void *Fold = nullptr;           // Real [maxI * pitch]: owned rows before the pass
+  uint32_t *didx = nullptr;       // [sum_q cap_q] list of rank q at doff[q]
+  void *dval = nullptr;           // Real [sum_q cap_q]
+  long long *dcnt = nullptr;      // [G] list lengths (device)
+  int *dblk = nullptr;            // [kDeltaBlocks] per-block change counts
+  std::vector<long long> doff, dcap;  // host: slot offsets / capacities (elements)
+  long long delta_sent = 0, full_equiv = 0;  // host: elements exchanged as deltas / as full rows
 };
+
+constexpr int kDeltaBlocks = 296;
 
 size_t real_size(const Context &c);
 

@@ -52,7 +52,8 @@ class Info(C.Structure):
                 ("mode_a", C.c_int32 * 3), ("mode_b", C.c_int32 * 3), ("xnorm2", C.c_double),
                 ("items", C.c_int64 * 3), ("split_rows", C.c_int64 * 3), ("device_bytes", C.c_int64),
                 ("kernels_per_sweep", C.c_int32), ("world_size", C.c_int32), ("world_rank", C.c_int32),
-                ("sharded_ranks", C.c_int32)]
+                ("sharded_ranks", C.c_int32), ("delta_exchange", C.c_int32), ("delta_elems_sent", C.c_int64),
+                ("full_elems_equiv", C.c_int64)]
 
 
 class SacdError(RuntimeError):
@@ -148,7 +149,7 @@ class Sacd:
     def __init__(self, coords, vals, dims, rank, seed, *, precision="f64", l_mode="diag", variant="gs",
                  device=-1, stream=None, use_graph=True, profile=False, nnz_per_item=0, mttkrp_variant=0,
                  world_size=1, world_rank=0, nccl_id=None, force_sharded=False, emulate_ranks=0, rows_variant=0, ablk_rows=0,
-                 gram_variant=0):
+                 gram_variant=0, exchange="full"):
         L = load_library()
         o = Options()
         L.sacd_default_options(C.byref(o))
@@ -169,6 +170,7 @@ class Sacd:
         o.reserved[0] = int(rows_variant)
         o.reserved[1] = int(ablk_rows)
         o.reserved[2] = int(gram_variant)
+        o.reserved[3] = {"full": 0, "delta": 1}[exchange]
         self._nccl_id = None
         if nccl_id is not None:
             self._nccl_id = C.create_string_buffer(bytes(nccl_id), 128)
@@ -244,7 +246,9 @@ class Sacd:
                     l_mode=i.l_mode, variant=i.variant, k=i.k, mode_a=list(i.mode_a), mode_b=list(i.mode_b),
                     xnorm2=i.xnorm2, items=list(i.items), split_rows=list(i.split_rows),
                     device_bytes=i.device_bytes, kernels_per_sweep=i.kernels_per_sweep,
-                    world_size=i.world_size, world_rank=i.world_rank, sharded_ranks=i.sharded_ranks)
+                    world_size=i.world_size, world_rank=i.world_rank, sharded_ranks=i.sharded_ranks,
+                    delta_exchange=i.delta_exchange, delta_elems_sent=i.delta_elems_sent,
+                    full_elems_equiv=i.full_elems_equiv)
 
     # -- component entry points
     def set_factors(self, mode, F):

@@ -516,6 +516,53 @@ def test_sharded_nccl_world1_matches_unsharded():
         assert factor_err(out[1][2][n], out[0][2][n]) <= 1e-10
 
 
+@pytest.mark.parametrize("G", [2, 3, 8])
+@pytest.mark.parametrize("precision", ["f64", "f32"])
+def test_delta_exchange_emulated_bitwise_equals_full(G, precision):
+    """with the delta exchange every pass resets the owned rows to their
+    pre-pass values and rebuilds them from the owners' (index, value) lists of changed
+    elements, so any compaction / apply error shows; the factors, f and E must equal the
+    full-row exchange bit for bit, and the oracle within the tolerances (fp64)."""
+    dims = (300, 200, 50)
+    c, v = ragged_tensor(dims, 20000, 8, heavy_rows=((2, 1, 3000), (0, 5, 900), (1, 199, 1500)))
+    res = []
+    for ex in ("full", "delta"):
+        with S(c, v, dims, 24, 17, precision=precision, nnz_per_item=256, emulate_ranks=G, exchange=ex) as g:
+            assert g.info()["delta_exchange"] == (ex == "delta")
+            g.iterate(8)
+            st = g.stats()
+            res.append((np.array([s["objective"] for s in st]), np.array([s["E"] for s in st]), g.factors()))
+    assert np.array_equal(res[0][0], res[1][0]) and np.array_equal(res[0][1], res[1][1])
+    for n in range(3):
+        assert np.array_equal(res[0][2][n], res[1][2][n])
+    if precision == "f64":
+        fg, Fg, Eg, brg, ora = run_pair(c, v, dims, 24, 17, 8, nnz_per_item=256, emulate_ranks=G, exchange="delta")
+        check_pair(fg, Fg, Eg, brg, ora)
+
+
+def test_delta_exchange_nccl_world1():
+    """The NCCL delta path (list lengths all-gathered and read on the host, lists broadcast,
+    eager sweeps) with a one-rank communicator equals the unsharded engine; the counters show
+    that lists were sent once the factors settle."""
+    cfg = SI.CONFIGS["c2"]
+    c, v = SI.make_tensor(cfg)
+    c, v = c.numpy(), v.numpy()
+    out = []
+    for kw in ({}, {"force_sharded": True, "exchange": "delta"}):
+        with S(c, v, cfg.dims, cfg.rank, cfg.seed, **kw) as g:
+            g.iterate(8)
+            st = g.stats()
+            out.append((np.array([s["objective"] for s in st]), np.array([s["E"] for s in st]), g.factors(),
+                        g.info()))
+    np.testing.assert_allclose(out[1][0], out[0][0], rtol=1e-12)
+    assert np.array_equal(out[1][1], out[0][1])
+    for n in range(3):
+        assert factor_err(out[1][2][n], out[0][2][n]) <= 1e-10
+    inf = out[1][3]
+    assert inf["delta_exchange"] == 1 and inf["full_elems_equiv"] > 0
+    assert 0 < inf["delta_elems_sent"] < inf["full_elems_equiv"]
+
+
 # ----------------------------------------------------------------------------- held-out evaluation (f3)
 @pytest.mark.parametrize("precision", ["f64", "f32"])
 @pytest.mark.parametrize("R", [5, 64, 200])

@@ -8,6 +8,10 @@
   row owners in rank order, owners run the row pass on their rows, the updated rows are
   all-gathered, Grams / ti / E are reduced in rank order.  The result must equal the
   unsharded oracle run (same decisions, same branch, f to 1e-12).
+* The delta exchange is emulated the same way: each owner lists the elements of
+  its rows that changed bit for bit (flat index, value), the list lengths are all-gathered
+  and every rank takes the lists when they are smaller than the rows (12 vs 8 bytes per
+  element), else the rows; the others apply the lists.  Same result as the oracle.
 """
 import os
 import socket
@@ -83,7 +87,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, K, q):
+def _worker(rank, world, port, K, q, delta=False):
     try:
         os.environ["MASTER_ADDR"] = "127.0.0.1"
         os.environ["MASTER_PORT"] = str(port)
@@ -99,6 +103,7 @@ def _worker(rank, world, port, K, q):
         zp = [np.zeros((dims[n], R)) for n in range(3)]
         hist = [[], [], []]
         fs, Es, brs = [], [], []
+        used_delta = [0]
         xn2 = float((v.astype(np.float64) ** 2).sum())
         for k in range(1, K + 1):
             Erow, brrow, mdot = [], [], 0.0
@@ -126,10 +131,36 @@ def _worker(rank, world, port, K, q):
                 Fn, zn, ti, E, Ech, md, _ = O.mode_pass(M[rlo:rhi], H, F[n][rlo:rhi], zp[n][rlo:rhi], br)
                 zp[n][rlo:rhi] = zn
                 # (4) updated rows all-gathered into the replicated factor
-                rows = [None] * world
-                dist.all_gather_object(rows, (rlo, rhi, Fn))
-                for (r0, r1, blk) in rows:
-                    F[n][r0:r1] = blk
+                if delta:
+                    old = F[n][rlo:rhi]
+                    ch = (Fn.view(np.int64) != old.view(np.int64)).reshape(-1)
+                    idx = np.nonzero(ch)[0] + rlo * R
+                    lst = (idx.astype(np.uint32), Fn.reshape(-1)[ch].copy())
+                    cnt = torch.tensor([len(idx)], dtype=torch.int64)
+                    cnts = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+                    dist.all_gather(cnts, cnt)
+                    nd = int(sum(int(x) for x in cnts))
+                    nfull = sum((plans[n][p2][3] - plans[n][p2][2]) * R for p2 in range(world))
+                    F[n][rlo:rhi] = Fn
+                    if nd * 12 < nfull * 8:
+                        lists = [None] * world
+                        dist.all_gather_object(lists, lst)
+                        flat = F[n].reshape(-1)
+                        for p2, (ix, vals) in enumerate(lists):
+                            assert len(ix) == int(cnts[p2])
+                            if p2 != rank:
+                                flat[ix.astype(np.int64)] = vals
+                        used_delta[0] += 1
+                    else:
+                        rows = [None] * world
+                        dist.all_gather_object(rows, (rlo, rhi, Fn))
+                        for (r0, r1, blk) in rows:
+                            F[n][r0:r1] = blk
+                else:
+                    rows = [None] * world
+                    dist.all_gather_object(rows, (rlo, rhi, Fn))
+                    for (r0, r1, blk) in rows:
+                        F[n][r0:r1] = blk
                 # (5) scalars reduced in rank order
                 sc = [None] * world
                 dist.all_gather_object(sc, (ti, E, md))
@@ -150,27 +181,29 @@ def _worker(rank, world, port, K, q):
             Es.append(Erow)
             brs.append(brrow)
         if rank == 0:
-            q.put((fs, Es, brs, [x.copy() for x in F]))
+            q.put((fs, Es, brs, [x.copy() for x in F], used_delta[0]))
         dist.destroy_process_group()
     except Exception as ex:  # surface worker failures to the parent
         q.put(("error", repr(ex)))
         raise
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_sharded_sweeps_equal_unsharded_oracle(plan, world):
-    K = 4
+@pytest.mark.parametrize("world,delta", [(2, False), (3, False), (2, True), (3, True)])
+def test_sharded_sweeps_equal_unsharded_oracle(plan, world, delta):
+    K = 6 if delta else 4
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, K, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, K, q, delta)) for r in range(world)]
     for p in procs:
         p.start()
     res = q.get(timeout=300)
     for p in procs:
         p.join(timeout=120)
     assert res[0] != "error", res
-    fs, Es, brs, F = res
+    fs, Es, brs, F, used = res
+    if delta:
+        assert used > 0
     dims, R, seed = (40, 30, 20), 4, 3
     c, v = SI.tiny_tensor(dims, 0.08, 5)
     ora = O.sacd_run(c.numpy(), v.numpy(), dims, R, seed, K)
