@@ -193,11 +193,10 @@ static void build_items_segments(const std::vector<long long> &seg_start, const 
 }
 
 // Does the selected MTTKRP kernel read the 16-byte nonzero records (nzm)?  Only those
-// kernels can run an a-blocked execution order (the warp fiber kernel and the R <= 16
-// kernel read the canonical SoA arrays).
+// kernels can run an a-blocked execution order (the warp fiber kernel, variant 1, and the
+// R <= 16 kernel read the canonical SoA arrays).
 static bool mttkrp_reads_nzm(const Context &c) {
   if (c.pitch < 32 || c.opt.mttkrp_variant == 1) return false;
-  if (c.opt.precision == SACD_F64 && c.pitch >= 256 && c.opt.mttkrp_variant == 0) return false;
   return true;
 }
 

@@ -1864,7 +1864,12 @@ struct Impl {
           else gol(k_mttkrp_lean<Real, RT, SW8, 2, 2>, SW8);
         }
         else if (sizeof(Real) == 8 && RT >= 256) {
-          go(k_mttkrp_fiber<Real, RT, 1, fiber_min_blocks<Real, RT>()>);  // default, fp64, R > 128
+          // fp64, R > 128: one warp per item, 8 fp64 columns per lane (variant 22; measured on
+          // B200 on c5 R=256: 13.7 vs 28.6 ms per sweep for the warp fiber kernel, variant 1)
+          constexpr int SWW = RT / 8 > 32 ? 32 : RT / 8;
+          const long long lb = (n_items * SWW + 255) / 256;
+          k_mttkrp_lean<Real, RT, SWW, 1, 2><<<(unsigned)lb, 256, 0, c.stream>>>(items, n_items, md.nzm, A, B, out,
+                                                                                partial);
         } else if (sizeof(Real) == 8 && RT <= 64 && md.n_fibers > 0 && c.nnz >= 2 * md.n_fibers) {
           // fp64, R <= 64, mean fiber length >= 2 (the Zipf configs c3, c4): one warp per item
           // (2 fp64 columns per lane at R = 64) at 48 registers / 40 warps per SM.  Measured on

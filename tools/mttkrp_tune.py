@@ -19,13 +19,15 @@ ap.add_argument("--variants", default="1,10,11,12,13,14,15,0")
 ap.add_argument("--nnz-per-item", type=int, default=0)
 ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--sweeps", type=int, default=0, help="SaCD sweeps before timing (sparse factors)")
+ap.add_argument("--ablk", type=int, default=0, help="a-blocked execution order: a-rows per block (0 = canonical)")
 a = ap.parse_args()
 cfg = SI.CONFIGS[a.config]
 R = a.rank or cfg.rank
 c, v = SI.make_tensor(cfg, device="cuda")
 ref = None
 for var in [int(x) for x in a.variants.split(",")]:
-    g = Sacd(c, v, cfg.dims, R, cfg.seed, precision=a.precision, mttkrp_variant=var, nnz_per_item=a.nnz_per_item)
+    g = Sacd(c, v, cfg.dims, R, cfg.seed, precision=a.precision, mttkrp_variant=var, nnz_per_item=a.nnz_per_item,
+             ablk_rows=a.ablk)
     if a.sweeps:
         g.iterate(a.sweeps)
     ms = [g.time_mttkrp(n, a.reps) for n in range(3)]
@@ -33,6 +35,6 @@ for var in [int(x) for x in a.variants.split(",")]:
     same = "ref" if ref is None else ("bitwise-equal" if np.array_equal(M0, ref) else f"DIFF {np.abs(M0-ref).max():.3e}")
     if ref is None:
         ref = M0
-    print(f"{a.config} {a.precision} R={R} T={a.nnz_per_item or 1024} k={a.sweeps} variant {var}: ms per mode "
+    print(f"{a.config} {a.precision} R={R} T={a.nnz_per_item or 1024} k={a.sweeps} ablk={a.ablk} variant {var}: ms per mode "
           f"{ms[0]:.3f} {ms[1]:.3f} {ms[2]:.3f}  sum {sum(ms):.3f}  {same}", flush=True)
     g.close()
