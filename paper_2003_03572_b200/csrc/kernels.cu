@@ -525,7 +525,11 @@ __device__ __forceinline__ void prefetch_rows(const uint4 &m, bool valid, const 
   }
 }
 
-template <typename Real, int RT, int SW, int D, int MINB, int PF = 0>
+// XS: how the batch's per-nonzero b index / x reach every lane of the worker: 0 = warp
+// shuffles (1 for the b index, 2 for x in fp64), 1 = x through a shared-memory broadcast
+// (one wavefront instead of two shuffles), 2 = the b index and x as one 16-byte
+// shared-memory broadcast per nonzero.
+template <typename Real, int RT, int SW, int D, int MINB, int PF = 0, int XS = 0>
 __global__ void __launch_bounds__(256, MINB) k_mttkrp_lean(const WorkItem *__restrict__ items, long long n_items,
                                                           const uint4 *__restrict__ nzm,
                                                           const Real *__restrict__ A, const Real *__restrict__ B,
@@ -542,6 +546,10 @@ __global__ void __launch_bounds__(256, MINB) k_mttkrp_lean(const WorkItem *__res
   const int slot = (int)items[item].slot;
   const Real *Al = A + lane * VEC;
   const Real *Bl = B + lane * VEC;
+  __shared__ __align__(16) Real xsb[XS == 1 ? 2 : 1][XS == 1 ? 256 : 1];
+  __shared__ __align__(16) uint4 rsb[XS == 2 ? 2 : 1][XS == 2 ? 256 : 1];
+  const int wbase = threadIdx.x & ~(SW - 1);
+  int par = 0;
   SR arow;
   Real acc[E], facc[E];
 #pragma unroll
@@ -567,20 +575,53 @@ __global__ void __launch_bounds__(256, MINB) k_mttkrp_lean(const WorkItem *__res
     // x of this lane's nonzero, converted once per batch (F2F runs on the narrow XU pipe:
     // converting per nonzero in every lane of the worker made the fp64 kernel XU-bound)
     const Real xl = (Real)__uint_as_float(my.z);
+    if constexpr (XS == 1) {
+      par ^= 1;
+      xsb[par][threadIdx.x] = xl;
+      __syncwarp(mask);
+    } else if constexpr (XS == 2) {
+      par ^= 1;
+      uint4 r;
+      r.x = my.y;
+      r.y = 0u;
+      if constexpr (sizeof(Real) == 8) {
+        r.z = (uint32_t)__double2loint((double)xl);
+        r.w = (uint32_t)__double2hiint((double)xl);
+      } else {
+        r.z = __float_as_uint((float)xl);
+        r.w = 0u;
+      }
+      rsb[par][threadIdx.x] = r;
+      __syncwarp(mask);
+    }
     uint32_t fb[SW];
+    Real xr[D + 1];
     SR bb[D + 1];
+    auto fetch = [&](int j) {  // b index + flags (and, XS == 2, x) of nonzero j of the batch
+      if constexpr (XS == 2) {
+        const uint4 r = rsb[par][wbase + j];
+        fb[j] = r.x;
+        if constexpr (sizeof(Real) == 8) xr[j % (D + 1)] = __hiloint2double((int)r.w, (int)r.z);
+        else xr[j % (D + 1)] = __uint_as_float(r.z);
+      } else {
+        fb[j] = __shfl_sync(mask, my.y, j, SW);
+      }
+    };
 #pragma unroll
     for (int j = 0; j < D && j < SW; ++j) {
-      fb[j] = __shfl_sync(mask, my.y, j, SW);
+      fetch(j);
       bb[j % (D + 1)].load(Bl + (long long)(fb[j] & kIdxMask) * RT);
     }
 #pragma unroll
     for (int j = 0; j < SW; ++j) {
       if (j + D < SW) {
-        fb[j + D] = __shfl_sync(mask, my.y, j + D, SW);
+        fetch(j + D);
         bb[(j + D) % (D + 1)].load(Bl + (long long)(fb[j + D] & kIdxMask) * RT);
       }
-      const Real x = __shfl_sync(mask, xl, j, SW);
+      Real x;
+      if constexpr (XS == 2) x = xr[j % (D + 1)];
+      else if constexpr (XS == 1) x = xsb[par][wbase + j];
+      else x = __shfl_sync(mask, xl, j, SW);
       if (fb[j] & kFiberStart) {
 #pragma unroll
         for (int k = 0; k < E; ++k) {  // close the previous fiber: acc += a * facc
@@ -1856,6 +1897,12 @@ struct Impl {
           else if (var == 47) gol(k_mttkrp_lean<Real, RT, SW4, 1, 3, 3>, SW4);
           else if (var == 48) gol(k_mttkrp_lean<Real, RT, SW8, 1, 2, 1>, SW8);
           else if (var == 49) gol(k_mttkrp_lean<Real, RT, SW8, 1, 2, 3>, SW8);
+          // shared-memory broadcast of x (XS = 1) or of the b index and x (XS = 2)
+          else if (var == 30) gol(k_mttkrp_lean<Real, RT, sub_warp_lanes<Real, RT>(), 1, 5, 0, 1>, sub_warp_lanes<Real, RT>());
+          else if (var == 31) gol(k_mttkrp_lean<Real, RT, sub_warp_lanes<Real, RT>(), 1, 5, 0, 2>, sub_warp_lanes<Real, RT>());
+          else if (var == 32) gol(k_mttkrp_lean<Real, RT, SW4, 1, 3, 0, 1>, SW4);
+          else if (var == 33) gol(k_mttkrp_lean<Real, RT, SW4, 1, 3, 0, 2>, SW4);
+          else if (var == 34) gol(k_mttkrp_lean<Real, RT, sub_warp_lanes<Real, RT>(), 2, 5, 0, 2>, sub_warp_lanes<Real, RT>());
           else if (var == 40) gol(k_mttkrp_lean<Real, RT, sub_warp_lanes<Real, RT>(), 1, 6>, sub_warp_lanes<Real, RT>());
           else if (var == 41) gol(k_mttkrp_lean<Real, RT, sub_warp_lanes<Real, RT>(), 1, 5>, sub_warp_lanes<Real, RT>());
           else if (var == 42) gol(k_mttkrp_lean<Real, RT, sub_warp_lanes<Real, RT>(), 2, 5>, sub_warp_lanes<Real, RT>());
@@ -1875,10 +1922,14 @@ struct Impl {
           // (2 fp64 columns per lane at R = 64) at 48 registers / 40 warps per SM.  Measured on
           // B200 (tools/mttkrp_tune.py, variant 41): c4 13.65 vs 15.17 ms per sweep, c3 1.22 vs
           // 1.28; on the uniform c5 (fibers of length ~1) it loses, so those keep the default.
+          // x reaches the lanes through a shared-memory broadcast (XS = 1, one L1 wavefront
+          // instead of two shuffles; the kernel is bound by the L1 data path: c4 12.11 vs
+          // 13.66 ms, variant 30); with two workers per warp (R = 32) the b index and x go as
+          // one 16-byte broadcast (XS = 2; c3 1.195 vs 1.227 ms, variant 31).
           constexpr int SWF = sub_warp_lanes<Real, RT>();
           const long long lb = (n_items * SWF + 255) / 256;
-          k_mttkrp_lean<Real, RT, SWF, 1, 5><<<(unsigned)lb, 256, 0, c.stream>>>(items, n_items, md.nzm, A, B, out,
-                                                                                partial);
+          k_mttkrp_lean<Real, RT, SWF, 1, 5, 0, SWF == 32 ? 1 : 2><<<(unsigned)lb, 256, 0, c.stream>>>(
+              items, n_items, md.nzm, A, B, out, partial);
         } else {
           // default (measured on B200, tools/mttkrp_tune.py): the lean sub-warp kernel with
           // 4 fp64 / 8 fp32 columns per lane
