@@ -5,6 +5,9 @@
 #include <string.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <new>
 #include <vector>
 
@@ -402,6 +405,7 @@ static int sync_if_device(const void *a, const void *b) {
 static int init_impl(Context *c, const uint32_t *coords, const float *vals, uint64_t seed) {
   const size_t rs = real_size(*c);
   cudaStream_t s = c->stream;
+  InitTimer tm;
   SACD_TRY(sync_if_device(coords, vals));
   SACD_CUDA_TRY(cudaMalloc(&c->st, sizeof(DevState)));
   SACD_CUDA_TRY(cudaMemsetAsync(c->st, 0, sizeof(DevState), s));
@@ -419,10 +423,12 @@ static int init_impl(Context *c, const uint32_t *coords, const float *vals, uint
     SACD_CUDA_TRY(cudaMemcpyAsync(dc, coords, (size_t)c->nnz * 12, cudaMemcpyDefault, s));
     SACD_CUDA_TRY(cudaMemcpyAsync(dv, vals, (size_t)c->nnz * 4, cudaMemcpyDefault, s));
   }
+  tm.mark(s, "H2D copy of the COO");
   int rc = build_layouts(*c, dc, dv);
   cudaFreeAsync(dc, s);
   cudaFreeAsync(dv, s);
   SACD_TRY(rc);
+  tm.mark(s, "layouts (sort, gather)");
 
   // partitions (host planning over row_ptr, once)
   const long long T = c->opt.nnz_per_item > 0 ? c->opt.nnz_per_item : 1024;
@@ -593,13 +599,16 @@ static int init_impl(Context *c, const uint32_t *coords, const float *vals, uint
     SACD_CUDA_TRY(cudaMalloc(&c->xrow, (size_t)c->G * P * rs));
     SACD_CUDA_TRY(cudaMalloc(&c->xstats, (size_t)c->G * (4 + (size_t)R * R) * 8));
   }
+  tm.mark(s, "work items, buffers");
   SACD_TRY(launch_setup(*c));
   SACD_TRY(launch_init_factors(*c, seed));
   for (int n = 0; n < 3; ++n) SACD_TRY(launch_gram(*c, n));
   SACD_TRY(c->sharded ? launch_sharded_initial_fit(*c) : launch_initial_fit(*c));
   SACD_CUDA_TRY(cudaStreamSynchronize(s));
+  tm.mark(s, "init factors, Grams, f^0");
   SACD_TRY(capture_graph(*c));
   SACD_CUDA_TRY(cudaStreamSynchronize(s));
+  tm.mark(s, "graph capture");
   return SACD_OK;
 }
 
@@ -1016,16 +1025,28 @@ int sacd_layout(sacd_ctx *c, int32_t mode, uint32_t *idx_a, uint32_t *idx_b, flo
   }
   ModeData &md = c->m[mode];
   int rc = SACD_OK;
+  uint32_t *tmp = nullptr;
+  if (!md.idx_a && c->nnz) {  // no SoA copies: unpack the canonical 16-byte records
+    if (cudaMalloc(&tmp, (size_t)c->nnz * 12) != cudaSuccess) {
+      cudaGetLastError();
+      set_error("sacd_layout: out of device memory");
+      return SACD_ENOMEM;
+    }
+    rc = launch_unpack_nzm(*c, md.nzm, c->nnz, tmp, tmp + c->nnz, reinterpret_cast<float *>(tmp + 2 * c->nnz));
+  }
+  const uint32_t *sa = md.idx_a ? md.idx_a : tmp, *sb = md.idx_b ? md.idx_b : (tmp ? tmp + c->nnz : nullptr);
+  const float *sv = md.val ? md.val : (tmp ? reinterpret_cast<const float *>(tmp + 2 * c->nnz) : nullptr);
   if (rc == SACD_OK && idx_a && c->nnz) {
-    rc = dev_read(c, idx_a, md.idx_a, (size_t)c->nnz * 4);
+    rc = dev_read(c, idx_a, sa, (size_t)c->nnz * 4);
     for (long long e = 0; rc == SACD_OK && e < c->nnz; ++e) idx_a[e] &= kIdxMask;  // strip the flag bits
   }
   if (rc == SACD_OK && idx_b && c->nnz) {
-    rc = dev_read(c, idx_b, md.idx_b, (size_t)c->nnz * 4);
+    rc = dev_read(c, idx_b, sb, (size_t)c->nnz * 4);
     for (long long e = 0; rc == SACD_OK && e < c->nnz; ++e) idx_b[e] &= kIdxMask;
   }
-  if (rc == SACD_OK && val && c->nnz) rc = dev_read(c, val, md.val, (size_t)c->nnz * 4);
+  if (rc == SACD_OK && val && c->nnz) rc = dev_read(c, val, sv, (size_t)c->nnz * 4);
   if (rc == SACD_OK && row_ptr) rc = dev_read(c, row_ptr, md.row_ptr, (size_t)(md.I + 1) * 8);
+  if (tmp) cudaFree(tmp);
   return sticky(c, rc);
 }
 

@@ -2380,6 +2380,22 @@ int launch_mode_update(Context &c, int mode, int branch_override, bool begin_swe
 
 int launch_initial_fit(Context &c) { SACD_DISPATCH(c, I_::initial_fit(c)); }
 
+__global__ void k_unpack_nzm(const uint4 *__restrict__ nzm, long long n, uint32_t *__restrict__ ia,
+                             uint32_t *__restrict__ ib, float *__restrict__ v) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+    const uint4 r = nzm[e];
+    ia[e] = r.x;
+    ib[e] = r.y;
+    v[e] = __uint_as_float(r.z);
+  }
+}
+
+int launch_unpack_nzm(Context &c, const uint4 *nzm, long long nnz, uint32_t *ia, uint32_t *ib, float *v) {
+  if (nnz > 0) k_unpack_nzm<<<grid1d(nnz), 256, 0, c.stream>>>(nzm, nnz, ia, ib, v);
+  SACD_CUDA_TRY(cudaGetLastError());
+  return SACD_OK;
+}
+
 int launch_range_check(Context &c, const uint32_t *coords, long long n, int *flag) {
   if (n > 0) k_range_check<<<grid1d(n), 256, 0, c.stream>>>(coords, n, c.dims[0], c.dims[1], c.dims[2], flag);
   SACD_CUDA_TRY(cudaGetLastError());

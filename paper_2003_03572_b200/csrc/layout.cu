@@ -68,10 +68,12 @@ __global__ void k_gather(const uint32_t *__restrict__ coords, const float *__res
     const uint32_t fl = (fiber_start ? kFiberStart : 0u) | (row_start ? kRowStart : 0u);
     const uint32_t xa = coords[3 * p + a] | fl, xb = coords[3 * p + b] | fl;
     const float x = vals[p];
-    ia[e] = xa;
-    ib[e] = xb;
-    in_[e] = (uint32_t)row;
-    v[e] = x;
+    if (ia) {  // SoA copies only when a kernel of this context reads them (layout_needs_soa)
+      ia[e] = xa;
+      ib[e] = xb;
+      in_[e] = (uint32_t)row;
+      v[e] = x;
+    }
     nzm[e] = make_uint4(xa, xb, __float_as_uint(x), (uint32_t)row);
     fs = fiber_start;
     }
@@ -98,12 +100,15 @@ __global__ void k_row_ptr(const unsigned long long *__restrict__ keys, long long
 
 // ||X||^2 = sum x^2 in fp64: fixed grid of per-block partials, then one block in order.
 constexpr int kNormBlocks = 296;
-__global__ void k_norm_partial(const float *__restrict__ v, long long nnz, double *__restrict__ part) {
+__global__ void k_norm_partial(const uint4 *__restrict__ nzm, long long nnz, double *__restrict__ part) {
   __shared__ double sh[256];
   const long long per = (nnz + gridDim.x - 1) / gridDim.x;
   const long long e0 = blockIdx.x * per, e1 = min(nnz, e0 + per);
   double s = 0.0;
-  for (long long e = e0 + threadIdx.x; e < e1; e += blockDim.x) s += (double)v[e] * (double)v[e];
+  for (long long e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+    const double x = (double)__uint_as_float(nzm[e].z);
+    s += x * x;
+  }
   sh[threadIdx.x] = s;
   __syncthreads();
   for (int o = 128; o > 0; o >>= 1) {
@@ -253,6 +258,7 @@ int build_layouts(Context &c, const uint32_t *coords, const float *vals) {
   const long long nnz = c.nnz;
   cudaStream_t s = c.stream;
   int *flags = nullptr;
+  InitTimer tm;
   SACD_CUDA_TRY(cudaMallocAsync(&flags, 4 * sizeof(unsigned long long), s));  // flags | fiber counts [3]
   SACD_CUDA_TRY(cudaMemsetAsync(flags, 0, 4 * sizeof(unsigned long long), s));
   unsigned long long *nfib = reinterpret_cast<unsigned long long *>(flags) + 1;
@@ -289,24 +295,32 @@ int build_layouts(Context &c, const uint32_t *coords, const float *vals) {
     ModeData &md = c.m[n];
     const int a = md.a, b = md.b;
     const unsigned long long Ia = (unsigned long long)c.dims[a], Ib = (unsigned long long)c.dims[b];
-    SACD_CUDA_TRY(cudaMallocAsync(&md.idx_a, ne * 4, s));
-    SACD_CUDA_TRY(cudaMallocAsync(&md.idx_b, ne * 4, s));
-    SACD_CUDA_TRY(cudaMallocAsync(&md.idx_n, ne * 4, s));
-    SACD_CUDA_TRY(cudaMallocAsync(&md.val, ne * 4, s));
+    const bool soa = layout_needs_soa(c);
+    if (soa) {
+      SACD_CUDA_TRY(cudaMallocAsync(&md.idx_a, ne * 4, s));
+      SACD_CUDA_TRY(cudaMallocAsync(&md.idx_b, ne * 4, s));
+      SACD_CUDA_TRY(cudaMallocAsync(&md.idx_n, ne * 4, s));
+      SACD_CUDA_TRY(cudaMallocAsync(&md.val, ne * 4, s));
+    }
     SACD_CUDA_TRY(cudaMallocAsync(&md.nzm, ne * 16, s));
     SACD_CUDA_TRY(cudaMallocAsync(&md.row_ptr, (size_t)(md.I + 1) * 8, s));
-    c.device_bytes += (long long)ne * 32 + (md.I + 1) * 8;
+    c.device_bytes += (long long)ne * (soa ? 32 : 16) + (md.I + 1) * 8;
+    tm.mark(s, "  layout: allocations");
     if (nnz > 0) {
       k_make_keys<<<grid_for(nnz), 256, 0, s>>>(coords, nnz, n, a, b, Ia, Ib, keys, pos);
+      tm.mark(s, "  layout: keys");
       const int end_bit = bits_for((unsigned long long)c.dims[n] * Ia * Ib - 1ULL);
       SACD_CUDA_TRY(
           cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys, keys2, pos, pos2, (int)nnz, 0, end_bit, s));
+      tm.mark(s, "  layout: radix sort");
       k_check_dup<<<grid_for(nnz), 256, 0, s>>>(keys2, nnz, flags);
       k_gather<<<grid_for(nnz), 256, 0, s>>>(coords, vals, pos2, keys2, nnz, a, b, Ib, Ia * Ib, md.idx_a, md.idx_b,
                                              md.idx_n, md.val, md.nzm, nfib + n);
+      tm.mark(s, "  layout: dup check + gather");
     }
     k_row_ptr<<<grid_for(md.I + 1), 256, 0, s>>>(keys2, nnz, md.I, Ia * Ib, md.row_ptr);
     SACD_CUDA_TRY(cudaGetLastError());
+    tm.mark(s, "  layout: row_ptr");
   }
   SACD_CUDA_TRY(cudaMemcpyAsync(&hflags, flags, sizeof(int), cudaMemcpyDeviceToHost, s));
   unsigned long long hfib[3] = {0, 0, 0};
@@ -314,7 +328,7 @@ int build_layouts(Context &c, const uint32_t *coords, const float *vals) {
   // ||X||^2 in mode-0 layout order
   double *part = nullptr;
   SACD_CUDA_TRY(cudaMallocAsync(&part, kNormBlocks * sizeof(double), s));
-  k_norm_partial<<<kNormBlocks, 256, 0, s>>>(c.m[0].val, nnz, part);
+  k_norm_partial<<<kNormBlocks, 256, 0, s>>>(c.m[0].nzm, nnz, part);  // mode-0 order, canonical here
   k_norm_final<<<1, 32, 0, s>>>(part, kNormBlocks, c.st);
   SACD_CUDA_TRY(cudaGetLastError());
   SACD_CUDA_TRY(cudaStreamSynchronize(s));

@@ -5,6 +5,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -34,6 +37,19 @@ struct Status {
     int rc_ = (call);           \
     if (rc_ != SACD_OK) return rc_; \
   } while (0)
+
+// SACD_INIT_TIMING=1 prints the wall time of each sacd_init phase to stderr (diagnostics)
+struct InitTimer {
+  bool on = getenv("SACD_INIT_TIMING") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(cudaStream_t s, const char *what) {
+    if (!on) return;
+    cudaStreamSynchronize(s);
+    const auto n = std::chrono::steady_clock::now();
+    fprintf(stderr, "[sacd_init] %-32s %8.1f ms\n", what, std::chrono::duration<double, std::milli>(n - t).count());
+    t = n;
+  }
+};
 
 // ------------------------------------------------------------------ device structures
 // One MTTKRP work item: either whole rows [row0,row1) whose nonzeros are [nz0,nz1), or
@@ -189,6 +205,13 @@ constexpr int kDeltaBlocks = 296;
 
 size_t real_size(const Context &c);
 
+// The per-mode SoA copies of the layout (idx_a, idx_b, idx_n, val) are read only by the R <= 16
+// MTTKRP kernel, the warp fiber kernel (variant 1) and the a-blocked order builder; every
+// other path reads the 16-byte records (nzm), which also serve the canonical readback.
+inline bool layout_needs_soa(const Context &c) {
+  return c.pitch < 32 || c.opt.mttkrp_variant == 1 || c.opt.reserved[1] > 0;
+}
+
 ShardPlan plan_shard(const long long *row_ptr, long long I, int world, int rank);
 
 // layout.cu
@@ -205,6 +228,7 @@ int launch_mode_update(Context &c, int mode, int branch_override, bool begin_swe
                        uint8_t *decisions_dev);
 int launch_gram(Context &c, int mode);
 int launch_initial_fit(Context &c);
+int launch_unpack_nzm(Context &c, const uint4 *nzm, long long nnz, uint32_t *ia, uint32_t *ib, float *v);
 int launch_range_check(Context &c, const uint32_t *coords_dev, long long n, int *flag_dev);
 int launch_predict(Context &c, const uint32_t *coords_dev, long long n, const float *vals_dev, double *out_dev,
                    double *part_dev, double *sse_dev);  // vals/out/sse may be null

@@ -57,10 +57,14 @@ def ragged_tensor(dims, nnz, seed, heavy_rows=((0, 0, 300),)):
 
 # ----------------------------------------------------------------------------- layout / init
 @pytest.mark.parametrize("nnz_per_item", [0, 16])
-def test_layout_bit_exact(nnz_per_item):
+@pytest.mark.parametrize("R", [6, 40])
+def test_layout_bit_exact(nnz_per_item, R):
+    """P1: the device layouts equal the oracle's bit for bit.  R = 6 keeps the SoA copies
+    (the R <= 16 kernel reads them); R = 40 keeps only the 16-byte records, which the
+    readback unpacks."""
     dims = (37, 23, 51)
     c, v = ragged_tensor(dims, 3000, 5, heavy_rows=((0, 3, 400), (1, 7, 300), (2, 50, 500)))
-    with S(c, v, dims, 6, 1, nnz_per_item=nnz_per_item) as g:
+    with S(c, v, dims, R, 1, nnz_per_item=nnz_per_item) as g:
         info = g.info()
         assert info["nnz"] == len(v)
         for n in range(3):
