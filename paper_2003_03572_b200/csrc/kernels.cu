@@ -1917,19 +1917,28 @@ struct Impl {
           const long long lb = (n_items * SWW + 255) / 256;
           k_mttkrp_lean<Real, RT, SWW, 1, 2><<<(unsigned)lb, 256, 0, c.stream>>>(items, n_items, md.nzm, A, B, out,
                                                                                 partial);
-        } else if (sizeof(Real) == 8 && RT <= 64 && md.n_fibers > 0 && c.nnz >= 2 * md.n_fibers) {
-          // fp64, R <= 64, mean fiber length >= 2 (the Zipf configs c3, c4): one warp per item
-          // (2 fp64 columns per lane at R = 64) at 48 registers / 40 warps per SM.  Measured on
-          // B200 (tools/mttkrp_tune.py, variant 41): c4 13.65 vs 15.17 ms per sweep, c3 1.22 vs
-          // 1.28; on the uniform c5 (fibers of length ~1) it loses, so those keep the default.
-          // x reaches the lanes through a shared-memory broadcast (XS = 1, one L1 wavefront
-          // instead of two shuffles; the kernel is bound by the L1 data path: c4 12.11 vs
-          // 13.66 ms, variant 30); with two workers per warp (R = 32) the b index and x go as
-          // one 16-byte broadcast (XS = 2; c3 1.195 vs 1.227 ms, variant 31).
-          constexpr int SWF = sub_warp_lanes<Real, RT>();
-          const long long lb = (n_items * SWF + 255) / 256;
-          k_mttkrp_lean<Real, RT, SWF, 1, 5, 0, SWF == 32 ? 1 : 2><<<(unsigned)lb, 256, 0, c.stream>>>(
-              items, n_items, md.nzm, A, B, out, partial);
+        } else if (sizeof(Real) == 8 && (RT == 64 || (RT == 32 && md.n_fibers > 0 && c.nnz >= 2 * md.n_fibers))) {
+          // fp64, R = 33..64 (and R = 17..32 with a mean fiber length >= 2, the Zipf config
+          // c3): one warp per item (2 fp64 columns per lane at R = 64) at 48 registers / 40
+          // warps per SM (variant 41: c4 13.65 vs 15.17 ms per sweep, c3 1.22 vs 1.28).  x
+          // reaches the lanes through a shared-memory broadcast (XS = 1: one L1 wavefront
+          // instead of two shuffles on the L1-data-path-bound kernel; variant 30: c4 12.11 vs
+          // 13.66 ms, c5 R=64 4.02 vs 4.42); with two workers per warp (R = 32) the b index
+          // and x go as one 16-byte broadcast (XS = 2; variant 31: c3 1.195 vs 1.227 ms).
+          if constexpr (sizeof(Real) == 8 && (RT == 64 || RT == 32)) {
+            constexpr int SWF = sub_warp_lanes<Real, RT>();
+            const long long lb = (n_items * SWF + 255) / 256;
+            k_mttkrp_lean<Real, RT, SWF, 1, 5, 0, SWF == 32 ? 1 : 2><<<(unsigned)lb, 256, 0, c.stream>>>(
+                items, n_items, md.nzm, A, B, out, partial);
+          }
+        } else if (sizeof(Real) == 8 && RT == 128) {
+          // fp64, R = 65..128: 4 columns per lane, one warp per item, x broadcast through shared
+          // memory (variant 32: c5 R=128 6.54 vs 6.95 ms, c4 R=128 21.5 vs 26.0 ms per sweep)
+          if constexpr (sizeof(Real) == 8 && RT == 128) {
+            const long long lb = (n_items * 32 + 255) / 256;
+            k_mttkrp_lean<Real, RT, 32, 1, 3, 0, 1><<<(unsigned)lb, 256, 0, c.stream>>>(items, n_items, md.nzm, A,
+                                                                                       B, out, partial);
+          }
         } else {
           // default (measured on B200, tools/mttkrp_tune.py): the lean sub-warp kernel with
           // 4 fp64 / 8 fp32 columns per lane
