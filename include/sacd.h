@@ -121,7 +121,7 @@ typedef struct {
   int32_t precision;
   int32_t l_mode, variant;
   int32_t k;        /* completed sweeps                                                      */
-  int32_t mode_a[3], mode_b[3]; /* the "a" (shorter) and "b" other modes of each layout     */
+  int32_t mode_a[3], mode_b[3]; /* the "a" (longer) and "b" other modes of each layout      */
   double xnorm2;    /* ||X||^2 in fp64                                                       */
   int64_t items[3]; /* MTTKRP work items per mode                                            */
   int64_t split_rows[3];
@@ -137,7 +137,7 @@ void sacd_default_options(sacd_options *opt);
 
 /* Build a context: validate the COO tensor, copy it to the device, build the three
  * mode-sorted layouts (Table 2 slices Omega^U_q, Omega^V_p, Omega^W_s; key (i_n, i_a, i_b)
- * with a the shorter other mode), compute ||X||^2 (fp64), initialise the factors
+ * with a the longer other mode, reading L1), compute ||X||^2 (fp64), initialise the factors
  * uniformly in [0,1) from `seed` (Alg 1 input; reading C12) and their Grams, and
  * capture the sweep graph.
  *   coords : host or device, nnz x 3 uint32 (q,p,s), 0-based.   vals : host or device, fp32.

@@ -407,6 +407,17 @@ static int init_impl(Context *c, const uint32_t *coords, const float *vals, uint
   cudaStream_t s = c->stream;
   InitTimer tm;
   SACD_TRY(sync_if_device(coords, vals));
+  {
+    // keep memory returned to the device's default pool mapped (the layout build's
+    // multi-GB temporaries are stream-ordered allocations): mapping fresh physical memory
+    // dominated sacd_init, and a second context in the process then reuses it
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, c->device) == cudaSuccess) {
+      unsigned long long thr = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    cudaGetLastError();
+  }
   SACD_CUDA_TRY(cudaMalloc(&c->st, sizeof(DevState)));
   SACD_CUDA_TRY(cudaMemsetAsync(c->st, 0, sizeof(DevState), s));
   for (int n = 0; n < 3; ++n) {

@@ -1,8 +1,9 @@
 // layout.cu -- per-mode sorted nonzero layout, built once on device by sacd_init.
 //
 // The paper's slices Omega^U_q, Omega^V_p, Omega^W_s (Table 2) become,
-// per mode n, the nonzeros sorted by the key (i_n, i_a, i_b) where a is the shorter other
-// mode (ties -> lower mode id) and b the remaining one; row_ptr[i] .. row_ptr[i+1] is the
+// per mode n, the nonzeros sorted by the key (i_n, i_a, i_b) where a is the longer other
+// mode (ties -> lower mode id; reading L1) and b the remaining one, so the fiber-
+// factored MTTKRP gathers the shorter factor per nonzero; row_ptr[i] .. row_ptr[i+1] is the
 // slice of row i.  This replaces the unfolding X_(n) (Lemma 4), which
 // is never materialised.  Keys are unique (duplicates are rejected), so the order
 // is unique and equals the oracle's bit for bit.

@@ -100,7 +100,7 @@ struct DevState {
 
 struct ModeData {
   long long I = 0;
-  int a = 0, b = 0;               // the other modes ("a" = shorter)
+  int a = 0, b = 0;               // the other modes ("a" = the longer, L1)
   uint32_t *idx_a = nullptr, *idx_b = nullptr, *idx_n = nullptr;  // idx_a has flag bits
   float *val = nullptr;
   uint4 *nzm = nullptr;           // per nonzero {idx_a|flags, idx_b|flags, bits(val), row}: one 16-byte load
