@@ -583,7 +583,12 @@ static int init_impl(Context *c, const uint32_t *coords, const float *vals, uint
     SACD_CUDA_TRY(cudaMemset(c->dcnt, 0, (size_t)c->G * 8));
     c->device_bytes += (long long)((size_t)maxI * P * rs + (size_t)tot * (4 + rs));
   }
-  c->gram_blocks = (int)std::min<long long>(296, std::max<long long>(1, (maxI + 63) / 64));
+  // row ranges of the Gram partials: 148 for the DMMA kernel (one per SM per panel pair; the
+  // fixed-order reduce then reads half as many partials: c4 0.73 -> 0.57 ms per sweep in
+  // eager timing vs 296), 296 for the FMA kernel
+  const long long gcap = (c->opt.precision == SACD_F64 && c->pitch >= 32) ? 148 : 296;
+  c->gram_blocks = (int)std::min<long long>(gcap, std::max<long long>(1, (maxI + 63) / 64));
+  if (getenv("SACD_GRAM_BLOCKS")) c->gram_blocks = std::max(1, atoi(getenv("SACD_GRAM_BLOCKS")));  // tuning
   SACD_CUDA_TRY(cudaMalloc(&c->M, (size_t)((maxI + 31) / 32 * 32) * P * rs));
   if (c->opt.variant == SACD_VARIANT_SNAPSHOT) {  // snapshot importances of one pass (TT layout)
     SACD_CUDA_TRY(cudaMalloc(&c->Zs, (size_t)((maxI + 31) / 32 * 32) * P * rs));

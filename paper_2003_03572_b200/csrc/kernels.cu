@@ -2002,8 +2002,7 @@ struct Impl {
     SACD_TRY(sharded_mttkrp_merge(c, mode));
     SACD_TRY(prepare(c, mode, branch_override, begin_sweep, 1));
     if (c.delta) SACD_TRY(delta_snapshot(c, mode));
-    constexpr int TR = rows_per_block<RT>();
-    constexpr size_t smem = rows_smem_bytes<Real, RT>();
+    const long long TR = rows_tr(c, 0);
     constexpr int GT = gram_gt<RT>();
     constexpr int TG = gram_tg<GT>();
     constexpr int NBP = RT / GT;
@@ -2220,8 +2219,8 @@ struct Impl {
     Real *M = reinterpret_cast<Real *>(c.M);
     SACD_TRY(mttkrp(c, mode, M));
     SACD_TRY(prepare(c, mode, branch_override, begin_sweep, 1));
-    constexpr int TR = rows_per_block<RT>();
-    constexpr size_t smem = rows_smem_bytes<Real, RT>();
+    const int vflags0 = c.opt.variant == SACD_VARIANT_SNAPSHOT ? 2 : (c.opt.variant == SACD_VARIANT_JACOBI ? 1 : 0);
+    const long long TR = rows_tr(c, vflags0);
     const long long nblk = (md.I + TR - 1) / TR;
     double *ti_part = c.row_part, *md_part = c.row_part + c.max_row_blocks;
     long long *e_part = c.cnt_part, *ech_part = c.cnt_part + c.max_row_blocks;
@@ -2278,6 +2277,16 @@ struct Impl {
 
   // the fused row update over rows [rlo, rhi) (nblk blocks); opt.reserved[0] = 1 reads H
   // from global memory (L1) instead of staging it in shared memory
+  // rows per block of the row-update launch for these flags (the DMMA kernel: kMmaWarps x 32)
+  static constexpr bool kRowsMma = sizeof(Real) == 8 && RT <= 64 && rows_per_block<RT>() == 128;
+  static constexpr int kMmaWarps = 4;  // 5 (160 rows, 2 blocks per SM) measured 2.41 vs 1.72 ms: L1 too small
+  static int rows_tr(const Context &c, int vflags) {
+    if constexpr (kRowsMma) {
+      if (c.opt.reserved[0] == 0 && vflags == 0) return kMmaWarps * 32;
+    }
+    return rows_per_block<RT>();
+  }
+
   static int rows(Context &c, long long nblk, long long rlo, long long rhi, int mode, const Real *M, uint8_t *dec,
                   double *ti_part, double *md_part, long long *e_part, long long *ech_part, int vflags = 0) {
     constexpr int TR = rows_per_block<RT>();
@@ -2290,10 +2299,11 @@ struct Impl {
                                                       md_part, e_part, ech_part, vflags,
                                                       reinterpret_cast<Real *>(c.Zs));
     };
-    if constexpr (sizeof(Real) == 8 && RT <= 64 && rows_per_block<RT>() == 128) {
+    if constexpr (kRowsMma) {
       if (c.opt.reserved[0] == 0 && vflags == 0) {  // default for fp64, R <= 64: out-of-block gradient on DMMA
         if (nblk > 0)
-          k_sacd_rows_mma<RT, 4><<<(unsigned)nblk, 128, rows_mma_smem_bytes<RT, 4>(), c.stream>>>(
+          k_sacd_rows_mma<RT, kMmaWarps><<<(unsigned)nblk, kMmaWarps * 32, rows_mma_smem_bytes<RT, kMmaWarps>(),
+                                            c.stream>>>(
               rlo, rhi, c.R, mode, c.opt.l_mode, md.row_ptr, reinterpret_cast<const double *>(M),
               reinterpret_cast<double *>(md.F), reinterpret_cast<double *>(md.Z),
               reinterpret_cast<const double *>(c.Hr), c.st, dec, ti_part, md_part, e_part, ech_part);
@@ -2314,9 +2324,9 @@ struct Impl {
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rows_smem_bytes<Real, RT>()));
     SACD_CUDA_TRY(cudaFuncSetAttribute(k_sacd_rows<Real, RT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)rows_smem_bytes<Real, RT, false>()));
-    if constexpr (sizeof(Real) == 8 && RT <= 64 && rows_per_block<RT>() == 128)
-      SACD_CUDA_TRY(cudaFuncSetAttribute(k_sacd_rows_mma<RT, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)rows_mma_smem_bytes<RT, 4>()));
+    if constexpr (kRowsMma)
+      SACD_CUDA_TRY(cudaFuncSetAttribute(k_sacd_rows_mma<RT, kMmaWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)rows_mma_smem_bytes<RT, kMmaWarps>()));
     return SACD_OK;
   }
 };
