@@ -331,6 +331,20 @@ def main():
                 "sweep_hbm_frac": (bcomp / (ms_max / K / 1e3) / 1e9) / hbm_peak,
                 "sweep_hbm_frac_8TBs": (bcomp / (ms_max / K / 1e3) / 1e9) / 8000.0,
                 "kernel_ms_per_sweep": {k: v[0] / K for k, v in kc.items()}}
+    # The MTTKRP is bound by the L1 data path, not HBM: every nonzero gathers
+    # one b-row and every fiber one a-row of R_pad * s bytes through L1, plus its 16-byte
+    # record.  Peak = 148 SMs x 128 B/clk x the max SM clock (B200_PROFILING.md unit counts).
+    pitch = info["pitch"]
+    fib = info.get("fibers", [0, 0, 0])
+    if world == 1 and all(f > 0 for f in fib):
+        gathered = sum((nnz + fib[n]) * pitch * s + 16 * nnz for n in range(3)) / 3
+        l1_peak = 148 * 128 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e9
+        roofline["l1_gather"] = {"achieved": gathered / (mt_ms / 1e3) / 1e9, "peak": l1_peak, "unit": "GB/s",
+                                 "frac": gathered / (mt_ms / 1e3) / 1e9 / l1_peak,
+                                 "bytes_per_launch": gathered,
+                                 "what": "factor-row gathers (nnz + fibers) x R_pad x s + 16 B records per MTTKRP "
+                                         "launch through L1, vs 148 SM x 128 B/clk; ncu shows the L1 data pipe "
+                                         "at 80-84% of peak in the U/V modes (wavefronts incl. broadcasts)"}
 
     # ---- end to end through the public API with host (pinned) buffers
     e2e = None

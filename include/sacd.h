@@ -131,6 +131,7 @@ typedef struct {
   int32_t delta_exchange;   /* 1: sharded passes exchange changed elements          */
   int64_t delta_elems_sent; /* NCCL delta exchange so far: elements sent as (index, value) ...  */
   int64_t full_elems_equiv; /* ... and the elements the full-row exchange would have sent       */
+  int64_t fibers[3];        /* distinct (i_n, i_a) per layout: the MTTKRP's per-fiber gathers    */
 } sacd_info;
 
 void sacd_default_options(sacd_options *opt);

@@ -1110,6 +1110,7 @@ int sacd_get_info(sacd_ctx *c, sacd_info *o) {
   o->delta_exchange = c->delta ? 1 : 0;
   o->delta_elems_sent = c->delta_sent;
   o->full_elems_equiv = c->full_equiv;
+  for (int n = 0; n < 3; ++n) o->fibers[n] = c->m[n].n_fibers;
   int k = 0;
   int rc = dev_read(c, &k, reinterpret_cast<const char *>(c->st) + offsetof(DevState, k), sizeof(int));
   if (rc == SACD_OK)
