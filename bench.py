@@ -356,6 +356,11 @@ def main():
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
+        if world > 1:  # a fresh NCCL id for the second communicator (ids are single-use)
+            obj = [nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            shard_kw = dict(shard_kw, nccl_id=obj[0])
+            dist.barrier()
         t0 = time.perf_counter()
         g2 = Sacd(hc, hv, cfg.dims, R, cfg.seed, precision=args.precision, stream=stream.cuda_stream,
                   nnz_per_item=args.nnz_per_item, device=local, **shard_kw)
