@@ -1263,6 +1263,171 @@ __global__ void __launch_bounds__(WPB * 32)
   }
 }
 
+// The same row update for R > 64 (fp64): one warp (32 rows) per block; the B fragments of
+// a column block (R/4 k-steps) are loaded 16 k-steps at a time, the next chunk in flight
+// while the current one feeds the DMMAs; the in-block H values come from L1.  The FMA
+// kernel this replaces waited on one L2 round trip of H per 4 gradient terms.
+template <int RT>
+__global__ void __launch_bounds__(32)
+    k_sacd_rows_mma_big(long long row_begin, long long row_end, int R, int mode, int l_mode,
+                        const long long *__restrict__ row_ptr, const double *__restrict__ M, double *__restrict__ F,
+                        double *__restrict__ Z, const double *__restrict__ H, const DevState *__restrict__ st,
+                        uint8_t *__restrict__ dec, double *__restrict__ ti_part, double *__restrict__ md_part,
+                        long long *__restrict__ e_part, long long *__restrict__ ech_part) {
+  constexpr int US = RT + 2;
+  constexpr int C = 8;
+  constexpr int TS = 2 * C + 2;
+  constexpr int KC = 16;  // k-steps per B-fragment chunk
+  static_assert(RT % (4 * KC) == 0, "R pitch must be a multiple of 64");
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double *Us = reinterpret_cast<double *>(smem_raw);
+  double *Tw = Us + 32 * US;
+  const int lane = threadIdx.x;
+  const int g = lane >> 2, t = lane & 3;
+  const long long row0 = row_begin + (long long)blockIdx.x * 32;
+  const int nrows = (int)min(32LL, row_end - row0);
+  const double *Fg = F + row0 * RT;
+  static_assert(((RT + 2) * 8) % 16 == 0, "row stride must keep 16-byte chunks aligned");
+  for (int x = lane; x < 32 * RT / 2; x += 32) {
+    const int r = (2 * x) / RT, col = (2 * x) % RT;
+    if (r < nrows) cp_async<16>(Us + r * US + col, Fg + 2 * x);
+    else *reinterpret_cast<double2 *>(Us + r * US + col) = make_double2(0.0, 0.0);
+  }
+  cp_async_wait_all();
+  __syncwarp();
+  const int branch = st->branch[mode];
+  const double Lf = st->Lfrob[mode];
+  const int kmax = (R + 3) / 4;
+
+  double ti = 0.0, md = 0.0;
+  long long E = 0, Ech = 0;
+  const bool active = lane < nrows;
+  const long long row = row0 + lane;
+  double *u = Us + lane * US;
+  const bool empty = active ? row_ptr[row] == row_ptr[row + 1] : true;
+  double *zp = Z + tt<RT>(active ? row : row0, 0);
+  const double *Uw = Us + g * US + t;
+  for (int c0 = 0; c0 < R; c0 += C) {
+    const int kb = c0 / 4;
+    double mt[C], zv[C];
+#pragma unroll
+    for (int k = 0; k < C; ++k) {
+      const int x = lane + 32 * k, rl = x / C, cl = x % C;
+      const long long rg = row0 + rl;
+      mt[k] = (rg < row_end) ? __ldg(M + rg * RT + c0 + cl) : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < C; ++q) zv[q] = active ? zp[32 * (c0 + q)] : 0.0;
+    double cacc[2][4][2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int m = 0; m < 4; ++m) cacc[h][m][0] = cacc[h][m][1] = 0.0;
+    auto load_chunk = [&](int k0, double (&b)[KC]) {
+#pragma unroll
+      for (int j = 0; j < KC; ++j) {
+        const int kk = k0 + j;
+        b[j] = (kk == kb || kk == kb + 1 || kk >= kmax) ? 0.0 : __ldg(H + (4 * kk + t) * RT + c0 + g);
+      }
+    };
+    double bc[KC], bn[KC];
+    load_chunk(0, bc);
+    for (int k0 = 0; k0 < kmax; k0 += KC) {
+      if (k0 + KC < kmax) load_chunk(k0 + KC, bn);
+#pragma unroll
+      for (int j = 0; j < KC; ++j) {
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          const double a = Uw[8 * m * US + 4 * (k0 + j)];
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                       : "+d"(cacc[j & 1][m][0]), "+d"(cacc[j & 1][m][1])
+                       : "d"(a), "d"(bc[j]));
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < KC; ++j) bc[j] = bn[j];
+    }
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      Tw[(8 * m + g) * TS + 2 * t] = cacc[0][m][0] + cacc[1][m][0];
+      Tw[(8 * m + g) * TS + 2 * t + 1] = cacc[0][m][1] + cacc[1][m][1];
+    }
+#pragma unroll
+    for (int k = 0; k < C; ++k) {
+      const int x = lane + 32 * k, rl = x / C, cl = x % C;
+      Tw[rl * TS + C + cl] = mt[k];
+    }
+    __syncwarp();
+    if (active) {
+      double acc[C], mv[C], ub[C];
+#pragma unroll
+      for (int q = 0; q < C; ++q) {
+        acc[q] = Tw[lane * TS + q];
+        mv[q] = empty ? 0.0 : Tw[lane * TS + C + q];
+        ub[q] = u[c0 + q];
+      }
+#pragma unroll
+      for (int q = 0; q < C; ++q) {
+        const int r = c0 + q;
+        if (r < R) {
+          const double *Hr_ = H + (long long)r * RT + c0;
+          const double h = __ldg(Hr_ + q);
+          double z = 0.0;
+          bool sel = false;
+          if (h != 0.0) {
+            double sg = acc[q];
+#pragma unroll
+            for (int qq = 0; qq < C; ++qq) sg = fma(ub[qq], __ldg(Hr_ + qq), sg);
+            const double gr = sg - mv[q];                  // Eq 14
+            const double ur = ub[q];
+            const double un = fmax(0.0, ur - gr / h);      // Eq 11-13
+            const double d = un - ur;                      // Eq 12
+            const double L = l_mode ? Lf : h;
+            z = -gr * d - (L * 0.5) * d * d;               // Eq 20
+            const double zpr = zv[q];
+            sel = (branch == SACD_BR_FIRST) ? (z > 0.0)
+                                            : ((branch == SACD_BR_EQ24) ? (z - zpr > 0.0) : (zpr - z > 0.0));
+            if (sel) {
+              ub[q] = un;
+              E += 1;
+              if (d != 0.0) Ech += 1;
+            }
+          }
+          zv[q] = z;
+          ti += z;
+          md += ub[q] * mv[q];
+          if (dec) dec[row * R + r] = (uint8_t)sel;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < C; ++q) u[c0 + q] = ub[q];
+#pragma unroll
+      for (int q = 0; q < C; ++q) zp[32 * (c0 + q)] = zv[q];
+    }
+    __syncwarp();
+  }
+  double *Fo = F + row0 * RT;
+  for (int x = lane; x < nrows * RT; x += 32) Fo[x] = Us[(x / RT) * US + (x % RT)];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ti += __shfl_xor_sync(0xffffffffu, ti, o);
+    md += __shfl_xor_sync(0xffffffffu, md, o);
+    E += __shfl_xor_sync(0xffffffffu, E, o);
+    Ech += __shfl_xor_sync(0xffffffffu, Ech, o);
+  }
+  if (lane == 0) {
+    ti_part[blockIdx.x] = ti;
+    md_part[blockIdx.x] = md;
+    e_part[blockIdx.x] = E;
+    ech_part[blockIdx.x] = Ech;
+  }
+}
+
+template <int RT>
+__host__ __device__ constexpr size_t rows_mma_big_smem_bytes() {
+  return (size_t)32 * (RT + 2) * 8 + (size_t)32 * 18 * 8;
+}
+
 template <int RT, int WPB>
 __host__ __device__ constexpr size_t rows_mma_smem_bytes() {
   return (size_t)WPB * 32 * (RT + 2) * 8 + (size_t)WPB * 32 * 18 * 8 + (size_t)RT * 8 * 8;
@@ -2279,10 +2444,14 @@ struct Impl {
   // from global memory (L1) instead of staging it in shared memory
   // rows per block of the row-update launch for these flags (the DMMA kernel: kMmaWarps x 32)
   static constexpr bool kRowsMma = sizeof(Real) == 8 && RT <= 64 && rows_per_block<RT>() == 128;
+  static constexpr bool kRowsMmaBig = sizeof(Real) == 8 && RT >= 128;
   static constexpr int kMmaWarps = 4;  // 5 (160 rows, 2 blocks per SM) measured 2.41 vs 1.72 ms: L1 too small
   static int rows_tr(const Context &c, int vflags) {
     if constexpr (kRowsMma) {
       if (c.opt.reserved[0] == 0 && vflags == 0) return kMmaWarps * 32;
+    }
+    if constexpr (kRowsMmaBig) {
+      if (c.opt.reserved[0] == 0 && vflags == 0) return 32;
     }
     return rows_per_block<RT>();
   }
@@ -2311,6 +2480,17 @@ struct Impl {
         return SACD_OK;
       }
     }
+    if constexpr (kRowsMmaBig) {
+      if (c.opt.reserved[0] == 0 && vflags == 0) {  // fp64, R > 64: DMMA gradient, one warp per block
+        if (nblk > 0)
+          k_sacd_rows_mma_big<RT><<<(unsigned)nblk, 32, rows_mma_big_smem_bytes<RT>(), c.stream>>>(
+              rlo, rhi, c.R, mode, c.opt.l_mode, md.row_ptr, reinterpret_cast<const double *>(M),
+              reinterpret_cast<double *>(md.F), reinterpret_cast<double *>(md.Z),
+              reinterpret_cast<const double *>(c.Hr), c.st, dec, ti_part, md_part, e_part, ech_part);
+        SACD_CUDA_TRY(cudaGetLastError());
+        return SACD_OK;
+      }
+    }
     // reserved[0]: 1 = the FMA kernel with H read from global memory (L1), else (0 for the
     // other pitches / precisions, 2) the FMA kernel with H staged in shared memory
     if (c.opt.reserved[0] == 1) go(k_sacd_rows<Real, RT, false>, rows_smem_bytes<Real, RT, false>());
@@ -2327,6 +2507,9 @@ struct Impl {
     if constexpr (kRowsMma)
       SACD_CUDA_TRY(cudaFuncSetAttribute(k_sacd_rows_mma<RT, kMmaWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)rows_mma_smem_bytes<RT, kMmaWarps>()));
+    if constexpr (kRowsMmaBig)
+      SACD_CUDA_TRY(cudaFuncSetAttribute(k_sacd_rows_mma_big<RT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)rows_mma_big_smem_bytes<RT>()));
     return SACD_OK;
   }
 };
