@@ -402,7 +402,7 @@ def main():
                            **({"exchange_elems_sent": info_end["delta_elems_sent"],
                                "exchange_elems_full_equiv": info_end["full_elems_equiv"]}
                               if world > 1 and info_end.get("delta_exchange") else {}),
-                           "l2": "inputs larger than L2 (mode layouts %.2f GB > 126 MB), no flush" % (36 * nnz / 1e9),
+                           "l2": "inputs larger than L2 (16-byte nonzero records of the three modes: %.2f GB > 126 MB), no flush" % (48 * nnz / 1e9),
                            "b_comp_bytes_per_sweep": bcomp, "gen_seconds": t_gen,
                            "mttkrp_items": info["items"], "split_rows": info["split_rows"],
                            "objective_after": f_final, "fit_after": fit_final},
