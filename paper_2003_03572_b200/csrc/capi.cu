@@ -583,11 +583,14 @@ static int init_impl(Context *c, const uint32_t *coords, const float *vals, uint
     SACD_CUDA_TRY(cudaMemset(c->dcnt, 0, (size_t)c->G * 8));
     c->device_bytes += (long long)((size_t)maxI * P * rs + (size_t)tot * (4 + rs));
   }
-  // row ranges of the Gram partials: 148 for the DMMA kernel (one per SM per panel pair; the
-  // fixed-order reduce then reads half as many partials: c4 0.73 -> 0.57 ms per sweep in
-  // eager timing vs 296), 296 for the FMA kernel
+  // row ranges of the Gram partials: at most 148 for the DMMA kernel (one per SM per panel
+  // pair; the fixed-order reduce then reads half as many partials: c4 0.73 -> 0.57 ms per
+  // sweep in eager timing vs 296) and 296 for the FMA kernel; at least 64 rows each, and at
+  // least 2048 for fp64 R > 64 (36 / 10 panel pairs already fill the GPU: c5 R=256 Gram
+  // 0.35 -> 0.22 ms, R=128 0.19 -> 0.16)
   const long long gcap = (c->opt.precision == SACD_F64 && c->pitch >= 32) ? 148 : 296;
-  c->gram_blocks = (int)std::min<long long>(gcap, std::max<long long>(1, (maxI + 63) / 64));
+  const long long grows = (c->opt.precision == SACD_F64 && c->pitch >= 128) ? 2048 : 64;
+  c->gram_blocks = (int)std::min<long long>(gcap, std::max<long long>(1, (maxI + grows - 1) / grows));
   if (getenv("SACD_GRAM_BLOCKS")) c->gram_blocks = std::max(1, atoi(getenv("SACD_GRAM_BLOCKS")));  // tuning
   SACD_CUDA_TRY(cudaMalloc(&c->M, (size_t)((maxI + 31) / 32 * 32) * P * rs));
   if (c->opt.variant == SACD_VARIANT_SNAPSHOT) {  // snapshot importances of one pass (TT layout)
