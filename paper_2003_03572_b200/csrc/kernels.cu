@@ -832,11 +832,11 @@ __global__ void __launch_bounds__(256) k_fix2(const SplitRow *__restrict__ split
 // ------------------------------------------------------------------ H, L and the branch
 // H = G_a * G_b (Eq 10), L = ||H||_F (Alg 1), branch by reading C10.
 template <typename Real, int RT>
-__global__ void __launch_bounds__(256) k_prepare(int mode, int R, const double *__restrict__ Ga,
-                                                 const double *__restrict__ Gb, double *__restrict__ Hd,
-                                                 Real *__restrict__ Hr, DevState *st, int branch_override,
-                                                 int begin_sweep, int variant, int write_state) {
-  __shared__ double red[256];
+__global__ void __launch_bounds__(1024) k_prepare(int mode, int R, const double *__restrict__ Ga,
+                                                  const double *__restrict__ Gb, double *__restrict__ Hd,
+                                                  Real *__restrict__ Hr, DevState *st, int branch_override,
+                                                  int begin_sweep, int variant, int write_state) {
+  __shared__ double red[1024];
   double ss = 0.0;
   for (int x = threadIdx.x; x < RT * RT; x += blockDim.x) {
     const int r = x / RT, t = x - (x / RT) * RT;
@@ -850,7 +850,7 @@ __global__ void __launch_bounds__(256) k_prepare(int mode, int R, const double *
   }
   red[threadIdx.x] = ss;
   __syncthreads();
-  for (int o = 128; o > 0; o >>= 1) {
+  for (int o = 512; o > 0; o >>= 1) {
     if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
     __syncthreads();
   }
@@ -2371,7 +2371,7 @@ struct Impl {
   static int prepare(Context &c, int mode, int branch_override, bool begin_sweep, int write_state) {
     ModeData &md = c.m[mode];
     int pe = prof_begin(c, 2);
-    k_prepare<Real, RT><<<1, 256, 0, c.stream>>>(mode, c.R, c.m[md.a].G, c.m[md.b].G, c.Hd,
+    k_prepare<Real, RT><<<1, 1024, 0, c.stream>>>(mode, c.R, c.m[md.a].G, c.m[md.b].G, c.Hd,
                                                  reinterpret_cast<Real *>(c.Hr), c.st, branch_override,
                                                  begin_sweep ? 1 : 0, c.opt.variant, write_state);
     SACD_CUDA_TRY(cudaGetLastError());
