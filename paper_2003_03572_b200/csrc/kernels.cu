@@ -2069,6 +2069,7 @@ struct Impl {
           else if (var == 33) gol(k_mttkrp_lean<Real, RT, SW4, 1, 3, 0, 2>, SW4);
           else if (var == 34) gol(k_mttkrp_lean<Real, RT, sub_warp_lanes<Real, RT>(), 2, 5, 0, 2>, sub_warp_lanes<Real, RT>());
           else if (var == 35) gol(k_mttkrp_lean<Real, RT, sub_warp_lanes<Real, RT>(), 1, 6, 0, 1>, sub_warp_lanes<Real, RT>());
+          else if (var == 36) gol(k_mttkrp_lean<Real, RT, SW8, 1, 2, 0, 1>, SW8);
           else if (var == 40) gol(k_mttkrp_lean<Real, RT, sub_warp_lanes<Real, RT>(), 1, 6>, sub_warp_lanes<Real, RT>());
           else if (var == 41) gol(k_mttkrp_lean<Real, RT, sub_warp_lanes<Real, RT>(), 1, 5>, sub_warp_lanes<Real, RT>());
           else if (var == 42) gol(k_mttkrp_lean<Real, RT, sub_warp_lanes<Real, RT>(), 2, 5>, sub_warp_lanes<Real, RT>());
@@ -2077,12 +2078,13 @@ struct Impl {
           else gol(k_mttkrp_lean<Real, RT, SW8, 2, 2>, SW8);
         }
         else if (sizeof(Real) == 8 && RT >= 256) {
-          // fp64, R > 128: one warp per item, 8 fp64 columns per lane (variant 22; measured on
-          // B200 on c5 R=256: 13.7 vs 28.6 ms per sweep for the warp fiber kernel, variant 1)
+          // fp64, R > 128: one warp per item, 8 fp64 columns per lane, x broadcast through
+          // shared memory (variant 36; c5 R=256: 12.7 ms per sweep vs 13.7 with shuffles,
+          // variant 22, and 28.6 for the warp fiber kernel, variant 1)
           constexpr int SWW = RT / 8 > 32 ? 32 : RT / 8;
           const long long lb = (n_items * SWW + 255) / 256;
-          k_mttkrp_lean<Real, RT, SWW, 1, 2><<<(unsigned)lb, 256, 0, c.stream>>>(items, n_items, md.nzm, A, B, out,
-                                                                                partial);
+          k_mttkrp_lean<Real, RT, SWW, 1, 2, 0, 1><<<(unsigned)lb, 256, 0, c.stream>>>(items, n_items, md.nzm, A, B,
+                                                                                      out, partial);
         } else if (sizeof(Real) == 8 && (RT == 64 || (RT == 32 && md.n_fibers > 0 && c.nnz >= 2 * md.n_fibers))) {
           // fp64, R = 33..64 (and R = 17..32 with a mean fiber length >= 2, the Zipf config
           // c3): one warp per item (2 fp64 columns per lane at R = 64) at 48 registers / 40
