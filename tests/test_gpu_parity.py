@@ -310,7 +310,7 @@ def test_end_to_end_c2_10_sweeps():
     check_pair(fg, Fg, Eg, brg, ora)
 
 
-@pytest.mark.parametrize("R", [1, 8, 33, 128])
+@pytest.mark.parametrize("R", [1, 8, 33, 100, 128, 200])
 def test_end_to_end_ragged_ranks(R):
     dims = (300, 200, 50)
     c, v = ragged_tensor(dims, 20000, 8, heavy_rows=((2, 1, 3000), (0, 5, 900)))
