@@ -341,6 +341,12 @@ static void destroy(sacd_ctx *c) {
   cudaFree(c->xstats);
   if (c->comm) ncclCommDestroy(reinterpret_cast<ncclComm_t>(c->comm));
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  {
+    // return the stream-ordered allocations' memory kept mapped by the pool (see init_impl)
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, c->device) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+    cudaGetLastError();
+  }
   delete c;
 }
 
@@ -408,9 +414,9 @@ static int init_impl(Context *c, const uint32_t *coords, const float *vals, uint
   InitTimer tm;
   SACD_TRY(sync_if_device(coords, vals));
   {
-    // keep memory returned to the device's default pool mapped (the layout build's
-    // multi-GB temporaries are stream-ordered allocations): mapping fresh physical memory
-    // dominated sacd_init, and a second context in the process then reuses it
+    // keep memory returned to the device's default pool mapped while the context lives (the
+    // layout build's multi-GB temporaries are stream-ordered allocations and mapping fresh
+    // physical memory dominated sacd_init); sacd_free trims the pool again
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, c->device) == cudaSuccess) {
       unsigned long long thr = ~0ull;
