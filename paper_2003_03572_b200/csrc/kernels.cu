@@ -2253,6 +2253,14 @@ struct Impl {
       return SACD_OK;
     }
     if (c.capturing) return nccl_broadcast_rows(c, mode);  // kernel count only; never replayed
+    // a small factor (c4's W: 5 MB) goes as full rows: cheaper than the host round trip for
+    // the list lengths
+    if ((double)c.m[mode].I * c.pitch * sizeof(Real) < 16.0 * (1 << 20)) {
+      long long nf = 0;
+      for (int q = 0; q < c.G; ++q) nf += (c.all_plans[mode][q].rhi - c.all_plans[mode][q].rlo) * c.pitch;
+      c.full_equiv += nf;
+      return nccl_broadcast_rows(c, mode);
+    }
     SACD_TRY(nccl_allgather_inplace(c, c.dcnt, 1, 2));
     std::vector<long long> h(c.G);
     SACD_CUDA_TRY(cudaMemcpyAsync(h.data(), c.dcnt, (size_t)c.G * 8, cudaMemcpyDeviceToHost, c.stream));
