@@ -179,6 +179,36 @@ def test_one_pass_teacher_forced_f64(R, branch, l_mode):
             g.set_factors(n, Fn)
 
 
+@pytest.mark.parametrize("cfg_name,K", [("c2", 10), ("c3", 6)])
+def test_flip_census_every_pass(cfg_name, K):
+    """SURVEY 8(c) flip census, fp64: for every mode pass of a K-sweep run, one oracle pass
+    from the GPU's own state before that pass (factors, z_prev, the device's ti history and
+    branch rule) reproduces the GPU's decisions, E and ti; the census of mismatches must be
+    empty.  This pins the selection dynamics pass by pass, not only end to end."""
+    cfg = SI.CONFIGS[cfg_name]
+    c, v = SI.make_tensor(cfg)
+    c, v = c.numpy(), v.numpy()
+    dims, R = cfg.dims, cfg.rank
+    hist = [[], [], []]
+    census = 0
+    with S(c, v, dims, R, cfg.seed) as g:
+        for k in range(1, K + 1):
+            for n in range(3):
+                F = g.factors()
+                Z = g.get_zprev(n)
+                out = g.mode_update(n, decisions=True)
+                M = O.mttkrp(c, v, dims, n, F)
+                H = O.mode_hessian(F, dims, n)
+                br = O.branch(k, hist[n])
+                Fn, zp, ti, E, Ech, md, dec = O.mode_pass(M, H, F[n], Z, br, decisions=True)
+                census += int((out["decisions"] != dec).sum())
+                assert out["E"] == E and out["E_changed"] == Ech
+                assert abs(out["ti"] - ti) <= 1e-9 * max(1.0, abs(ti))
+                assert factor_err(g.factors(n), Fn) <= 1e-9
+                hist[n].append(out["ti"])
+    assert census == 0
+
+
 def test_one_pass_teacher_forced_f32_flip_census():
     """fp32 state: decisions agree except near-ties (|z| <= 1e-6 max|z| for the FIRST rule)."""
     dims, R = (80, 60, 40), 16
