@@ -1,0 +1,634 @@
+// k_rows.inc.cuh -- part of kernels.cu (included inside namespace sacd { namespace { ... } }).
+// H, L and the branch (A2) and the fused SaCD row update (A4): FMA and DMMA kernels.
+// Paper citations "P:n" are PAPER.md lines; readings Cn / L1 / C10' are DESIGN.md section 3.
+// NOT a standalone header: it relies on the helpers defined at the top of kernels.cu.
+
+// ------------------------------------------------------------------ H, L and the branch
+// H = G_a * G_b (Eq 10), L = ||H||_F (Alg 1), branch by reading C10.
+template <typename Real, int RT>
+__global__ void __launch_bounds__(1024) k_prepare(int mode, int R, const double *__restrict__ Ga,
+                                                  const double *__restrict__ Gb, double *__restrict__ Hd,
+                                                  Real *__restrict__ Hr, DevState *st, int branch_override,
+                                                  int begin_sweep, int variant, int write_state) {
+  __shared__ double red[1024];
+  double ss = 0.0;
+  for (int x = threadIdx.x; x < RT * RT; x += blockDim.x) {
+    const int r = x / RT, t = x - (x / RT) * RT;
+    double h = 0.0;
+    if (r < R && t < R) {
+      h = Ga[r * R + t] * Gb[r * R + t];
+      Hd[r * R + t] = h;
+      ss += h * h;
+    }
+    Hr[x] = (Real)h;
+  }
+  red[threadIdx.x] = ss;
+  __syncthreads();
+  for (int o = 512; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0 && write_state) {
+    if (begin_sweep) st->k += 1;
+    int br;
+    if (branch_override >= 0) br = branch_override;
+    else if (variant == SACD_VARIANT_SELECT_OFF || st->nhist[mode] == 0) br = SACD_BR_FIRST;
+    else if (st->nhist[mode] == 1) br = SACD_BR_EQ24;
+    else br = (st->ti1[mode] > st->ti2[mode]) ? SACD_BR_EQ27 : SACD_BR_EQ24;
+    st->branch[mode] = br;
+    st->Lfrob[mode] = sqrt(red[0]);
+  }
+}
+
+// ------------------------------------------------------------------ fused row update
+// One thread per row (rows are independent given A and B: Eq ucap).  The block's
+// rows are staged in shared memory with an odd stride (RT+1) so the per-thread column
+// walk is bank-conflict free; H is staged in shared memory when it fits.
+template <typename Real, int RT, bool HS>
+__global__ void __launch_bounds__(rows_per_block<RT>())
+    k_sacd_rows(long long row_begin, long long row_end, int R, int mode, int l_mode,
+                const long long *__restrict__ row_ptr,
+                const Real *__restrict__ M, Real *__restrict__ F,
+                Real *__restrict__ Z, const Real *__restrict__ Hr, const DevState *__restrict__ st,
+                uint8_t *__restrict__ dec, double *__restrict__ ti_part, double *__restrict__ md_part,
+                long long *__restrict__ e_part, long long *__restrict__ ech_part, int vflags = 0,
+                Real *__restrict__ Zs = nullptr) {
+  // vflags (reading variants): 1 = JACOBI gradients from the rows at pass start
+  // (Lemma 2 literal); 2 = SCORE only (with 1: the snapshot z of every element into Zs, ti,
+  // no update); 4 = SNAP (Gauss-Seidel updates gated by the snapshot Zs, z_prev <- Zs)
+  const bool jac = vflags & 1, score = vflags & 2, snap = vflags & 4;
+  constexpr int TR = rows_per_block<RT>();
+  constexpr int US = RT + 1;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Real *Hs = reinterpret_cast<Real *>(smem_raw);
+  Real *Us = reinterpret_cast<Real *>(smem_raw + (HS ? (size_t)RT * RT * sizeof(Real) : 0));
+  __shared__ double red_d[2][TR / 32];
+  __shared__ long long red_l[2][TR / 32];
+
+  const int tid = threadIdx.x;
+  const long long row0 = row_begin + (long long)blockIdx.x * TR;
+  const int nrows = (int)min((long long)TR, row_end - row0);
+  if (HS) {
+    constexpr int PER = 16 / (int)sizeof(Real);
+    for (int x = tid; x < RT * RT / PER; x += TR) cp_async<16>(Hs + PER * x, Hr + PER * x);
+  }
+  const Real *Fg = F + row0 * RT;
+  for (int x = tid; x < nrows * RT; x += TR) cp_async<(int)sizeof(Real)>(Us + (x / RT) * US + (x % RT), Fg + x);
+  cp_async_wait_all();
+  __syncthreads();
+  const Real *H = HS ? Hs : Hr;
+  const int branch = st->branch[mode];
+  const Real Lf = (Real)st->Lfrob[mode];
+
+  using VV = V16<Real>;
+  using VT = typename VV::T;
+  constexpr int VEC = VV::N;
+  constexpr int C = 8;  // column block: each u_j read from shared memory feeds C FMAs
+  double ti = 0.0, md = 0.0;
+  long long E = 0, Ech = 0;
+  // M is row-major (written by the MTTKRP as whole rows): each warp transposes the 32 x C
+  // block of its rows through a small shared tile, so global reads stay coalesced.
+  __shared__ Real Mst[TR / 32][32][C + 1];
+  const int lane = tid & 31, wp = tid >> 5;
+  const bool active = tid < nrows;
+  {
+    const long long row = row0 + tid;
+    Real *u = Us + tid * US;
+    const bool empty = active ? row_ptr[row] == row_ptr[row + 1] : true;  // empty slice: m = 0
+    Real *zp = Z + tt<RT>(active ? row : row0, 0);         // z_prev in the TT layout
+    Real *zsp = (score || snap) ? Zs + tt<RT>(active ? row : row0, 0) : nullptr;
+    for (int c0 = 0; c0 < R; c0 += C) {
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < C; ++k) {
+        const int x = lane + 32 * k, rl = x / C, cl = x % C;
+        const long long rg = row0 + wp * 32 + rl;
+        Mst[wp][rl][cl] = (rg < row_end) ? M[rg * RT + c0 + cl] : Real(0);
+      }
+      __syncwarp();
+      if (!active) continue;
+      // (1) out-of-block part of the gradient with the current row (columns < c0 already
+      //     updated), Eq 14:  acc_q = sum_{j not in block} u_j h_(j, c0+q)   (H symmetric)
+      Real acc[C];
+#pragma unroll
+      for (int q = 0; q < C; ++q) acc[q] = Real(0);
+      auto accumulate = [&](int j) {
+        const Real uj = u[j];
+        const VT *hj = reinterpret_cast<const VT *>(H + j * RT + c0);
+#pragma unroll
+        for (int x = 0; x < C / VEC; ++x) {
+          Real hv[VEC];
+          VV::get(hj[x], hv);
+#pragma unroll
+          for (int y = 0; y < VEC; ++y) acc[x * VEC + y] = fma(uj, hv[y], acc[x * VEC + y]);
+        }
+      };
+#pragma unroll 4
+      for (int j = 0; j < c0; ++j) accumulate(j);
+#pragma unroll 4
+      for (int j = c0 + C; j < R; ++j) accumulate(j);
+      Real mv[C], zv[C], ub[C], zs[C];
+#pragma unroll
+      for (int q = 0; q < C; ++q) {
+        mv[q] = Mst[wp][lane][q];
+        zv[q] = score ? Real(0) : zp[32 * (c0 + q)];
+        zs[q] = snap ? zsp[32 * (c0 + q)] : Real(0);
+      }
+#pragma unroll
+      for (int q = 0; q < C; ++q) ub[q] = u[c0 + q];
+      if (empty) {
+#pragma unroll
+        for (int q = 0; q < C; ++q) mv[q] = Real(0);
+      }
+      // (2) Gauss-Seidel inside the block (C9): column r adds the in-block terms from the
+      //     CURRENT block values ub (never by subtracting old ones, so a gradient whose
+      //     other terms are exactly zero is computed exactly, as in the oracle).
+#pragma unroll
+      for (int q = 0; q < C; ++q) {
+        const int r = c0 + q;
+        if (r < R) {
+          const Real *Hr_ = H + r * RT;
+          const Real h = Hr_[r];
+          Real z = Real(0);
+          bool sel = false;
+          if (h != Real(0)) {
+            Real sg = acc[q];
+#pragma unroll
+            for (int qq = 0; qq < C; ++qq) sg = fma(jac ? u[c0 + qq] : ub[qq], Hr_[c0 + qq], sg);
+            const Real g = sg - mv[q];                     // Eq 14
+            const Real ur = ub[q];
+            const Real un = fmax(Real(0), ur - g / h);     // Eq 11-13
+            const Real d = un - ur;                        // Eq 12
+            const Real L = l_mode ? Lf : h;
+            z = -g * d - (L * Real(0.5)) * d * d;          // Eq 20
+            const Real zpr = zv[q];
+            const Real zg = snap ? zs[q] : z;  // the score the gate sees
+            sel = !score && ((branch == SACD_BR_FIRST) ? (zg > Real(0))
+                                                       : ((branch == SACD_BR_EQ24) ? (zg - zpr > Real(0))
+                                                                                   : (zpr - zg > Real(0))));
+            if (sel) {
+              ub[q] = un;
+              E += 1;
+              if (d != Real(0)) Ech += 1;
+            }
+          }
+          if (snap) z = zs[q];
+          zv[q] = z;                                       // z_prev <- z always (C8)
+          ti += (double)z;                                 // Eq 25
+          md += (double)ub[q] * (double)mv[q];
+          if (dec && !score) dec[row * R + r] = (uint8_t)sel;
+        }
+      }
+      if (score) {
+#pragma unroll
+        for (int q = 0; q < C; ++q) zsp[32 * (c0 + q)] = zv[q];
+        continue;
+      }
+      if (jac) {  // the staged rows keep the pass-start values; updates go straight to F
+#pragma unroll
+        for (int q = 0; q < C; ++q)
+          if (c0 + q < R) F[row * RT + c0 + q] = ub[q];
+      } else {
+#pragma unroll
+        for (int q = 0; q < C; ++q) u[c0 + q] = ub[q];
+      }
+#pragma unroll
+      for (int q = 0; q < C; ++q) zp[32 * (c0 + q)] = zv[q];
+    }
+  }
+  __syncthreads();
+  Real *Fo = F + row0 * RT;
+  if (!jac && !score)
+    for (int x = tid; x < nrows * RT; x += TR) Fo[x] = Us[(x / RT) * US + (x % RT)];
+
+  // fixed-order block reduction of (ti, md, E, Ech)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ti += __shfl_xor_sync(0xffffffffu, ti, o);
+    md += __shfl_xor_sync(0xffffffffu, md, o);
+    E += __shfl_xor_sync(0xffffffffu, E, o);
+    Ech += __shfl_xor_sync(0xffffffffu, Ech, o);
+  }
+  const int w = tid >> 5;
+  if ((tid & 31) == 0) {
+    red_d[0][w] = ti;
+    red_d[1][w] = md;
+    red_l[0][w] = E;
+    red_l[1][w] = Ech;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double a = 0.0, b = 0.0;
+    long long c = 0, d = 0;
+    for (int k = 0; k < TR / 32; ++k) {
+      a += red_d[0][k];
+      b += red_d[1][k];
+      c += red_l[0][k];
+      d += red_l[1][k];
+    }
+    ti_part[blockIdx.x] = a;
+    md_part[blockIdx.x] = b;
+    e_part[blockIdx.x] = c;
+    ech_part[blockIdx.x] = d;
+  }
+}
+
+// Fused row update with the out-of-block gradient on the fp64 tensor cores (Real = double,
+// RT <= 64).  Same semantics and per-row order of operations as k_sacd_rows: for column block
+// [c0, c0+8) the out-of-block part acc_q = sum_{j not in block} u_j h_(j,c0+q) of every row
+// of a warp (32 rows) is one (32 x RT) x (RT x 8) product of the CURRENT rows (columns < c0
+// already updated this pass, Gauss-Seidel C9) with H, issued as DMMA m8n8k4 (4 row tiles x
+// the k-steps outside the block, in ascending k); the in-block Gauss-Seidel step then runs
+// one thread per row exactly as in k_sacd_rows.  Fragments: A[m][k] = u[8mt+m][4kk+k] held
+// by lane (g = lane >> 2, t = lane & 3) as Us[8mt+g][4kk+t]; B[k][n] = H[4kk+k][c0+n] as
+// H[4kk+t][c0+g] (from L1: H is read-only and shared by every block); C[g][2t + {0,1}].
+// The accumulator tile and the block's M tile are transposed to one-row-per-thread through
+// a per-warp shared tile.  Shared memory: Us (rows x (RT+2), conflict-free for both the
+// fragment reads and the 16-byte row walks) + 32 x 18 doubles per warp.
+template <int RT, int WPB>
+__global__ void __launch_bounds__(WPB * 32)
+    k_sacd_rows_mma(long long row_begin, long long row_end, int R, int mode, int l_mode,
+                    const long long *__restrict__ row_ptr, const double *__restrict__ M, double *__restrict__ F,
+                    double *__restrict__ Z, const double *__restrict__ H, const DevState *__restrict__ st,
+                    uint8_t *__restrict__ dec, double *__restrict__ ti_part, double *__restrict__ md_part,
+                    long long *__restrict__ e_part, long long *__restrict__ ech_part) {
+  constexpr int TR = WPB * 32;
+  constexpr int US = RT + 2;
+  constexpr int C = 8;
+  constexpr int TS = 2 * C + 2;
+  constexpr int NKS = RT / 4;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double *Us = reinterpret_cast<double *>(smem_raw);
+  double *Hd = Us + TR * US + WPB * 32 * TS;  // the 8 x 8 diagonal blocks of H: [RT/8][8][8]
+  __shared__ double red_d[2][WPB];
+  __shared__ long long red_l[2][WPB];
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, wp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  double *Tw = Us + TR * US + wp * 32 * TS;
+  const long long row0 = row_begin + (long long)blockIdx.x * TR;
+  const int nrows = (int)min((long long)TR, row_end - row0);
+  const double *Fg = F + row0 * RT;
+  static_assert(((RT + 2) * 8) % 16 == 0, "row stride must keep 16-byte chunks aligned");
+  for (int x = tid; x < TR * RT / 2; x += TR) {  // 16-byte chunks
+    const int r = (2 * x) / RT, col = (2 * x) % RT;
+    if (r < nrows) cp_async<16>(Us + r * US + col, Fg + 2 * x);
+    else *reinterpret_cast<double2 *>(Us + r * US + col) = make_double2(0.0, 0.0);
+  }
+  cp_async_wait_all();
+  for (int x = tid; x < RT * C; x += TR) {
+    const int b = x / (C * C), q = (x / C) % C, qq = x % C;
+    Hd[x] = H[(b * C + q) * RT + b * C + qq];
+  }
+  __syncthreads();
+  const int branch = st->branch[mode];
+  const double Lf = st->Lfrob[mode];
+  const int kmax = (R + 3) / 4;  // k-steps past R multiply zero padding
+
+  double ti = 0.0, md = 0.0;
+  long long E = 0, Ech = 0;
+  const bool active = tid < nrows;
+  const long long row = row0 + tid;
+  double *u = Us + tid * US;
+  const bool empty = active ? row_ptr[row] == row_ptr[row + 1] : true;  // empty slice: m = 0
+  double *zp = Z + tt<RT>(active ? row : row0, 0);
+  const double *Uw = Us + (wp * 32 + g) * US + t;
+
+  // software pipeline over column blocks: the B fragments, the M tile and this thread's
+  // z_prev of block c0 + 8 are loaded while block c0 is processed (all read-only here)
+  double bf[NKS], mt[C], zv[C];
+  auto load_block = [&](int c, double (&b)[NKS], double (&mm)[C], double (&zz)[C]) {
+    const int kb = c / 4;
+#pragma unroll
+    for (int kk = 0; kk < NKS; ++kk)
+      b[kk] = (kk == kb || kk == kb + 1 || kk >= kmax) ? 0.0 : __ldg(H + (4 * kk + t) * RT + c + g);
+#pragma unroll
+    for (int k = 0; k < C; ++k) {
+      const int x = lane + 32 * k, rl = x / C, cl = x % C;
+      const long long rg = row0 + wp * 32 + rl;
+      mm[k] = (rg < row_end) ? __ldg(M + rg * RT + c + cl) : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < C; ++q) zz[q] = (active && c + q < RT) ? zp[32 * (c + q)] : 0.0;
+  };
+  load_block(0, bf, mt, zv);
+  for (int c0 = 0; c0 < R; c0 += C) {
+    double bfn[NKS], mtn[C], zvn[C];
+    if (c0 + C < R) load_block(c0 + C, bfn, mtn, zvn);
+    // (1) out-of-block gradient of the warp's 32 rows on the tensor cores: all k-steps
+    //     unrolled, the block's own k-steps (and those past R) with a zero B fragment (adding
+    //     0 * a leaves an accumulator unchanged); even / odd k-steps in two sets of tiles
+    double cacc[2][4][2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int m = 0; m < 4; ++m) cacc[h][m][0] = cacc[h][m][1] = 0.0;
+#pragma unroll
+    for (int kk = 0; kk < NKS; ++kk) {
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const double a = Uw[8 * m * US + 4 * kk];
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                     : "+d"(cacc[kk & 1][m][0]), "+d"(cacc[kk & 1][m][1])
+                     : "d"(a), "d"(bf[kk]));
+      }
+    }
+    // (2) accumulators and the block's M tile to one row per thread
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      Tw[(8 * m + g) * TS + 2 * t] = cacc[0][m][0] + cacc[1][m][0];
+      Tw[(8 * m + g) * TS + 2 * t + 1] = cacc[0][m][1] + cacc[1][m][1];
+    }
+#pragma unroll
+    for (int k = 0; k < C; ++k) {
+      const int x = lane + 32 * k, rl = x / C, cl = x % C;
+      Tw[rl * TS + C + cl] = mt[k];
+    }
+    __syncwarp();
+    if (active) {
+      double acc[C], mv[C], ub[C];
+#pragma unroll
+      for (int q = 0; q < C; ++q) {
+        acc[q] = Tw[lane * TS + q];
+        mv[q] = empty ? 0.0 : Tw[lane * TS + C + q];
+        ub[q] = u[c0 + q];
+      }
+      const double *Hb = Hd + (c0 / C) * C * C;
+      // (3) in-block Gauss-Seidel (C9), as k_sacd_rows
+#pragma unroll
+      for (int q = 0; q < C; ++q) {
+        const int r = c0 + q;
+        if (r < R) {
+          const double h = Hb[q * C + q];
+          double z = 0.0;
+          bool sel = false;
+          if (h != 0.0) {
+            double sg = acc[q];
+#pragma unroll
+            for (int qq = 0; qq < C; ++qq) sg = fma(ub[qq], Hb[q * C + qq], sg);
+            const double gr = sg - mv[q];                  // Eq 14
+            const double ur = ub[q];
+            const double un = fmax(0.0, ur - gr / h);      // Eq 11-13
+            const double d = un - ur;                      // Eq 12
+            const double L = l_mode ? Lf : h;
+            z = -gr * d - (L * 0.5) * d * d;               // Eq 20
+            const double zpr = zv[q];
+            sel = (branch == SACD_BR_FIRST) ? (z > 0.0)
+                                            : ((branch == SACD_BR_EQ24) ? (z - zpr > 0.0) : (zpr - z > 0.0));
+            if (sel) {
+              ub[q] = un;
+              E += 1;
+              if (d != 0.0) Ech += 1;
+            }
+          }
+          zv[q] = z;                                       // z_prev <- z always (C8)
+          ti += z;                                         // Eq 25
+          md += ub[q] * mv[q];
+          if (dec) dec[row * R + r] = (uint8_t)sel;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < C; ++q) u[c0 + q] = ub[q];
+#pragma unroll
+      for (int q = 0; q < C; ++q) zp[32 * (c0 + q)] = zv[q];
+    }
+    __syncwarp();  // the updated block columns feed the next block's fragments; Tw is reused
+#pragma unroll
+    for (int kk = 0; kk < NKS; ++kk) bf[kk] = bfn[kk];
+#pragma unroll
+    for (int q = 0; q < C; ++q) {
+      mt[q] = mtn[q];
+      zv[q] = zvn[q];
+    }
+  }
+  __syncthreads();
+  double *Fo = F + row0 * RT;
+  for (int x = tid; x < nrows * RT; x += TR) Fo[x] = Us[(x / RT) * US + (x % RT)];
+
+  // fixed-order block reduction of (ti, md, E, Ech)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ti += __shfl_xor_sync(0xffffffffu, ti, o);
+    md += __shfl_xor_sync(0xffffffffu, md, o);
+    E += __shfl_xor_sync(0xffffffffu, E, o);
+    Ech += __shfl_xor_sync(0xffffffffu, Ech, o);
+  }
+  if (lane == 0) {
+    red_d[0][wp] = ti;
+    red_d[1][wp] = md;
+    red_l[0][wp] = E;
+    red_l[1][wp] = Ech;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double a = 0.0, b = 0.0;
+    long long c = 0, d = 0;
+    for (int k = 0; k < WPB; ++k) {
+      a += red_d[0][k];
+      b += red_d[1][k];
+      c += red_l[0][k];
+      d += red_l[1][k];
+    }
+    ti_part[blockIdx.x] = a;
+    md_part[blockIdx.x] = b;
+    e_part[blockIdx.x] = c;
+    ech_part[blockIdx.x] = d;
+  }
+}
+
+// The same row update for R > 64 (fp64): one warp (32 rows) per block; the B fragments of
+// a column block (R/4 k-steps) are loaded 16 k-steps at a time, the next chunk in flight
+// while the current one feeds the DMMAs; the in-block H values come from L1.  The FMA
+// kernel this replaces waited on one L2 round trip of H per 4 gradient terms.
+template <int RT>
+__global__ void __launch_bounds__(32)
+    k_sacd_rows_mma_big(long long row_begin, long long row_end, int R, int mode, int l_mode,
+                        const long long *__restrict__ row_ptr, const double *__restrict__ M, double *__restrict__ F,
+                        double *__restrict__ Z, const double *__restrict__ H, const DevState *__restrict__ st,
+                        uint8_t *__restrict__ dec, double *__restrict__ ti_part, double *__restrict__ md_part,
+                        long long *__restrict__ e_part, long long *__restrict__ ech_part) {
+  constexpr int US = RT + 2;
+  constexpr int C = 8;
+  constexpr int TS = 2 * C + 2;
+  constexpr int KC = 16;  // k-steps per B-fragment chunk
+  static_assert(RT % (4 * KC) == 0, "R pitch must be a multiple of 64");
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double *Us = reinterpret_cast<double *>(smem_raw);
+  double *Tw = Us + 32 * US;
+  const int lane = threadIdx.x;
+  const int g = lane >> 2, t = lane & 3;
+  const long long row0 = row_begin + (long long)blockIdx.x * 32;
+  const int nrows = (int)min(32LL, row_end - row0);
+  const double *Fg = F + row0 * RT;
+  static_assert(((RT + 2) * 8) % 16 == 0, "row stride must keep 16-byte chunks aligned");
+  for (int x = lane; x < 32 * RT / 2; x += 32) {
+    const int r = (2 * x) / RT, col = (2 * x) % RT;
+    if (r < nrows) cp_async<16>(Us + r * US + col, Fg + 2 * x);
+    else *reinterpret_cast<double2 *>(Us + r * US + col) = make_double2(0.0, 0.0);
+  }
+  cp_async_wait_all();
+  __syncwarp();
+  const int branch = st->branch[mode];
+  const double Lf = st->Lfrob[mode];
+  const int kmax = (R + 3) / 4;
+
+  double ti = 0.0, md = 0.0;
+  long long E = 0, Ech = 0;
+  const bool active = lane < nrows;
+  const long long row = row0 + lane;
+  double *u = Us + lane * US;
+  const bool empty = active ? row_ptr[row] == row_ptr[row + 1] : true;
+  double *zp = Z + tt<RT>(active ? row : row0, 0);
+  const double *Uw = Us + g * US + t;
+  for (int c0 = 0; c0 < R; c0 += C) {
+    const int kb = c0 / 4;
+    double mt[C], zv[C];
+#pragma unroll
+    for (int k = 0; k < C; ++k) {
+      const int x = lane + 32 * k, rl = x / C, cl = x % C;
+      const long long rg = row0 + rl;
+      mt[k] = (rg < row_end) ? __ldg(M + rg * RT + c0 + cl) : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < C; ++q) zv[q] = active ? zp[32 * (c0 + q)] : 0.0;
+    double cacc[2][4][2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int m = 0; m < 4; ++m) cacc[h][m][0] = cacc[h][m][1] = 0.0;
+    auto load_chunk = [&](int k0, double (&b)[KC]) {
+#pragma unroll
+      for (int j = 0; j < KC; ++j) {
+        const int kk = k0 + j;
+        b[j] = (kk == kb || kk == kb + 1 || kk >= kmax) ? 0.0 : __ldg(H + (4 * kk + t) * RT + c0 + g);
+      }
+    };
+    double bc[KC], bn[KC];
+    load_chunk(0, bc);
+    for (int k0 = 0; k0 < kmax; k0 += KC) {
+      if (k0 + KC < kmax) load_chunk(k0 + KC, bn);
+#pragma unroll
+      for (int j = 0; j < KC; ++j) {
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          const double a = Uw[8 * m * US + 4 * (k0 + j)];
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                       : "+d"(cacc[j & 1][m][0]), "+d"(cacc[j & 1][m][1])
+                       : "d"(a), "d"(bc[j]));
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < KC; ++j) bc[j] = bn[j];
+    }
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      Tw[(8 * m + g) * TS + 2 * t] = cacc[0][m][0] + cacc[1][m][0];
+      Tw[(8 * m + g) * TS + 2 * t + 1] = cacc[0][m][1] + cacc[1][m][1];
+    }
+#pragma unroll
+    for (int k = 0; k < C; ++k) {
+      const int x = lane + 32 * k, rl = x / C, cl = x % C;
+      Tw[rl * TS + C + cl] = mt[k];
+    }
+    __syncwarp();
+    if (active) {
+      double acc[C], mv[C], ub[C];
+#pragma unroll
+      for (int q = 0; q < C; ++q) {
+        acc[q] = Tw[lane * TS + q];
+        mv[q] = empty ? 0.0 : Tw[lane * TS + C + q];
+        ub[q] = u[c0 + q];
+      }
+#pragma unroll
+      for (int q = 0; q < C; ++q) {
+        const int r = c0 + q;
+        if (r < R) {
+          const double *Hr_ = H + (long long)r * RT + c0;
+          const double h = __ldg(Hr_ + q);
+          double z = 0.0;
+          bool sel = false;
+          if (h != 0.0) {
+            double sg = acc[q];
+#pragma unroll
+            for (int qq = 0; qq < C; ++qq) sg = fma(ub[qq], __ldg(Hr_ + qq), sg);
+            const double gr = sg - mv[q];                  // Eq 14
+            const double ur = ub[q];
+            const double un = fmax(0.0, ur - gr / h);      // Eq 11-13
+            const double d = un - ur;                      // Eq 12
+            const double L = l_mode ? Lf : h;
+            z = -gr * d - (L * 0.5) * d * d;               // Eq 20
+            const double zpr = zv[q];
+            sel = (branch == SACD_BR_FIRST) ? (z > 0.0)
+                                            : ((branch == SACD_BR_EQ24) ? (z - zpr > 0.0) : (zpr - z > 0.0));
+            if (sel) {
+              ub[q] = un;
+              E += 1;
+              if (d != 0.0) Ech += 1;
+            }
+          }
+          zv[q] = z;
+          ti += z;
+          md += ub[q] * mv[q];
+          if (dec) dec[row * R + r] = (uint8_t)sel;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < C; ++q) u[c0 + q] = ub[q];
+#pragma unroll
+      for (int q = 0; q < C; ++q) zp[32 * (c0 + q)] = zv[q];
+    }
+    __syncwarp();
+  }
+  double *Fo = F + row0 * RT;
+  for (int x = lane; x < nrows * RT; x += 32) Fo[x] = Us[(x / RT) * US + (x % RT)];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ti += __shfl_xor_sync(0xffffffffu, ti, o);
+    md += __shfl_xor_sync(0xffffffffu, md, o);
+    E += __shfl_xor_sync(0xffffffffu, E, o);
+    Ech += __shfl_xor_sync(0xffffffffu, Ech, o);
+  }
+  if (lane == 0) {
+    ti_part[blockIdx.x] = ti;
+    md_part[blockIdx.x] = md;
+    e_part[blockIdx.x] = E;
+    ech_part[blockIdx.x] = Ech;
+  }
+}
+
+template <int RT>
+__host__ __device__ constexpr size_t rows_mma_big_smem_bytes() {
+  return (size_t)32 * (RT + 2) * 8 + (size_t)32 * 18 * 8;
+}
+
+template <int RT, int WPB>
+__host__ __device__ constexpr size_t rows_mma_smem_bytes() {
+  return (size_t)WPB * 32 * (RT + 2) * 8 + (size_t)WPB * 32 * 18 * 8 + (size_t)RT * 8 * 8;
+}
+
+// sum_r F_ir M_ir per row block (initial objective f^0)
+template <typename Real, int RT>
+__global__ void k_fm_dot(long long row_begin, long long row_end, int R, const long long *__restrict__ row_ptr,
+                         const Real *__restrict__ F,
+                         const Real *__restrict__ M,
+                         double *__restrict__ ti_part, double *__restrict__ md_part, long long *__restrict__ e_part,
+                         long long *__restrict__ ech_part) {
+  constexpr int TR = rows_per_block<RT>();
+  __shared__ double red[TR];
+  const long long row = row_begin + (long long)blockIdx.x * TR + threadIdx.x;
+  double s = 0.0;
+  if (row < row_end && row_ptr[row] != row_ptr[row + 1])
+    for (int r = 0; r < R; ++r) s += (double)F[row * RT + r] * (double)M[row * RT + r];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0;
+    for (int k = 0; k < TR; ++k) a += red[k];
+    md_part[blockIdx.x] = a;
+    ti_part[blockIdx.x] = 0.0;
+    e_part[blockIdx.x] = 0;
+    ech_part[blockIdx.x] = 0;
+  }
+}
+

@@ -14,6 +14,11 @@
 //
 // Determinism: no floating-point atomics anywhere; every reduction has a fixed order, so
 // reruns are bitwise identical (unchanged elements recompute the same z exactly).
+//
+// The kernels live in fragments included below (one translation unit): k_mttkrp.inc.cuh
+// (A3), k_rows.inc.cuh (A2 H / branch, A4 row update), k_gram.inc.cuh (Gram refresh),
+// k_pass.inc.cuh (pass records / objective, delta exchange, sharding helpers, predict).
+// This file keeps the helpers, the launch implementations (Impl) and the C++ entry points.
 #include <math.h>
 
 #include <nccl.h>
@@ -127,1861 +132,10 @@ __global__ void k_init_factors(Real *__restrict__ F, long long I, int R, int RT,
   }
 }
 
-// ------------------------------------------------------------------ sparse MTTKRP
-// One warp per work item.  Lanes tile the row's R columns with 16-byte vectors (float4 /
-// double2); when a row needs fewer than 32 lanes, the warp splits into G groups that take
-// every G-th nonzero of the row and are combined by a fixed xor-shuffle tree at row end.
-template <typename Real, int RT>
-__global__ void __launch_bounds__(256) k_mttkrp(const WorkItem *__restrict__ items, long long n_items,
-                                                const long long *__restrict__ row_ptr,
-                                                const uint32_t *__restrict__ ia, const uint32_t *__restrict__ ib,
-                                                const float *__restrict__ val, const Real *__restrict__ A,
-                                                const Real *__restrict__ B, Real *__restrict__ M,
-                                                Real *__restrict__ partial) {
-  using VV = V16<Real>;
-  using VT = typename VV::T;
-  constexpr int VEC = VV::N;
-  constexpr int NV = RT / VEC;
-  constexpr int LPN = NV < 32 ? NV : 32;
-  constexpr int VPL = NV / LPN;
-  constexpr int G = 32 / LPN;
-  const int lane = threadIdx.x & 31;
-  const long long item = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (item >= n_items) return;
-  const WorkItem it = items[item];
-  const int grp = lane / LPN, sub = lane % LPN;
-  for (int row = it.row0; row < it.row1; ++row) {
-    long long s = row_ptr[row], t = row_ptr[row + 1];
-    if (s < it.nz0) s = it.nz0;
-    if (t > it.nz1) t = it.nz1;
-    Real acc[VPL][VEC];
-#pragma unroll
-    for (int v = 0; v < VPL; ++v)
-#pragma unroll
-      for (int c = 0; c < VEC; ++c) acc[v][c] = Real(0);
-    for (long long e = s + grp; e < t; e += G) {
-      const Real x = (Real)ld_stream_f32(val + e);
-      const VT *ap = reinterpret_cast<const VT *>(A + (long long)(ld_stream_u32(ia + e) & kIdxMask) * RT);
-      const VT *bp = reinterpret_cast<const VT *>(B + (long long)(ld_stream_u32(ib + e) & kIdxMask) * RT);
-#pragma unroll
-      for (int v = 0; v < VPL; ++v) {
-        Real av[VEC], bv[VEC];
-        VV::get(__ldg(ap + sub + v * LPN), av);
-        VV::get(__ldg(bp + sub + v * LPN), bv);
-#pragma unroll
-        for (int c = 0; c < VEC; ++c) acc[v][c] = fma(x * av[c], bv[c], acc[v][c]);
-      }
-    }
-#pragma unroll
-    for (int off = LPN; off < 32; off <<= 1)
-#pragma unroll
-      for (int v = 0; v < VPL; ++v)
-#pragma unroll
-        for (int c = 0; c < VEC; ++c) acc[v][c] += __shfl_xor_sync(0xffffffffu, acc[v][c], off);
-    if (grp == 0) {
-      if (it.slot >= 0) {
-        VT *dv = reinterpret_cast<VT *>(partial + it.slot * RT);
-#pragma unroll
-        for (int v = 0; v < VPL; ++v) dv[sub + v * LPN] = VV::make(acc[v]);
-      } else {
-        VT *dv = reinterpret_cast<VT *>(M + (long long)row * RT);
-#pragma unroll
-        for (int v = 0; v < VPL; ++v) dv[sub + v * LPN] = VV::make(acc[v]);
-      }
-    }
-  }
-}
-
-// Wide-row MTTKRP (R > 16): one warp per work item, lane l owns columns [l*E, l*E+E),
-// E = RT/32, so every factor-row gather is one coalesced RT*sizeof(Real)-byte warp access.
-//  * The warp loads 32 nonzeros' (idx_a|flags, idx_b, x, row) with coalesced streaming
-//    loads and broadcasts them by shuffle.
-//  * Fiber factoring: the layout is sorted by (i_n, i_a, i_b), so a run of
-//    equal i_a inside a row is a fiber, and m_i = sum_fibers a_(i_a) * (sum_e x_e b_(i_b(e))):
-//    one a-row gather per fiber.  Fiber / row starts are precomputed flag bits of idx_a
-//    (built with the layout), so the per-nonzero path is: 3 shuffles, one b-row gather
-//    (prefetched one nonzero ahead), E FMAs.
-//  * Rows are flushed to M[row] when a row starts; empty rows are never touched (the row
-//    update reads row_ptr and uses m = 0 for them).  Split items (slot >= 0) hold a segment
-//    of one heavy row and flush to their partial slot.
-// Default occupancy target of k_mttkrp_fiber (measured on B200 with tools/mttkrp_tune.py:
-// the kernel is latency-bound, so the most resident warps that fit without spilling win).
-template <typename Real, int RT>
-__host__ __device__ constexpr int fiber_min_blocks() {
-  return (RT / 32) * sizeof(Real) <= 8 ? 7 : ((RT / 32) * sizeof(Real) <= 16 ? 6 : ((RT / 32) * sizeof(Real) <= 32 ? 4 : 2));
-}
-
-template <typename Real, int E>
-struct LaneRow {
-  Real v[E];
-  __device__ __forceinline__ void load(const Real *p) {
-    if constexpr (E * sizeof(Real) >= 16) {
-      using VV = V16<Real>;
-#pragma unroll
-      for (int k = 0; k < (int)(E * sizeof(Real) / 16); ++k)
-        VV::get(__ldg(reinterpret_cast<const typename VV::T *>(p) + k), v + k * VV::N);
-    } else if constexpr (E * sizeof(Real) == 8) {
-      if constexpr (sizeof(Real) == 8) {
-        v[0] = __ldg(p);
-      } else {
-        const float2 t = __ldg(reinterpret_cast<const float2 *>(p));
-        v[0] = t.x;
-        v[1] = t.y;
-      }
-    } else {
-      v[0] = __ldg(p);
-    }
-  }
-  __device__ __forceinline__ void store(Real *p) const {
-    if constexpr (E * sizeof(Real) >= 16) {
-      using VV = V16<Real>;
-#pragma unroll
-      for (int k = 0; k < (int)(E * sizeof(Real) / 16); ++k)
-        reinterpret_cast<typename VV::T *>(p)[k] = VV::make(v + k * VV::N);
-    } else {
-#pragma unroll
-      for (int k = 0; k < E; ++k) p[k] = v[k];
-    }
-  }
-};
-
-template <typename Real, int RT, int NB, int MINB>
-__global__ void __launch_bounds__(256, MINB) k_mttkrp_fiber(const WorkItem *__restrict__ items, long long n_items,
-                                                      const uint32_t *__restrict__ ia,
-                                                      const uint32_t *__restrict__ ib,
-                                                      const float *__restrict__ val,
-                                                      const uint32_t *__restrict__ in_,
-                                                      const Real *__restrict__ A, const Real *__restrict__ B,
-                                                      Real *__restrict__ M, Real *__restrict__ partial) {
-  constexpr int E = RT / 32;
-  const int lane = threadIdx.x & 31;
-  const long long item = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (item >= n_items) return;
-  const WorkItem it = items[item];
-  if (it.nz0 >= it.nz1) return;
-  const Real *Al = A + lane * E;
-  const Real *Bl = B + lane * E;
-  LaneRow<Real, E> arow;
-  Real acc[E], facc[E];
-#pragma unroll
-  for (int k = 0; k < E; ++k) acc[k] = facc[k] = arow.v[k] = Real(0);
-  long long cur_row = -1;
-  Real *Ml = M + lane * E;
-  auto flush = [&]() {
-    LaneRow<Real, E> o;
-#pragma unroll
-    for (int k = 0; k < E; ++k) {
-      o.v[k] = acc[k];
-      acc[k] = Real(0);
-    }
-    if (it.slot >= 0) o.store(partial + it.slot * RT + lane * E);
-    else if (cur_row >= 0) o.store(Ml + cur_row * RT);
-  };
-  auto step = [&](uint32_t fa, float xf, const LaneRow<Real, E> &b, uint32_t my_n, int j) {
-    if (fa & kFiberStart) {
-#pragma unroll
-      for (int k = 0; k < E; ++k) {            // close the previous fiber: acc += a * facc
-        acc[k] = fma(arow.v[k], facc[k], acc[k]);
-        facc[k] = Real(0);
-      }
-      if (fa & kRowStart) {
-        flush();
-        cur_row = __shfl_sync(0xffffffffu, my_n, j);
-      }
-      arow.load(Al + (long long)(fa & kIdxMask) * RT);
-    }
-    const Real x = (Real)xf;
-#pragma unroll
-    for (int k = 0; k < E; ++k) facc[k] = fma(x, b.v[k], facc[k]);
-  };
-  for (long long base = it.nz0; base < it.nz1; base += 32) {
-    const int cnt = (int)min(32LL, it.nz1 - base);
-    uint32_t my_a = 0, my_b = 0, my_n = 0;
-    float my_x = 0.f;
-    if (lane < cnt) {
-      my_a = ld_stream_u32(ia + base + lane);
-      my_b = ld_stream_u32(ib + base + lane);
-      my_x = ld_stream_f32(val + base + lane);
-      my_n = ld_stream_u32(in_ + base + lane);
-    }
-    if (base == it.nz0 && lane == 0) my_a |= kFiberStart | kRowStart;  // an item starts a row/fiber
-    // batches of NB b-row gathers in flight per warp, then consumed in order
-    for (int jb = 0; jb < cnt; jb += NB) {
-      LaneRow<Real, E> bb[NB];
-#pragma unroll
-      for (int u = 0; u < NB; ++u) {
-        const uint32_t eb = __shfl_sync(0xffffffffu, my_b, (jb + u) & 31);
-        if (jb + u < cnt) bb[u].load(Bl + (long long)(eb & kIdxMask) * RT);
-      }
-#pragma unroll
-      for (int u = 0; u < NB; ++u) {
-        const int j = (jb + u) & 31;
-        const uint32_t fa = __shfl_sync(0xffffffffu, my_a, j);
-        const float xf = __shfl_sync(0xffffffffu, my_x, j);
-        if (jb + u < cnt) step(fa, xf, bb[u], my_n, j);
-      }
-    }
-  }
-#pragma unroll
-  for (int k = 0; k < E; ++k) acc[k] = fma(arow.v[k], facc[k], acc[k]);
-  flush();
-}
-
-// Sub-warp fiber MTTKRP (R > 16): a worker of SW lanes (8, 16 or 32) per work item, so one
-// warp runs 32/SW items at once and every shuffle instruction serves all of them.
-//  * Lane l of a worker owns the 16-byte column chunks k*SW + l (k < NV), so each chunk
-//    load of a factor row is one contiguous SW*16-byte access (full sectors).
-//  * The fiber / row flag bits ride on idx_b (layout.cu), so a nonzero costs two shuffles
-//    (b index + flags, value); the a index and the row id are fetched only at fiber / row
-//    starts.  The next batch's metadata is prefetched one batch ahead.
-//  * NB b-rows (and, with PA, the a-rows of fibers starting among them) are issued before
-//    any is consumed, so a worker keeps NB gathers in flight.
-// Same arithmetic and order as k_mttkrp_fiber: m_i = sum_fibers a (.) (sum_e x_e b_e).
-template <typename Real, int RT>
-__host__ __device__ constexpr int sub_warp_lanes() {  // 16 bytes of a row per lane, at most 32 lanes
-  return RT * (int)sizeof(Real) / 16 > 32 ? 32 : RT * (int)sizeof(Real) / 16;
-}
-
-template <typename Real, int RT, int SW>
-struct SubRow {
-  using VV = V16<Real>;
-  using VT = typename VV::T;
-  static constexpr int NV = RT / VV::N / SW;  // 16-byte chunks per lane
-  static constexpr int E = NV * VV::N;
-  Real v[E];
-  // p = row base + lane * VEC
-  __device__ __forceinline__ void load(const Real *p) {
-#pragma unroll
-    for (int k = 0; k < NV; ++k) VV::get(__ldg(reinterpret_cast<const VT *>(p) + k * SW), v + k * VV::N);
-  }
-  __device__ __forceinline__ void store(Real *p) const { store_from(p, v); }
-  __device__ static __forceinline__ void store_from(Real *p, const Real (&x)[E]) {
-#pragma unroll
-    for (int k = 0; k < NV; ++k) {
-      Real t[VV::N];
-#pragma unroll
-      for (int c = 0; c < VV::N; ++c) t[c] = x[k * VV::N + c];
-      reinterpret_cast<VT *>(p)[k * SW] = VV::make(t);
-    }
-  }
-};
-
-__device__ __forceinline__ uint4 ld_stream_u4(const uint4 *p) {
-  uint4 v;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-               : "l"(p));
-  return v;
-}
-
-// Chunk support mask of each factor row: bit k = 16-byte chunk k (elements
-// [k*VEC, (k+1)*VEC)) holds a nonzero.  One warp per row (lane k tests chunk k); rows of at
-// most 32 chunks (RT * sizeof(Real) <= 512).  SaCD's projection leaves most factor entries
-// exactly zero (tools/factor_stats.py: ~80% on c4), and the skipping MTTKRP uses these masks
-// to gather only chunks where both the a-row and the b-row are nonzero.
-template <typename Real, int RT>
-__global__ void __launch_bounds__(256) k_chunk_mask(const Real *__restrict__ F, long long I,
-                                                   uint32_t *__restrict__ cmask) {
-  using VV = V16<Real>;
-  constexpr int NCH = RT / VV::N;
-  static_assert(NCH <= 32, "chunk masks hold at most 32 chunks");
-  const int lane = threadIdx.x & 31;
-  const long long w0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
-  for (long long row = w0; row < I; row += nw) {
-    bool nz = false;
-    if (lane < NCH) {
-      Real v[VV::N];
-      VV::get(__ldg(reinterpret_cast<const typename VV::T *>(F + row * RT) + lane), v);
-#pragma unroll
-      for (int c = 0; c < VV::N; ++c) nz |= (v[c] != Real(0));
-    }
-    const uint32_t m = __ballot_sync(0xffffffffu, nz);
-    if (lane == 0) cmask[row] = m;
-  }
-}
-
-template <typename Real, int RT, int SW, int NB, int MINB>
-__global__ void __launch_bounds__(256, MINB) k_mttkrp_sw(const WorkItem *__restrict__ items, long long n_items,
-                                                        const uint4 *__restrict__ nzm,
-                                                        const Real *__restrict__ A, const Real *__restrict__ B,
-                                                        Real *__restrict__ M, Real *__restrict__ partial) {
-  using SR = SubRow<Real, RT, SW>;
-  constexpr int E = SR::E;
-  constexpr int VEC = V16<Real>::N;
-  static_assert(SR::NV >= 1, "row narrower than a sub-warp of 16-byte chunks");
-  const int lane = threadIdx.x & (SW - 1);
-  const unsigned mask = SW == 32 ? 0xffffffffu : (((1u << SW) - 1u) << (threadIdx.x & 31 & ~(SW - 1)));
-  const int shift = threadIdx.x & 31 & ~(SW - 1);  // this worker's lanes in a ballot
-  const long long item = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / SW;
-  if (item >= n_items) return;
-  const long long nz0 = items[item].nz0, nz1 = items[item].nz1;
-  const int slot = (int)items[item].slot;
-  if (nz0 >= nz1) return;
-  const Real *Al = A + lane * VEC;
-  const Real *Bl = B + lane * VEC;
-  SR arow, anext;
-  Real acc[E], facc[E];
-#pragma unroll
-  for (int k = 0; k < E; ++k) acc[k] = facc[k] = arow.v[k] = anext.v[k] = Real(0);
-  int cur_row = -1;
-  bool need_next = true;  // the a-row of the next fiber start is not in flight yet
-  for (long long base = nz0; base < nz1; base += SW) {
-    const int cnt = (int)min((long long)SW, nz1 - base);
-    // this batch's metadata: lane l holds nonzero base + l as {a|flags, b|flags, x, row}
-    uint4 my = make_uint4(0u, 0u, 0u, 0u);
-    if (lane < cnt) my = __ldg(nzm + base + lane);
-    if (base + SW + lane < nz1) asm volatile("prefetch.global.L1 [%0];" ::"l"(nzm + base + SW + lane));
-    if (base == nz0 && lane == 0) my.y |= kFiberStart | kRowStart;  // an item starts a row and a fiber
-    // fiber starts of this batch (bit j = nonzero base + j)
-    const unsigned fmask = (__ballot_sync(mask, (my.y & kFiberStart) != 0) >> shift) &
-                           (SW == 32 ? 0xffffffffu : ((1u << SW) - 1u));
-    if (need_next && fmask) {
-      const int j0 = __ffs(fmask) - 1;
-      anext.load(Al + (long long)(__shfl_sync(mask, my.x, j0, SW) & kIdxMask) * RT);
-      need_next = false;
-    }
-    for (int jb = 0; jb < cnt; jb += NB) {
-      SR bb[NB];
-      uint32_t fb[NB];
-      float xf[NB];
-#pragma unroll
-      for (int u = 0; u < NB; ++u) {  // NB gathers in flight (rows past cnt read row 0: harmless)
-        const int j = (jb + u) & (SW - 1);
-        fb[u] = __shfl_sync(mask, my.y, j, SW);
-        xf[u] = __uint_as_float(__shfl_sync(mask, my.z, j, SW));
-        bb[u].load(Bl + (long long)(fb[u] & kIdxMask) * RT);
-      }
-#pragma unroll
-      for (int u = 0; u < NB; ++u) {
-        if (jb + u < cnt) {
-          const int j = jb + u;
-          if (fb[u] & kFiberStart) {
-#pragma unroll
-            for (int k = 0; k < E; ++k) {  // close the previous fiber: acc += a * facc
-              acc[k] = fma(arow.v[k], facc[k], acc[k]);
-              facc[k] = Real(0);
-            }
-            if (fb[u] & kRowStart) {
-              const int nrow = (int)__shfl_sync(mask, my.w, j, SW);
-              if (slot >= 0) SR::store_from(partial + (long long)slot * RT + lane * VEC, acc);
-              else if (cur_row >= 0) SR::store_from(M + (long long)cur_row * RT + lane * VEC, acc);
-#pragma unroll
-              for (int k = 0; k < E; ++k) acc[k] = Real(0);
-              cur_row = nrow;
-            }
-#pragma unroll
-            for (int k = 0; k < E; ++k) arow.v[k] = anext.v[k];
-            // issue the a-row of the next fiber start (in this batch, else at the next batch)
-            const unsigned rest = j + 1 < 32 ? (fmask & ~((2u << j) - 1u)) : 0u;
-            if (rest) {
-              const int jn = __ffs(rest) - 1;
-              anext.load(Al + (long long)(__shfl_sync(mask, my.x, jn, SW) & kIdxMask) * RT);
-            } else {
-              need_next = true;
-            }
-          }
-          const Real x = (Real)xf[u];
-#pragma unroll
-          for (int k = 0; k < E; ++k) facc[k] = fma(x, bb[u].v[k], facc[k]);
-        }
-      }
-    }
-  }
-#pragma unroll
-  for (int k = 0; k < E; ++k) acc[k] = fma(arow.v[k], facc[k], acc[k]);
-  if (slot >= 0) SR::store_from(partial + (long long)slot * RT + lane * VEC, acc);
-  else if (cur_row >= 0) SR::store_from(M + (long long)cur_row * RT + lane * VEC, acc);
-}
-
-// Lean sub-warp fiber MTTKRP.  The MTTKRP is issue-bound (ncu: ~34 warp instructions per
-// nonzero in the warp-per-item kernel), so this kernel minimises instructions per nonzero:
-//  * SW lanes per worker (32/SW workers per warp), each lane holding E = RT/SW columns, so
-//    every shuffle / address / branch instruction serves 32/SW nonzeros at once;
-//  * the batch loop is fully unrolled over SW nonzeros; entries past the end carry x = 0,
-//    b = 0 and no flags, so they add exact zeros instead of needing predicates;
-//  * b-rows are prefetched D nonzeros ahead (registers renamed by the unroll), and the
-//    next batch's 16-byte metadata is in flight while the current batch is consumed.
-// Same arithmetic and order as k_mttkrp_fiber (bitwise-equal results).
-// Prefetch of a batch's factor rows into L2 (PF = 1: a-rows of fiber starts; 3: also the
-// b-rows) or L1 (PF = 2: a-rows): the per-fiber a-row gathers miss L2 on big factors and
-// their latency is otherwise exposed at the next fiber close, ~2.7 nonzeros later.
-template <typename Real, int RT, int PF>
-__device__ __forceinline__ void prefetch_rows(const uint4 &m, bool valid, const Real *A, const Real *B) {
-  constexpr int LINES = (RT * (int)sizeof(Real) + 127) / 128;
-  if (!valid) return;
-  if (m.y & kFiberStart) {
-    const char *pa = reinterpret_cast<const char *>(A + (long long)(m.x & kIdxMask) * RT);
-#pragma unroll
-    for (int k = 0; k < LINES; ++k) {
-      if (PF == 2) asm volatile("prefetch.global.L1 [%0];" ::"l"(pa + 128 * k));
-      else asm volatile("prefetch.global.L2 [%0];" ::"l"(pa + 128 * k));
-    }
-  }
-  if (PF == 3) {
-    const char *pb = reinterpret_cast<const char *>(B + (long long)(m.y & kIdxMask) * RT);
-#pragma unroll
-    for (int k = 0; k < LINES; ++k) asm volatile("prefetch.global.L2 [%0];" ::"l"(pb + 128 * k));
-  }
-}
-
-// XS: how the batch's per-nonzero b index / x reach every lane of the worker: 0 = warp
-// shuffles (1 for the b index, 2 for x in fp64), 1 = x through a shared-memory broadcast
-// (one wavefront instead of two shuffles), 2 = the b index and x as one 16-byte
-// shared-memory broadcast per nonzero.
-template <typename Real, int RT, int SW, int D, int MINB, int PF = 0, int XS = 0>
-__global__ void __launch_bounds__(256, MINB) k_mttkrp_lean(const WorkItem *__restrict__ items, long long n_items,
-                                                          const uint4 *__restrict__ nzm,
-                                                          const Real *__restrict__ A, const Real *__restrict__ B,
-                                                          Real *__restrict__ M, Real *__restrict__ partial) {
-  using SR = SubRow<Real, RT, SW>;
-  constexpr int E = SR::E;
-  constexpr int VEC = V16<Real>::N;
-  static_assert(SR::NV >= 1, "row narrower than a sub-warp of 16-byte chunks");
-  const int lane = threadIdx.x & (SW - 1);
-  const unsigned mask = SW == 32 ? 0xffffffffu : (((1u << SW) - 1u) << (threadIdx.x & 31 & ~(SW - 1)));
-  const long long item = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / SW;
-  if (item >= n_items) return;
-  const long long nz0 = items[item].nz0, nz1 = items[item].nz1;
-  const int slot = (int)items[item].slot;
-  const Real *Al = A + lane * VEC;
-  const Real *Bl = B + lane * VEC;
-  __shared__ __align__(16) Real xsb[XS == 1 ? 2 : 1][XS == 1 ? 256 : 1];
-  __shared__ __align__(16) uint4 rsb[XS == 2 ? 2 : 1][XS == 2 ? 256 : 1];
-  const int wbase = threadIdx.x & ~(SW - 1);
-  int par = 0;
-  SR arow;
-  Real acc[E], facc[E];
-#pragma unroll
-  for (int k = 0; k < E; ++k) acc[k] = facc[k] = arow.v[k] = Real(0);
-  int cur_row = -1;
-  uint4 my = make_uint4(0u, 0u, 0u, 0u);
-  if (nz0 + lane < nz1) my = ld_stream_u4(nzm + nz0 + lane);
-  uint4 nx = make_uint4(0u, 0u, 0u, 0u);  // PF: metadata one batch ahead, rows prefetched
-  if constexpr (PF > 0) {
-    if (nz0 + SW + lane < nz1) nx = ld_stream_u4(nzm + nz0 + SW + lane);
-    prefetch_rows<Real, RT, PF>(my, nz0 + lane < nz1, A, B);
-  }
-  if (lane == 0) my.y |= kFiberStart | kRowStart;  // an item starts a row and a fiber
-  for (long long base = nz0; base < nz1; base += SW) {
-    uint4 nx2 = make_uint4(0u, 0u, 0u, 0u);
-    if constexpr (PF > 0) {
-      if (base + 2 * SW + lane < nz1) nx2 = ld_stream_u4(nzm + base + 2 * SW + lane);
-      prefetch_rows<Real, RT, PF>(nx, base + SW + lane < nz1, A, B);
-    } else {
-      nx = make_uint4(0u, 0u, 0u, 0u);  // lanes past the end must carry x = 0 and no flags
-      if (base + SW + lane < nz1) nx = ld_stream_u4(nzm + base + SW + lane);
-    }
-    // x of this lane's nonzero, converted once per batch (F2F runs on the narrow XU pipe:
-    // converting per nonzero in every lane of the worker made the fp64 kernel XU-bound)
-    const Real xl = (Real)__uint_as_float(my.z);
-    if constexpr (XS == 1) {
-      par ^= 1;
-      xsb[par][threadIdx.x] = xl;
-      __syncwarp(mask);
-    } else if constexpr (XS == 2) {
-      par ^= 1;
-      uint4 r;
-      r.x = my.y;
-      r.y = 0u;
-      if constexpr (sizeof(Real) == 8) {
-        r.z = (uint32_t)__double2loint((double)xl);
-        r.w = (uint32_t)__double2hiint((double)xl);
-      } else {
-        r.z = __float_as_uint((float)xl);
-        r.w = 0u;
-      }
-      rsb[par][threadIdx.x] = r;
-      __syncwarp(mask);
-    }
-    uint32_t fb[SW];
-    Real xr[D + 1];
-    SR bb[D + 1];
-    auto fetch = [&](int j) {  // b index + flags (and, XS == 2, x) of nonzero j of the batch
-      if constexpr (XS == 2) {
-        const uint4 r = rsb[par][wbase + j];
-        fb[j] = r.x;
-        if constexpr (sizeof(Real) == 8) xr[j % (D + 1)] = __hiloint2double((int)r.w, (int)r.z);
-        else xr[j % (D + 1)] = __uint_as_float(r.z);
-      } else {
-        fb[j] = __shfl_sync(mask, my.y, j, SW);
-      }
-    };
-#pragma unroll
-    for (int j = 0; j < D && j < SW; ++j) {
-      fetch(j);
-      bb[j % (D + 1)].load(Bl + (long long)(fb[j] & kIdxMask) * RT);
-    }
-#pragma unroll
-    for (int j = 0; j < SW; ++j) {
-      if (j + D < SW) {
-        fetch(j + D);
-        bb[(j + D) % (D + 1)].load(Bl + (long long)(fb[j + D] & kIdxMask) * RT);
-      }
-      Real x;
-      if constexpr (XS == 2) x = xr[j % (D + 1)];
-      else if constexpr (XS == 1) x = xsb[par][wbase + j];
-      else x = __shfl_sync(mask, xl, j, SW);
-      if (fb[j] & kFiberStart) {
-#pragma unroll
-        for (int k = 0; k < E; ++k) {  // close the previous fiber: acc += a * facc
-          acc[k] = fma(arow.v[k], facc[k], acc[k]);
-          facc[k] = Real(0);
-        }
-        if (fb[j] & kRowStart) {
-          if (slot >= 0) SR::store_from(partial + (long long)slot * RT + lane * VEC, acc);
-          else if (cur_row >= 0) SR::store_from(M + (long long)cur_row * RT + lane * VEC, acc);
-#pragma unroll
-          for (int k = 0; k < E; ++k) acc[k] = Real(0);
-          cur_row = (int)__shfl_sync(mask, my.w, j, SW);
-        }
-        arow.load(Al + (long long)(__shfl_sync(mask, my.x, j, SW) & kIdxMask) * RT);
-      }
-#pragma unroll
-      for (int k = 0; k < E; ++k) facc[k] = fma(x, bb[j % (D + 1)].v[k], facc[k]);
-    }
-    my = nx;
-    if constexpr (PF > 0) nx = nx2;
-  }
-#pragma unroll
-  for (int k = 0; k < E; ++k) acc[k] = fma(arow.v[k], facc[k], acc[k]);
-  if (slot >= 0) SR::store_from(partial + (long long)slot * RT + lane * VEC, acc);
-  else if (cur_row >= 0) SR::store_from(M + (long long)cur_row * RT + lane * VEC, acc);
-}
-
-// Support-skipping lean MTTKRP (exact).  Per nonzero, only the 16-byte chunks where both the
-// fiber's a-row and the nonzero's b-row are nonzero (chunk masks, k_chunk_mask) are gathered
-// and accumulated; a-rows are gathered only on their nonzero chunks.  Bitwise equal to the
-// dense kernels: a skipped b chunk is zero (x*0 adds an exact zero), and a column whose a
-// entry is zero only ever enters M as fma(0, facc, acc) = acc.  Lane l of a worker owns the
-// chunks k*SW + l, i.e. bit k*SW + l of a mask.  The masks of a batch's nonzeros are
-// gathered one batch ahead (lane l: masks of its nonzero's a- and b-rows).
-template <typename Real, int RT, int SW, int D, int MINB>
-__global__ void __launch_bounds__(256, MINB) k_mttkrp_skip(const WorkItem *__restrict__ items, long long n_items,
-                                                          const uint4 *__restrict__ nzm,
-                                                          const Real *__restrict__ A, const Real *__restrict__ B,
-                                                          const uint32_t *__restrict__ cmA,
-                                                          const uint32_t *__restrict__ cmB,
-                                                          Real *__restrict__ M, Real *__restrict__ partial) {
-  using SR = SubRow<Real, RT, SW>;
-  using VV = V16<Real>;
-  using VT = typename VV::T;
-  constexpr int E = SR::E;
-  constexpr int NV = SR::NV;
-  constexpr int VEC = VV::N;
-  static_assert(NV >= 1, "row narrower than a sub-warp of 16-byte chunks");
-  static_assert(RT / VEC <= 32, "chunk masks hold at most 32 chunks");
-  const int lane = threadIdx.x & (SW - 1);
-  const unsigned mask = SW == 32 ? 0xffffffffu : (((1u << SW) - 1u) << (threadIdx.x & 31 & ~(SW - 1)));
-  const long long item = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / SW;
-  if (item >= n_items) return;
-  const long long nz0 = items[item].nz0, nz1 = items[item].nz1;
-  const int slot = (int)items[item].slot;
-  const Real *Al = A + lane * VEC;
-  const Real *Bl = B + lane * VEC;
-  Real arow[E], acc[E], facc[E];
-#pragma unroll
-  for (int k = 0; k < E; ++k) acc[k] = facc[k] = arow[k] = Real(0);
-  uint32_t am_cur = 0;  // chunk mask of the current fiber's a-row
-  int cur_row = -1;
-  // batch t: metadata `my` and the combined / a masks of its nonzeros; batch t+1: `nx`
-  // (metadata) whose masks are gathered at the start of batch t; batch t+2: `nx2`.
-  uint4 my = make_uint4(0u, 0u, 0u, 0u), nx = make_uint4(0u, 0u, 0u, 0u);
-  if (nz0 + lane < nz1) my = ld_stream_u4(nzm + nz0 + lane);
-  if (nz0 + SW + lane < nz1) nx = ld_stream_u4(nzm + nz0 + SW + lane);
-  if (lane == 0) my.y |= kFiberStart | kRowStart;  // an item starts a row and a fiber
-  uint32_t my_am = 0, my_m = 0;
-  if (nz0 + lane < nz1) {
-    my_am = __ldg(cmA + (my.x & kIdxMask));
-    my_m = my_am & __ldg(cmB + (my.y & kIdxMask));
-  }
-  for (long long base = nz0; base < nz1; base += SW) {
-    uint4 nx2 = make_uint4(0u, 0u, 0u, 0u);
-    if (base + 2 * SW + lane < nz1) nx2 = ld_stream_u4(nzm + base + 2 * SW + lane);
-    uint32_t nx_am = 0, nx_m = 0;
-    if (base + SW + lane < nz1) {
-      nx_am = __ldg(cmA + (nx.x & kIdxMask));
-      nx_m = nx_am & __ldg(cmB + (nx.y & kIdxMask));
-    }
-    const Real xl = (Real)__uint_as_float(my.z);  // one XU conversion per lane per batch
-    uint32_t fb[SW], mb[SW];
-    Real bb[D + 1][E];
-    auto issue = [&](int j) {
-      fb[j] = __shfl_sync(mask, my.y, j, SW);
-      mb[j] = __shfl_sync(mask, my_m, j, SW);
-      const VT *p = reinterpret_cast<const VT *>(Bl + (long long)(fb[j] & kIdxMask) * RT);
-#pragma unroll
-      for (int k = 0; k < NV; ++k)
-        if ((mb[j] >> (k * SW + lane)) & 1u) VV::get(__ldg(p + k * SW), &bb[j % (D + 1)][k * VEC]);
-    };
-#pragma unroll
-    for (int j = 0; j < D && j < SW; ++j) issue(j);
-#pragma unroll
-    for (int j = 0; j < SW; ++j) {
-      if (j + D < SW) issue(j + D);
-      const Real x = __shfl_sync(mask, xl, j, SW);
-      if (fb[j] & kFiberStart) {
-#pragma unroll
-        for (int k = 0; k < NV; ++k) {  // close the previous fiber on its a-row's nonzero chunks
-          const bool on = (am_cur >> (k * SW + lane)) & 1u;
-#pragma unroll
-          for (int cc = 0; cc < VEC; ++cc) {
-            if (on) acc[k * VEC + cc] = fma(arow[k * VEC + cc], facc[k * VEC + cc], acc[k * VEC + cc]);
-            facc[k * VEC + cc] = Real(0);
-          }
-        }
-        if (fb[j] & kRowStart) {
-          if (slot >= 0) SR::store_from(partial + (long long)slot * RT + lane * VEC, acc);
-          else if (cur_row >= 0) SR::store_from(M + (long long)cur_row * RT + lane * VEC, acc);
-#pragma unroll
-          for (int k = 0; k < E; ++k) acc[k] = Real(0);
-          cur_row = (int)__shfl_sync(mask, my.w, j, SW);
-        }
-        am_cur = __shfl_sync(mask, my_am, j, SW);
-        const VT *p = reinterpret_cast<const VT *>(Al + (long long)(__shfl_sync(mask, my.x, j, SW) & kIdxMask) * RT);
-#pragma unroll
-        for (int k = 0; k < NV; ++k)
-          if ((am_cur >> (k * SW + lane)) & 1u) VV::get(__ldg(p + k * SW), &arow[k * VEC]);
-      }
-#pragma unroll
-      for (int k = 0; k < NV; ++k) {
-        if ((mb[j] >> (k * SW + lane)) & 1u) {
-#pragma unroll
-          for (int cc = 0; cc < VEC; ++cc)
-            facc[k * VEC + cc] = fma(x, bb[j % (D + 1)][k * VEC + cc], facc[k * VEC + cc]);
-        }
-      }
-    }
-    my = nx;
-    nx = nx2;
-    my_am = nx_am;
-    my_m = nx_m;
-  }
-#pragma unroll
-  for (int k = 0; k < NV; ++k) {
-    const bool on = (am_cur >> (k * SW + lane)) & 1u;
-#pragma unroll
-    for (int cc = 0; cc < VEC; ++cc)
-      if (on) acc[k * VEC + cc] = fma(arow[k * VEC + cc], facc[k * VEC + cc], acc[k * VEC + cc]);
-  }
-  if (slot >= 0) SR::store_from(partial + (long long)slot * RT + lane * VEC, acc);
-  else if (cur_row >= 0) SR::store_from(M + (long long)cur_row * RT + lane * VEC, acc);
-}
-
-// Heavy rows split across items: M_row = sum of the row's partial slots, in two levels so
-// that a row with thousands of slots (a 10%-of-nnz slice) is summed in parallel:
-//   level 1: one warp per FixChunk sums its <= kFixChunk slots (4 independent running sums
-//            over slots j = u mod 4, combined in u order) -> M[row] or a level-2 row;
-//   level 2: one warp per split row with several chunks sums its chunk rows in order.
-// Fixed orders throughout: deterministic.
-template <typename Real, int RT>
-__global__ void __launch_bounds__(256) k_fix1(const FixChunk *__restrict__ chunks, long long n,
-                                              const Real *__restrict__ partial, Real *__restrict__ buf,
-                                              Real *__restrict__ M) {
-  constexpr int CPL = RT >= 32 ? RT / 32 : 1;  // columns per lane: c = lane + 32 q
-  const int lane = threadIdx.x & 31;
-  const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (w >= n) return;
-  const FixChunk fc = chunks[w];
-  Real acc[4][CPL];
-#pragma unroll
-  for (int u = 0; u < 4; ++u)
-#pragma unroll
-    for (int q = 0; q < CPL; ++q) acc[u][q] = Real(0);
-  for (int j0 = 0; j0 < fc.nslots; j0 += 4) {
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      if (j0 + u < fc.nslots) {
-        const Real *p = partial + (fc.slot0 + j0 + u) * RT;
-#pragma unroll
-        for (int q = 0; q < CPL; ++q)
-          if (lane + 32 * q < RT) acc[u][q] += p[lane + 32 * q];
-      }
-    }
-  }
-  Real *dst = fc.out < 0 ? M + (long long)(-fc.out - 1) * RT : buf + (long long)fc.out * RT;
-#pragma unroll
-  for (int q = 0; q < CPL; ++q)
-    if (lane + 32 * q < RT) dst[lane + 32 * q] = (acc[0][q] + acc[1][q]) + (acc[2][q] + acc[3][q]);
-}
-
-template <typename Real, int RT>
-__global__ void __launch_bounds__(256) k_fix2(const SplitRow *__restrict__ splits, long long n,
-                                              const Real *__restrict__ buf, Real *__restrict__ M) {
-  constexpr int CPL = RT >= 32 ? RT / 32 : 1;
-  const int lane = threadIdx.x & 31;
-  const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (w >= n) return;
-  const SplitRow sr = splits[w];
-  const long long nch = (sr.nslots + kFixChunk - 1) / kFixChunk;
-  if (nch <= 1) return;  // written by level 1
-  Real acc[CPL];
-#pragma unroll
-  for (int q = 0; q < CPL; ++q) acc[q] = Real(0);
-  for (long long k = 0; k < nch; ++k) {
-    const Real *p = buf + (sr.chunk0 + k) * RT;
-#pragma unroll
-    for (int q = 0; q < CPL; ++q)
-      if (lane + 32 * q < RT) acc[q] += p[lane + 32 * q];
-  }
-#pragma unroll
-  for (int q = 0; q < CPL; ++q)
-    if (lane + 32 * q < RT) M[(long long)sr.row * RT + lane + 32 * q] = acc[q];
-}
-
-// ------------------------------------------------------------------ H, L and the branch
-// H = G_a * G_b (Eq 10), L = ||H||_F (Alg 1), branch by reading C10.
-template <typename Real, int RT>
-__global__ void __launch_bounds__(1024) k_prepare(int mode, int R, const double *__restrict__ Ga,
-                                                  const double *__restrict__ Gb, double *__restrict__ Hd,
-                                                  Real *__restrict__ Hr, DevState *st, int branch_override,
-                                                  int begin_sweep, int variant, int write_state) {
-  __shared__ double red[1024];
-  double ss = 0.0;
-  for (int x = threadIdx.x; x < RT * RT; x += blockDim.x) {
-    const int r = x / RT, t = x - (x / RT) * RT;
-    double h = 0.0;
-    if (r < R && t < R) {
-      h = Ga[r * R + t] * Gb[r * R + t];
-      Hd[r * R + t] = h;
-      ss += h * h;
-    }
-    Hr[x] = (Real)h;
-  }
-  red[threadIdx.x] = ss;
-  __syncthreads();
-  for (int o = 512; o > 0; o >>= 1) {
-    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0 && write_state) {
-    if (begin_sweep) st->k += 1;
-    int br;
-    if (branch_override >= 0) br = branch_override;
-    else if (variant == SACD_VARIANT_SELECT_OFF || st->nhist[mode] == 0) br = SACD_BR_FIRST;
-    else if (st->nhist[mode] == 1) br = SACD_BR_EQ24;
-    else br = (st->ti1[mode] > st->ti2[mode]) ? SACD_BR_EQ27 : SACD_BR_EQ24;
-    st->branch[mode] = br;
-    st->Lfrob[mode] = sqrt(red[0]);
-  }
-}
-
-// ------------------------------------------------------------------ fused row update
-// One thread per row (rows are independent given A and B: Eq ucap).  The block's
-// rows are staged in shared memory with an odd stride (RT+1) so the per-thread column
-// walk is bank-conflict free; H is staged in shared memory when it fits.
-template <typename Real, int RT, bool HS>
-__global__ void __launch_bounds__(rows_per_block<RT>())
-    k_sacd_rows(long long row_begin, long long row_end, int R, int mode, int l_mode,
-                const long long *__restrict__ row_ptr,
-                const Real *__restrict__ M, Real *__restrict__ F,
-                Real *__restrict__ Z, const Real *__restrict__ Hr, const DevState *__restrict__ st,
-                uint8_t *__restrict__ dec, double *__restrict__ ti_part, double *__restrict__ md_part,
-                long long *__restrict__ e_part, long long *__restrict__ ech_part, int vflags = 0,
-                Real *__restrict__ Zs = nullptr) {
-  // vflags (reading variants): 1 = JACOBI gradients from the rows at pass start
-  // (Lemma 2 literal); 2 = SCORE only (with 1: the snapshot z of every element into Zs, ti,
-  // no update); 4 = SNAP (Gauss-Seidel updates gated by the snapshot Zs, z_prev <- Zs)
-  const bool jac = vflags & 1, score = vflags & 2, snap = vflags & 4;
-  constexpr int TR = rows_per_block<RT>();
-  constexpr int US = RT + 1;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  Real *Hs = reinterpret_cast<Real *>(smem_raw);
-  Real *Us = reinterpret_cast<Real *>(smem_raw + (HS ? (size_t)RT * RT * sizeof(Real) : 0));
-  __shared__ double red_d[2][TR / 32];
-  __shared__ long long red_l[2][TR / 32];
-
-  const int tid = threadIdx.x;
-  const long long row0 = row_begin + (long long)blockIdx.x * TR;
-  const int nrows = (int)min((long long)TR, row_end - row0);
-  if (HS) {
-    constexpr int PER = 16 / (int)sizeof(Real);
-    for (int x = tid; x < RT * RT / PER; x += TR) cp_async<16>(Hs + PER * x, Hr + PER * x);
-  }
-  const Real *Fg = F + row0 * RT;
-  for (int x = tid; x < nrows * RT; x += TR) cp_async<(int)sizeof(Real)>(Us + (x / RT) * US + (x % RT), Fg + x);
-  cp_async_wait_all();
-  __syncthreads();
-  const Real *H = HS ? Hs : Hr;
-  const int branch = st->branch[mode];
-  const Real Lf = (Real)st->Lfrob[mode];
-
-  using VV = V16<Real>;
-  using VT = typename VV::T;
-  constexpr int VEC = VV::N;
-  constexpr int C = 8;  // column block: each u_j read from shared memory feeds C FMAs
-  double ti = 0.0, md = 0.0;
-  long long E = 0, Ech = 0;
-  // M is row-major (written by the MTTKRP as whole rows): each warp transposes the 32 x C
-  // block of its rows through a small shared tile, so global reads stay coalesced.
-  __shared__ Real Mst[TR / 32][32][C + 1];
-  const int lane = tid & 31, wp = tid >> 5;
-  const bool active = tid < nrows;
-  {
-    const long long row = row0 + tid;
-    Real *u = Us + tid * US;
-    const bool empty = active ? row_ptr[row] == row_ptr[row + 1] : true;  // empty slice: m = 0
-    Real *zp = Z + tt<RT>(active ? row : row0, 0);         // z_prev in the TT layout
-    Real *zsp = (score || snap) ? Zs + tt<RT>(active ? row : row0, 0) : nullptr;
-    for (int c0 = 0; c0 < R; c0 += C) {
-      __syncwarp();
-#pragma unroll
-      for (int k = 0; k < C; ++k) {
-        const int x = lane + 32 * k, rl = x / C, cl = x % C;
-        const long long rg = row0 + wp * 32 + rl;
-        Mst[wp][rl][cl] = (rg < row_end) ? M[rg * RT + c0 + cl] : Real(0);
-      }
-      __syncwarp();
-      if (!active) continue;
-      // (1) out-of-block part of the gradient with the current row (columns < c0 already
-      //     updated), Eq 14:  acc_q = sum_{j not in block} u_j h_(j, c0+q)   (H symmetric)
-      Real acc[C];
-#pragma unroll
-      for (int q = 0; q < C; ++q) acc[q] = Real(0);
-      auto accumulate = [&](int j) {
-        const Real uj = u[j];
-        const VT *hj = reinterpret_cast<const VT *>(H + j * RT + c0);
-#pragma unroll
-        for (int x = 0; x < C / VEC; ++x) {
-          Real hv[VEC];
-          VV::get(hj[x], hv);
-#pragma unroll
-          for (int y = 0; y < VEC; ++y) acc[x * VEC + y] = fma(uj, hv[y], acc[x * VEC + y]);
-        }
-      };
-#pragma unroll 4
-      for (int j = 0; j < c0; ++j) accumulate(j);
-#pragma unroll 4
-      for (int j = c0 + C; j < R; ++j) accumulate(j);
-      Real mv[C], zv[C], ub[C], zs[C];
-#pragma unroll
-      for (int q = 0; q < C; ++q) {
-        mv[q] = Mst[wp][lane][q];
-        zv[q] = score ? Real(0) : zp[32 * (c0 + q)];
-        zs[q] = snap ? zsp[32 * (c0 + q)] : Real(0);
-      }
-#pragma unroll
-      for (int q = 0; q < C; ++q) ub[q] = u[c0 + q];
-      if (empty) {
-#pragma unroll
-        for (int q = 0; q < C; ++q) mv[q] = Real(0);
-      }
-      // (2) Gauss-Seidel inside the block (C9): column r adds the in-block terms from the
-      //     CURRENT block values ub (never by subtracting old ones, so a gradient whose
-      //     other terms are exactly zero is computed exactly, as in the oracle).
-#pragma unroll
-      for (int q = 0; q < C; ++q) {
-        const int r = c0 + q;
-        if (r < R) {
-          const Real *Hr_ = H + r * RT;
-          const Real h = Hr_[r];
-          Real z = Real(0);
-          bool sel = false;
-          if (h != Real(0)) {
-            Real sg = acc[q];
-#pragma unroll
-            for (int qq = 0; qq < C; ++qq) sg = fma(jac ? u[c0 + qq] : ub[qq], Hr_[c0 + qq], sg);
-            const Real g = sg - mv[q];                     // Eq 14
-            const Real ur = ub[q];
-            const Real un = fmax(Real(0), ur - g / h);     // Eq 11-13
-            const Real d = un - ur;                        // Eq 12
-            const Real L = l_mode ? Lf : h;
-            z = -g * d - (L * Real(0.5)) * d * d;          // Eq 20
-            const Real zpr = zv[q];
-            const Real zg = snap ? zs[q] : z;  // the score the gate sees
-            sel = !score && ((branch == SACD_BR_FIRST) ? (zg > Real(0))
-                                                       : ((branch == SACD_BR_EQ24) ? (zg - zpr > Real(0))
-                                                                                   : (zpr - zg > Real(0))));
-            if (sel) {
-              ub[q] = un;
-              E += 1;
-              if (d != Real(0)) Ech += 1;
-            }
-          }
-          if (snap) z = zs[q];
-          zv[q] = z;                                       // z_prev <- z always (C8)
-          ti += (double)z;                                 // Eq 25
-          md += (double)ub[q] * (double)mv[q];
-          if (dec && !score) dec[row * R + r] = (uint8_t)sel;
-        }
-      }
-      if (score) {
-#pragma unroll
-        for (int q = 0; q < C; ++q) zsp[32 * (c0 + q)] = zv[q];
-        continue;
-      }
-      if (jac) {  // the staged rows keep the pass-start values; updates go straight to F
-#pragma unroll
-        for (int q = 0; q < C; ++q)
-          if (c0 + q < R) F[row * RT + c0 + q] = ub[q];
-      } else {
-#pragma unroll
-        for (int q = 0; q < C; ++q) u[c0 + q] = ub[q];
-      }
-#pragma unroll
-      for (int q = 0; q < C; ++q) zp[32 * (c0 + q)] = zv[q];
-    }
-  }
-  __syncthreads();
-  Real *Fo = F + row0 * RT;
-  if (!jac && !score)
-    for (int x = tid; x < nrows * RT; x += TR) Fo[x] = Us[(x / RT) * US + (x % RT)];
-
-  // fixed-order block reduction of (ti, md, E, Ech)
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    ti += __shfl_xor_sync(0xffffffffu, ti, o);
-    md += __shfl_xor_sync(0xffffffffu, md, o);
-    E += __shfl_xor_sync(0xffffffffu, E, o);
-    Ech += __shfl_xor_sync(0xffffffffu, Ech, o);
-  }
-  const int w = tid >> 5;
-  if ((tid & 31) == 0) {
-    red_d[0][w] = ti;
-    red_d[1][w] = md;
-    red_l[0][w] = E;
-    red_l[1][w] = Ech;
-  }
-  __syncthreads();
-  if (tid == 0) {
-    double a = 0.0, b = 0.0;
-    long long c = 0, d = 0;
-    for (int k = 0; k < TR / 32; ++k) {
-      a += red_d[0][k];
-      b += red_d[1][k];
-      c += red_l[0][k];
-      d += red_l[1][k];
-    }
-    ti_part[blockIdx.x] = a;
-    md_part[blockIdx.x] = b;
-    e_part[blockIdx.x] = c;
-    ech_part[blockIdx.x] = d;
-  }
-}
-
-// Fused row update with the out-of-block gradient on the fp64 tensor cores (Real = double,
-// RT <= 64).  Same semantics and per-row order of operations as k_sacd_rows: for column block
-// [c0, c0+8) the out-of-block part acc_q = sum_{j not in block} u_j h_(j,c0+q) of every row
-// of a warp (32 rows) is one (32 x RT) x (RT x 8) product of the CURRENT rows (columns < c0
-// already updated this pass, Gauss-Seidel C9) with H, issued as DMMA m8n8k4 (4 row tiles x
-// the k-steps outside the block, in ascending k); the in-block Gauss-Seidel step then runs
-// one thread per row exactly as in k_sacd_rows.  Fragments: A[m][k] = u[8mt+m][4kk+k] held
-// by lane (g = lane >> 2, t = lane & 3) as Us[8mt+g][4kk+t]; B[k][n] = H[4kk+k][c0+n] as
-// H[4kk+t][c0+g] (from L1: H is read-only and shared by every block); C[g][2t + {0,1}].
-// The accumulator tile and the block's M tile are transposed to one-row-per-thread through
-// a per-warp shared tile.  Shared memory: Us (rows x (RT+2), conflict-free for both the
-// fragment reads and the 16-byte row walks) + 32 x 18 doubles per warp.
-template <int RT, int WPB>
-__global__ void __launch_bounds__(WPB * 32)
-    k_sacd_rows_mma(long long row_begin, long long row_end, int R, int mode, int l_mode,
-                    const long long *__restrict__ row_ptr, const double *__restrict__ M, double *__restrict__ F,
-                    double *__restrict__ Z, const double *__restrict__ H, const DevState *__restrict__ st,
-                    uint8_t *__restrict__ dec, double *__restrict__ ti_part, double *__restrict__ md_part,
-                    long long *__restrict__ e_part, long long *__restrict__ ech_part) {
-  constexpr int TR = WPB * 32;
-  constexpr int US = RT + 2;
-  constexpr int C = 8;
-  constexpr int TS = 2 * C + 2;
-  constexpr int NKS = RT / 4;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  double *Us = reinterpret_cast<double *>(smem_raw);
-  double *Hd = Us + TR * US + WPB * 32 * TS;  // the 8 x 8 diagonal blocks of H: [RT/8][8][8]
-  __shared__ double red_d[2][WPB];
-  __shared__ long long red_l[2][WPB];
-
-  const int tid = threadIdx.x;
-  const int lane = tid & 31, wp = tid >> 5;
-  const int g = lane >> 2, t = lane & 3;
-  double *Tw = Us + TR * US + wp * 32 * TS;
-  const long long row0 = row_begin + (long long)blockIdx.x * TR;
-  const int nrows = (int)min((long long)TR, row_end - row0);
-  const double *Fg = F + row0 * RT;
-  static_assert(((RT + 2) * 8) % 16 == 0, "row stride must keep 16-byte chunks aligned");
-  for (int x = tid; x < TR * RT / 2; x += TR) {  // 16-byte chunks
-    const int r = (2 * x) / RT, col = (2 * x) % RT;
-    if (r < nrows) cp_async<16>(Us + r * US + col, Fg + 2 * x);
-    else *reinterpret_cast<double2 *>(Us + r * US + col) = make_double2(0.0, 0.0);
-  }
-  cp_async_wait_all();
-  for (int x = tid; x < RT * C; x += TR) {
-    const int b = x / (C * C), q = (x / C) % C, qq = x % C;
-    Hd[x] = H[(b * C + q) * RT + b * C + qq];
-  }
-  __syncthreads();
-  const int branch = st->branch[mode];
-  const double Lf = st->Lfrob[mode];
-  const int kmax = (R + 3) / 4;  // k-steps past R multiply zero padding
-
-  double ti = 0.0, md = 0.0;
-  long long E = 0, Ech = 0;
-  const bool active = tid < nrows;
-  const long long row = row0 + tid;
-  double *u = Us + tid * US;
-  const bool empty = active ? row_ptr[row] == row_ptr[row + 1] : true;  // empty slice: m = 0
-  double *zp = Z + tt<RT>(active ? row : row0, 0);
-  const double *Uw = Us + (wp * 32 + g) * US + t;
-
-  // software pipeline over column blocks: the B fragments, the M tile and this thread's
-  // z_prev of block c0 + 8 are loaded while block c0 is processed (all read-only here)
-  double bf[NKS], mt[C], zv[C];
-  auto load_block = [&](int c, double (&b)[NKS], double (&mm)[C], double (&zz)[C]) {
-    const int kb = c / 4;
-#pragma unroll
-    for (int kk = 0; kk < NKS; ++kk)
-      b[kk] = (kk == kb || kk == kb + 1 || kk >= kmax) ? 0.0 : __ldg(H + (4 * kk + t) * RT + c + g);
-#pragma unroll
-    for (int k = 0; k < C; ++k) {
-      const int x = lane + 32 * k, rl = x / C, cl = x % C;
-      const long long rg = row0 + wp * 32 + rl;
-      mm[k] = (rg < row_end) ? __ldg(M + rg * RT + c + cl) : 0.0;
-    }
-#pragma unroll
-    for (int q = 0; q < C; ++q) zz[q] = (active && c + q < RT) ? zp[32 * (c + q)] : 0.0;
-  };
-  load_block(0, bf, mt, zv);
-  for (int c0 = 0; c0 < R; c0 += C) {
-    double bfn[NKS], mtn[C], zvn[C];
-    if (c0 + C < R) load_block(c0 + C, bfn, mtn, zvn);
-    // (1) out-of-block gradient of the warp's 32 rows on the tensor cores: all k-steps
-    //     unrolled, the block's own k-steps (and those past R) with a zero B fragment (adding
-    //     0 * a leaves an accumulator unchanged); even / odd k-steps in two sets of tiles
-    double cacc[2][4][2];
-#pragma unroll
-    for (int h = 0; h < 2; ++h)
-#pragma unroll
-      for (int m = 0; m < 4; ++m) cacc[h][m][0] = cacc[h][m][1] = 0.0;
-#pragma unroll
-    for (int kk = 0; kk < NKS; ++kk) {
-#pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        const double a = Uw[8 * m * US + 4 * kk];
-        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                     : "+d"(cacc[kk & 1][m][0]), "+d"(cacc[kk & 1][m][1])
-                     : "d"(a), "d"(bf[kk]));
-      }
-    }
-    // (2) accumulators and the block's M tile to one row per thread
-#pragma unroll
-    for (int m = 0; m < 4; ++m) {
-      Tw[(8 * m + g) * TS + 2 * t] = cacc[0][m][0] + cacc[1][m][0];
-      Tw[(8 * m + g) * TS + 2 * t + 1] = cacc[0][m][1] + cacc[1][m][1];
-    }
-#pragma unroll
-    for (int k = 0; k < C; ++k) {
-      const int x = lane + 32 * k, rl = x / C, cl = x % C;
-      Tw[rl * TS + C + cl] = mt[k];
-    }
-    __syncwarp();
-    if (active) {
-      double acc[C], mv[C], ub[C];
-#pragma unroll
-      for (int q = 0; q < C; ++q) {
-        acc[q] = Tw[lane * TS + q];
-        mv[q] = empty ? 0.0 : Tw[lane * TS + C + q];
-        ub[q] = u[c0 + q];
-      }
-      const double *Hb = Hd + (c0 / C) * C * C;
-      // (3) in-block Gauss-Seidel (C9), as k_sacd_rows
-#pragma unroll
-      for (int q = 0; q < C; ++q) {
-        const int r = c0 + q;
-        if (r < R) {
-          const double h = Hb[q * C + q];
-          double z = 0.0;
-          bool sel = false;
-          if (h != 0.0) {
-            double sg = acc[q];
-#pragma unroll
-            for (int qq = 0; qq < C; ++qq) sg = fma(ub[qq], Hb[q * C + qq], sg);
-            const double gr = sg - mv[q];                  // Eq 14
-            const double ur = ub[q];
-            const double un = fmax(0.0, ur - gr / h);      // Eq 11-13
-            const double d = un - ur;                      // Eq 12
-            const double L = l_mode ? Lf : h;
-            z = -gr * d - (L * 0.5) * d * d;               // Eq 20
-            const double zpr = zv[q];
-            sel = (branch == SACD_BR_FIRST) ? (z > 0.0)
-                                            : ((branch == SACD_BR_EQ24) ? (z - zpr > 0.0) : (zpr - z > 0.0));
-            if (sel) {
-              ub[q] = un;
-              E += 1;
-              if (d != 0.0) Ech += 1;
-            }
-          }
-          zv[q] = z;                                       // z_prev <- z always (C8)
-          ti += z;                                         // Eq 25
-          md += ub[q] * mv[q];
-          if (dec) dec[row * R + r] = (uint8_t)sel;
-        }
-      }
-#pragma unroll
-      for (int q = 0; q < C; ++q) u[c0 + q] = ub[q];
-#pragma unroll
-      for (int q = 0; q < C; ++q) zp[32 * (c0 + q)] = zv[q];
-    }
-    __syncwarp();  // the updated block columns feed the next block's fragments; Tw is reused
-#pragma unroll
-    for (int kk = 0; kk < NKS; ++kk) bf[kk] = bfn[kk];
-#pragma unroll
-    for (int q = 0; q < C; ++q) {
-      mt[q] = mtn[q];
-      zv[q] = zvn[q];
-    }
-  }
-  __syncthreads();
-  double *Fo = F + row0 * RT;
-  for (int x = tid; x < nrows * RT; x += TR) Fo[x] = Us[(x / RT) * US + (x % RT)];
-
-  // fixed-order block reduction of (ti, md, E, Ech)
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    ti += __shfl_xor_sync(0xffffffffu, ti, o);
-    md += __shfl_xor_sync(0xffffffffu, md, o);
-    E += __shfl_xor_sync(0xffffffffu, E, o);
-    Ech += __shfl_xor_sync(0xffffffffu, Ech, o);
-  }
-  if (lane == 0) {
-    red_d[0][wp] = ti;
-    red_d[1][wp] = md;
-    red_l[0][wp] = E;
-    red_l[1][wp] = Ech;
-  }
-  __syncthreads();
-  if (tid == 0) {
-    double a = 0.0, b = 0.0;
-    long long c = 0, d = 0;
-    for (int k = 0; k < WPB; ++k) {
-      a += red_d[0][k];
-      b += red_d[1][k];
-      c += red_l[0][k];
-      d += red_l[1][k];
-    }
-    ti_part[blockIdx.x] = a;
-    md_part[blockIdx.x] = b;
-    e_part[blockIdx.x] = c;
-    ech_part[blockIdx.x] = d;
-  }
-}
-
-// The same row update for R > 64 (fp64): one warp (32 rows) per block; the B fragments of
-// a column block (R/4 k-steps) are loaded 16 k-steps at a time, the next chunk in flight
-// while the current one feeds the DMMAs; the in-block H values come from L1.  The FMA
-// kernel this replaces waited on one L2 round trip of H per 4 gradient terms.
-template <int RT>
-__global__ void __launch_bounds__(32)
-    k_sacd_rows_mma_big(long long row_begin, long long row_end, int R, int mode, int l_mode,
-                        const long long *__restrict__ row_ptr, const double *__restrict__ M, double *__restrict__ F,
-                        double *__restrict__ Z, const double *__restrict__ H, const DevState *__restrict__ st,
-                        uint8_t *__restrict__ dec, double *__restrict__ ti_part, double *__restrict__ md_part,
-                        long long *__restrict__ e_part, long long *__restrict__ ech_part) {
-  constexpr int US = RT + 2;
-  constexpr int C = 8;
-  constexpr int TS = 2 * C + 2;
-  constexpr int KC = 16;  // k-steps per B-fragment chunk
-  static_assert(RT % (4 * KC) == 0, "R pitch must be a multiple of 64");
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  double *Us = reinterpret_cast<double *>(smem_raw);
-  double *Tw = Us + 32 * US;
-  const int lane = threadIdx.x;
-  const int g = lane >> 2, t = lane & 3;
-  const long long row0 = row_begin + (long long)blockIdx.x * 32;
-  const int nrows = (int)min(32LL, row_end - row0);
-  const double *Fg = F + row0 * RT;
-  static_assert(((RT + 2) * 8) % 16 == 0, "row stride must keep 16-byte chunks aligned");
-  for (int x = lane; x < 32 * RT / 2; x += 32) {
-    const int r = (2 * x) / RT, col = (2 * x) % RT;
-    if (r < nrows) cp_async<16>(Us + r * US + col, Fg + 2 * x);
-    else *reinterpret_cast<double2 *>(Us + r * US + col) = make_double2(0.0, 0.0);
-  }
-  cp_async_wait_all();
-  __syncwarp();
-  const int branch = st->branch[mode];
-  const double Lf = st->Lfrob[mode];
-  const int kmax = (R + 3) / 4;
-
-  double ti = 0.0, md = 0.0;
-  long long E = 0, Ech = 0;
-  const bool active = lane < nrows;
-  const long long row = row0 + lane;
-  double *u = Us + lane * US;
-  const bool empty = active ? row_ptr[row] == row_ptr[row + 1] : true;
-  double *zp = Z + tt<RT>(active ? row : row0, 0);
-  const double *Uw = Us + g * US + t;
-  for (int c0 = 0; c0 < R; c0 += C) {
-    const int kb = c0 / 4;
-    double mt[C], zv[C];
-#pragma unroll
-    for (int k = 0; k < C; ++k) {
-      const int x = lane + 32 * k, rl = x / C, cl = x % C;
-      const long long rg = row0 + rl;
-      mt[k] = (rg < row_end) ? __ldg(M + rg * RT + c0 + cl) : 0.0;
-    }
-#pragma unroll
-    for (int q = 0; q < C; ++q) zv[q] = active ? zp[32 * (c0 + q)] : 0.0;
-    double cacc[2][4][2];
-#pragma unroll
-    for (int h = 0; h < 2; ++h)
-#pragma unroll
-      for (int m = 0; m < 4; ++m) cacc[h][m][0] = cacc[h][m][1] = 0.0;
-    auto load_chunk = [&](int k0, double (&b)[KC]) {
-#pragma unroll
-      for (int j = 0; j < KC; ++j) {
-        const int kk = k0 + j;
-        b[j] = (kk == kb || kk == kb + 1 || kk >= kmax) ? 0.0 : __ldg(H + (4 * kk + t) * RT + c0 + g);
-      }
-    };
-    double bc[KC], bn[KC];
-    load_chunk(0, bc);
-    for (int k0 = 0; k0 < kmax; k0 += KC) {
-      if (k0 + KC < kmax) load_chunk(k0 + KC, bn);
-#pragma unroll
-      for (int j = 0; j < KC; ++j) {
-#pragma unroll
-        for (int m = 0; m < 4; ++m) {
-          const double a = Uw[8 * m * US + 4 * (k0 + j)];
-          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                       : "+d"(cacc[j & 1][m][0]), "+d"(cacc[j & 1][m][1])
-                       : "d"(a), "d"(bc[j]));
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < KC; ++j) bc[j] = bn[j];
-    }
-#pragma unroll
-    for (int m = 0; m < 4; ++m) {
-      Tw[(8 * m + g) * TS + 2 * t] = cacc[0][m][0] + cacc[1][m][0];
-      Tw[(8 * m + g) * TS + 2 * t + 1] = cacc[0][m][1] + cacc[1][m][1];
-    }
-#pragma unroll
-    for (int k = 0; k < C; ++k) {
-      const int x = lane + 32 * k, rl = x / C, cl = x % C;
-      Tw[rl * TS + C + cl] = mt[k];
-    }
-    __syncwarp();
-    if (active) {
-      double acc[C], mv[C], ub[C];
-#pragma unroll
-      for (int q = 0; q < C; ++q) {
-        acc[q] = Tw[lane * TS + q];
-        mv[q] = empty ? 0.0 : Tw[lane * TS + C + q];
-        ub[q] = u[c0 + q];
-      }
-#pragma unroll
-      for (int q = 0; q < C; ++q) {
-        const int r = c0 + q;
-        if (r < R) {
-          const double *Hr_ = H + (long long)r * RT + c0;
-          const double h = __ldg(Hr_ + q);
-          double z = 0.0;
-          bool sel = false;
-          if (h != 0.0) {
-            double sg = acc[q];
-#pragma unroll
-            for (int qq = 0; qq < C; ++qq) sg = fma(ub[qq], __ldg(Hr_ + qq), sg);
-            const double gr = sg - mv[q];                  // Eq 14
-            const double ur = ub[q];
-            const double un = fmax(0.0, ur - gr / h);      // Eq 11-13
-            const double d = un - ur;                      // Eq 12
-            const double L = l_mode ? Lf : h;
-            z = -gr * d - (L * 0.5) * d * d;               // Eq 20
-            const double zpr = zv[q];
-            sel = (branch == SACD_BR_FIRST) ? (z > 0.0)
-                                            : ((branch == SACD_BR_EQ24) ? (z - zpr > 0.0) : (zpr - z > 0.0));
-            if (sel) {
-              ub[q] = un;
-              E += 1;
-              if (d != 0.0) Ech += 1;
-            }
-          }
-          zv[q] = z;
-          ti += z;
-          md += ub[q] * mv[q];
-          if (dec) dec[row * R + r] = (uint8_t)sel;
-        }
-      }
-#pragma unroll
-      for (int q = 0; q < C; ++q) u[c0 + q] = ub[q];
-#pragma unroll
-      for (int q = 0; q < C; ++q) zp[32 * (c0 + q)] = zv[q];
-    }
-    __syncwarp();
-  }
-  double *Fo = F + row0 * RT;
-  for (int x = lane; x < nrows * RT; x += 32) Fo[x] = Us[(x / RT) * US + (x % RT)];
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    ti += __shfl_xor_sync(0xffffffffu, ti, o);
-    md += __shfl_xor_sync(0xffffffffu, md, o);
-    E += __shfl_xor_sync(0xffffffffu, E, o);
-    Ech += __shfl_xor_sync(0xffffffffu, Ech, o);
-  }
-  if (lane == 0) {
-    ti_part[blockIdx.x] = ti;
-    md_part[blockIdx.x] = md;
-    e_part[blockIdx.x] = E;
-    ech_part[blockIdx.x] = Ech;
-  }
-}
-
-template <int RT>
-__host__ __device__ constexpr size_t rows_mma_big_smem_bytes() {
-  return (size_t)32 * (RT + 2) * 8 + (size_t)32 * 18 * 8;
-}
-
-template <int RT, int WPB>
-__host__ __device__ constexpr size_t rows_mma_smem_bytes() {
-  return (size_t)WPB * 32 * (RT + 2) * 8 + (size_t)WPB * 32 * 18 * 8 + (size_t)RT * 8 * 8;
-}
-
-// sum_r F_ir M_ir per row block (initial objective f^0)
-template <typename Real, int RT>
-__global__ void k_fm_dot(long long row_begin, long long row_end, int R, const long long *__restrict__ row_ptr,
-                         const Real *__restrict__ F,
-                         const Real *__restrict__ M,
-                         double *__restrict__ ti_part, double *__restrict__ md_part, long long *__restrict__ e_part,
-                         long long *__restrict__ ech_part) {
-  constexpr int TR = rows_per_block<RT>();
-  __shared__ double red[TR];
-  const long long row = row_begin + (long long)blockIdx.x * TR + threadIdx.x;
-  double s = 0.0;
-  if (row < row_end && row_ptr[row] != row_ptr[row + 1])
-    for (int r = 0; r < R; ++r) s += (double)F[row * RT + r] * (double)M[row * RT + r];
-  red[threadIdx.x] = s;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double a = 0.0;
-    for (int k = 0; k < TR; ++k) a += red[k];
-    md_part[blockIdx.x] = a;
-    ti_part[blockIdx.x] = 0.0;
-    e_part[blockIdx.x] = 0;
-    ech_part[blockIdx.x] = 0;
-  }
-}
-
-// ------------------------------------------------------------------ Gram G = F^T F (fp64)
-// Fixed grid: blockIdx.x = a contiguous row range, blockIdx.y = a pair (bi <= bj) of GT-wide
-// column panels (one pair unless R > 128).  Each thread owns a T x T tile; inside a
-// diagonal panel pair only tiles with ty <= tx work.  Partials are reduced in block order.
-template <int RT>
-__host__ __device__ constexpr int gram_gt() {
-  return RT < 128 ? RT : 128;
-}
-
-template <typename Real, int RT>
-__global__ void __launch_bounds__(gram_tg<gram_gt<RT>()>() * gram_tg<gram_gt<RT>()>())
-    k_gram_partial(long long row_begin, long long row_end, int R, const Real *__restrict__ F,
-                   double *__restrict__ part) {
-  // Thread (ty, tx) of a TG x TG grid owns entries (bi*GT + ty + TG*a, bj*GT + tx + TG*b),
-  // a, b < T: for a fixed staged row the warp reads TG consecutive values (conflict-free)
-  // and a few broadcast ones.  A diagonal panel pair also computes its lower half
-  // (redundant); the reduce reads the (min, max) entry.
-  constexpr int GT = gram_gt<RT>();
-  constexpr int TG = gram_tg<GT>();
-  constexpr int T = GT / TG;
-  constexpr int CH = GT >= 128 ? 16 : 32;
-  __shared__ double Fa[CH][GT + 1];
-  __shared__ double Fb[CH][GT + 1];
-  constexpr int NB = RT / GT;
-  int bi = 0, bj = 0;
-  {
-    int y = blockIdx.y;
-    for (int a = 0; a < NB; ++a) {
-      if (y < NB - a) {
-        bi = a;
-        bj = a + y;
-        break;
-      }
-      y -= NB - a;
-    }
-  }
-  const int tid = threadIdx.x;
-  const int ty = tid / TG, tx = tid % TG;
-  const long long per = (row_end - row_begin + gridDim.x - 1) / gridDim.x;
-  const long long i0 = row_begin + (long long)blockIdx.x * per;
-  const long long i1 = min(row_end, i0 + per);
-  double acc[T][T];
-#pragma unroll
-  for (int a = 0; a < T; ++a)
-#pragma unroll
-    for (int b = 0; b < T; ++b) acc[a][b] = 0.0;
-  for (long long c0 = i0; c0 < i1; c0 += CH) {
-    const int nr = (int)min((long long)CH, i1 - c0);
-    __syncthreads();
-    for (int x = tid; x < nr * GT; x += TG * TG) {
-      const int k = x / GT, col = x % GT;
-      Fa[k][col] = (double)F[(c0 + k) * RT + bi * GT + col];
-      Fb[k][col] = (double)F[(c0 + k) * RT + bj * GT + col];
-    }
-    __syncthreads();
-    for (int k = 0; k < nr; ++k) {
-      double av[T], bv[T];
-#pragma unroll
-      for (int a = 0; a < T; ++a) av[a] = Fa[k][ty + TG * a];
-#pragma unroll
-      for (int b = 0; b < T; ++b) bv[b] = Fb[k][tx + TG * b];
-#pragma unroll
-      for (int a = 0; a < T; ++a)
-#pragma unroll
-        for (int b = 0; b < T; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
-    }
-  }
-  double *p = part + (long long)blockIdx.x * R * R;
-#pragma unroll
-  for (int a = 0; a < T; ++a)
-#pragma unroll
-    for (int b = 0; b < T; ++b) {
-      const int r = bi * GT + ty + TG * a, t = bj * GT + tx + TG * b;
-      if (r < R && t < R) p[r * R + t] = acc[a][b];
-    }
-}
-
-// fp64 Gram on the tensor cores (DMMA, mma.sync m8n8k4 f64): G = F^T F as a GEMM with
-// M = N = RT (columns) and K = rows.  blockIdx.x = a contiguous row range (as
-// k_gram_partial), blockIdx.y = an upper-triangle pair (qi <= qj) of 32-column panels; the
-// 4 warps of a block take 4 contiguous sub-ranges of the rows (multiples of 4), each lane
-// holding a 32 x 32 quadrant as 4 x 4 m8n8 tiles, and the warps' quadrants are summed in
-// warp order through shared memory.  Fragments (PTX m8n8k4 .f64): A[m][k] = F[i0+k][r0+m]
-// is held by lane (g = lane >> 2, t = lane & 3) as F[i0+t][r0+g]; B[k][n] = F[i0+k][c0+n]
-// as F[i0+t][c0+g]; C[g][2t + {0,1}].  Same partial contract as k_gram_partial (entries
-// r <= t of every panel pair are written; the reduce reads those).
-template <int RT>
-__global__ void __launch_bounds__(128) k_gram_dmma(long long row_begin, long long row_end, int R,
-                                                   const double *__restrict__ F, double *__restrict__ part) {
-  constexpr int NP = RT / 32;
-  int qi = 0, qj = 0;
-  {
-    int y = blockIdx.y;
-    for (int a = 0; a < NP; ++a) {
-      if (y < NP - a) {
-        qi = a;
-        qj = a + y;
-        break;
-      }
-      y -= NP - a;
-    }
-  }
-  __shared__ double red[3][32 * 32];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int g = lane >> 2, t = lane & 3;
-  const long long per = (row_end - row_begin + gridDim.x - 1) / gridDim.x;
-  const long long b0 = row_begin + (long long)blockIdx.x * per;
-  const long long b1 = min(row_end, b0 + per);
-  const long long wper = ((b1 - b0 + 3) / 4 + 3) / 4 * 4;  // rows per warp, multiple of 4
-  const long long i0 = min(b1, b0 + w * wper), i1 = min(b1, i0 + wper);
-  double acc[4][4][2];
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-  const double *Fa = F + qi * 32 + g;
-  const double *Fb = F + qj * 32 + g;
-  for (long long r0 = i0; r0 < i1; r0 += 8) {
-    double av[2][4], bv[2][4];
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const long long row = r0 + 4 * h + t;
-      const bool ok = row < i1;
-#pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        av[h][m] = ok ? __ldg(Fa + row * RT + 8 * m) : 0.0;
-        bv[h][m] = ok ? __ldg(Fb + row * RT + 8 * m) : 0.0;
-      }
-    }
-#pragma unroll
-    for (int h = 0; h < 2; ++h)
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b)
-          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                       : "+d"(acc[a][b][0]), "+d"(acc[a][b][1])
-                       : "d"(av[h][a]), "d"(bv[h][b]));
-  }
-  // fixed-order sum of the 4 warps' quadrants
-  if (w > 0) {
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-      for (int b = 0; b < 4; ++b)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) red[w - 1][(8 * a + g) * 32 + 8 * b + 2 * t + e] = acc[a][b][e];
-  }
-  __syncthreads();
-  if (w == 0) {
-    double *p = part + (long long)blockIdx.x * R * R;
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-      for (int b = 0; b < 4; ++b)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int x = (8 * a + g) * 32 + 8 * b + 2 * t + e;
-          const double v = ((acc[a][b][e] + red[0][x]) + red[1][x]) + red[2][x];
-          const int r = qi * 32 + 8 * a + g, c = qj * 32 + 8 * b + 2 * t + e;
-          if (r < R && c < R && (qi < qj || r <= c)) p[r * R + c] = v;
-        }
-  }
-}
-
-// G[r][t] = sum over blocks (in order) of the upper-triangle partial; mirrored exactly.
-__global__ void k_gram_reduce(int R, int nblk, const double *__restrict__ part, double *__restrict__ G) {
-  const int x = blockIdx.x * blockDim.x + threadIdx.x;
-  if (x >= R * R) return;
-  const int r = x / R, t = x % R;
-  const int src = (r <= t) ? (r * R + t) : (t * R + r);
-  // (an entry with r <= t lies in panel pair (r/GT, t/GT) with bi <= bj, which wrote it)
-  double s = 0.0;
-  for (int b = 0; b < nblk; ++b) s += part[(long long)b * R * R + src];
-  G[x] = s;
-}
-
-// ------------------------------------------------------------------ finalize a mode pass
-// flags: 1 = record the pass (ti/E/history), 2 = compute f (needs all three Grams),
-//        4 = push a stats-ring record (end of sweep)
-// Record a finished pass in the device state (thread 0 only).
-// flags: 1 = record the pass (ti/E/history), 2 = compute f, 4 = push a stats-ring record.
-__device__ void apply_pass(DevState *st, int mode, double ti, double md, long long E, long long Ech, double mn,
-                           int flags) {
-  if (flags & 1) {
-    st->ti_cur[mode] = ti;
-    st->E[mode] = E;
-    st->Ech[mode] = Ech;
-    st->ti2[mode] = st->ti1[mode];
-    st->ti1[mode] = ti;
-    st->nhist[mode] += 1;
-  }
-  if (mode == 2) st->mdot = md;
-  if (flags & 2) {
-    const double f = st->xnorm2 - 2.0 * md + mn;
-    st->f = f;
-    st->fit = st->xnorm2 > 0.0 ? 1.0 - sqrt(f > 0.0 ? f : 0.0) / sqrt(st->xnorm2) : 0.0;
-  }
-  if (flags & 4) {
-    sacd_iter_stats &rec = st->ring[st->ring_count % kRing];
-    rec.k = st->k;
-    rec.objective = st->f;
-    rec.fit = st->fit;
-    for (int n = 0; n < 3; ++n) {
-      rec.branch[n] = st->branch[n];
-      rec.ti[n] = st->ti_cur[n];
-      rec.E[n] = st->E[n];
-      rec.E_changed[n] = st->Ech[n];
-    }
-    st->ring_count += 1;
-  }
-}
-
-// Fixed-order reduction of the per-block partials of a pass.  flags as apply_pass, plus
-// 8 = local: write (ti, md, E, Ech) to local_out[0..3] and leave the state alone (sharded).
-__global__ void __launch_bounds__(1024) k_finalize(int mode, long long nblk, const double *__restrict__ ti_part,
-                                                   const double *__restrict__ md_part,
-                                                   const long long *__restrict__ e_part,
-                                                   const long long *__restrict__ ech_part, const double *G0,
-                                                   const double *G1, const double *G2, int R, DevState *st,
-                                                   int flags, double *local_out) {
-  __shared__ double sd[3][1024];
-  __shared__ long long sl[2][1024];
-  const int tid = threadIdx.x;
-  double ti = 0.0, md = 0.0, mn = 0.0;
-  long long E = 0, Ech = 0;
-  for (long long b = tid; b < nblk; b += 1024) {
-    ti += ti_part[b];
-    md += md_part[b];
-    E += e_part[b];
-    Ech += ech_part[b];
-  }
-  if ((flags & 2) && !(flags & 8))
-    for (int x = tid; x < R * R; x += 1024) mn += G0[x] * G1[x] * G2[x];
-  sd[0][tid] = ti;
-  sd[1][tid] = md;
-  sd[2][tid] = mn;
-  sl[0][tid] = E;
-  sl[1][tid] = Ech;
-  __syncthreads();
-  for (int o = 512; o > 0; o >>= 1) {
-    if (tid < o) {
-      sd[0][tid] += sd[0][tid + o];
-      sd[1][tid] += sd[1][tid + o];
-      sd[2][tid] += sd[2][tid + o];
-      sl[0][tid] += sl[0][tid + o];
-      sl[1][tid] += sl[1][tid + o];
-    }
-    __syncthreads();
-  }
-  if (tid == 0) {
-    if (flags & 8) {
-      local_out[0] = sd[0][0];
-      local_out[1] = sd[1][0];
-      local_out[2] = (double)sl[0][0];
-      local_out[3] = (double)sl[1][0];
-    } else {
-      apply_pass(st, mode, sd[0][0], sd[1][0], sl[0][0], sl[1][0], sd[2][0], flags);
-    }
-  }
-}
-
-// ------------------------------------------------------------------ delta exchange
-// Changed elements of F over [lo, hi) (element indices of the padded row-major factor),
-// compared bit for bit against Fold (so a +0 / -0 flip is sent too and every replica stays
-// bitwise identical).  Two passes over a fixed grid of kDeltaBlocks contiguous chunks: count,
-// then write in index order (warp ballots + block prefix), so the lists are deterministic.
-template <typename Real>
-__device__ __forceinline__ bool elem_changed(const Real *F, const Real *Fo, long long i) {
-  if constexpr (sizeof(Real) == 8)
-    return __double_as_longlong(F[i]) != __double_as_longlong(Fo[i]);
-  else
-    return __float_as_uint(F[i]) != __float_as_uint(Fo[i]);
-}
-
-template <typename Real>
-__global__ void __launch_bounds__(256) k_delta_count(long long lo, long long hi, const Real *__restrict__ F,
-                                                     const Real *__restrict__ Fo, int *__restrict__ blk) {
-  __shared__ int red[8];
-  const long long per = (hi - lo + gridDim.x - 1) / gridDim.x;
-  const long long b0 = lo + (long long)blockIdx.x * per, b1 = min(hi, b0 + per);
-  int n = 0;
-  for (long long i = b0 + threadIdx.x; i < b1; i += blockDim.x) n += elem_changed(F, Fo, i);
-  for (int o = 16; o > 0; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = n;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int t = 0;
-    for (int w = 0; w < 8; ++w) t += red[w];
-    blk[blockIdx.x] = t;
-  }
-}
-
-template <typename Real>
-__global__ void __launch_bounds__(256) k_delta_write(long long lo, long long hi, const Real *__restrict__ F,
-                                                     const Real *__restrict__ Fo, const int *__restrict__ blk,
-                                                     uint32_t *__restrict__ idx, Real *__restrict__ val,
-                                                     long long *__restrict__ count) {
-  __shared__ int wcnt[8];
-  __shared__ long long base_s;
-  const long long per = (hi - lo + gridDim.x - 1) / gridDim.x;
-  const long long b0 = lo + (long long)blockIdx.x * per, b1 = min(hi, b0 + per);
-  if (threadIdx.x == 0) {
-    long long b = 0;
-    for (int k = 0; k < (int)blockIdx.x; ++k) b += blk[k];
-    base_s = b;
-    if (blockIdx.x == gridDim.x - 1) *count = b + blk[blockIdx.x];
-  }
-  __syncthreads();
-  long long base = base_s;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (long long t0 = b0; t0 < b1; t0 += blockDim.x) {
-    const long long i = t0 + threadIdx.x;
-    const bool ch = i < b1 && elem_changed(F, Fo, i);
-    const unsigned bal = __ballot_sync(0xffffffffu, ch);
-    if (lane == 0) wcnt[w] = __popc(bal);
-    __syncthreads();
-    int before = 0, tot = 0;
-    for (int k = 0; k < 8; ++k) {
-      before += k < w ? wcnt[k] : 0;
-      tot += wcnt[k];
-    }
-    if (ch) {
-      const long long o = base + before + __popc(bal & ((1u << lane) - 1u));
-      idx[o] = (uint32_t)i;
-      val[o] = F[i];
-    }
-    base += tot;
-    __syncthreads();
-  }
-}
-
-template <typename Real>
-__global__ void k_delta_apply(const uint32_t *__restrict__ idx, const Real *__restrict__ val,
-                              const long long *__restrict__ count, Real *__restrict__ F) {
-  const long long n = *count;
-  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x)
-    F[idx[k]] = val[k];
-}
-
-// Snapshot variant (reading C10'): ti^k = fixed-order sum of the score pass's block partials
-// (the same tree as k_finalize, so the recorded ti equals it bitwise); the branch of THIS
-// pass: k == 1 (no history) the z > 0 rule, else Eq 27 iff ti^k > ti^{k-1}.
-__global__ void __launch_bounds__(1024) k_snapshot_branch(int mode, long long nblk, const double *__restrict__ ti_part,
-                                                          DevState *st, int branch_override) {
-  __shared__ double sd[1024];
-  const int tid = threadIdx.x;
-  double ti = 0.0;
-  for (long long b = tid; b < nblk; b += 1024) ti += ti_part[b];
-  sd[tid] = ti;
-  __syncthreads();
-  for (int o = 512; o > 0; o >>= 1) {
-    if (tid < o) sd[tid] += sd[tid + o];
-    __syncthreads();
-  }
-  if (tid == 0) {
-    int br;
-    if (branch_override >= 0) br = branch_override;
-    else if (st->nhist[mode] == 0) br = SACD_BR_FIRST;
-    else br = (sd[0] > st->ti1[mode]) ? SACD_BR_EQ27 : SACD_BR_EQ24;
-    st->branch[mode] = br;
-  }
-}
-
-// ------------------------------------------------------------------ sharded-engine kernels
-// Every rank q writes its head row id / partial row into slot q of the exchange buffers
-// and its (ti, md, E, Ech, Gram partial) into slot q of the stats buffer; NCCL all-gathers
-// them in place (or, with emulated ranks on one GPU, they are already all local).
-template <typename Real, int RT>
-__global__ void k_pack_head(long long head, const Real *__restrict__ M, long long *__restrict__ id_slot,
-                            Real *__restrict__ row_slot) {
-  for (int c = threadIdx.x; c < RT; c += blockDim.x) row_slot[c] = head >= 0 ? M[head * RT + c] : Real(0);
-  if (threadIdx.x == 0) *id_slot = head;
-}
-
-template <typename Real, int RT>
-__global__ void k_copy_rows_tt(long long rlo, long long rhi, const Real *__restrict__ src, Real *__restrict__ dst) {
-  for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < (rhi - rlo) * RT;
-       x += (long long)gridDim.x * blockDim.x) {
-    const long long i = rlo + x / RT;
-    const int c = (int)(x % RT);
-    dst[i * RT + c] = src[i * RT + c];
-  }
-}
-
-// The owner adds the head partials of the other ranks to its rows, in rank order.
-template <typename Real, int RT>
-__global__ void k_merge_heads(int G, long long rlo, long long rhi, const long long *__restrict__ ids,
-                              const Real *__restrict__ rows, Real *__restrict__ M) {
-  for (int q = 0; q < G; ++q) {
-    const long long id = ids[q];
-    if (id >= rlo && id < rhi)
-      for (int c = threadIdx.x; c < RT; c += blockDim.x) M[id * RT + c] += rows[(long long)q * RT + c];
-  }
-}
-
-// Sum the G ranks' slots in rank order: Gram (if flags & 32) and (ti, md, E, Ech); then
-// apply the pass to the device state.  stats slot layout: [ti, md, E, Ech, Gram R x R].
-__global__ void __launch_bounds__(1024) k_finalize_global(int mode, int G, int R, const double *__restrict__ stats,
-                                                          double *Gout, const double *G0, const double *G1,
-                                                          const double *G2, DevState *st, int flags) {
-  __shared__ double red[1024];
-  const int tid = threadIdx.x;
-  const long long slot = 4 + (long long)R * R;
-  if (flags & 32) {
-    for (int x = tid; x < R * R; x += 1024) {
-      double s = 0.0;
-      for (int q = 0; q < G; ++q) s += stats[q * slot + 4 + x];
-      Gout[x] = s;
-    }
-    __syncthreads();
-  }
-  double mn = 0.0;
-  if (flags & 2)
-    for (int x = tid; x < R * R; x += 1024) mn += G0[x] * G1[x] * G2[x];
-  red[tid] = mn;
-  __syncthreads();
-  for (int o = 512; o > 0; o >>= 1) {
-    if (tid < o) red[tid] += red[tid + o];
-    __syncthreads();
-  }
-  if (tid == 0) {
-    double ti = 0.0, md = 0.0, E = 0.0, Ech = 0.0;
-    for (int q = 0; q < G; ++q) {
-      ti += stats[q * slot + 0];
-      md += stats[q * slot + 1];
-      E += stats[q * slot + 2];
-      Ech += stats[q * slot + 3];
-    }
-    apply_pass(st, mode, ti, md, (long long)E, (long long)Ech, red[0], flags & 7);
-  }
-}
-
-// host-order fp64 (rows x R) <-> device Real (row-major with pitch RT, or TT tiles)
-__device__ __forceinline__ long long dev_index(long long i, int r, int RT, bool ttl) {
-  return ttl ? (i >> 5) * (32LL * RT) + (long long)r * 32 + (i & 31) : i * RT + r;
-}
-
-template <typename Real>
-__global__ void k_convert_in(const double *__restrict__ src, long long rows, int R, int RT, Real *__restrict__ dst,
-                             bool ttl) {
-  for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < rows * RT;
-       x += (long long)gridDim.x * blockDim.x) {
-    const long long i = x / RT;
-    const int r = (int)(x - i * RT);
-    dst[dev_index(i, r, RT, ttl)] = r < R ? (Real)src[i * R + r] : Real(0);
-  }
-}
-
-template <typename Real>
-__global__ void k_convert_out(const Real *__restrict__ src, long long rows, int R, int RT, double *__restrict__ dst,
-                              bool ttl) {
-  for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < rows * R;
-       x += (long long)gridDim.x * blockDim.x) {
-    const long long i = x / R;
-    const int r = (int)(x - i * R);
-    dst[x] = (double)src[dev_index(i, r, RT, ttl)];
-  }
-}
-
-
-// ------------------------------------------------------------------ held-out evaluation
-// Eq 8 at test coordinates: one warp per entry, lane l multiplies columns
-// l, l+32, ... and the warp sums them by a fixed xor tree.  With vals != nullptr also the
-// squared error (Eq 30), reduced per block in a fixed order into part[block].
-template <typename Real, int RT>
-__global__ void __launch_bounds__(256) k_predict(const uint32_t *__restrict__ coords, long long n,
-                                                 const Real *__restrict__ U, const Real *__restrict__ V,
-                                                 const Real *__restrict__ W, const float *__restrict__ vals,
-                                                 double *__restrict__ out, double *__restrict__ part) {
-  constexpr int CPL = RT >= 32 ? RT / 32 : 1;
-  __shared__ double red[8];
-  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
-  const long long e = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  double se = 0.0;
-  if (e < n) {
-    const long long q = coords[3 * e], p = coords[3 * e + 1], s = coords[3 * e + 2];
-    double xh = 0.0;
-#pragma unroll
-    for (int k = 0; k < CPL; ++k) {
-      const int c = lane + 32 * k;
-      if (c < RT) xh += (double)U[q * RT + c] * (double)V[p * RT + c] * (double)W[s * RT + c];
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) xh += __shfl_xor_sync(0xffffffffu, xh, o);
-    if (lane == 0) {
-      if (out) out[e] = xh;
-      if (vals) {
-        const double d = (double)vals[e] - xh;
-        se = d * d;
-      }
-    }
-  }
-  if (part) {
-    if (lane == 0) red[wp] = se;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double t = 0.0;
-      for (int k = 0; k < 8; ++k) t += red[k];
-      part[blockIdx.x] = t;
-    }
-  }
-}
-
-__global__ void k_range_check(const uint32_t *__restrict__ coords, long long n, long long d0, long long d1,
-                              long long d2, int *__restrict__ flag) {
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x)
-    if (coords[3 * e] >= d0 || coords[3 * e + 1] >= d1 || coords[3 * e + 2] >= d2) atomicOr(flag, 1);
-}
-
-// fixed-order sum of the block partials (one block)
-__global__ void __launch_bounds__(1024) k_sum_parts(const double *__restrict__ part, long long nb,
-                                                    double *__restrict__ out) {
-  __shared__ double sd[1024];
-  double t = 0.0;
-  for (long long b = threadIdx.x; b < nb; b += 1024) t += part[b];
-  sd[threadIdx.x] = t;
-  __syncthreads();
-  for (int o = 512; o > 0; o >>= 1) {
-    if (threadIdx.x < o) sd[threadIdx.x] += sd[threadIdx.x + o];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) *out = sd[0];
-}
+#include "k_mttkrp.inc.cuh"
+#include "k_rows.inc.cuh"
+#include "k_gram.inc.cuh"
+#include "k_pass.inc.cuh"
 
 // ------------------------------------------------------------------ launch implementations
 template <typename Real, int RT>
