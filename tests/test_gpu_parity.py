@@ -332,6 +332,41 @@ def test_reading_variants_rejected_by_sharded_engine():
             S(c.numpy(), v.numpy(), cfg.dims, cfg.rank, cfg.seed, variant=variant, emulate_ranks=2)
 
 
+def test_c2_full_iteration_count_parity():
+    """c2 at its BASELINE iteration count (50 sweeps) against the oracle: f per sweep, factors,
+    branch and E, plus the invariants (f non-increasing, factors >= 0, E <= I R)."""
+    cfg = SI.CONFIGS["c2"]
+    c, v = SI.make_tensor(cfg)
+    c, v = c.numpy(), v.numpy()
+    fg, Fg, Eg, brg, ora = run_pair(c, v, cfg.dims, cfg.rank, cfg.seed, cfg.iters)
+    check_pair(fg, Fg, Eg, brg, ora)
+    assert np.array_equal(Eg, ora["E"])
+    assert (np.diff(fg) <= 1e-12 * fg[0]).all()
+    for n in range(3):
+        assert (Fg[n] >= 0).all() and (Eg[:, n] <= cfg.dims[n] * cfg.rank).all()
+
+
+def test_c3_full_iteration_count_properties():
+    """c3 for its 50 sweeps on the GPU alone: f non-increasing (Lemma 3 under reading C9),
+    factors >= 0, E <= I R, and the final f equal to the sparse-explicit objective of the
+    returned factors (oracle, Eq 6-7)."""
+    cfg = SI.CONFIGS["c3"]
+    c, v = SI.make_tensor(cfg)
+    c, v = c.numpy(), v.numpy()
+    with S(c, v, cfg.dims, cfg.rank, cfg.seed) as g:
+        f0 = g.fit()[0]
+        g.iterate(cfg.iters)
+        st = g.stats()
+        F = g.factors()
+    f = np.array([f0] + [s["objective"] for s in st])
+    assert (np.diff(f) <= 1e-12 * f[0]).all()
+    for n in range(3):
+        assert (F[n] >= 0).all()
+        assert all(s["E"][n] <= cfg.dims[n] * cfg.rank for s in st)
+    fs = O.objective_sparse(c, v, cfg.dims, F)
+    assert abs(f[-1] - fs) <= 1e-9 * fs
+
+
 def test_end_to_end_c2_10_sweeps():
     cfg = SI.CONFIGS["c2"]
     c, v = SI.make_tensor(cfg)
