@@ -406,19 +406,17 @@ __device__ __forceinline__ void prefetch_rows(const uint4 &m, bool valid, const 
 // shuffles (1 for the b index, 2 for x in fp64), 1 = x through a shared-memory broadcast
 // (one wavefront instead of two shuffles), 2 = the b index and x as one 16-byte
 // shared-memory broadcast per nonzero.
-template <typename Real, int RT, int SW, int D, int MINB, int PF = 0, int XS = 0>
-__global__ void __launch_bounds__(256, MINB) k_mttkrp_lean(const WorkItem *__restrict__ items, long long n_items,
-                                                          const uint4 *__restrict__ nzm,
-                                                          const Real *__restrict__ A, const Real *__restrict__ B,
-                                                          Real *__restrict__ M, Real *__restrict__ partial) {
+template <typename Real, int RT, int SW, int D, int PF, int XS>
+__device__ __forceinline__ void lean_item(long long item, const WorkItem *__restrict__ items,
+                                          const uint4 *__restrict__ nzm, const Real *__restrict__ A,
+                                          const Real *__restrict__ B, Real *__restrict__ M,
+                                          Real *__restrict__ partial) {
   using SR = SubRow<Real, RT, SW>;
   constexpr int E = SR::E;
   constexpr int VEC = V16<Real>::N;
   static_assert(SR::NV >= 1, "row narrower than a sub-warp of 16-byte chunks");
   const int lane = threadIdx.x & (SW - 1);
   const unsigned mask = SW == 32 ? 0xffffffffu : (((1u << SW) - 1u) << (threadIdx.x & 31 & ~(SW - 1)));
-  const long long item = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / SW;
-  if (item >= n_items) return;
   const long long nz0 = items[item].nz0, nz1 = items[item].nz1;
   const int slot = (int)items[item].slot;
   const Real *Al = A + lane * VEC;
@@ -524,6 +522,37 @@ __global__ void __launch_bounds__(256, MINB) k_mttkrp_lean(const WorkItem *__res
   for (int k = 0; k < E; ++k) acc[k] = fma(arow.v[k], facc[k], acc[k]);
   if (slot >= 0) SR::store_from(partial + (long long)slot * RT + lane * VEC, acc);
   else if (cur_row >= 0) SR::store_from(M + (long long)cur_row * RT + lane * VEC, acc);
+}
+
+template <typename Real, int RT, int SW, int D, int MINB, int PF = 0, int XS = 0>
+__global__ void __launch_bounds__(256, MINB) k_mttkrp_lean(const WorkItem *__restrict__ items, long long n_items,
+                                                          const uint4 *__restrict__ nzm,
+                                                          const Real *__restrict__ A, const Real *__restrict__ B,
+                                                          Real *__restrict__ M, Real *__restrict__ partial) {
+  const long long item = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / SW;
+  if (item >= n_items) return;
+  lean_item<Real, RT, SW, D, PF, XS>(item, items, nzm, A, B, M, partial);
+}
+
+// Dynamic scheduling (one worker per warp): a fixed grid of resident warps takes items from
+// a device counter (reset to 0 before the launch), so no launch ends on a partly-filled
+// last wave -- that tail grew to ~50% of a sharded rank's MTTKRP, whose launch covers only
+// about 2 waves of items.  Results do not depend on which warp takes which item.
+template <typename Real, int RT, int D, int MINB, int PF = 0, int XS = 0>
+__global__ void __launch_bounds__(256, MINB) k_mttkrp_lean_dyn(const WorkItem *__restrict__ items, long long n_items,
+                                                              const uint4 *__restrict__ nzm,
+                                                              const Real *__restrict__ A, const Real *__restrict__ B,
+                                                              Real *__restrict__ M, Real *__restrict__ partial,
+                                                              unsigned long long *__restrict__ counter) {
+  const int lane = threadIdx.x & 31;
+  for (;;) {
+    unsigned long long it = 0;
+    if (lane == 0) it = atomicAdd(counter, 1ull);
+    it = __shfl_sync(0xffffffffu, it, 0);
+    if ((long long)it >= n_items) break;
+    __syncwarp();  // the warp's shared broadcast slots may still be read for its previous item
+    lean_item<Real, RT, 32, D, PF, XS>((long long)it, items, nzm, A, B, M, partial);
+  }
 }
 
 // Support-skipping lean MTTKRP (exact).  Per nonzero, only the 16-byte chunks where both the

@@ -147,6 +147,22 @@ struct Impl {
                      reinterpret_cast<Real *>(c.partial));
   }
 
+  // the dynamically scheduled lean kernel (one worker per warp): a grid of resident blocks
+  // only, items from c.item_ctr (reset here, stream-ordered)
+  template <int D, int MINB, int XS>
+  static void launch_dyn(Context &c, const WorkItem *items, long long n_items, const uint4 *nzm, const Real *A,
+                         const Real *B, Real *out, Real *partial) {
+    int per_sm = 0;
+    auto kern = k_mttkrp_lean_dyn<Real, RT, D, MINB, 0, XS>;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0);
+    if (per_sm < 1) per_sm = 1;
+    const long long need = (n_items * 32 + 255) / 256;
+    const long long grid = std::min<long long>(need, (long long)per_sm * c.num_sms);
+    cudaMemsetAsync(c.item_ctr, 0, sizeof(unsigned long long), c.stream);
+    kern<<<(unsigned)std::max<long long>(1, grid), 256, 0, c.stream>>>(items, n_items, nzm, A, B, out, partial,
+                                                                       c.item_ctr);
+  }
+
   static int mttkrp_on(Context &c, int mode, const WorkItem *items, long long n_items, const SplitRow *splits,
                        long long n_splits, const FixChunk *chunks, long long n_chunks, Real *out, Real *partial) {
     ModeData &md = c.m[mode];
@@ -224,6 +240,11 @@ struct Impl {
           else if (var == 34) gol(k_mttkrp_lean<Real, RT, sub_warp_lanes<Real, RT>(), 2, 5, 0, 2>, sub_warp_lanes<Real, RT>());
           else if (var == 35) gol(k_mttkrp_lean<Real, RT, sub_warp_lanes<Real, RT>(), 1, 6, 0, 1>, sub_warp_lanes<Real, RT>());
           else if (var == 36) gol(k_mttkrp_lean<Real, RT, SW8, 1, 2, 0, 1>, SW8);
+          else if (var == 39) {
+            if constexpr (sizeof(Real) == 8 && RT == 64) launch_dyn<1, 6, 1>(c, items, n_items, md.nzm, A, B, out, partial);
+            if constexpr (sizeof(Real) == 8 && RT == 128) launch_dyn<1, 3, 1>(c, items, n_items, md.nzm, A, B, out, partial);
+            if constexpr (sizeof(Real) == 8 && RT == 256) launch_dyn<1, 2, 1>(c, items, n_items, md.nzm, A, B, out, partial);
+          }
           else if (var == 40) gol(k_mttkrp_lean<Real, RT, sub_warp_lanes<Real, RT>(), 1, 6>, sub_warp_lanes<Real, RT>());
           else if (var == 41) gol(k_mttkrp_lean<Real, RT, sub_warp_lanes<Real, RT>(), 1, 5>, sub_warp_lanes<Real, RT>());
           else if (var == 42) gol(k_mttkrp_lean<Real, RT, sub_warp_lanes<Real, RT>(), 2, 5>, sub_warp_lanes<Real, RT>());
@@ -235,10 +256,8 @@ struct Impl {
           // fp64, R > 128: one warp per item, 8 fp64 columns per lane, x broadcast through
           // shared memory (variant 36; c5 R=256: 12.7 ms per sweep vs 13.7 with shuffles,
           // variant 22, and 28.6 for the warp fiber kernel, variant 1)
-          constexpr int SWW = RT / 8 > 32 ? 32 : RT / 8;
-          const long long lb = (n_items * SWW + 255) / 256;
-          k_mttkrp_lean<Real, RT, SWW, 1, 2, 0, 1><<<(unsigned)lb, 256, 0, c.stream>>>(items, n_items, md.nzm, A, B,
-                                                                                      out, partial);
+          // Dynamically scheduled (items from a counter; c5 R=256 12.6 vs 13.1 ms, variant 39).
+          if constexpr (sizeof(Real) == 8 && RT == 256) launch_dyn<1, 2, 1>(c, items, n_items, md.nzm, A, B, out, partial);
         } else if (sizeof(Real) == 8 && (RT == 64 || (RT == 32 && md.n_fibers > 0 && c.nnz >= 2 * md.n_fibers))) {
           // fp64, R = 33..64 (and R = 17..32 with a mean fiber length >= 2, the Zipf config
           // c3): one warp per item (2 fp64 columns per lane at R = 64) at 48 registers / 40
@@ -247,21 +266,24 @@ struct Impl {
           // instead of two shuffles on the L1-data-path-bound kernel; variant 30: c4 12.11 vs
           // 13.66 ms, c5 R=64 4.02 vs 4.42); with two workers per warp (R = 32) the b index
           // and x go as one 16-byte broadcast (XS = 2; variant 31: c3 1.195 vs 1.227 ms).
-          if constexpr (sizeof(Real) == 8 && (RT == 64 || RT == 32)) {
+          if constexpr (sizeof(Real) == 8 && RT == 64) {
+            // R = 64: 40 registers / 48 warps per SM (variant 35: c4 11.75 vs 12.11 ms), dynamically
+            // scheduled from a work counter (variant 39: c4 11.06, c5 R=64 3.29 vs 3.82 ms; a
+            // sharded rank's launch covers only ~2 waves of items, where the static grid lost
+            // up to a third to the last wave)
+            launch_dyn<1, 6, 1>(c, items, n_items, md.nzm, A, B, out, partial);
+          } else if constexpr (sizeof(Real) == 8 && RT == 32) {
             constexpr int SWF = sub_warp_lanes<Real, RT>();
             const long long lb = (n_items * SWF + 255) / 256;
-            // R = 64: 40 registers / 48 warps per SM (variant 35: c4 11.75 vs 12.11 ms, c5 R=64
-            // 3.82 vs 4.02; small spills at the batch boundary)
-            k_mttkrp_lean<Real, RT, SWF, 1, SWF == 32 ? 6 : 5, 0, SWF == 32 ? 1 : 2><<<(unsigned)lb, 256, 0, c.stream>>>(
-                items, n_items, md.nzm, A, B, out, partial);
+            k_mttkrp_lean<Real, RT, SWF, 1, 5, 0, 2><<<(unsigned)lb, 256, 0, c.stream>>>(items, n_items, md.nzm, A, B,
+                                                                                        out, partial);
           }
         } else if (sizeof(Real) == 8 && RT == 128) {
           // fp64, R = 65..128: 4 columns per lane, one warp per item, x broadcast through shared
           // memory (variant 32: c5 R=128 6.54 vs 6.95 ms, c4 R=128 21.5 vs 26.0 ms per sweep)
           if constexpr (sizeof(Real) == 8 && RT == 128) {
-            const long long lb = (n_items * 32 + 255) / 256;
-            k_mttkrp_lean<Real, RT, 32, 1, 3, 0, 1><<<(unsigned)lb, 256, 0, c.stream>>>(items, n_items, md.nzm, A,
-                                                                                       B, out, partial);
+            // dynamically scheduled (variant 39: c5 R=128 6.38 vs 6.58, c4 R=128 18.8 vs 21.6 ms)
+            launch_dyn<1, 3, 1>(c, items, n_items, md.nzm, A, B, out, partial);
           }
         } else {
           // default (measured on B200, tools/mttkrp_tune.py): the lean sub-warp kernel with

@@ -157,6 +157,8 @@ struct Context {
   // scratch
   void *M = nullptr;              // Real[ceil32(maxI) * pitch] (TT layout)
   void *Zs = nullptr;             // Real[ceil32(maxI) * pitch] snapshot z of a pass (SNAPSHOT variant)
+  unsigned long long *item_ctr = nullptr;  // work counter of the dynamically scheduled MTTKRP
+  int num_sms = 0;
   void *partial = nullptr;        // Real[max slots * pitch]
   void *fixbuf = nullptr;         // Real[max chunks * pitch] (level-2 fix-up rows)
   void *Hr = nullptr;             // Real[pitch * pitch]
