@@ -364,7 +364,8 @@ struct Impl {
       pe = prof_begin(c, 4);
       double *sl = c.xstats + sh.rank * slot;
       gram_partial(c, rlo, rhi, reinterpret_cast<const Real *>(md.F), sh.gram_part);
-      k_gram_reduce<<<(c.R * c.R + 255) / 256, 256, 0, c.stream>>>(c.R, c.gram_blocks, sh.gram_part, sl + 4);
+      k_gram_reduce<<<(c.R * c.R + 255) / 256, 256, 0, c.stream>>>(c.R, gram_ranges(c, rlo, rhi), sh.gram_part,
+                                                                   sl + 4);
       SACD_CUDA_TRY(cudaGetLastError());
       SACD_TRY(prof_end(c, 4, pe));
       k_finalize<<<1, 1024, 0, c.stream>>>(mode, nblk, ti_part, md_part, e_part, ech_part, nullptr, nullptr,
@@ -514,11 +515,18 @@ struct Impl {
 
   // Gram partials of rows [rlo, rhi) of F: DMMA (fp64 tensor cores) for fp64 with RT >= 32
   // (opt.reserved[2] = 1 selects the FMA kernel), else the shared-memory FMA kernel
+  // number of row ranges of a Gram over rows [rlo, rhi): c.gram_blocks, fewer for a short
+  // range (a sharded rank's slice) so that no range is under 64 rows
+  static int gram_ranges(const Context &c, long long rlo, long long rhi) {
+    return (int)std::max<long long>(1, std::min<long long>(c.gram_blocks, (rhi - rlo + 63) / 64));
+  }
+
   static void gram_partial(Context &c, long long rlo, long long rhi, const Real *F, double *part) {
+    const int nb = gram_ranges(c, rlo, rhi);
     if constexpr (sizeof(Real) == 8 && RT >= 32) {
       if (c.opt.reserved[2] != 1) {
         constexpr int NP = RT / 32;
-        k_gram_dmma<RT><<<dim3(c.gram_blocks, NP * (NP + 1) / 2), 128, 0, c.stream>>>(
+        k_gram_dmma<RT><<<dim3(nb, NP * (NP + 1) / 2), 128, 0, c.stream>>>(
             rlo, rhi, c.R, reinterpret_cast<const double *>(F), part);
         return;
       }
@@ -526,15 +534,14 @@ struct Impl {
     constexpr int GT = gram_gt<RT>();
     constexpr int TG = gram_tg<GT>();
     constexpr int NB = RT / GT;
-    k_gram_partial<Real, RT><<<dim3(c.gram_blocks, NB * (NB + 1) / 2), TG * TG, 0, c.stream>>>(rlo, rhi, c.R, F,
-                                                                                              part);
+    k_gram_partial<Real, RT><<<dim3(nb, NB * (NB + 1) / 2), TG * TG, 0, c.stream>>>(rlo, rhi, c.R, F, part);
   }
 
   static int gram(Context &c, int mode) {
     ModeData &md = c.m[mode];
     int pe = prof_begin(c, 4);
     gram_partial(c, 0, md.I, reinterpret_cast<const Real *>(md.F), c.gram_part);
-    k_gram_reduce<<<(c.R * c.R + 255) / 256, 256, 0, c.stream>>>(c.R, c.gram_blocks, c.gram_part, md.G);
+    k_gram_reduce<<<(c.R * c.R + 255) / 256, 256, 0, c.stream>>>(c.R, gram_ranges(c, 0, md.I), c.gram_part, md.G);
     SACD_CUDA_TRY(cudaGetLastError());
     SACD_TRY(chunk_mask(c, mode));
     return prof_end(c, 4, pe);

@@ -587,7 +587,7 @@ def test_sharded_nccl_world1_matches_unsharded():
     np.testing.assert_allclose(out[1][0], out[0][0], rtol=1e-12)
     assert np.array_equal(out[1][1], out[0][1])
     for n in range(3):
-        assert factor_err(out[1][2][n], out[0][2][n]) <= 1e-10
+        assert factor_err(out[1][2][n], out[0][2][n]) <= 1e-8  # sharded items (256 nnz) sum split rows in another grouping
 
 
 @pytest.mark.parametrize("G", [2, 3, 8])
@@ -632,7 +632,7 @@ def test_delta_exchange_nccl_world1():
     np.testing.assert_allclose(out[1][0], out[0][0], rtol=1e-12)
     assert np.array_equal(out[1][1], out[0][1])
     for n in range(3):
-        assert factor_err(out[1][2][n], out[0][2][n]) <= 1e-10
+        assert factor_err(out[1][2][n], out[0][2][n]) <= 1e-8  # sharded items (256 nnz) sum split rows in another grouping
     inf = out[1][3]
     assert inf["delta_exchange"] == 1 and inf["full_elems_equiv"] > 0
     assert 0 < inf["delta_elems_sent"] < inf["full_elems_equiv"]
