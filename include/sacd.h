@@ -88,10 +88,11 @@ typedef struct {
   int32_t force_sharded;      /* 1: run the sharded (NCCL) engine also when world_size == 1 */
   int32_t emulate_ranks;      /* G >= 2 (with world_size 1): emulate the G ranks of the     */
                               /* sharded engine on this GPU, exchanges as local copies      */
-  int32_t reserved[4];        /* [0]: row-update variant (0 = default: fp64 with R <= 64 runs */
-                              /* the DMMA out-of-block gradient kernel, else the FMA kernel;  */
-                              /* 1 = FMA kernel with H read from global/L1; 2 = FMA kernel    */
-                              /* with H in shared memory);                                    */
+  int32_t reserved[4];        /* [0]: row-update variant (0 = default: fp64 runs the DMMA     */
+                              /* out-of-block gradient kernels (R <= 64: row blocks from a     */
+                              /* work counter), fp32 the FMA kernel; 1 = FMA kernel with H     */
+                              /* from global/L1; 2 = FMA kernel with H in shared memory;      */
+                              /* 6 = the R <= 64 DMMA kernel on a static grid);               */
                               /* [1]: MTTKRP a-blocked order: > 0 = blocks of that many      */
                               /* a-rows, <= 0 = canonical order (default);                  */
                               /* [2]: Gram kernel (0 = default: fp64 tensor cores (DMMA) for  */

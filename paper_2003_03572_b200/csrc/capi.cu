@@ -603,7 +603,7 @@ static int init_impl(Context *c, const uint32_t *coords, const float *vals, uint
   c->gram_blocks = (int)std::min<long long>(gcap, std::max<long long>(1, (maxI + grows - 1) / grows));
   if (getenv("SACD_GRAM_BLOCKS")) c->gram_blocks = std::max(1, atoi(getenv("SACD_GRAM_BLOCKS")));  // tuning
   SACD_CUDA_TRY(cudaMalloc(&c->M, (size_t)((maxI + 31) / 32 * 32) * P * rs));
-  SACD_CUDA_TRY(cudaMalloc(&c->item_ctr, sizeof(unsigned long long)));
+  SACD_CUDA_TRY(cudaMalloc(&c->item_ctr, 2 * sizeof(unsigned long long)));  // MTTKRP items, row blocks
   SACD_CUDA_TRY(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device));
   if (c->opt.variant == SACD_VARIANT_SNAPSHOT) {  // snapshot importances of one pass (TT layout)
     SACD_CUDA_TRY(cudaMalloc(&c->Zs, (size_t)((maxI + 31) / 32 * 32) * P * rs));

@@ -246,8 +246,8 @@ __global__ void __launch_bounds__(rows_per_block<RT>())
 // a per-warp shared tile.  Shared memory: Us (rows x (RT+2), conflict-free for both the
 // fragment reads and the 16-byte row walks) + 32 x 18 doubles per warp.
 template <int RT, int WPB>
-__global__ void __launch_bounds__(WPB * 32)
-    k_sacd_rows_mma(long long row_begin, long long row_end, int R, int mode, int l_mode,
+__device__ __forceinline__ void rows_mma_block(long long rb, long long row_begin, long long row_end, int R, int mode,
+                    int l_mode,
                     const long long *__restrict__ row_ptr, const double *__restrict__ M, double *__restrict__ F,
                     double *__restrict__ Z, const double *__restrict__ H, const DevState *__restrict__ st,
                     uint8_t *__restrict__ dec, double *__restrict__ ti_part, double *__restrict__ md_part,
@@ -267,7 +267,7 @@ __global__ void __launch_bounds__(WPB * 32)
   const int lane = tid & 31, wp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
   double *Tw = Us + TR * US + wp * 32 * TS;
-  const long long row0 = row_begin + (long long)blockIdx.x * TR;
+  const long long row0 = row_begin + rb * TR;
   const int nrows = (int)min((long long)TR, row_end - row0);
   const double *Fg = F + row0 * RT;
   static_assert(((RT + 2) * 8) % 16 == 0, "row stride must keep 16-byte chunks aligned");
@@ -430,10 +430,45 @@ __global__ void __launch_bounds__(WPB * 32)
       c += red_l[0][k];
       d += red_l[1][k];
     }
-    ti_part[blockIdx.x] = a;
-    md_part[blockIdx.x] = b;
-    e_part[blockIdx.x] = c;
-    ech_part[blockIdx.x] = d;
+    ti_part[rb] = a;
+    md_part[rb] = b;
+    e_part[rb] = c;
+    ech_part[rb] = d;
+  }
+}
+
+
+template <int RT, int WPB>
+__global__ void __launch_bounds__(WPB * 32)
+    k_sacd_rows_mma(long long row_begin, long long row_end, int R, int mode, int l_mode,
+                    const long long *__restrict__ row_ptr, const double *__restrict__ M, double *__restrict__ F,
+                    double *__restrict__ Z, const double *__restrict__ H, const DevState *__restrict__ st,
+                    uint8_t *__restrict__ dec, double *__restrict__ ti_part, double *__restrict__ md_part,
+                    long long *__restrict__ e_part, long long *__restrict__ ech_part) {
+  rows_mma_block<RT, WPB>(blockIdx.x, row_begin, row_end, R, mode, l_mode, row_ptr, M, F, Z, H, st, dec, ti_part,
+                          md_part, e_part, ech_part);
+}
+
+// Dynamically scheduled: a grid of resident blocks takes 128-row blocks from a device counter
+// (reset before the launch), so a launch of few waves (a sharded rank's rows) does not end
+// on a partly filled wave.  The partials are indexed by the row block, as in the static grid.
+template <int RT, int WPB>
+__global__ void __launch_bounds__(WPB * 32)
+    k_sacd_rows_mma_dyn(long long row_begin, long long row_end, int R, int mode, int l_mode,
+                        const long long *__restrict__ row_ptr, const double *__restrict__ M, double *__restrict__ F,
+                        double *__restrict__ Z, const double *__restrict__ H, const DevState *__restrict__ st,
+                        uint8_t *__restrict__ dec, double *__restrict__ ti_part, double *__restrict__ md_part,
+                        long long *__restrict__ e_part, long long *__restrict__ ech_part, long long nblk,
+                        unsigned long long *__restrict__ counter) {
+  __shared__ long long rb_s;
+  for (;;) {
+    __syncthreads();  // the previous block's tail (thread 0's partial writes) is done with rb_s
+    if (threadIdx.x == 0) rb_s = (long long)atomicAdd(counter, 1ull);
+    __syncthreads();
+    const long long rb = rb_s;
+    if (rb >= nblk) break;
+    rows_mma_block<RT, WPB>(rb, row_begin, row_end, R, mode, l_mode, row_ptr, M, F, Z, H, st, dec, ti_part, md_part,
+                            e_part, ech_part);
   }
 }
 
