@@ -449,10 +449,18 @@ static int init_impl(Context *c, const uint32_t *coords, const float *vals, uint
   tm.mark(s, "layouts (sort, gather)");
 
   // partitions (host planning over row_ptr, once)
-  // nonzeros per MTTKRP work item: 1024, or 256 for a sharded rank, whose launches cover few
-  // waves of items and would otherwise idle while the last long items finish (c4, 8
-  // emulated ranks: MTTKRP 17.2 -> 13.2 ms summed over the ranks)
-  const long long T = c->opt.nnz_per_item > 0 ? c->opt.nnz_per_item : (c->sharded ? 256 : 1024);
+  // nonzeros per MTTKRP work item (measured on B200, profiles/r01_item_size_sweep.txt): enough
+  // items to fill every SM several times over, else the launch idles while the last long
+  // items finish.  1024 for the 1e8-nonzero c4 and for R > 64 (c5 R=256: 256-item runs lose
+  // 2%); 256 for mid-size tensors (c2 0.25 -> 0.08 ms, c3 1.21 -> 1.08, c5 R=8/16 -14..16%)
+  // and for a sharded rank (c4, 8 emulated ranks: 17.2 -> 13.2 ms summed); 64 under 1e5
+  // nonzeros (c1 0.095 -> 0.041 ms).
+  long long T = 1024;
+  if (c->opt.nnz_per_item > 0) T = c->opt.nnz_per_item;
+  else if (c->sharded) T = 256;
+  else if (c->pitch >= 128 || c->nnz >= 50000000LL) T = 1024;
+  else if (c->nnz < 100000) T = 64;
+  else T = 256;
   long long max_slots = 1, maxI = 1, max_chunks = 1;
   std::vector<long long> rps[3];
   for (int n = 0; n < 3; ++n) {
