@@ -83,7 +83,9 @@ typedef struct {
   void *stream;               /* cudaStream_t to run on, or NULL = library-owned stream     */
   int32_t use_graph;          /* 1 (default): sacd_iterate replays a captured CUDA graph    */
   int32_t profile;            /* 1: time every kernel class with CUDA events (no graph)     */
-  int32_t nnz_per_item;       /* MTTKRP work-item size in nonzeros (0 = default)            */
+  int32_t nnz_per_item;       /* MTTKRP work-item size in nonzeros (0 = by problem size:    */
+                              /* 1024 for >= 5e7 nonzeros or R > 64, 256 for sharded ranks   */
+                              /* and mid-size tensors, 64 under 1e5 nonzeros)                */
   int32_t mttkrp_variant;     /* MTTKRP tuning variant (0 = default; tools/mttkrp_tune.py)  */
   int32_t force_sharded;      /* 1: run the sharded (NCCL) engine also when world_size == 1 */
   int32_t emulate_ranks;      /* G >= 2 (with world_size 1): emulate the G ranks of the     */
