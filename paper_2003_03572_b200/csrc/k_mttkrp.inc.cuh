@@ -538,6 +538,25 @@ __global__ void __launch_bounds__(256, MINB) k_mttkrp_lean(const WorkItem *__res
 // a device counter (reset to 0 before the launch), so no launch ends on a partly-filled
 // last wave -- that tail grew to ~50% of a sharded rank's MTTKRP, whose launch covers only
 // about 2 waves of items.  Results do not depend on which warp takes which item.
+// The same for SW < 32 (several workers per warp): every worker takes its own items.
+template <typename Real, int RT, int SW, int D, int MINB, int PF = 0, int XS = 0>
+__global__ void __launch_bounds__(256, MINB) k_mttkrp_lean_dyn_sw(const WorkItem *__restrict__ items,
+                                                                 long long n_items, const uint4 *__restrict__ nzm,
+                                                                 const Real *__restrict__ A, const Real *__restrict__ B,
+                                                                 Real *__restrict__ M, Real *__restrict__ partial,
+                                                                 unsigned long long *__restrict__ counter) {
+  const int lane = threadIdx.x & (SW - 1);
+  const unsigned mask = SW == 32 ? 0xffffffffu : (((1u << SW) - 1u) << (threadIdx.x & 31 & ~(SW - 1)));
+  for (;;) {
+    unsigned long long it = 0;
+    if (lane == 0) it = atomicAdd(counter, 1ull);
+    it = __shfl_sync(mask, it, 0, SW);
+    if ((long long)it >= n_items) break;
+    __syncwarp(mask);
+    lean_item<Real, RT, SW, D, PF, XS>((long long)it, items, nzm, A, B, M, partial);
+  }
+}
+
 template <typename Real, int RT, int D, int MINB, int PF = 0, int XS = 0>
 __global__ void __launch_bounds__(256, MINB) k_mttkrp_lean_dyn(const WorkItem *__restrict__ items, long long n_items,
                                                               const uint4 *__restrict__ nzm,
