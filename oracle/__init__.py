@@ -21,8 +21,10 @@ import subprocess
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SRC = os.path.join(HERE, "sacd_oracle.c")
-LIB = os.path.join(HERE, "liboracle.so")
+# ORACLE_SRC / ORACLE_LIB: used only by tests/test_oracle_mutations.py, which compiles
+# deliberately broken copies of the oracle to show that the pins catch each mutation.
+SRC = os.environ.get("ORACLE_SRC", os.path.join(HERE, "sacd_oracle.c"))
+LIB = os.environ.get("ORACLE_LIB", os.path.join(HERE, "liboracle.so"))
 
 BR_FIRST, BR_EQ24, BR_EQ27 = 0, 1, 2
 VAR_GS_LAGGED, VAR_SELECT_OFF, VAR_JACOBI, VAR_SNAPSHOT = 0, 1, 2, 3

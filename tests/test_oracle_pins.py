@@ -259,6 +259,64 @@ def test_frobenius_importance_is_a_lower_bound():
     _, zf, *_ = O.mode_pass(M, H, F[0], np.zeros_like(F[0]), O.BR_FIRST, l_mode=O.L_FROB)
     # compare column 0 only (later columns see different GS histories)
     assert (zf[:, 0] <= zd[:, 0] + 1e-15).all()
+    # strict where the step moves: ||H||_F > h_00 whenever H has another nonzero entry, and
+    # z_diag - z_frob = (||H||_F - h_00) d^2 / 2 (Eq 20) with the same g and d
+    Fd, *_ = O.mode_pass(M, H, F[0], np.zeros_like(F[0]), O.BR_FIRST, l_mode=O.L_DIAG)
+    moved = Fd[:, 0] != F[0][:, 0]
+    assert moved.any()
+    assert (zf[moved, 0] < zd[moved, 0]).all()
+    d = Fd[moved, 0] - F[0][moved, 0]
+    np.testing.assert_allclose(zd[moved, 0] - zf[moved, 0], (O.frobenius(H) - H[0, 0]) * d * d / 2,
+                               rtol=1e-9, atol=0)
+
+
+@pytest.mark.parametrize("case", ["frob_diag_H", "frob_full_H"])
+def test_frobenius_importance_golden(golden, case):
+    """Alg 1's L = ||H||_F inside Eq 20, on hand-derived one-row passes
+    (tests/golden/frob_and_echanged.json): pins that the FROB pass really uses ||H||_F
+    (incl. off-diagonal entries), not h_rr."""
+    g = golden["frob_and_echanged"][case]
+    M, H = np.array([g["m"]]), np.array(g["H"])
+    u = np.array([g["u"]])
+    for l_mode, key in ((O.L_DIAG, "z_diag"), (O.L_FROB, "z_frob")):
+        Fn, zp, ti, E, Ech, md, dec = O.mode_pass(M, H, u, np.zeros_like(u), O.BR_FIRST, l_mode=l_mode,
+                                                 decisions=True)
+        np.testing.assert_allclose(zp[0], g[key], rtol=0, atol=1e-15)
+        np.testing.assert_array_equal(Fn[0], g["u_new"])
+        assert E == g["E"] and Ech == g["E_changed"]
+        assert abs(ti - sum(g[key])) <= 1e-15
+
+
+@pytest.mark.parametrize("case", ["echanged_zero_step", "echanged_mixed_row"])
+def test_echanged_golden(golden, case):
+    """E vs E_changed (Lemma 4; reading C14): an EQ27 selection with d = 0 counts in E
+    but not in E_changed (tests/golden/frob_and_echanged.json)."""
+    g = golden["frob_and_echanged"][case]
+    M, H = np.array([g["m"]]), np.array(g["H"])
+    u, zprev = np.array([g["u"]]), np.array([g["zprev"]])
+    br = {"EQ24": O.BR_EQ24, "EQ27": O.BR_EQ27, "FIRST": O.BR_FIRST}[g["branch"]]
+    Fn, zp, ti, E, Ech, md, dec = O.mode_pass(M, H, u, zprev, br, decisions=True)
+    np.testing.assert_array_equal(Fn[0], g["u_new"])
+    np.testing.assert_allclose(zp[0], g["z"], rtol=0, atol=1e-15)
+    np.testing.assert_array_equal(dec[0], g["selected"])
+    assert E == g["E"] and Ech == g["E_changed"]
+
+
+@pytest.mark.parametrize("branch", [0, 1, 2])
+def test_echanged_counts_selected_elements_that_moved(branch):
+    """C14 on a random pass: E = #decisions, E_changed = #(selected and value changed),
+    counted here from the pass's own before / after factors."""
+    dims, R = (7, 6, 5), 4
+    c, v, F = rand_inst(dims, 0.5, R, 11)
+    M = O.mttkrp(c, v, dims, 0, F)
+    H = O.mode_hessian(F, dims, 0)
+    rng = np.random.default_rng(3)
+    zprev = rng.uniform(-0.2, 0.2, size=F[0].shape)
+    zprev[rng.uniform(size=zprev.shape) < 0.3] = 0.0
+    Fn, zp, ti, E, Ech, md, dec = O.mode_pass(M, H, F[0], zprev, branch, decisions=True)
+    assert E == int(dec.sum())
+    assert Ech == int((dec.astype(bool) & (Fn != F[0])).sum())
+    assert (Fn[~dec.astype(bool)] == F[0][~dec.astype(bool)]).all()
 
 
 def test_hand_trace(golden):
