@@ -42,6 +42,7 @@ def parse():
     p.add_argument("--precision", default="f64", choices=["f64", "f32"])
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--reps", type=int, default=5, help="SURVEY 8(d): repetitions with a fresh sacd_init (N = 1)")
     p.add_argument("--nnz-per-item", type=int, default=0)
     p.add_argument("--exchange", default="delta", choices=["full", "delta"],
                    help="N > 1: factor-row exchange of the sharded engine (SURVEY f2 delta lists, or full rows)")
@@ -104,89 +105,130 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------- algorithmic bytes
 def algorithmic_bytes(cfg_dims, nnz, R, s):
-    """Per mode n: MTTKRP = 12 nnz (idx_a, idx_b, val) + 8 (I_n+1) (row_ptr)
-    + (I_a + I_b) R s (each other-factor row once) + I_n R s (M write);
-    row update = 5 I_n R s (M read, F read+write, z_prev read+write).
-    B_comp per sweep = sum over modes of MTTKRP + row update - M round trip."""
+    """SURVEY 8(d)'s compulsory bytes, with s-byte factor / z_prev elements (s = 8 in the fp64
+    build) and Rp = 4 ceil(R/4):
+      MTTKRP of mode n : 12 nnz (idx_a, idx_b, val) + 4 (I_n + 1) (row_ptr)
+                         + (I_a + I_b) Rp s (every other-factor row once)      -- no M write:
+                         8(d) counts M as kept on chip (the fused design);
+      row update n     : 2 I_n Rp s (own factor read + write) + 2 I_n R s (z_prev read + write);
+      B_comp per sweep : the sum of both over the three modes."""
     d = cfg_dims
+    Rp = 4 * ((R + 3) // 4)
     out = {}
     for n in range(3):
         a, b = [m for m in range(3) if m != n]
-        mt = 12 * nnz + 8 * (d[n] + 1) + (d[a] + d[b]) * R * s + d[n] * R * s
-        rows = 5 * d[n] * R * s
+        mt = 12 * nnz + 4 * (d[n] + 1) + (d[a] + d[b]) * Rp * s
+        rows = 2 * d[n] * Rp * s + 2 * d[n] * R * s
         out[n] = (mt, rows)
-    bcomp = sum(12 * nnz + 8 * (d[n] + 1) + (sum(d) - d[n]) * R * s + 4 * d[n] * R * s for n in range(3))
+    bcomp = sum(out[n][0] + out[n][1] for n in range(3))
     return out, bcomp
 
 
 # ----------------------------------------------------------------------------- oracle (CPU) leg
 class OracleSweepSample:
-    """The fp64 oracle's per-sweep work on a bounded sample, scaled to the full workload.
+    """The fp64 oracle's sweep (oracle.sacd_run, as it stands) on a bounded sample of rows.
 
-    One oracle sweep (oracle.sacd_run) does, per mode n: Gram of the two other factors,
-    MTTKRP over all nonzeros, the row pass over all I_n rows; plus the three Grams for the
-    objective -- i.e. each factor's Gram three times.  The MTTKRP cost is linear in the
-    nonzeros and the Gram / row-pass cost linear in the rows, so we time
-      * oracle.mttkrp_layout on every `nz_step`-th nonzero (full dims), x nz_step, and
-      * 3 x oracle.gram + oracle.mode_pass on every `row_step`-th row, x row_step,
-    with the oracle's own functions, as they stand, on all host cores.  Layout building
-    (init work, not per sweep) is done untimed in the constructor."""
+    Per sweep, ora_sacd_run does for each mode n: the Grams of the two other factors, their
+    Hadamard product, the MTTKRP of every row of mode n over its full slice, and the row pass;
+    then the three Grams for the objective -- so every factor's Gram three times.  A step here
+    runs exactly those oracle functions on every `step`-th row of each mode (with each
+    sampled row's FULL slice, so fibers and slice lengths are those of the workload):
+      * mttkrp_layout of the sampled rows (output: the sampled rows only),
+      * mode_pass of the sampled rows (M, H, z_prev of those rows),
+      * 3 x gram of every `step`-th row of each factor.
+    The full-sweep time is estimated by scaling the MTTKRP by nnz / sampled nnz and the row
+    pass and Grams by rows / sampled rows (each is linear in what it is scaled by).  Layout
+    building (init work) happens untimed in the constructor.  ms_per_step reports the time
+    actually spent per step; value = 1 / (estimated full-sweep seconds)."""
 
-    def __init__(self, c, v, dims, R, seed, nz_step, row_step):
+    def __init__(self, c, v, dims, R, seed, step):
         import oracle as O
         O.build()
-        self.O, self.dims, self.R = O, dims, R
-        self.nz_step, self.row_step = nz_step, row_step
-        self.F = O.init_factors(dims, R, seed)
-        cs, vs = np.ascontiguousarray(c[::nz_step]), np.ascontiguousarray(v[::nz_step])
-        self.n_sample = len(vs)
-        self.lay = [O.layout(cs, vs, dims, n) for n in range(3)]
-        self.H = [O.mode_hessian(self.F, dims, n) for n in range(3)]
-        self.rows = [np.ascontiguousarray(self.F[n][::row_step]) for n in range(3)]
-
-    def seconds(self):
-        O = self.O
-        t = 0.0
+        self.O, self.dims, self.R, self.step = O, dims, R, step
+        F = O.init_factors(dims, R, seed)
+        self.F = F
+        self.sub = []
+        self.nnz = len(v)
+        self.nnz_s = 0
         for n in range(3):
-            a, b = O.other_modes(self.dims, n)
-            ia, ib, vv, rp = self.lay[n]
+            a, b = O.other_modes(dims, n)
+            rows = np.arange(0, dims[n], step, dtype=np.int64)
+            mask = (c[:, n].astype(np.int64) % step) == 0
+            cs, vs = c[mask].copy(), v[mask]
+            cs[:, n] = cs[:, n] // step
+            d2 = list(dims)
+            d2[n] = len(rows)
+            lay = O.layout(cs, vs, d2, n)
+            H = O.hadamard(O.gram(F[a]), O.gram(F[b]))
+            self.sub.append((a, b, lay, np.ascontiguousarray(F[n][rows]), H, len(vs)))
+            self.nnz_s += len(vs)
+        self.gsub = [np.ascontiguousarray(F[n][::step]) for n in range(3)]
+
+    def step_seconds(self):
+        """(seconds actually spent, estimated full-sweep seconds)"""
+        O = self.O
+        spent, full = 0.0, 0.0
+        for n in range(3):
+            a, b, (ia, ib, vv, rp), Fs, H, nnz_n = self.sub[n]
             t0 = time.perf_counter()
-            O.mttkrp_layout(rp, ia, ib, vv, self.F[a], self.F[b])
-            t += (time.perf_counter() - t0) * self.nz_step
-            Fs = self.rows[n]
-            Ms = np.zeros_like(Fs)
+            M = O.mttkrp_layout(rp, ia, ib, vv, self.F[a], self.F[b])
+            t1 = time.perf_counter()
+            O.mode_pass(M, H, Fs, np.zeros_like(Fs), O.BR_FIRST)
+            t2 = time.perf_counter()
+            spent += t2 - t0
+            full += (t1 - t0) * (self.nnz / max(nnz_n, 1)) + (t2 - t1) * (self.dims[n] / max(len(Fs), 1))
+        for n in range(3):
             t0 = time.perf_counter()
             for _ in range(3):
-                O.gram(Fs)
-            O.mode_pass(Ms, self.H[n], Fs, np.zeros_like(Fs), O.BR_FIRST)
-            t += (time.perf_counter() - t0) * self.row_step
-        return t
+                O.gram(self.gsub[n])
+            t1 = time.perf_counter()
+            spent += t1 - t0
+            full += (t1 - t0) * (self.dims[n] / max(len(self.gsub[n]), 1))
+        return spent, full
 
-    def describe(self, nnz):
-        return (f"oracle per-sweep work as it stands: mttkrp_layout on every {self.nz_step}th nonzero "
-                f"({self.n_sample} of {nnz}) x{self.nz_step}, plus 3 x gram + mode_pass on every "
-                f"{self.row_step}th row x{self.row_step}; layouts built untimed; all host cores")
+    def describe(self):
+        return (f"oracle sweep functions as they stand (mttkrp_layout + mode_pass of every {self.step}th row of each "
+                f"mode over its full slice: {self.nnz_s} of 3x{self.nnz} slice nonzeros; 3 x gram of every "
+                f"{self.step}th factor row), scaled by nnz / rows share to one sweep; layouts built untimed")
 
 
-def sample_steps(nnz, rows_total):
-    nz_step = max(1, nnz // 2_000_000)
-    row_step = max(1, rows_total // 100_000)
-    return nz_step, row_step
+def sample_step(nnz):
+    """rows step: ~1e7 slice nonzeros per step (3 modes) on c4, i.e. a few seconds of oracle work"""
+    return max(1, int(round(3 * nnz / 1e7)))
 
 
 def cpu_baseline(c, v, dims, R, seed, nnz, reps=3):
     import oracle as O
-    nz_step, row_step = sample_steps(nnz, sum(dims))
-    s = OracleSweepSample(c, v, dims, R, seed, nz_step, row_step)
-    ts = [s.seconds() for _ in range(reps)]
-    t = float(np.median(ts))
-    return {"value": 1.0 / t, "unit": UNIT, "cores": O.max_threads(), "kind": "oracle",
-            "sample": s.describe(nnz) + f"; median of {reps}", "seconds_per_sweep": t}
+    smp = OracleSweepSample(c, v, dims, R, seed, sample_step(nnz))
+    res = [smp.step_seconds() for _ in range(reps)]
+    full = float(np.median([r[1] for r in res]))
+    spent = float(np.median([r[0] for r in res]))
+    out = {"value": 1.0 / full, "unit": UNIT, "cores": O.max_threads(), "kind": "oracle",
+           "sample": smp.describe() + f"; median of {reps}", "seconds_per_sweep": full,
+           "sample_seconds": spent}
+    try:  # the committed full-sweep measurement of the same oracle (tools/oracle_timing.py)
+        for ln in open(os.path.join(ROOT, "profiles", "r02_oracle_full_sweeps.jsonl")):
+            r = json.loads(ln)
+            if r.get("config") == _cfg_name_for(dims) and r.get("rank") == R and r.get("threads") == r.get("host_cores"):
+                out["measured_full_sweep"] = {"seconds_per_sweep": r["seconds_per_sweep"], "threads": r["threads"],
+                                              "source": "profiles/r02_oracle_full_sweeps.jsonl"}
+    except (OSError, ValueError):
+        pass
+    return out
+
+
+def _cfg_name_for(dims):
+    import sacd_inputs as SI
+    for k, cfg in SI.CONFIGS.items():
+        if tuple(cfg.dims) == tuple(dims):
+            return k
+    return None
 
 
 def run_reference(args, cfg, R):
-    """--impl reference: the fp64 oracle on the box's host cores (rank 0 only); each step
-    is the sampled oracle sweep of OracleSweepSample, scaled to the full workload."""
+    """--impl reference: the fp64 oracle on the box's host cores (rank 0 only); each step is
+    the bounded row sample of OracleSweepSample (seconds actually spent = ms_per_step), value =
+    1 / the estimated full-sweep time."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -197,21 +239,22 @@ def run_reference(args, cfg, R):
     c, v = SI.make_tensor(cfg, device=dev)
     c, v = c.cpu().numpy().astype(np.uint32), v.cpu().numpy()
     nnz = len(v)
-    nz_step, row_step = sample_steps(nnz, sum(cfg.dims))
-    smp = OracleSweepSample(c, v, cfg.dims, R, cfg.seed, nz_step, row_step)
+    smp = OracleSweepSample(c, v, cfg.dims, R, cfg.seed, sample_step(nnz))
     K = args.steps if args.steps is not None else 5
     for _ in range(args.warmup):
-        smp.seconds()
-    ts = [smp.seconds() for _ in range(K)]
-    t_full = float(np.mean(ts))
+        smp.step_seconds()
+    res = [smp.step_seconds() for _ in range(K)]
+    t_full = float(np.mean([r[1] for r in res]))
+    t_step = float(np.mean([r[0] for r in res]))
     val = 1.0 / t_full
     cores = O.max_threads()
-    sample = smp.describe(nnz)
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": K, "warmup": args.warmup, "ms_per_step": 1e3 * t_full, "higher_is_better": True,
+            "steps": K, "warmup": args.warmup, "ms_per_step": 1e3 * t_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": cfg.name, "dims": list(cfg.dims), "nnz": cfg.nnz, "rank": R},
-            "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "config": {"workload": cfg.name, "dims": list(cfg.dims), "nnz": cfg.nnz, "rank": R,
+                       "sweep_fraction_per_step": t_step / t_full,
+                       "estimated_seconds_per_full_sweep": t_full},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": smp.describe()},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "gpu_launches": 0}
     print(json.dumps(line), flush=True)
@@ -261,8 +304,11 @@ def main():
     stream = torch.cuda.Stream()
 
     # ---- device-resident timed region (kernel-class events on the launching stream)
+    torch.cuda.synchronize()
+    t_init = time.perf_counter()
     g = Sacd(coords, vals, cfg.dims, R, cfg.seed, precision=args.precision, stream=stream.cuda_stream,
              profile=False, nnz_per_item=args.nnz_per_item, device=local, **shard_kw)
+    init_s = time.perf_counter() - t_init   # sacd_init from device-resident COO (layouts, init, graph)
     info = g.info()
     g.iterate(W)
     g.sync()
@@ -292,6 +338,8 @@ def main():
     g.set_profile(False)
     f_final, fit_final = g.fit()
     info_end = g.info()
+    st_all = g.stats()
+    sweep_ms_dev = [r["ms"] for r in st_all[W:W + K]]  # per-sweep device time (sacd_iter_stats.ms)
     ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
@@ -346,13 +394,38 @@ def main():
                                          "launch through L1, vs 148 SM x 128 B/clk; ncu shows the L1 data pipe "
                                          "at 80-84% of peak in the U/V modes (wavefronts incl. broadcasts)"}
 
+    # ---- SURVEY 8(d) protocol: repetitions, each with a fresh sacd_init (N = 1)
+    g.close()
+    del g
+    reps = [{"sweeps_per_s": value, "init_s": init_s}]
+    if world == 1 and args.reps > 1:
+        for _ in range(args.reps - 1):
+            torch.cuda.synchronize()
+            t = time.perf_counter()
+            gr = Sacd(coords, vals, cfg.dims, R, cfg.seed, precision=args.precision, stream=stream.cuda_stream,
+                      nnz_per_item=args.nnz_per_item, device=local)
+            ti_ = time.perf_counter() - t
+            gr.iterate(W)
+            gr.sync()
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            gr.iterate(K)
+            a1.record(stream)
+            a1.synchronize()
+            reps.append({"sweeps_per_s": K / (a0.elapsed_time(a1) / 1e3), "init_s": ti_})
+            gr.close()
+    rv = [r["sweeps_per_s"] for r in reps]
+    ri = [r["init_s"] for r in reps]
+    repetitions = {"n": len(reps), "sweeps_per_s": {"median": float(np.median(rv)), "min": min(rv), "max": max(rv)},
+                   "init_s": {"median": float(np.median(ri)), "min": min(ri), "max": max(ri)},
+                   "what": "each repetition: fresh sacd_init (device-resident COO), W warm-up sweeps, K timed "
+                           "sweeps (CUDA events); the first one is the headline value"}
+
     # ---- end to end through the public API with host (pinned) buffers
     e2e = None
     if not args.no_e2e:
         hc = coords.cpu().pin_memory()
         hv = vals.cpu().pin_memory()
-        g.close()
-        del g
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -364,10 +437,16 @@ def main():
         t0 = time.perf_counter()
         g2 = Sacd(hc, hv, cfg.dims, R, cfg.seed, precision=args.precision, stream=stream.cuda_stream,
                   nnz_per_item=args.nnz_per_item, device=local, **shard_kw)
+        t1 = time.perf_counter()
         g2.iterate(K)
+        g2.sync()
+        t2 = time.perf_counter()
         Fs = g2.factors()
+        t3 = time.perf_counter()
         f2, _ = g2.fit()
         t_e2e = time.perf_counter() - t0
+        phases = {"init_h2d_layout_s": t1 - t0, "iterate_s": t2 - t1, "factors_d2h_s": t3 - t2,
+                  "fit_s": t_e2e - (t3 - t0)}
         te = torch.tensor([t_e2e], dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
@@ -376,11 +455,9 @@ def main():
         h2d = nnz * 16
         d2h = sum(x.nbytes for x in Fs) + 16
         e2e = {"value": K / t_e2e, "unit": UNIT, "h2d_bytes_per_step": h2d / K, "d2h_bytes_per_step": d2h / K,
-               "seconds": t_e2e,
+               "seconds": t_e2e, "phases": phases,
                "what": "sacd_init from pinned host COO (H2D + device layout sort) + sacd_iterate(K) + "
                        "sacd_factors (D2H, all modes) + sacd_fit; bytes per step = totals / K"}
-    else:
-        g.close()
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -407,7 +484,12 @@ def main():
                            "mttkrp_items": info["items"], "split_rows": info["split_rows"],
                            "objective_after": f_final, "fit_after": fit_final},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
-                "clocks": clk}
+                "clocks": clk, "init_s": init_s, "repetitions": repetitions,
+                "sweep_ms_device": {"median": float(np.median(sweep_ms_dev)) if sweep_ms_dev else None,
+                                    "min": min(sweep_ms_dev) if sweep_ms_dev else None,
+                                    "max": max(sweep_ms_dev) if sweep_ms_dev else None,
+                                    "what": "sacd_iter_stats.ms of the K timed sweeps (%globaltimer, first kernel "
+                                            "of the sweep to the end of its objective kernel)"}}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

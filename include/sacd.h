@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define SACD_ABI_VERSION 1
+#define SACD_ABI_VERSION 2
 
 typedef struct sacd_ctx sacd_ctx; /* opaque; owned by the library until sacd_free */
 
@@ -114,6 +114,8 @@ typedef struct {
   double ti[3];          /* total importance ti^k per mode (Eq 25)                    */
   int64_t E[3];          /* #elements selected (Lemma 4)                              */
   int64_t E_changed[3];  /* #selected with a nonzero step (C14)                              */
+  double ms;             /* device time of the sweep: %globaltimer at its first kernel to the   */
+                         /* end of its objective kernel (FitReport per-sweep time)  */
 } sacd_iter_stats;
 
 typedef struct {

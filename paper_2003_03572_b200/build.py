@@ -10,6 +10,10 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 SOURCES = ["capi.cu", "kernels.cu", "layout.cu"]
 OUT = os.path.join(HERE, "libsacd.so")
+# library flavours: the product build, the MTTKRP tuning-variant build (tools/mttkrp_tune.py,
+# test_mttkrp_variants_bitwise) and the device-assert build (tests/test_debug_build.py)
+FLAVOURS = {"default": ("libsacd.so", []), "tuning": ("libsacd_tuning.so", ["-DSACD_TUNING"]),
+            "debug": ("libsacd_debug.so", ["-DSACD_DEBUG"])}
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 def _nccl_dir():
@@ -29,29 +33,71 @@ FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-li
 LIBS = [f"-L{NCCL}/lib", "-l:libnccl.so.2", f"-Xlinker", f"-rpath={NCCL}/lib"]
 
 
-def _stale() -> bool:
-    if not os.path.exists(OUT):
+def _paths(flavour):
+    out = os.path.join(HERE, FLAVOURS[flavour][0])
+    return out, out + ".stamp"
+
+
+def _fingerprint(flavour="default") -> str:
+    """sha256 over every csrc file, sacd.h, this file, the flags and the nvcc version: the .so
+    is rebuilt whenever any of them differs from the stamp written next to it (a prebuilt
+    .so that travels to the GPU box is reused only if it is exactly HEAD's build)."""
+    import hashlib
+    h = hashlib.sha256()
+    deps = sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC)) + [os.path.join(ROOT, "include", "sacd.h"),
+                                                                        os.path.abspath(__file__)]
+    for d in deps:
+        h.update(d.encode())
+        with open(d, "rb") as fh:
+            h.update(fh.read())
+    h.update(repr((FLAGS, LIBS, SOURCES, FLAVOURS[flavour])).encode())
+    try:
+        h.update(subprocess.run([NVCC, "--version"], capture_output=True, text=True).stdout.encode())
+    except OSError:
+        h.update(b"no-nvcc")
+    return h.hexdigest()
+
+
+def _stale(flavour="default") -> bool:
+    out, stamp = _paths(flavour)
+    if not os.path.exists(out) or not os.path.exists(stamp):
         return True
-    t = os.path.getmtime(OUT)
-    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(ROOT, "include", "sacd.h")]
-    return any(os.path.getmtime(d) > t for d in deps)
+    with open(stamp) as fh:
+        return fh.read().strip() != _fingerprint(flavour)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, flavour: str = "default") -> str:
+    OUT, STAMP = _paths(flavour)
+    if not force and not _stale(flavour):
         return OUT
-    cmd = [NVCC, *FLAGS, "-o", OUT + ".tmp", *[os.path.join(CSRC, s) for s in SOURCES], *LIBS]
-    log = os.path.join(HERE, "build.log")
+    cmd = [NVCC, *FLAGS, *FLAVOURS[flavour][1], "-o", OUT + ".tmp", *[os.path.join(CSRC, s) for s in SOURCES], *LIBS]
+    log = os.path.join(HERE, f"build_{flavour}.log")
     with open(log, "w") as fh:
         r = subprocess.run(cmd, stdout=fh, stderr=subprocess.STDOUT)
     if r.returncode != 0:
         sys.stderr.write(open(log).read()[-6000:])
         raise RuntimeError(f"nvcc failed ({r.returncode}); see {log}")
     os.replace(OUT + ".tmp", OUT)
+    with open(STAMP, "w") as fh:
+        fh.write(_fingerprint(flavour) + "\n")
     if verbose:
         print(f"built {OUT}")
     return OUT
 
 
+def build_gather_bench(verbose: bool = False) -> str:
+    """tools/gather_bench (the measured gather peak of the MTTKRP's composite roofline)."""
+    src = os.path.join(ROOT, "tools", "gather_bench.cu")
+    out = os.path.join(ROOT, "tools", "gather_bench")
+    if os.path.exists(out) and os.path.getmtime(out) >= os.path.getmtime(src):
+        return out
+    subprocess.run([NVCC, "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-o", out,
+                    src], check=True)
+    if verbose:
+        print(f"built {out}")
+    return out
+
+
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
+    fl = next((a.split("=", 1)[1] for a in sys.argv if a.startswith("--flavour=")), "default")
+    build(force="--force" in sys.argv, verbose=True, flavour=fl)

@@ -538,6 +538,7 @@ static int init_impl(Context *c, const uint32_t *coords, const float *vals, uint
       }
       SACD_CUDA_TRY(cudaMalloc(&sh.M, (size_t)((maxI + 31) / 32 * 32) * c->pitch * rs));
       SACD_CUDA_TRY(cudaMalloc(&sh.partial, (size_t)slots_k * c->pitch * rs));
+      c->max_slots = std::max(c->max_slots, slots_k);
       c->device_bytes += (long long)((size_t)maxI * c->pitch * rs + (size_t)slots_k * c->pitch * rs);
     }
     // NCCL communicator (one rank per process; emulated ranks need none)
@@ -619,6 +620,10 @@ static int init_impl(Context *c, const uint32_t *coords, const float *vals, uint
   }
   SACD_CUDA_TRY(cudaMalloc(&c->partial, (size_t)max_slots * P * rs));
   SACD_CUDA_TRY(cudaMalloc(&c->fixbuf, (size_t)max_chunks * P * rs));
+  // sharded ranks write their own partial buffers (>= their slots); c->max_slots keeps the
+  // smallest buffer any launch may index (debug bounds)
+  c->max_slots = c->sharded ? c->max_slots : max_slots;
+  c->max_chunks = max_chunks;
   c->device_bytes += (long long)((size_t)max_chunks * P * rs);
   SACD_CUDA_TRY(cudaMalloc(&c->Hr, (size_t)P * P * rs));
   SACD_CUDA_TRY(cudaMalloc(&c->Hd, (size_t)R * R * 8));
@@ -758,6 +763,27 @@ int sacd_init(sacd_ctx **out, const uint32_t *coords, const float *vals, int64_t
     set_error("sacd_init: the JACOBI / SNAPSHOT variants run unsharded only");
     return SACD_EINVAL;
   }
+#ifndef SACD_TUNING
+  if (o.mttkrp_variant != 0) {
+    set_error("sacd_init: mttkrp_variant != 0 needs the tuning build (libsacd_tuning.so, -DSACD_TUNING)");
+    return SACD_EINVAL;
+  }
+#else
+  {
+    // every tuning variant that has a kernel for this precision / pitch (others would launch
+    // no MTTKRP at all and leave M stale)
+    const int v = o.mttkrp_variant;
+    int p = 8;
+    while (p < rank) p <<= 1;
+    const bool f64 = o.precision == SACD_F64;
+    const bool ok = v == 0 || (p >= 32 && (v == 1 || (v >= 10 && v <= 15) || (v >= 20 && v <= 49 && (v != 39 || f64)) ||
+                                           (v >= 50 && v <= 59 && f64 && p == 64)));
+    if (!ok) {
+      set_error("sacd_init: mttkrp_variant has no kernel for this precision / rank");
+      return SACD_EINVAL;
+    }
+  }
+#endif
   if (o.world_size < 1 || o.rank < 0 || o.rank >= o.world_size || o.emulate_ranks < 0 ||
       (o.emulate_ranks > 1 && o.world_size != 1)) {
     set_error("sacd_init: bad world_size / rank / emulate_ranks");

@@ -26,6 +26,8 @@ __global__ void __launch_bounds__(256) k_mttkrp(const WorkItem *__restrict__ ite
   const long long item = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (item >= n_items) return;
   const WorkItem it = items[item];
+  SACD_DBG(SACD_DASSERT(it.nz0 < it.nz1 && it.nz1 <= g_dbg.nnz && it.slot < g_dbg.nslots && it.row0 < it.row1 &&
+                        it.row1 <= g_dbg.In));
   const int grp = lane / LPN, sub = lane % LPN;
   for (int row = it.row0; row < it.row1; ++row) {
     long long s = row_ptr[row], t = row_ptr[row + 1];
@@ -38,8 +40,10 @@ __global__ void __launch_bounds__(256) k_mttkrp(const WorkItem *__restrict__ ite
       for (int c = 0; c < VEC; ++c) acc[v][c] = Real(0);
     for (long long e = s + grp; e < t; e += G) {
       const Real x = (Real)ld_stream_f32(val + e);
-      const VT *ap = reinterpret_cast<const VT *>(A + (long long)(ld_stream_u32(ia + e) & kIdxMask) * RT);
-      const VT *bp = reinterpret_cast<const VT *>(B + (long long)(ld_stream_u32(ib + e) & kIdxMask) * RT);
+      const uint32_t ea = ld_stream_u32(ia + e) & kIdxMask, eb = ld_stream_u32(ib + e) & kIdxMask;
+      SACD_DBG(SACD_DASSERT(ea < g_dbg.Ia && eb < g_dbg.Ib));
+      const VT *ap = reinterpret_cast<const VT *>(A + (long long)ea * RT);
+      const VT *bp = reinterpret_cast<const VT *>(B + (long long)eb * RT);
 #pragma unroll
       for (int v = 0; v < VPL; ++v) {
         Real av[VEC], bv[VEC];
@@ -405,12 +409,20 @@ __device__ __forceinline__ void prefetch_rows(const uint4 &m, bool valid, const 
 // XS: how the batch's per-nonzero b index / x reach every lane of the worker: 0 = warp
 // shuffles (1 for the b index, 2 for x in fp64), 1 = x through a shared-memory broadcast
 // (one wavefront instead of two shuffles), 2 = the b index and x as one 16-byte
-// shared-memory broadcast per nonzero.
+// shared-memory broadcast per nonzero, 3 = as 2 with the workers' slots padded apart (two
+// workers of a warp read different banks: one wavefront serves both), 4 = every value of the
+// tensor equals xu (e.g. binary tensors; detected at sacd_init): no x broadcast at all, x =
+// xu for the batch's nonzeros and 0 past the item's end.
+template <int XS>
+__device__ __forceinline__ int xs_slot(int t) {
+  return XS == 3 ? t + (t >> 4) : t;
+}
+
 template <typename Real, int RT, int SW, int D, int PF, int XS>
 __device__ __forceinline__ void lean_item(long long item, const WorkItem *__restrict__ items,
                                           const uint4 *__restrict__ nzm, const Real *__restrict__ A,
                                           const Real *__restrict__ B, Real *__restrict__ M,
-                                          Real *__restrict__ partial) {
+                                          Real *__restrict__ partial, Real xu) {
   using SR = SubRow<Real, RT, SW>;
   constexpr int E = SR::E;
   constexpr int VEC = V16<Real>::N;
@@ -419,10 +431,11 @@ __device__ __forceinline__ void lean_item(long long item, const WorkItem *__rest
   const unsigned mask = SW == 32 ? 0xffffffffu : (((1u << SW) - 1u) << (threadIdx.x & 31 & ~(SW - 1)));
   const long long nz0 = items[item].nz0, nz1 = items[item].nz1;
   const int slot = (int)items[item].slot;
+  SACD_DBG(SACD_DASSERT(nz0 >= 0 && nz0 < nz1 && nz1 <= g_dbg.nnz && slot < g_dbg.nslots));
   const Real *Al = A + lane * VEC;
   const Real *Bl = B + lane * VEC;
   __shared__ __align__(16) Real xsb[XS == 1 ? 2 : 1][XS == 1 ? 256 : 1];
-  __shared__ __align__(16) uint4 rsb[XS == 2 ? 2 : 1][XS == 2 ? 256 : 1];
+  __shared__ __align__(16) uint4 rsb[(XS == 2 || XS == 3) ? 2 : 1][(XS == 2 || XS == 3) ? 272 : 1];
   const int wbase = threadIdx.x & ~(SW - 1);
   int par = 0;
   SR arow;
@@ -454,7 +467,7 @@ __device__ __forceinline__ void lean_item(long long item, const WorkItem *__rest
       par ^= 1;
       xsb[par][threadIdx.x] = xl;
       __syncwarp(mask);
-    } else if constexpr (XS == 2) {
+    } else if constexpr (XS == 2 || XS == 3) {
       par ^= 1;
       uint4 r;
       r.x = my.y;
@@ -466,21 +479,22 @@ __device__ __forceinline__ void lean_item(long long item, const WorkItem *__rest
         r.z = __float_as_uint((float)xl);
         r.w = 0u;
       }
-      rsb[par][threadIdx.x] = r;
+      rsb[par][xs_slot<XS>(threadIdx.x)] = r;
       __syncwarp(mask);
     }
     uint32_t fb[SW];
     Real xr[D + 1];
     SR bb[D + 1];
     auto fetch = [&](int j) {  // b index + flags (and, XS == 2, x) of nonzero j of the batch
-      if constexpr (XS == 2) {
-        const uint4 r = rsb[par][wbase + j];
+      if constexpr (XS == 2 || XS == 3) {
+        const uint4 r = rsb[par][xs_slot<XS>(wbase + j)];
         fb[j] = r.x;
         if constexpr (sizeof(Real) == 8) xr[j % (D + 1)] = __hiloint2double((int)r.w, (int)r.z);
         else xr[j % (D + 1)] = __uint_as_float(r.z);
       } else {
         fb[j] = __shfl_sync(mask, my.y, j, SW);
       }
+      SACD_DBG(SACD_DASSERT((fb[j] & kIdxMask) < g_dbg.Ib));
     };
 #pragma unroll
     for (int j = 0; j < D && j < SW; ++j) {
@@ -494,8 +508,9 @@ __device__ __forceinline__ void lean_item(long long item, const WorkItem *__rest
         bb[(j + D) % (D + 1)].load(Bl + (long long)(fb[j + D] & kIdxMask) * RT);
       }
       Real x;
-      if constexpr (XS == 2) x = xr[j % (D + 1)];
+      if constexpr (XS == 2 || XS == 3) x = xr[j % (D + 1)];
       else if constexpr (XS == 1) x = xsb[par][wbase + j];
+      else if constexpr (XS == 4) x = (base + j < nz1) ? xu : Real(0);
       else x = __shfl_sync(mask, xl, j, SW);
       if (fb[j] & kFiberStart) {
 #pragma unroll
@@ -509,8 +524,11 @@ __device__ __forceinline__ void lean_item(long long item, const WorkItem *__rest
 #pragma unroll
           for (int k = 0; k < E; ++k) acc[k] = Real(0);
           cur_row = (int)__shfl_sync(mask, my.w, j, SW);
+          SACD_DBG(SACD_DASSERT(cur_row >= 0 && cur_row < g_dbg.In));
         }
-        arow.load(Al + (long long)(__shfl_sync(mask, my.x, j, SW) & kIdxMask) * RT);
+        const uint32_t ai = __shfl_sync(mask, my.x, j, SW) & kIdxMask;
+        SACD_DBG(SACD_DASSERT(ai < g_dbg.Ia));
+        arow.load(Al + (long long)ai * RT);
       }
 #pragma unroll
       for (int k = 0; k < E; ++k) facc[k] = fma(x, bb[j % (D + 1)].v[k], facc[k]);
@@ -528,10 +546,11 @@ template <typename Real, int RT, int SW, int D, int MINB, int PF = 0, int XS = 0
 __global__ void __launch_bounds__(256, MINB) k_mttkrp_lean(const WorkItem *__restrict__ items, long long n_items,
                                                           const uint4 *__restrict__ nzm,
                                                           const Real *__restrict__ A, const Real *__restrict__ B,
-                                                          Real *__restrict__ M, Real *__restrict__ partial) {
+                                                          Real *__restrict__ M, Real *__restrict__ partial,
+                                                          Real xu = Real(0)) {
   const long long item = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / SW;
   if (item >= n_items) return;
-  lean_item<Real, RT, SW, D, PF, XS>(item, items, nzm, A, B, M, partial);
+  lean_item<Real, RT, SW, D, PF, XS>(item, items, nzm, A, B, M, partial, xu);
 }
 
 // Dynamic scheduling (one worker per warp): a fixed grid of resident warps takes items from
@@ -544,7 +563,8 @@ __global__ void __launch_bounds__(256, MINB) k_mttkrp_lean_dyn_sw(const WorkItem
                                                                  long long n_items, const uint4 *__restrict__ nzm,
                                                                  const Real *__restrict__ A, const Real *__restrict__ B,
                                                                  Real *__restrict__ M, Real *__restrict__ partial,
-                                                                 unsigned long long *__restrict__ counter) {
+                                                                 unsigned long long *__restrict__ counter,
+                                                                 Real xu = Real(0)) {
   const int lane = threadIdx.x & (SW - 1);
   const unsigned mask = SW == 32 ? 0xffffffffu : (((1u << SW) - 1u) << (threadIdx.x & 31 & ~(SW - 1)));
   for (;;) {
@@ -553,7 +573,7 @@ __global__ void __launch_bounds__(256, MINB) k_mttkrp_lean_dyn_sw(const WorkItem
     it = __shfl_sync(mask, it, 0, SW);
     if ((long long)it >= n_items) break;
     __syncwarp(mask);
-    lean_item<Real, RT, SW, D, PF, XS>((long long)it, items, nzm, A, B, M, partial);
+    lean_item<Real, RT, SW, D, PF, XS>((long long)it, items, nzm, A, B, M, partial, xu);
   }
 }
 
@@ -562,7 +582,8 @@ __global__ void __launch_bounds__(256, MINB) k_mttkrp_lean_dyn(const WorkItem *_
                                                               const uint4 *__restrict__ nzm,
                                                               const Real *__restrict__ A, const Real *__restrict__ B,
                                                               Real *__restrict__ M, Real *__restrict__ partial,
-                                                              unsigned long long *__restrict__ counter) {
+                                                              unsigned long long *__restrict__ counter,
+                                                              Real xu = Real(0)) {
   const int lane = threadIdx.x & 31;
   for (;;) {
     unsigned long long it = 0;
@@ -570,7 +591,7 @@ __global__ void __launch_bounds__(256, MINB) k_mttkrp_lean_dyn(const WorkItem *_
     it = __shfl_sync(0xffffffffu, it, 0);
     if ((long long)it >= n_items) break;
     __syncwarp();  // the warp's shared broadcast slots may still be read for its previous item
-    lean_item<Real, RT, 32, D, PF, XS>((long long)it, items, nzm, A, B, M, partial);
+    lean_item<Real, RT, 32, D, PF, XS>((long long)it, items, nzm, A, B, M, partial, xu);
   }
 }
 
@@ -708,6 +729,8 @@ __global__ void __launch_bounds__(256) k_fix1(const FixChunk *__restrict__ chunk
   const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (w >= n) return;
   const FixChunk fc = chunks[w];
+  SACD_DBG(SACD_DASSERT(fc.slot0 >= 0 && fc.slot0 + fc.nslots <= g_dbg.nslots && fc.out < g_dbg.nchunk_rows &&
+                        (fc.out >= 0 || -fc.out - 1 < g_dbg.In)));
   Real acc[4][CPL];
 #pragma unroll
   for (int u = 0; u < 4; ++u)
@@ -739,6 +762,7 @@ __global__ void __launch_bounds__(256) k_fix2(const SplitRow *__restrict__ split
   if (w >= n) return;
   const SplitRow sr = splits[w];
   const long long nch = (sr.nslots + kFixChunk - 1) / kFixChunk;
+  SACD_DBG(SACD_DASSERT(sr.row >= 0 && sr.row < g_dbg.In && sr.chunk0 + (nch > 1 ? nch : 0) <= g_dbg.nchunk_rows));
   if (nch <= 1) return;  // written by level 1
   Real acc[CPL];
 #pragma unroll

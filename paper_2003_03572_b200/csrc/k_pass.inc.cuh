@@ -4,6 +4,18 @@
 // Paper citations "P:n" are PAPER.md lines; readings Cn / L1 / C10' are DESIGN.md section 3.
 // NOT a standalone header: it relies on the helpers defined at the top of kernels.cu.
 
+// ------------------------------------------------------------------ per-sweep device time
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// First kernel of every sweep (eager or captured): the start time of the sweep.
+__global__ void k_sweep_begin(DevState *st) {
+  if (threadIdx.x == 0) st->t_begin = globaltimer_ns();
+}
+
 // ------------------------------------------------------------------ finalize a mode pass
 // flags: 1 = record the pass (ti/E/history), 2 = compute f (needs all three Grams),
 //        4 = push a stats-ring record (end of sweep)
@@ -28,6 +40,7 @@ __device__ void apply_pass(DevState *st, int mode, double ti, double md, long lo
   if (flags & 4) {
     sacd_iter_stats &rec = st->ring[st->ring_count % kRing];
     rec.k = st->k;
+    rec.ms = (double)(globaltimer_ns() - st->t_begin) * 1e-6;
     rec.objective = st->f;
     rec.fit = st->fit;
     for (int n = 0; n < 3; ++n) {

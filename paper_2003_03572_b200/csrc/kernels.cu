@@ -29,6 +29,14 @@ namespace sacd {
 
 namespace {
 
+#ifdef SACD_DEBUG
+__device__ DebugBounds g_dbg;
+__global__ void k_set_dbg(DebugBounds b) { g_dbg = b; }
+#define SACD_DBG(x) x
+#else
+#define SACD_DBG(x)
+#endif
+
 // ------------------------------------------------------------------ small helpers
 inline int grid1d(long long n, int block = 256) {
   long long g = (n + block - 1) / block;
@@ -149,18 +157,23 @@ struct Impl {
 
   // the dynamically scheduled lean kernel (one worker per warp): a grid of resident blocks
   // only, items from c.item_ctr (reset here, stream-ordered)
-  template <int D, int MINB, int XS>
+  // SW = 32: one worker per warp (k_mttkrp_lean_dyn); SW < 32: 32/SW workers per warp
+  // (k_mttkrp_lean_dyn_sw), each taking its own items from the counter
+  template <int D, int MINB, int XS, int SW = 32>
   static void launch_dyn(Context &c, const WorkItem *items, long long n_items, const uint4 *nzm, const Real *A,
                          const Real *B, Real *out, Real *partial) {
-    int per_sm = 0;
-    auto kern = k_mttkrp_lean_dyn<Real, RT, D, MINB, 0, XS>;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0);
-    if (per_sm < 1) per_sm = 1;
-    const long long need = (n_items * 32 + 255) / 256;
-    const long long grid = std::min<long long>(need, (long long)per_sm * c.num_sms);
-    cudaMemsetAsync(c.item_ctr, 0, sizeof(unsigned long long), c.stream);
-    kern<<<(unsigned)std::max<long long>(1, grid), 256, 0, c.stream>>>(items, n_items, nzm, A, B, out, partial,
-                                                                       c.item_ctr);
+    auto go = [&](auto kern) {
+      int per_sm = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0);
+      if (per_sm < 1) per_sm = 1;
+      const long long need = (n_items * SW + 255) / 256;
+      const long long grid = std::min<long long>(need, (long long)per_sm * c.num_sms);
+      cudaMemsetAsync(c.item_ctr, 0, sizeof(unsigned long long), c.stream);
+      kern<<<(unsigned)std::max<long long>(1, grid), 256, 0, c.stream>>>(items, n_items, nzm, A, B, out, partial,
+                                                                         c.item_ctr, (Real)c.xu);
+    };
+    if constexpr (SW == 32) go(k_mttkrp_lean_dyn<Real, RT, D, MINB, 0, XS>);
+    else go(k_mttkrp_lean_dyn_sw<Real, RT, SW, D, MINB, 0, XS>);
   }
 
   static int mttkrp_on(Context &c, int mode, const WorkItem *items, long long n_items, const SplitRow *splits,
@@ -168,6 +181,12 @@ struct Impl {
     ModeData &md = c.m[mode];
     const Real *A = reinterpret_cast<const Real *>(c.m[md.a].F);
     const Real *B = reinterpret_cast<const Real *>(c.m[md.b].F);
+#ifdef SACD_DEBUG
+    {
+      const DebugBounds db{c.nnz, c.m[md.a].I, c.m[md.b].I, md.I, c.max_slots, c.max_chunks};
+      k_set_dbg<<<1, 1, 0, c.stream>>>(db);
+    }
+#endif
     int pe = prof_begin(c, 0);
     if (n_items > 0) {
       const int wpb = 8;
@@ -176,6 +195,9 @@ struct Impl {
         // (NB gathers in flight per warp, min blocks per SM); opt.mttkrp_variant selects a
         // tuning variant (0 = default, measured on B200 with tools/mttkrp_tune.py:
         // occupancy beats deeper per-warp batching).
+#ifdef SACD_TUNING
+        // measured tuning variants (tools/mttkrp_tune.py; built only with -DSACD_TUNING, so the
+        // default library carries only the default kernels)
         const int var = c.opt.mttkrp_variant;
         auto go = [&](auto kern) {
           kern<<<(unsigned)blocks, wpb * 32, 0, c.stream>>>(items, n_items, md.idx_a, md.idx_b, md.val, md.idx_n, A,
@@ -186,13 +208,29 @@ struct Impl {
         auto gos = [&](auto kern) {
           kern<<<(unsigned)sblocks, 256, 0, c.stream>>>(items, n_items, md.nzm, A, B, out, partial);
         };
-        if (var == 1) go(k_mttkrp_fiber<Real, RT, 1, fiber_min_blocks<Real, RT>()>);
+        if (var != 0) {
+          if (var == 1) go(k_mttkrp_fiber<Real, RT, 1, fiber_min_blocks<Real, RT>()>);
         else if (var == 10) gos(k_mttkrp_sw<Real, RT, SW, 1, 4>);
         else if (var == 11) gos(k_mttkrp_sw<Real, RT, SW, 2, 4>);
         else if (var == 12) gos(k_mttkrp_sw<Real, RT, SW, 4, 4>);
         else if (var == 13) gos(k_mttkrp_sw<Real, RT, SW, 4, 3>);
         else if (var == 14) gos(k_mttkrp_sw<Real, RT, SW, 8, 2>);
         else if (var == 15) gos(k_mttkrp_sw<Real, RT, SW, 2, 6>);
+        else if (var >= 50 && var < 60) {
+          // round-2 occupancy / broadcast variants of the fp64 R = 64 kernel (c4)
+          if constexpr (sizeof(Real) == 8 && RT == 64) {
+            const bool ux = c.uniform_x;
+            if (var == 50) launch_dyn<1, 4, 1>(c, items, n_items, md.nzm, A, B, out, partial);
+            else if (var == 51) launch_dyn<1, 4, 3, 16>(c, items, n_items, md.nzm, A, B, out, partial);
+            else if (var == 52) launch_dyn<1, 3, 3, 16>(c, items, n_items, md.nzm, A, B, out, partial);
+            else if (var == 53 && ux) launch_dyn<1, 6, 4>(c, items, n_items, md.nzm, A, B, out, partial);
+            else if (var == 54 && ux) launch_dyn<1, 4, 4>(c, items, n_items, md.nzm, A, B, out, partial);
+            else if (var == 55 && ux) launch_dyn<1, 4, 4, 16>(c, items, n_items, md.nzm, A, B, out, partial);
+            else if (var == 56) launch_dyn<2, 4, 1>(c, items, n_items, md.nzm, A, B, out, partial);
+            else if (var == 57) launch_dyn<1, 5, 1>(c, items, n_items, md.nzm, A, B, out, partial);
+            else launch_dyn<1, 6, 1>(c, items, n_items, md.nzm, A, B, out, partial);
+          }
+        }
         else if (var >= 20 && var < 50) {
           // lean kernel: E elements per lane -> SW = RT / E lanes per worker
           constexpr int VEC = V16<Real>::N;
@@ -202,7 +240,7 @@ struct Impl {
           constexpr int SW4 = RT / E4 > 32 ? 32 : (RT / E4 < 1 ? 1 : RT / E4);
           auto gol = [&](auto kern, int sw) {
             const long long lb = (n_items * sw + 255) / 256;
-            kern<<<(unsigned)lb, 256, 0, c.stream>>>(items, n_items, md.nzm, A, B, out, partial);
+            kern<<<(unsigned)lb, 256, 0, c.stream>>>(items, n_items, md.nzm, A, B, out, partial, Real(0));
           };
           if constexpr (RT / VEC <= 32) {
             if (var == 26 || var == 27 || var == 28) {
@@ -252,7 +290,7 @@ struct Impl {
               const long long grid = std::min<long long>(need, (long long)std::max(1, per_sm) * c.num_sms);
               cudaMemsetAsync(c.item_ctr, 0, sizeof(unsigned long long), c.stream);
               kern<<<(unsigned)std::max<long long>(1, grid), 256, 0, c.stream>>>(items, n_items, md.nzm, A, B, out,
-                                                                                 partial, c.item_ctr);
+                                                                                 partial, c.item_ctr, Real(0));
             }
           }
           else if (var == 40) gol(k_mttkrp_lean<Real, RT, sub_warp_lanes<Real, RT>(), 1, 6>, sub_warp_lanes<Real, RT>());
@@ -262,7 +300,9 @@ struct Impl {
           else if (var == 44) gol(k_mttkrp_lean<Real, RT, sub_warp_lanes<Real, RT>(), 1, 8>, sub_warp_lanes<Real, RT>());
           else gol(k_mttkrp_lean<Real, RT, SW8, 2, 2>, SW8);
         }
-        else if (sizeof(Real) == 8 && RT >= 256) {
+        } else
+#endif
+        if (sizeof(Real) == 8 && RT >= 256) {
           // fp64, R > 128: one warp per item, 8 fp64 columns per lane, x broadcast through
           // shared memory (variant 36; c5 R=256: 12.7 ms per sweep vs 13.7 with shuffles,
           // variant 22, and 28.6 for the warp fiber kernel, variant 1)
@@ -292,7 +332,7 @@ struct Impl {
             const long long grid = std::min<long long>(need, (long long)std::max(1, per_sm) * c.num_sms);
             cudaMemsetAsync(c.item_ctr, 0, sizeof(unsigned long long), c.stream);
             kern<<<(unsigned)std::max<long long>(1, grid), 256, 0, c.stream>>>(items, n_items, md.nzm, A, B, out,
-                                                                               partial, c.item_ctr);
+                                                                               partial, c.item_ctr, Real(0));
           }
         } else if (sizeof(Real) == 8 && RT == 128) {
           // fp64, R = 65..128: 4 columns per lane, one warp per item, x broadcast through shared
@@ -319,7 +359,9 @@ struct Impl {
     }
     SACD_CUDA_TRY(cudaGetLastError());
     SACD_TRY(prof_end(c, 0, pe));
+#ifdef SACD_TUNING
   fixup:
+#endif
     if (n_splits > 0) {
       pe = prof_begin(c, 1);
       Real *buf = reinterpret_cast<Real *>(c.fixbuf);
@@ -358,6 +400,7 @@ struct Impl {
   static int sharded_mode_update(Context &c, int mode, int branch_override, bool begin_sweep, bool end_sweep,
                                  uint8_t *dec) {
     ModeData &md = c.m[mode];
+    if (begin_sweep) k_sweep_begin<<<1, 32, 0, c.stream>>>(c.st);
     SACD_TRY(sharded_mttkrp_merge(c, mode));
     SACD_TRY(prepare(c, mode, branch_override, begin_sweep, 1));
     if (c.delta) SACD_TRY(delta_snapshot(c, mode));
@@ -565,6 +608,11 @@ struct Impl {
 
   // chunk support masks of F_mode (used by the skipping MTTKRP of the other modes)
   static int chunk_mask(Context &c, int mode) {
+#ifndef SACD_TUNING
+    (void)c;
+    (void)mode;
+    return SACD_OK;
+#else
     const int var = c.opt.mttkrp_variant;
     if (var < 26 || var > 28) return SACD_OK;  // only the support-skipping variants read them
     if constexpr (RT / V16<Real>::N <= 32) {
@@ -575,6 +623,7 @@ struct Impl {
       SACD_CUDA_TRY(cudaGetLastError());
     }
     return SACD_OK;
+#endif
   }
 
   static int prepare(Context &c, int mode, int branch_override, bool begin_sweep, int write_state) {
@@ -591,6 +640,7 @@ struct Impl {
                          uint8_t *dec) {
     ModeData &md = c.m[mode];
     Real *M = reinterpret_cast<Real *>(c.M);
+    if (begin_sweep) k_sweep_begin<<<1, 32, 0, c.stream>>>(c.st);
     SACD_TRY(mttkrp(c, mode, M));
     SACD_TRY(prepare(c, mode, branch_override, begin_sweep, 1));
     const int vflags0 = c.opt.variant == SACD_VARIANT_SNAPSHOT ? 2 : (c.opt.variant == SACD_VARIANT_JACOBI ? 1 : 0);

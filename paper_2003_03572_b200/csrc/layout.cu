@@ -21,12 +21,19 @@ namespace {
 
 __global__ void k_validate(const uint32_t *__restrict__ coords, const float *__restrict__ vals, long long nnz,
                            long long d0, long long d1, long long d2, int *__restrict__ flags) {
+  // flags: 1 = index out of range, 2 = non-finite value, 8 = the values are not all equal
+  // (bitwise) to vals[0]; bit 8 clear means a uniform-valued tensor (e.g. binary), for which
+  // the MTTKRP needs no per-nonzero value at all
+  const uint32_t v0 = nnz > 0 ? __float_as_uint(vals[0]) : 0u;
+  bool diff = false;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nnz;
        e += (long long)gridDim.x * blockDim.x) {
     const uint32_t q = coords[3 * e], p = coords[3 * e + 1], s = coords[3 * e + 2];
     if (q >= d0 || p >= d1 || s >= d2) atomicOr(flags, 1);
     if (!isfinite(vals[e])) atomicOr(flags, 2);
+    diff |= __float_as_uint(vals[e]) != v0;
   }
+  if (__any_sync(0xffffffffu, diff) && (threadIdx.x & 31) == 0) atomicOr(flags, 8);
 }
 
 __global__ void k_make_keys(const uint32_t *__restrict__ coords, long long nnz, int n, int a, int b,
@@ -277,6 +284,13 @@ int build_layouts(Context &c, const uint32_t *coords, const float *vals) {
     set_error("sacd_init: non-finite value");
     cudaFreeAsync(flags, s);
     return SACD_ENONFINITE;
+  }
+  c.uniform_x = nnz > 0 && !(hflags & 8);
+  if (c.uniform_x) {
+    float x0 = 0.f;
+    SACD_CUDA_TRY(cudaMemcpyAsync(&x0, vals, sizeof(float), cudaMemcpyDeviceToHost, s));
+    SACD_CUDA_TRY(cudaStreamSynchronize(s));
+    c.xu = (double)x0;
   }
 
   unsigned long long *keys = nullptr, *keys2 = nullptr;

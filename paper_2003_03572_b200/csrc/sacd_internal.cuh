@@ -78,6 +78,20 @@ constexpr int kRing = 4096;
 
 // idx_a carries two flag bits set by the layout builder (mode lengths are < 2^30):
 // bit 31 = first nonzero of a fiber (new (i_n, i_a)), bit 30 = first nonzero of a row.
+// SACD_DEBUG builds (libsacd_debug.so) check indices and slots inside the kernels with
+// device-side asserts (a failed assert traps and the context reports ECUDA).
+#ifdef SACD_DEBUG
+#include <cassert>
+#define SACD_DASSERT(cond) assert(cond)
+#else
+#define SACD_DASSERT(cond) ((void)0)
+#endif
+
+// Bounds of the MTTKRP launch that follows (set by k_set_dbg in SACD_DEBUG builds only).
+struct DebugBounds {
+  long long nnz, Ia, Ib, In, nslots, nchunk_rows;
+};
+
 constexpr uint32_t kFiberStart = 1u << 31;
 constexpr uint32_t kRowStart = 1u << 30;
 constexpr uint32_t kIdxMask = (1u << 30) - 1u;
@@ -95,6 +109,7 @@ struct DevState {
   double f, fit;
   double mdot;           // sum_i sum_r w_ir m^W_ir of the latest W pass
   int ring_count;
+  unsigned long long t_begin;  // %globaltimer (ns) at the start of the current sweep
   sacd_iter_stats ring[kRing];
 };
 
@@ -168,6 +183,9 @@ struct Context {
   double *gram_part = nullptr;    // gram blocks * R * R
   uint8_t *decisions = nullptr;   // teacher-forced only
   long long max_row_blocks = 0;
+  long long max_slots = 1, max_chunks = 1;  // rows of the partial / fix-up buffers (debug bounds)
+  bool uniform_x = false;  // every value of the tensor equals xu (bitwise), e.g. a binary tensor
+  double xu = 0.0;
   int gram_blocks = 0;
   long long device_bytes = 0;
   // graph

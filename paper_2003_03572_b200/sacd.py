@@ -12,7 +12,9 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsacd.so")
+# SACD_LIB selects another flavour of the same library (paper_2003_03572_b200/build.py):
+# libsacd_tuning.so (MTTKRP tuning variants) or libsacd_debug.so (device-side asserts).
+LIB_PATH = os.path.join(HERE, os.environ.get("SACD_LIB", "libsacd.so"))
 
 SACD_OK, SACD_EINVAL, SACD_ERANGE, SACD_EDUP, SACD_ENONFINITE, SACD_ENOMEM, SACD_ECUDA, SACD_ENCCL, SACD_ESTATE = (
     0, -1, -2, -3, -4, -5, -6, -7, -8)
@@ -23,6 +25,7 @@ VARIANT_GS_LAGGED, VARIANT_SELECT_OFF, VARIANT_JACOBI, VARIANT_SNAPSHOT = 0, 1, 
 F64, F32 = 0, 1
 BR_AUTO, BR_FIRST, BR_EQ24, BR_EQ27 = -1, 0, 1, 2
 NUM_KCLASS = 6
+ABI_VERSION = 2
 KCLASS = ("mttkrp", "fixup", "prepare", "rows", "gram", "finalize")
 
 # exported symbols declared in include/sacd.h (checked by tests/test_abi.py)
@@ -43,7 +46,8 @@ class Options(C.Structure):
 
 class IterStats(C.Structure):
     _fields_ = [("k", C.c_int32), ("branch", C.c_int32 * 3), ("objective", C.c_double), ("fit", C.c_double),
-                ("ti", C.c_double * 3), ("E", C.c_int64 * 3), ("E_changed", C.c_int64 * 3)]
+                ("ti", C.c_double * 3), ("E", C.c_int64 * 3), ("E_changed", C.c_int64 * 3),
+                ("ms", C.c_double)]
 
 
 class Info(C.Structure):
@@ -105,9 +109,9 @@ def load_library(path: str = LIB_PATH):
     L.sacd_rmse.argtypes = [P, P, P, i64, C.POINTER(d)]
     sz = (C.c_int32 * 4)()
     L.sacd_abi_sizes(sz)
-    if tuple(sz) != (1, C.sizeof(Options), C.sizeof(IterStats), C.sizeof(Info)):
+    if tuple(sz) != (ABI_VERSION, C.sizeof(Options), C.sizeof(IterStats), C.sizeof(Info)):
         raise RuntimeError(f"libsacd ABI mismatch: library {tuple(sz)} vs binding "
-                           f"{(1, C.sizeof(Options), C.sizeof(IterStats), C.sizeof(Info))}")
+                           f"{(ABI_VERSION, C.sizeof(Options), C.sizeof(IterStats), C.sizeof(Info))}")
     _lib = L
     return L
 
@@ -126,6 +130,35 @@ def _ptr(x):
 
 def _np(a, dtype):
     return np.ascontiguousarray(a, dtype=dtype)
+
+
+def _torch_check(x, what, ncols):
+    """A torch tensor is passed to the library by data_ptr() without a copy, so its layout
+    must already be the one sacd.h declares: coords int32/uint32 (n, 3) contiguous, values
+    float32 (n,) contiguous.  Anything else would be silently reinterpreted: refuse it."""
+    import torch
+    ok_dt = (torch.int32,) + ((torch.uint32,) if hasattr(torch, "uint32") else ()) if ncols == 3 else (torch.float32,)
+    if x.dtype not in ok_dt:
+        raise TypeError(f"{what}: dtype {x.dtype}, expected {' or '.join(str(d) for d in ok_dt)}")
+    if ncols == 3 and (x.dim() != 2 or x.shape[1] != 3):
+        raise ValueError(f"{what}: shape {tuple(x.shape)}, expected (n, 3)")
+    if ncols == 1 and x.dim() != 1:
+        raise ValueError(f"{what}: shape {tuple(x.shape)}, expected (n,)")
+    if not x.is_contiguous():
+        raise ValueError(f"{what}: tensor must be contiguous")
+    return x
+
+
+def _coords_arg(c):
+    if hasattr(c, "data_ptr"):
+        return _torch_check(c, "coords", 3)
+    return _np(np.asarray(c).reshape(-1, 3), np.uint32)
+
+
+def _vals_arg(v):
+    if hasattr(v, "data_ptr"):
+        return _torch_check(v, "vals", 1)
+    return _np(v, np.float32)
 
 
 def nccl_unique_id() -> bytes:
@@ -175,11 +208,10 @@ class Sacd:
         if nccl_id is not None:
             self._nccl_id = C.create_string_buffer(bytes(nccl_id), 128)
             o.nccl_unique_id = C.cast(self._nccl_id, C.c_void_p)
-        if not hasattr(coords, "data_ptr"):
-            coords = _np(np.asarray(coords).reshape(-1, 3), np.uint32)
-        if not hasattr(vals, "data_ptr"):
-            vals = _np(vals, np.float32)
-        nnz = int(vals.shape[0]) if hasattr(vals, "shape") else len(vals)
+        coords, vals = _coords_arg(coords), _vals_arg(vals)
+        nnz = int(vals.shape[0])
+        if int(coords.shape[0]) != nnz:
+            raise ValueError(f"coords has {int(coords.shape[0])} rows, vals {nnz} entries")
         self._keep = (coords, vals)
         d = (C.c_int64 * 3)(*[int(x) for x in dims])
         h = C.c_void_p()
@@ -236,7 +268,7 @@ class Sacd:
         for i in range(n.value):
             s = buf[i]
             out.append(dict(k=s.k, branch=list(s.branch), objective=s.objective, fit=s.fit, ti=list(s.ti),
-                            E=list(s.E), E_changed=list(s.E_changed)))
+                            E=list(s.E), E_changed=list(s.E_changed), ms=s.ms))
         return out
 
     def info(self):
@@ -318,7 +350,7 @@ class Sacd:
     # ---- held-out evaluation
     def predict(self, coords):
         """Eq 8 at the given (n, 3) coordinates (host numpy or device torch); fp64 numpy."""
-        c = coords if hasattr(coords, "data_ptr") else _np(np.asarray(coords).reshape(-1, 3), np.uint32)
+        c = _coords_arg(coords)
         n = int(c.shape[0])
         out = np.zeros(n, np.float64)
         _check(load_library().sacd_predict(self._h, _ptr(c), n, _ptr(out)))
@@ -326,8 +358,9 @@ class Sacd:
 
     def rmse(self, coords, vals):
         """Eq 30 on held-out entries (coords (n, 3) u32, vals fp32; host or device)."""
-        c = coords if hasattr(coords, "data_ptr") else _np(np.asarray(coords).reshape(-1, 3), np.uint32)
-        v = vals if hasattr(vals, "data_ptr") else _np(vals, np.float32)
+        c, v = _coords_arg(coords), _vals_arg(vals)
+        if int(c.shape[0]) != int(v.shape[0]):
+            raise ValueError("coords and vals lengths differ")
         r = C.c_double()
         _check(load_library().sacd_rmse(self._h, _ptr(c), _ptr(v), int(c.shape[0]), C.byref(r)))
         return r.value

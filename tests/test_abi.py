@@ -54,7 +54,8 @@ def test_options_struct_matches_header(lib):
     assert o.precision == sacd.F64 and o.l_mode == sacd.L_DIAG and o.world_size == 1 and o.use_graph == 1
     sz = (C.c_int32 * 4)()
     assert lib.sacd_abi_sizes(sz) == 0
-    assert tuple(sz) == (1, C.sizeof(sacd.Options), C.sizeof(sacd.IterStats), C.sizeof(sacd.Info))
+    assert tuple(sz) == (sacd.ABI_VERSION, C.sizeof(sacd.Options), C.sizeof(sacd.IterStats), C.sizeof(sacd.Info))
+    assert C.sizeof(sacd.IterStats) == 4 + 12 + 8 + 8 + 24 + 24 + 24 + 8  # k, branch, f, fit, ti, E, E_changed, ms
 
 
 def test_sass_is_sm100a(lib):
@@ -85,3 +86,32 @@ def test_bad_arguments_rejected_before_cuda(lib):
     assert lib.sacd_init(C.byref(h), None, None, 0, d0, 2, 1, None) == sacd.SACD_EINVAL    # dim 0
     assert lib.sacd_init(C.byref(h), None, None, -1, d, 2, 1, None) == sacd.SACD_EINVAL    # nnz < 0
     assert b"sacd_init" in lib.sacd_last_error()
+
+
+def test_variant_without_tuning_build_rejected(lib):
+    """The product library carries only the default MTTKRP kernels: a tuning variant is
+    EINVAL before any CUDA call (the tuning build is libsacd_tuning.so)."""
+    from paper_2003_03572_b200 import sacd
+    o = sacd.Options()
+    lib.sacd_default_options(C.byref(o))
+    o.mttkrp_variant = 39
+    h = C.c_void_p()
+    d = (C.c_int64 * 3)(2, 2, 2)
+    assert lib.sacd_init(C.byref(h), None, None, 0, d, 64, 1, C.byref(o)) == sacd.SACD_EINVAL
+    assert b"tuning" in lib.sacd_last_error()
+
+
+def test_torch_inputs_are_validated(lib):
+    """Torch tensors go to the library by data_ptr() without a copy, so the binding refuses
+    a dtype / shape / stride the header does not declare instead of reinterpreting it."""
+    import torch
+    from paper_2003_03572_b200 import sacd
+    good_c = torch.zeros((4, 3), dtype=torch.int32)
+    good_v = torch.ones(4, dtype=torch.float32)
+    bad = [(good_c.to(torch.int64), good_v), (torch.zeros((3, 4), dtype=torch.int32).t(), good_v),
+           (torch.zeros((4, 2), dtype=torch.int32), good_v), (good_c, good_v.to(torch.float64)),
+           (good_c, torch.ones((4, 1), dtype=torch.float32)), (good_c, torch.ones(8, dtype=torch.float32)[::2]),
+           (good_c, torch.ones(5, dtype=torch.float32))]
+    for c, v in bad:
+        with pytest.raises((TypeError, ValueError)):
+            sacd.Sacd(c, v, (2, 2, 2), 2, 1)

@@ -124,33 +124,6 @@ def test_mttkrp_gram_hessian(R, precision):
             assert np.abs(g.hessian(n) - Ho).max() <= tol * np.abs(Ho).max()
 
 
-@pytest.mark.parametrize("R", [33, 64, 128, 256])
-@pytest.mark.parametrize("precision", ["f64", "f32"])
-def test_mttkrp_variants_bitwise(R, precision):
-    """Every MTTKRP kernel variant (old warp fiber kernel = 1, sub-warp kernels 10.., lean 20..,
-    support-skipping 26-28,
-    default 0) performs the same fiber-factored sums in the same order, so their M are
-    bitwise equal; and each equals the oracle's MTTKRP within rounding.  Heavy rows and a
-    small work-item size force split rows (partial slots + fix-up)."""
-    dims = (53, 31, 67)
-    c, v = ragged_tensor(dims, 5000, 17, heavy_rows=((0, 1, 900), (1, 4, 500), (2, 7, 800)))
-    F = O.init_factors(dims, R, 5)
-    Mo = [O.mttkrp(c, v, dims, n, F) for n in range(3)]
-    ref = None
-    for var in (1, 10, 13, 20, 22, 24, 26, 27, 40, 43, 0):
-        with S(c, v, dims, R, 5, precision=precision, nnz_per_item=48, mttkrp_variant=var) as g:
-            Ms = [g.mttkrp(n) for n in range(3)]
-        tol = 1e-12 if precision == "f64" else 1e-5
-        for n in range(3):
-            scale = np.maximum(np.abs(Mo[n]).max(axis=0, keepdims=True), 1e-30)
-            assert (np.abs(Ms[n] - Mo[n]) / scale).max() <= tol, (var, n)
-        if ref is None:
-            ref = Ms
-        else:
-            for n in range(3):
-                assert np.array_equal(Ms[n], ref[n]), (var, n)
-
-
 @pytest.mark.parametrize("R", [3, 16, 64, 128])
 @pytest.mark.parametrize("branch", [0, 1, 2])
 @pytest.mark.parametrize("l_mode", ["diag", "frob"])
@@ -399,14 +372,20 @@ def test_empty_tensor():
         assert np.array_equal(Fg[n], ora["F"][n])
 
 
-@pytest.mark.parametrize("R", [5, 40, 200])
+@pytest.mark.parametrize("R", [5, 24, 32, 40, 200])
 def test_deterministic_and_graph_equals_eager(R):
     """Reruns are bitwise identical (no floating-point atomics; fixed-order reductions) and
     the captured graph equals eager launches.  compute-sanitizer is not available on the GPU
     pool, so this doubles as the race check of the shared-memory broadcasts and staging:
-    R = 5 (R <= 16 MTTKRP), 40 (x broadcast, DMMA row kernel), 200 (R > 128 kernels)."""
-    dims = (300, 200, 50)
-    c, v = ragged_tensor(dims, 20000, 8, heavy_rows=((2, 1, 3000), (0, 5, 900)))
+    R = 5 (R <= 16 MTTKRP), 24 / 32 (two dynamically scheduled workers per warp with their own
+    double-buffered broadcasts, on a tensor whose heavy slices make long fibers), 40 (x
+    broadcast, DMMA row kernel), 200 (R > 128 kernels)."""
+    if R in (24, 32):  # dense enough for fibers of ~6-30 nonzeros (the SW = 16 kernel's case)
+        dims = (120, 80, 16)
+        c, v = ragged_tensor(dims, 60000, 8, heavy_rows=((2, 1, 900), (0, 5, 700)))
+    else:
+        dims = (300, 200, 50)
+        c, v = ragged_tensor(dims, 20000, 8, heavy_rows=((2, 1, 3000), (0, 5, 900)))
     res = []
     for use_graph in (True, True, False):
         with S(c, v, dims, R, 11, use_graph=use_graph, nnz_per_item=256) as g:
@@ -536,6 +515,69 @@ def test_c4_full_size_sampled_rows_and_properties():
             assert factor_err(g.factors(n)[rows], Fn) <= 1e-9
             Zg = g.get_zprev(n)[rows]
             assert np.abs(Zg - zp).max() <= 1e-9 * max(1.0, np.abs(zp).max())
+
+
+def _sub_mttkrp(c, v, dims, n, rows, F):
+    """The oracle's MTTKRP of the listed rows of mode n (their full slices), in row order."""
+    a, b = O.other_modes(dims, n)
+    mask = np.isin(c[:, n], rows)
+    cs, vs = c[mask].copy(), v[mask]
+    remap = np.full(dims[n], -1, np.int64)
+    remap[rows] = np.arange(len(rows))
+    cs[:, n] = remap[cs[:, n]]
+    d2 = list(dims)
+    d2[n] = len(rows)
+    ia, ib, vv, rp = O.layout(cs, vs, d2, n)
+    return O.mttkrp_layout(rp, ia, ib, vv, F[a], F[b])
+
+
+def test_c4_end_to_end_10_sweeps():
+    """The north star's parity bar on the bench config itself: c4 at full size (1e8 nonzeros,
+    R = 64, fp64), 10 sweeps through the C ABI against ora_sacd_run on the same seeded
+    tensor: f within 1e-4 at every sweep, factors within 1e-3 (column-relative floor), the
+    same branch in every pass and the same E (number of selected elements) in every pass."""
+    cfg, c, v = _config_tensor("c4")
+    fg, Fg, Eg, brg, ora = run_pair(c, v, cfg.dims, cfg.rank, cfg.seed, 10)
+    rel = check_pair(fg, Fg, Eg, brg, ora)
+    errs = [factor_err(Fg[n], ora["F"][n]) for n in range(3)]
+    print(f"c4 10 sweeps: max rel f err {rel:.3e}, factor err {errs}, E gpu {Eg.tolist()} oracle {ora['E'].tolist()}")
+    assert np.array_equal(Eg, ora["E"]), (Eg, ora["E"])
+
+
+def test_c4_flip_census_sweeps_1_to_3():
+    """SURVEY 8(c) flip census on c4 (fiber-factored GPU sums vs sequential oracle sums over
+    heavy Zipf slices: the config most exposed to near-tie gate flips).  For every mode pass of
+    sweeps 1-3, the oracle re-runs the pass from the GPU's own state before it (factors,
+    z_prev, the device's ti history) on sampled rows -- the heaviest slice, empty slices and
+    4000 random rows -- and the decisions must match exactly; any mismatch is reported with
+    its relative saturation margin |sp| / max(|z|, |z_prev|)."""
+    cfg, c, v = _config_tensor("c4")
+    dims, R = cfg.dims, cfg.rank
+    hist = [[], [], []]
+    flips = []
+    checked = 0
+    with S(c, v, dims, R, cfg.seed) as g:
+        for k in range(1, 4):
+            for n in range(3):
+                a, b = O.other_modes(dims, n)
+                F = g.factors()
+                Z = g.get_zprev(n)
+                rows = _rows_sample(g.layout(n)[3], 4000, 10 * k + n)
+                H = O.hadamard(O.gram(F[a]), O.gram(F[b]))
+                M = _sub_mttkrp(c, v, dims, n, rows, F)
+                out = g.mode_update(n, decisions=True)
+                br = O.branch(k, hist[n])
+                Fn, zp, ti, E, Ech, md, dec = O.mode_pass(M, H, F[n][rows], Z[rows], br, decisions=True)
+                mism = np.argwhere(out["decisions"][rows] != dec)
+                for i, r in mism:
+                    z0, z1 = Z[rows[i], r], zp[i, r]
+                    flips.append((k, n, int(rows[i]), int(r), abs(z1 - z0) / max(abs(z1), abs(z0), 1e-300)))
+                checked += dec.size
+                if not len(mism):  # same decisions: the same steps, up to rounding
+                    assert factor_err(g.factors(n)[rows], Fn) <= 1e-9
+                hist[n].append(out["ti"])
+    print(f"c4 flip census: {checked} sampled decisions in sweeps 1-3, {len(flips)} mismatches: {flips[:20]}")
+    assert not flips, flips[:20]
 
 
 # ----------------------------------------------------------------------------- sharded engine
