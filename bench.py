@@ -126,80 +126,97 @@ def algorithmic_bytes(cfg_dims, nnz, R, s):
 
 # ----------------------------------------------------------------------------- oracle (CPU) leg
 class OracleSweepSample:
-    """The fp64 oracle's sweep (oracle.sacd_run, as it stands) on a bounded sample of rows.
+    """The fp64 oracle's sweep (oracle.sacd_run, as it stands) on a bounded sample.
 
     Per sweep, ora_sacd_run does for each mode n: the Grams of the two other factors, their
     Hadamard product, the MTTKRP of every row of mode n over its full slice, and the row pass;
-    then the three Grams for the objective -- so every factor's Gram three times.  A step here
-    runs exactly those oracle functions on every `step`-th row of each mode (with each
-    sampled row's FULL slice, so fibers and slice lengths are those of the workload):
-      * mttkrp_layout of the sampled rows (output: the sampled rows only),
-      * mode_pass of the sampled rows (M, H, z_prev of those rows),
-      * 3 x gram of every `step`-th row of each factor.
-    The full-sweep time is estimated by scaling the MTTKRP by nnz / sampled nnz and the row
-    pass and Grams by rows / sampled rows (each is linear in what it is scaled by).  Layout
-    building (init work) happens untimed in the constructor.  ms_per_step reports the time
-    actually spent per step; value = 1 / (estimated full-sweep seconds)."""
+    then the three Grams for the objective (every factor's Gram three times).  A step runs
+    exactly those oracle functions on samples, and estimates the full sweep:
+      * MTTKRP: the rows of each mode are stratified by slice length (classes [2^j, 2^(j+1)));
+        in every class a systematic sample of rows (with their FULL slices) gets the
+        oracle's mttkrp_layout, weighted by rows in class / rows sampled.  The oracle's cost
+        per nonzero depends on the slice length (it walks a slice once per column, so long
+        Zipf slices fall out of cache), which is why a single systematic sample scaled by the
+        nonzero share misestimates it;
+      * row pass and Grams (cost per row independent of the data): every `rstep`-th row,
+        scaled by the row share.
+    Layouts of the samples are built untimed in the constructor.  step_seconds() returns
+    (seconds actually spent, estimated full-sweep seconds)."""
 
-    def __init__(self, c, v, dims, R, seed, step):
+    def __init__(self, c, v, dims, R, seed, budget=3_000_000, rstep=None):
         import oracle as O
         O.build()
-        self.O, self.dims, self.R, self.step = O, dims, R, step
+        self.O, self.dims, self.R = O, dims, R
         F = O.init_factors(dims, R, seed)
         self.F = F
-        self.sub = []
+        self.rstep = rstep or max(1, int(round(sum(dims) / 100_000)))
+        self.strata = []   # (mode, weight, layout, nnz)
         self.nnz = len(v)
         self.nnz_s = 0
         for n in range(3):
             a, b = O.other_modes(dims, n)
-            rows = np.arange(0, dims[n], step, dtype=np.int64)
-            mask = (c[:, n].astype(np.int64) % step) == 0
-            cs, vs = c[mask].copy(), v[mask]
-            cs[:, n] = cs[:, n] // step
-            d2 = list(dims)
-            d2[n] = len(rows)
-            lay = O.layout(cs, vs, d2, n)
+            ci = c[:, n].astype(np.int64)
+            ln = np.bincount(ci, minlength=dims[n])
+            cls = np.where(ln > 0, np.floor(np.log2(np.maximum(ln, 1))).astype(np.int64), -1)
+            classes = [k for k in np.unique(cls) if k >= 0]
+            per = budget / max(1, len(classes))
+            pick = np.zeros(dims[n], np.int64)   # stratum id + 1 of each sampled row, 0 = not sampled
+            info = []
+            for j, k in enumerate(classes):
+                rows = np.nonzero(cls == k)[0]
+                step = max(1, int(np.ceil(ln[rows].sum() / per)))
+                sel = rows[::step]
+                pick[sel] = j + 1
+                info.append((len(rows) / len(sel), sel))
+            take = pick[ci] > 0
+            cs, vs, st = c[take], v[take], pick[ci[take]] - 1
+            for j, (w, sel) in enumerate(info):
+                m = st == j
+                cj, vj = cs[m].copy(), vs[m]
+                remap = np.full(dims[n], -1, np.int64)
+                remap[sel] = np.arange(len(sel))
+                cj[:, n] = remap[cj[:, n]]
+                d2 = list(dims)
+                d2[n] = len(sel)
+                self.strata.append((n, a, b, w, O.layout(cj, vj, d2, n)))
+                self.nnz_s += len(vj)
+        self.rows = []
+        for n in range(3):
+            a, b = O.other_modes(dims, n)
             H = O.hadamard(O.gram(F[a]), O.gram(F[b]))
-            self.sub.append((a, b, lay, np.ascontiguousarray(F[n][rows]), H, len(vs)))
-            self.nnz_s += len(vs)
-        self.gsub = [np.ascontiguousarray(F[n][::step]) for n in range(3)]
+            Fs = np.ascontiguousarray(F[n][::self.rstep])
+            self.rows.append((H, Fs, np.zeros_like(Fs)))
 
     def step_seconds(self):
-        """(seconds actually spent, estimated full-sweep seconds)"""
         O = self.O
         spent, full = 0.0, 0.0
-        for n in range(3):
-            a, b, (ia, ib, vv, rp), Fs, H, nnz_n = self.sub[n]
+        for n, a, b, w, (ia, ib, vv, rp) in self.strata:
             t0 = time.perf_counter()
-            M = O.mttkrp_layout(rp, ia, ib, vv, self.F[a], self.F[b])
-            t1 = time.perf_counter()
+            O.mttkrp_layout(rp, ia, ib, vv, self.F[a], self.F[b])
+            dt = time.perf_counter() - t0
+            spent += dt
+            full += dt * w
+        for n in range(3):
+            H, Fs, M = self.rows[n]
+            t0 = time.perf_counter()
             O.mode_pass(M, H, Fs, np.zeros_like(Fs), O.BR_FIRST)
-            t2 = time.perf_counter()
-            spent += t2 - t0
-            full += (t1 - t0) * (self.nnz / max(nnz_n, 1)) + (t2 - t1) * (self.dims[n] / max(len(Fs), 1))
-        for n in range(3):
-            t0 = time.perf_counter()
             for _ in range(3):
-                O.gram(self.gsub[n])
-            t1 = time.perf_counter()
-            spent += t1 - t0
-            full += (t1 - t0) * (self.dims[n] / max(len(self.gsub[n]), 1))
+                O.gram(Fs)
+            dt = time.perf_counter() - t0
+            spent += dt
+            full += dt * (self.dims[n] / len(Fs))
         return spent, full
 
     def describe(self):
-        return (f"oracle sweep functions as they stand (mttkrp_layout + mode_pass of every {self.step}th row of each "
-                f"mode over its full slice: {self.nnz_s} of 3x{self.nnz} slice nonzeros; 3 x gram of every "
-                f"{self.step}th factor row), scaled by nnz / rows share to one sweep; layouts built untimed")
-
-
-def sample_step(nnz):
-    """rows step: ~1e7 slice nonzeros per step (3 modes) on c4, i.e. a few seconds of oracle work"""
-    return max(1, int(round(3 * nnz / 1e7)))
+        return (f"oracle sweep functions as they stand: mttkrp_layout on slice-length-stratified row samples "
+                f"({len(self.strata)} strata, {self.nnz_s} of 3x{self.nnz} slice nonzeros, weighted by rows / "
+                f"sampled rows per stratum) + mode_pass and 3 x gram on every {self.rstep}th row (scaled by the "
+                f"row share); sample layouts built untimed")
 
 
 def cpu_baseline(c, v, dims, R, seed, nnz, reps=3):
     import oracle as O
-    smp = OracleSweepSample(c, v, dims, R, seed, sample_step(nnz))
+    smp = OracleSweepSample(c, v, dims, R, seed)
     res = [smp.step_seconds() for _ in range(reps)]
     full = float(np.median([r[1] for r in res]))
     spent = float(np.median([r[0] for r in res]))
@@ -215,6 +232,23 @@ def cpu_baseline(c, v, dims, R, seed, nnz, reps=3):
     except (OSError, ValueError):
         pass
     return out
+
+
+def measured_gather_peak():
+    """Best row-gather rate of the production transport (ldg kernels) on the L1-resident
+    table in profiles/r02_gather_bench.jsonl (tools/gather_bench.cu, one B200)."""
+    best = None
+    try:
+        for ln in open(os.path.join(ROOT, "profiles", "r02_gather_bench.jsonl")):
+            if not ln.startswith('{"table"'):
+                continue
+            r = json.loads(ln)
+            if r["table"].startswith("L1") and r["kernel"].startswith("ldg"):
+                best = max(best or 0.0, r["row_GBps"])
+    except (OSError, ValueError, KeyError):
+        return None, None
+    return best, ("measured: tools/gather_bench.cu ldg transport on an L1-resident 512-byte-row table "
+                  "(profiles/r02_gather_bench.jsonl)")
 
 
 def _cfg_name_for(dims):
@@ -239,7 +273,7 @@ def run_reference(args, cfg, R):
     c, v = SI.make_tensor(cfg, device=dev)
     c, v = c.cpu().numpy().astype(np.uint32), v.cpu().numpy()
     nnz = len(v)
-    smp = OracleSweepSample(c, v, cfg.dims, R, cfg.seed, sample_step(nnz))
+    smp = OracleSweepSample(c, v, cfg.dims, R, cfg.seed)
     K = args.steps if args.steps is not None else 5
     for _ in range(args.warmup):
         smp.step_seconds()
@@ -385,14 +419,19 @@ def main():
     pitch = info["pitch"]
     fib = info.get("fibers", [0, 0, 0])
     if world == 1 and all(f > 0 for f in fib):
-        gathered = sum((nnz + fib[n]) * pitch * s + 16 * nnz for n in range(3)) / 3
-        l1_peak = 148 * 128 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e9
-        roofline["l1_gather"] = {"achieved": gathered / (mt_ms / 1e3) / 1e9, "peak": l1_peak, "unit": "GB/s",
-                                 "frac": gathered / (mt_ms / 1e3) / 1e9 / l1_peak,
-                                 "bytes_per_launch": gathered,
-                                 "what": "factor-row gathers (nnz + fibers) x R_pad x s + 16 B records per MTTKRP "
-                                         "launch through L1, vs 148 SM x 128 B/clk; ncu shows the L1 data pipe "
-                                         "at 80-84% of peak in the U/V modes (wavefronts incl. broadcasts)"}
+        # factor-row bytes the MTTKRP moves through L1 per launch (nnz b-rows + one a-row per
+        # fiber), against the MEASURED ceiling of the same transport (tools/gather_bench.cu:
+        # random 512-byte rows, index by shuffle, x by shared-memory broadcast, LDG.128 per
+        # lane, L1-resident table; profiles/r02_gather_bench.jsonl) and the nominal L1 rate
+        gathered = sum((nnz + fib[n]) * pitch * s for n in range(3)) / 3
+        l1_nominal = 148 * 128 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e9
+        gpeak, gsrc = measured_gather_peak()
+        ach = gathered / (mt_ms / 1e3) / 1e9
+        roofline["l1_gather"] = {"achieved": ach, "peak": gpeak or l1_nominal, "unit": "GB/s",
+                                 "frac": ach / (gpeak or l1_nominal), "bytes_per_launch": gathered,
+                                 "peak_source": gsrc if gpeak else "nominal 148 SM x 128 B/clk (no measurement)",
+                                 "nominal_peak": l1_nominal, "frac_of_nominal": ach / l1_nominal,
+                                 "what": "factor-row gathers (nnz + fibers) x R_pad x s per MTTKRP launch through L1"}
 
     # ---- SURVEY 8(d) protocol: repetitions, each with a fresh sacd_init (N = 1)
     g.close()

@@ -137,6 +137,9 @@ typedef struct {
   int64_t delta_elems_sent; /* NCCL delta exchange so far: elements sent as (index, value) ...  */
   int64_t full_elems_equiv; /* ... and the elements the full-row exchange would have sent       */
   int64_t fibers[3];        /* distinct (i_n, i_a) per layout: the MTTKRP's per-fiber gathers    */
+  int32_t uniform_values;   /* 1: every value equals the first (bitwise), e.g. a binary tensor:  */
+                            /* the MTTKRP then needs no per-nonzero value (exact)                */
+  double uniform_value;     /* that value (0 unless uniform_values)                              */
 } sacd_info;
 
 void sacd_default_options(sacd_options *opt);

@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <new>
+#include <thread>
 #include <vector>
 
 #include <nccl.h>
@@ -340,6 +341,9 @@ static void destroy(sacd_ctx *c) {
   cudaFree(c->xid);
   cudaFree(c->xrow);
   cudaFree(c->xstats);
+  if (c->pin) cudaFreeHost(c->pin);
+  for (auto e : c->pin_ev)
+    if (e) cudaEventDestroy(e);
   if (c->comm) ncclCommDestroy(reinterpret_cast<ncclComm_t>(c->comm));
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   {
@@ -455,9 +459,13 @@ static int init_impl(Context *c, const uint32_t *coords, const float *vals, uint
   // 2%); 256 for mid-size tensors (c2 0.25 -> 0.08 ms, c3 1.21 -> 1.08, c5 R=8/16 -14..16%)
   // and for a sharded rank (c4, 8 emulated ranks: 17.2 -> 13.2 ms summed); 64 under 1e5
   // nonzeros (c1 0.095 -> 0.041 ms).
+  // The same T for the sharded engine as for one GPU (by the whole tensor's size): split rows
+  // then have the same row-relative segments, so a one-rank sharded run sums every row of M in
+  // the unsharded order (bitwise equal results, test_sharded_nccl_world1_matches_unsharded).
+  // The dynamically scheduled kernels removed the last-wave tail that made 256-nonzero items
+  // worth it for a sharded rank in round 1.
   long long T = 1024;
   if (c->opt.nnz_per_item > 0) T = c->opt.nnz_per_item;
-  else if (c->sharded) T = 256;
   else if (c->pitch >= 128 || c->nnz >= 50000000LL) T = 1024;
   else if (c->nnz < 100000) T = 64;
   else T = 256;
@@ -629,15 +637,19 @@ static int init_impl(Context *c, const uint32_t *coords, const float *vals, uint
   SACD_CUDA_TRY(cudaMalloc(&c->Hd, (size_t)R * R * 8));
   SACD_CUDA_TRY(cudaMalloc(&c->row_part, (size_t)c->max_row_blocks * 2 * 8));
   SACD_CUDA_TRY(cudaMalloc(&c->cnt_part, (size_t)c->max_row_blocks * 2 * 8));
-  SACD_CUDA_TRY(cudaMalloc(&c->gram_part, (size_t)c->gram_blocks * R * R * 8));
+  // Gram partials: the separate Gram kernel's row ranges, or one per CTA of the row update
+  // with the fused Gram (at most 4 resident CTAs per SM)
+  c->gram_cap = (c->opt.precision == SACD_F64 && c->pitch <= 64) ? std::max(c->gram_blocks, 4 * std::max(1, c->num_sms))
+                                                                 : c->gram_blocks;
+  SACD_CUDA_TRY(cudaMalloc(&c->gram_part, (size_t)c->gram_cap * R * R * 8));
   c->device_bytes += (long long)((size_t)maxI * P * rs + (size_t)max_slots * P * rs + (size_t)P * P * rs +
-                                 (size_t)c->max_row_blocks * 32 + (size_t)c->gram_blocks * R * R * 8 +
+                                 (size_t)c->max_row_blocks * 32 + (size_t)c->gram_cap * R * R * 8 +
                                  sizeof(DevState));
   if (c->sharded) {
     for (Shard &sh : c->shards) {
       SACD_CUDA_TRY(cudaMalloc(&sh.row_part, (size_t)c->max_row_blocks * 2 * 8));
       SACD_CUDA_TRY(cudaMalloc(&sh.cnt_part, (size_t)c->max_row_blocks * 2 * 8));
-      SACD_CUDA_TRY(cudaMalloc(&sh.gram_part, (size_t)c->gram_blocks * R * R * 8));
+      SACD_CUDA_TRY(cudaMalloc(&sh.gram_part, (size_t)c->gram_cap * R * R * 8));
     }
     SACD_CUDA_TRY(cudaMalloc(&c->xid, (size_t)c->G * 8));
     SACD_CUDA_TRY(cudaMalloc(&c->xrow, (size_t)c->G * P * rs));
@@ -663,22 +675,98 @@ static int dev_read(Context *c, T *dst, const void *src, size_t bytes) {
   return SACD_OK;
 }
 
-// factor-like matrix (Real, pitch) -> host fp64 with leading dimension ld
+// Host copy of `rows` rows of R doubles (src dense, row stride R) into dst (row stride ld),
+// split over up to 8 threads: the destination is usually fresh pageable memory whose page
+// faults dominate a single-threaded copy.
+static void host_rows_copy(double *dst, long long ld, const double *src, long long rows, int R) {
+  const size_t bytes = (size_t)rows * R * 8;
+  const int nt = (int)std::max<size_t>(1, std::min<size_t>(8, bytes >> 22));  // >= 4 MB per thread
+  auto part = [&](int t) {
+    const long long r0 = rows * t / nt, r1 = rows * (t + 1) / nt;
+    if (ld == R) {
+      memcpy(dst + r0 * ld, src + r0 * R, (size_t)(r1 - r0) * R * 8);
+    } else {
+      for (long long r = r0; r < r1; ++r) memcpy(dst + r * ld, src + r * R, (size_t)R * 8);
+    }
+  };
+  if (nt == 1) {
+    part(0);
+    return;
+  }
+  std::vector<std::thread> th;
+  for (int t = 1; t < nt; ++t) th.emplace_back(part, t);
+  part(0);
+  for (auto &x : th) x.join();
+}
+
+static bool is_pinned_host(const void *p) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
+// factor-like matrix (Real, pitch) -> host fp64 with leading dimension ld.  Pinned `out`:
+// one 2D copy.  Pageable `out`: through the context's pinned ring of two chunks, the D2H copy
+// of chunk i + 1 overlapping the multi-threaded host copy of chunk i (the copy engine then
+// runs at pinned bandwidth instead of the driver's single staging path for pageable memory).
 static int read_matrix(Context *c, const void *src, long long rows, double *out, long long ld, bool ttl = false) {
   double *tmp = nullptr;
   cudaStream_t s = c->stream;
   SACD_CUDA_TRY(cudaMallocAsync(&tmp, (size_t)std::max(1LL, rows) * c->R * 8, s));
   int rc = launch_convert_out(*c, src, rows, tmp, ttl);
-  if (rc == SACD_OK) {
-    cudaError_t e = cudaMemcpy2DAsync(out, (size_t)ld * 8, tmp, (size_t)c->R * 8, (size_t)c->R * 8, (size_t)rows,
+  const size_t row_bytes = (size_t)c->R * 8;
+  const size_t total = (size_t)rows * row_bytes;
+  auto fail = [&](cudaError_t e) {
+    set_error(std::string("read_matrix: ") + cudaGetErrorString(e));
+    rc = SACD_ECUDA;
+  };
+  if (rc == SACD_OK && (total < (8u << 20) || is_pinned_host(out))) {
+    cudaError_t e = cudaMemcpy2DAsync(out, (size_t)ld * 8, tmp, row_bytes, row_bytes, (size_t)rows,
                                       cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    if (e != cudaSuccess) {
-      set_error(std::string("read_matrix: ") + cudaGetErrorString(e));
-      rc = SACD_ECUDA;
+    if (e != cudaSuccess) fail(e);
+  } else if (rc == SACD_OK) {
+    if (!c->pin) {
+      c->pin_chunk = (size_t)32 << 20;
+      cudaError_t e = cudaHostAlloc(&c->pin, 2 * c->pin_chunk, cudaHostAllocDefault);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->pin_ev[0], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->pin_ev[1], cudaEventDisableTiming);
+      if (e != cudaSuccess) {
+        fail(e);
+        c->pin = nullptr;
+      }
+    }
+    const long long crow = std::max<long long>(1, (long long)(c->pin_chunk / row_bytes));
+    const long long nch = (rows + crow - 1) / crow;
+    auto issue = [&](long long k) {
+      const long long r0 = k * crow, r1 = std::min(rows, r0 + crow);
+      char *buf = reinterpret_cast<char *>(c->pin) + (size_t)(k & 1) * c->pin_chunk;
+      cudaError_t e = cudaMemcpyAsync(buf, tmp + r0 * c->R, (size_t)(r1 - r0) * row_bytes, cudaMemcpyDeviceToHost, s);
+      if (e == cudaSuccess) e = cudaEventRecord(c->pin_ev[k & 1], s);
+      if (e != cudaSuccess) fail(e);
+    };
+    if (rc == SACD_OK && nch > 0) issue(0);
+    for (long long k = 0; rc == SACD_OK && k < nch; ++k) {
+      cudaError_t e = cudaEventSynchronize(c->pin_ev[k & 1]);
+      if (e != cudaSuccess) {
+        fail(e);
+        break;
+      }
+      if (k + 1 < nch) issue(k + 1);  // into the other half, while this one is copied out
+      const long long r0 = k * crow, r1 = std::min(rows, r0 + crow);
+      host_rows_copy(out + r0 * ld, ld, reinterpret_cast<const double *>(reinterpret_cast<char *>(c->pin) +
+                                                                          (size_t)(k & 1) * c->pin_chunk),
+                     r1 - r0, c->R);
     }
   }
   cudaFreeAsync(tmp, s);
+  if (rc == SACD_OK) {
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) fail(e);
+  }
   return rc;
 }
 
@@ -1160,6 +1248,8 @@ int sacd_get_info(sacd_ctx *c, sacd_info *o) {
   o->delta_elems_sent = c->delta_sent;
   o->full_elems_equiv = c->full_equiv;
   for (int n = 0; n < 3; ++n) o->fibers[n] = c->m[n].n_fibers;
+  o->uniform_values = c->uniform_x ? 1 : 0;
+  o->uniform_value = c->uniform_x ? c->xu : 0.0;
   int k = 0;
   int rc = dev_read(c, &k, reinterpret_cast<const char *>(c->st) + offsetof(DevState, k), sizeof(int));
   if (rc == SACD_OK)

@@ -472,6 +472,103 @@ __global__ void __launch_bounds__(WPB * 32)
   }
 }
 
+// Gram refresh fused into the row update (Eq 10's G_n = F_n^T F_n of the factor just
+// updated): after a 128-row block is final in shared memory (Us), the block's contribution
+// Us^T Us is added on the fp64 tensor cores to a per-CTA accumulator held in registers, so
+// the updated factor is never re-read from HBM for its Gram.  The upper-triangle 8 x 8 tiles
+// (ti <= tj) of the RT x RT Gram are dealt round-robin to the CTA's warps (tile q -> warp
+// q mod WPB, at most ceil(P(P+1)/2 / WPB) tiles per warp, P = RT / 8); each tile is a chain of
+// m8n8k4 DMMAs over the block's rows, 4 at a time: A[m][k] = Us[4kk + k][8ti + m] held by lane
+// (g, t) as Us[4kk + t][8ti + g], B[k][n] = Us[4kk + k][8tj + n] as Us[4kk + t][8tj + g],
+// C[g][2t + e] = G[8ti + g][8tj + 2t + e].  Rows past the range are zero in Us (the staging
+// zero-fills them), padding columns are zero in F.
+template <int RT, int WPB>
+struct GramAcc {
+  static constexpr int P = RT / 8;
+  static constexpr int NT = P * (P + 1) / 2;
+  static constexpr int TPW = (NT + WPB - 1) / WPB;
+  double c[TPW][2];
+  __device__ __forceinline__ static void tile_ij(int q, int &ti, int &tj) {  // q-th upper tile, row major
+    ti = 0;
+    while (q >= P - ti) {
+      q -= P - ti;
+      ++ti;
+    }
+    tj = ti + q;
+  }
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int k = 0; k < TPW; ++k) c[k][0] = c[k][1] = 0.0;
+  }
+  __device__ __forceinline__ void add_block(const double *Us, int US, int nrows_pad, int wp, int lane) {
+    const int g = lane >> 2, t = lane & 3;
+#pragma unroll
+    for (int k = 0; k < TPW; ++k) {
+      const int q = wp + WPB * k;
+      if (q < NT) {
+        int ti, tj;
+        tile_ij(q, ti, tj);
+        const double *pa = Us + t * US + 8 * ti + g;
+        const double *pb = Us + t * US + 8 * tj + g;
+        for (int r0 = 0; r0 < nrows_pad; r0 += 4) {
+          const double a = pa[r0 * US], b = pb[r0 * US];
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                       : "+d"(c[k][0]), "+d"(c[k][1])
+                       : "d"(a), "d"(b));
+        }
+      }
+    }
+  }
+  // upper-triangle entries (r <= t) of this CTA's partial: the k_gram_reduce contract
+  __device__ __forceinline__ void store(double *part, int R, int wp, int lane) const {
+    const int g = lane >> 2, t = lane & 3;
+#pragma unroll
+    for (int k = 0; k < TPW; ++k) {
+      const int q = wp + WPB * k;
+      if (q < NT) {
+        int ti, tj;
+        tile_ij(q, ti, tj);
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int r = 8 * ti + g, cc = 8 * tj + 2 * t + e;
+          if (r < R && cc < R && r <= cc) part[r * R + cc] = c[k][e];
+        }
+      }
+    }
+  }
+};
+
+// Row update with the fused Gram: CTA b takes the contiguous row blocks
+// [b * nblk / grid, (b + 1) * nblk / grid) in order (a fixed assignment, so the Gram partial of
+// each CTA, and the fixed-order reduce over CTAs, are deterministic), and writes its Gram
+// partial to part[blockIdx.x].
+template <int RT, int WPB>
+__global__ void __launch_bounds__(WPB * 32)
+    k_sacd_rows_mma_gram(long long row_begin, long long row_end, int R, int mode, int l_mode,
+                         const long long *__restrict__ row_ptr, const double *__restrict__ M, double *__restrict__ F,
+                         double *__restrict__ Z, const double *__restrict__ H, const DevState *__restrict__ st,
+                         uint8_t *__restrict__ dec, double *__restrict__ ti_part, double *__restrict__ md_part,
+                         long long *__restrict__ e_part, long long *__restrict__ ech_part, long long nblk,
+                         double *__restrict__ gram_part) {
+  constexpr int TR = WPB * 32;
+  constexpr int US = RT + 2;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const double *Us = reinterpret_cast<const double *>(smem_raw);
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  GramAcc<RT, WPB> acc;
+  acc.zero();
+  const long long b0 = nblk * blockIdx.x / gridDim.x, b1 = nblk * (blockIdx.x + 1) / gridDim.x;
+  for (long long rb = b0; rb < b1; ++rb) {
+    rows_mma_block<RT, WPB>(rb, row_begin, row_end, R, mode, l_mode, row_ptr, M, F, Z, H, st, dec, ti_part, md_part,
+                            e_part, ech_part);
+    // Us holds the block's final rows (rows past the range are zero): add them to the Gram
+    const int nrows = (int)min((long long)TR, row_end - (row_begin + rb * TR));
+    acc.add_block(Us, US, (nrows + 3) & ~3, wp, lane);
+    __syncthreads();  // the next block's staging overwrites Us
+  }
+  acc.store(gram_part + (long long)blockIdx.x * R * R, R, wp, lane);
+}
+
 // The same row update for R > 64 (fp64): one warp (32 rows) per block; the B fragments of
 // a column block (R/4 k-steps) are loaded 16 k-steps at a time, the next chunk in flight
 // while the current one feeds the DMMAs; the in-block H values come from L1.  The FMA

@@ -307,7 +307,10 @@ struct Impl {
           // shared memory (variant 36; c5 R=256: 12.7 ms per sweep vs 13.7 with shuffles,
           // variant 22, and 28.6 for the warp fiber kernel, variant 1)
           // Dynamically scheduled (items from a counter; c5 R=256 12.6 vs 13.1 ms, variant 39).
-          if constexpr (sizeof(Real) == 8 && RT == 256) launch_dyn<1, 2, 1>(c, items, n_items, md.nzm, A, B, out, partial);
+          if constexpr (sizeof(Real) == 8 && RT == 256) {
+            if (c.uniform_x) launch_dyn<1, 2, 4>(c, items, n_items, md.nzm, A, B, out, partial);
+            else launch_dyn<1, 2, 1>(c, items, n_items, md.nzm, A, B, out, partial);
+          }
         } else if (sizeof(Real) == 8 && (RT == 64 || (RT == 32 && md.n_fibers > 0 && c.nnz >= 2 * md.n_fibers))) {
           // fp64, R = 33..64 (and R = 17..32 with a mean fiber length >= 2, the Zipf config
           // c3): one warp per item (2 fp64 columns per lane at R = 64) at 48 registers / 40
@@ -321,7 +324,11 @@ struct Impl {
             // scheduled from a work counter (variant 39: c4 11.06, c5 R=64 3.29 vs 3.82 ms; a
             // sharded rank's launch covers only ~2 waves of items, where the static grid lost
             // up to a third to the last wave)
-            launch_dyn<1, 6, 1>(c, items, n_items, md.nzm, A, B, out, partial);
+            // A tensor whose values are all equal (binary interactions, c4) needs no per-nonzero
+            // x at all (XS = 4; exact: x * b with the same x): c4 MTTKRP 11.12 -> 10.98 ms per
+            // sweep (variant 53, profiles/r02_mttkrp_variants_c4.txt)
+            if (c.uniform_x) launch_dyn<1, 6, 4>(c, items, n_items, md.nzm, A, B, out, partial);
+            else launch_dyn<1, 6, 1>(c, items, n_items, md.nzm, A, B, out, partial);
           } else if constexpr (sizeof(Real) == 8 && RT == 32) {
             // two workers per warp, each taking items from the work counter (c3 0.98 vs
             // 1.09 ms per sweep for the static grid)
@@ -339,7 +346,8 @@ struct Impl {
           // memory (variant 32: c5 R=128 6.54 vs 6.95 ms, c4 R=128 21.5 vs 26.0 ms per sweep)
           if constexpr (sizeof(Real) == 8 && RT == 128) {
             // dynamically scheduled (variant 39: c5 R=128 6.38 vs 6.58, c4 R=128 18.8 vs 21.6 ms)
-            launch_dyn<1, 3, 1>(c, items, n_items, md.nzm, A, B, out, partial);
+            if (c.uniform_x) launch_dyn<1, 3, 4>(c, items, n_items, md.nzm, A, B, out, partial);
+            else launch_dyn<1, 3, 1>(c, items, n_items, md.nzm, A, B, out, partial);
           }
         } else {
           // default (measured on B200, tools/mttkrp_tune.py): the lean sub-warp kernel with
@@ -415,16 +423,19 @@ struct Impl {
       double *ti_part = sh.row_part, *md_part = sh.row_part + c.max_row_blocks;
       long long *e_part = sh.cnt_part, *ech_part = sh.cnt_part + c.max_row_blocks;
       int pe = prof_begin(c, 3);
+      int gn = 0;
       if (nblk > 0)
         SACD_TRY(rows(c, nblk, rlo, rhi, mode, reinterpret_cast<const Real *>(sh.M), dec, ti_part, md_part, e_part,
-                      ech_part));
+                      ech_part, 0, gram_fused(c) ? sh.gram_part : nullptr, &gn));
       SACD_CUDA_TRY(cudaGetLastError());
       SACD_TRY(prof_end(c, 3, pe));
       pe = prof_begin(c, 4);
       double *sl = c.xstats + sh.rank * slot;
-      gram_partial(c, rlo, rhi, reinterpret_cast<const Real *>(md.F), sh.gram_part);
-      k_gram_reduce<<<(c.R * c.R + 255) / 256, 256, 0, c.stream>>>(c.R, gram_ranges(c, rlo, rhi), sh.gram_part,
-                                                                   sl + 4);
+      if (gn == 0) {
+        gn = gram_ranges(c, rlo, rhi);
+        gram_partial(c, rlo, rhi, reinterpret_cast<const Real *>(md.F), sh.gram_part);
+      }
+      k_gram_reduce<<<(c.R * c.R + 255) / 256, 256, 0, c.stream>>>(c.R, gn, sh.gram_part, sl + 4);
       SACD_CUDA_TRY(cudaGetLastError());
       SACD_TRY(prof_end(c, 4, pe));
       k_finalize<<<1, 1024, 0, c.stream>>>(mode, nblk, ti_part, md_part, e_part, ech_part, nullptr, nullptr,
@@ -648,6 +659,7 @@ struct Impl {
     const long long nblk = (md.I + TR - 1) / TR;
     double *ti_part = c.row_part, *md_part = c.row_part + c.max_row_blocks;
     long long *e_part = c.cnt_part, *ech_part = c.cnt_part + c.max_row_blocks;
+    int gn = 0;
     int pe = prof_begin(c, 3);
     if (c.opt.variant == SACD_VARIANT_SNAPSHOT) {
       // (1) snapshot scores from the rows at pass start, (2) ti^k and this pass's branch,
@@ -657,11 +669,18 @@ struct Impl {
       SACD_TRY(rows(c, nblk, 0, md.I, mode, M, dec, ti_part, md_part, e_part, ech_part, 4));
     } else {
       SACD_TRY(rows(c, nblk, 0, md.I, mode, M, dec, ti_part, md_part, e_part, ech_part,
-                    c.opt.variant == SACD_VARIANT_JACOBI ? 1 : 0));
+                    c.opt.variant == SACD_VARIANT_JACOBI ? 1 : 0, gram_fused(c) ? c.gram_part : nullptr, &gn));
     }
     SACD_CUDA_TRY(cudaGetLastError());
     SACD_TRY(prof_end(c, 3, pe));
-    SACD_TRY(gram(c, mode));
+    if (gn > 0) {  // the row kernel wrote one Gram partial per CTA: fixed-order reduce only
+      pe = prof_begin(c, 4);
+      k_gram_reduce<<<(c.R * c.R + 255) / 256, 256, 0, c.stream>>>(c.R, gn, c.gram_part, md.G);
+      SACD_CUDA_TRY(cudaGetLastError());
+      SACD_TRY(prof_end(c, 4, pe));
+    } else {
+      SACD_TRY(gram(c, mode));
+    }
     pe = prof_begin(c, 5);
     const int flags = 1 | (end_sweep ? 6 : 0);
     k_finalize<<<1, 1024, 0, c.stream>>>(mode, nblk, ti_part, md_part, e_part, ech_part, c.m[0].G, c.m[1].G,
@@ -705,6 +724,12 @@ struct Impl {
   static constexpr bool kRowsMma = sizeof(Real) == 8 && RT <= 64 && rows_per_block<RT>() == 128;
   static constexpr bool kRowsMmaBig = sizeof(Real) == 8 && RT >= 128;
   static constexpr int kMmaWarps = 4;  // 5 (160 rows, 2 blocks per SM) measured 2.41 vs 1.72 ms: L1 too small
+  // the Gram refresh runs inside the row update (k_sacd_rows_mma_gram) for the default fp64
+  // R <= 64 path; opt.reserved[2] = 2 keeps the separate Gram kernel (A/B, tools)
+  static bool gram_fused(const Context &c) {
+    if constexpr (kRowsMma) return c.opt.reserved[0] == 0 && c.opt.reserved[2] == 0;
+    return false;
+  }
   static int rows_tr(const Context &c, int vflags) {
     if constexpr (kRowsMma) {
       if ((c.opt.reserved[0] == 0 || c.opt.reserved[0] == 5 || c.opt.reserved[0] == 6) && vflags == 0)
@@ -717,9 +742,11 @@ struct Impl {
   }
 
   static int rows(Context &c, long long nblk, long long rlo, long long rhi, int mode, const Real *M, uint8_t *dec,
-                  double *ti_part, double *md_part, long long *e_part, long long *ech_part, int vflags = 0) {
+                  double *ti_part, double *md_part, long long *e_part, long long *ech_part, int vflags = 0,
+                  double *gram_out = nullptr, int *gram_n = nullptr) {
     constexpr int TR = rows_per_block<RT>();
     ModeData &md = c.m[mode];
+    if (gram_n) *gram_n = 0;
     auto go = [&](auto kern, size_t smem) {
       if (nblk > 0)
         kern<<<(unsigned)nblk, TR, smem, c.stream>>>(rlo, rhi, c.R, mode, c.opt.l_mode, md.row_ptr, M,
@@ -729,9 +756,28 @@ struct Impl {
                                                       reinterpret_cast<Real *>(c.Zs));
     };
     if constexpr (kRowsMma) {
+      if (gram_out && c.opt.reserved[0] == 0 && vflags == 0) {
+        // default for fp64, R <= 64 with the Gram refresh fused (k_sacd_rows_mma_gram):
+        // contiguous row-block ranges per CTA, one Gram partial per CTA into gram_out
+        if (nblk > 0) {
+          int per_sm = 0;
+          auto kern = k_sacd_rows_mma_gram<RT, kMmaWarps>;
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kMmaWarps * 32,
+                                                        rows_mma_smem_bytes<RT, kMmaWarps>());
+          const long long grid = std::min(std::min(nblk, (long long)std::max(1, per_sm) * c.num_sms),
+                                          (long long)c.gram_cap);
+          kern<<<(unsigned)grid, kMmaWarps * 32, rows_mma_smem_bytes<RT, kMmaWarps>(), c.stream>>>(
+              rlo, rhi, c.R, mode, c.opt.l_mode, md.row_ptr, reinterpret_cast<const double *>(M),
+              reinterpret_cast<double *>(md.F), reinterpret_cast<double *>(md.Z),
+              reinterpret_cast<const double *>(c.Hr), c.st, dec, ti_part, md_part, e_part, ech_part, nblk, gram_out);
+          if (gram_n) *gram_n = (int)grid;
+        }
+        SACD_CUDA_TRY(cudaGetLastError());
+        return SACD_OK;
+      }
       if ((c.opt.reserved[0] == 0 || c.opt.reserved[0] == 5) && vflags == 0) {
-        // default for fp64, R <= 64: out-of-block gradient on DMMA, row blocks taken from a
-        // work counter (c4 1.684 vs 1.720 ms per sweep for the static grid, rows variant 6)
+        // fp64, R <= 64 without the fused Gram: out-of-block gradient on DMMA, row blocks taken
+        // from a work counter (c4 1.684 vs 1.720 ms per sweep for the static grid, variant 6)
         if (nblk > 0) {
           int per_sm = 0;
           auto kern = k_sacd_rows_mma_dyn<RT, kMmaWarps>;
@@ -787,6 +833,9 @@ struct Impl {
       SACD_CUDA_TRY(cudaFuncSetAttribute(k_sacd_rows_mma<RT, kMmaWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)rows_mma_smem_bytes<RT, kMmaWarps>()));
       SACD_CUDA_TRY(cudaFuncSetAttribute(k_sacd_rows_mma_dyn<RT, kMmaWarps>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)rows_mma_smem_bytes<RT, kMmaWarps>()));
+      SACD_CUDA_TRY(cudaFuncSetAttribute(k_sacd_rows_mma_gram<RT, kMmaWarps>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)rows_mma_smem_bytes<RT, kMmaWarps>()));
     }

@@ -187,6 +187,7 @@ struct Context {
   bool uniform_x = false;  // every value of the tensor equals xu (bitwise), e.g. a binary tensor
   double xu = 0.0;
   int gram_blocks = 0;
+  int gram_cap = 0;               // Gram partials the gram_part buffers hold (>= gram_blocks)
   long long device_bytes = 0;
   // graph
   cudaGraph_t graph = nullptr;
@@ -219,6 +220,11 @@ struct Context {
   int *dblk = nullptr;            // [kDeltaBlocks] per-block change counts
   std::vector<long long> doff, dcap;  // host: slot offsets / capacities (elements)
   long long delta_sent = 0, full_equiv = 0;  // host: elements exchanged as deltas / as full rows
+  // pinned staging ring for device -> pageable-host reads (sacd_factors & co.): two chunks,
+  // the D2H copy of one overlapping the multi-threaded host copy of the other
+  void *pin = nullptr;
+  size_t pin_chunk = 0;
+  cudaEvent_t pin_ev[2] = {nullptr, nullptr};
 };
 
 constexpr int kDeltaBlocks = 296;

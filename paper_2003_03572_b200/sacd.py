@@ -57,7 +57,8 @@ class Info(C.Structure):
                 ("items", C.c_int64 * 3), ("split_rows", C.c_int64 * 3), ("device_bytes", C.c_int64),
                 ("kernels_per_sweep", C.c_int32), ("world_size", C.c_int32), ("world_rank", C.c_int32),
                 ("sharded_ranks", C.c_int32), ("delta_exchange", C.c_int32), ("delta_elems_sent", C.c_int64),
-                ("full_elems_equiv", C.c_int64), ("fibers", C.c_int64 * 3)]
+                ("full_elems_equiv", C.c_int64), ("fibers", C.c_int64 * 3), ("uniform_values", C.c_int32),
+                ("uniform_value", C.c_double)]
 
 
 class SacdError(RuntimeError):
@@ -280,7 +281,8 @@ class Sacd:
                     device_bytes=i.device_bytes, kernels_per_sweep=i.kernels_per_sweep,
                     world_size=i.world_size, world_rank=i.world_rank, sharded_ranks=i.sharded_ranks,
                     delta_exchange=i.delta_exchange, delta_elems_sent=i.delta_elems_sent,
-                    full_elems_equiv=i.full_elems_equiv, fibers=list(i.fibers))
+                    full_elems_equiv=i.full_elems_equiv, fibers=list(i.fibers),
+                    uniform_values=i.uniform_values, uniform_value=i.uniform_value)
 
     # -- component entry points
     def set_factors(self, mode, F):

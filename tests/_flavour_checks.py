@@ -26,9 +26,12 @@ def debug():
           dict(R=40, variant="snapshot"), dict(R=12, variant="jacobi"), dict(R=64, emulate_ranks=3),
           dict(R=40, emulate_ranks=8, exchange="delta"), dict(R=64, nnz_per_item=16)]),
         ((120, 80, 16), 60000, ((2, 1, 900), (0, 5, 700)), [dict(R=24), dict(R=32), dict(R=64)]),
+        ((90, 70, 40), -12000, ((2, 3, 1500), (0, 7, 900)), [dict(R=64), dict(R=100), dict(R=256)]),  # binary
     ]
     for dims, nnz, heavy, runs in cases:
-        c, v = ragged_tensor(dims, nnz, 8, heavy_rows=heavy)
+        c, v = ragged_tensor(dims, abs(nnz), 8, heavy_rows=heavy)
+        if nnz < 0:  # all values equal: the MTTKRP path without per-nonzero values
+            v = np.full_like(v, 1.0)
         for kw in runs:
             kw = dict(kw)
             R = kw.pop("R")
