@@ -44,8 +44,10 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--reps", type=int, default=5, help="SURVEY 8(d): repetitions with a fresh sacd_init (N = 1)")
     p.add_argument("--nnz-per-item", type=int, default=0)
-    p.add_argument("--exchange", default="delta", choices=["full", "delta"],
-                   help="N > 1: factor-row exchange of the sharded engine (SURVEY f2 delta lists, or full rows)")
+    p.add_argument("--exchange", default="p2p", choices=["full", "delta", "p2p"],
+                   help="N > 1: factor-row exchange of the sharded engine: p2p = changed 16-byte chunks stored "
+                        "into the peers' replicas by a kernel over NVLink (CUDA IPC), device flags, graph-captured; "
+                        "delta = NCCL (index, value) lists (SURVEY f2); full = NCCL all-gather-v of the owned rows")
     return p.parse_args()
 
 
@@ -511,9 +513,11 @@ def main():
                 "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
                 "dtype": args.precision, "data": "synthetic",
                 "config": {"workload": cfg.name, "dims": list(cfg.dims), "nnz": nnz, "rank": R,
-                           "parallelism": (f"slice-sharded x{world} (NCCL; factor exchange: "
-                                           + ("changed elements as (index, value) lists, rows when smaller)"
-                                              if args.exchange == "delta" else "all-gather-v of owned rows)"))
+                           "parallelism": (f"slice-sharded x{world} (factor exchange: "
+                                           + {"delta": "NCCL lists of changed elements, rows when smaller)",
+                                              "full": "NCCL all-gather-v of owned rows)",
+                                              "p2p": "changed 16-byte chunks stored into peer replicas over "
+                                                     "NVLink by a kernel; NCCL for the small stats)"}[args.exchange])
                            if world > 1 else "single GPU",
                            **({"exchange_elems_sent": info_end["delta_elems_sent"],
                                "exchange_elems_full_equiv": info_end["full_elems_equiv"]}

@@ -102,7 +102,11 @@ typedef struct {
                               /* [3]: sharded exchange (0 = full owned rows, graph-captured;   */
                               /* 1 = delta: only the changed elements as (index, value) lists, */
                               /* full rows when those are smaller; NCCL sweeps then run eagerly */
-                              /* because the list lengths are read on the host)               */
+                              /* because the list lengths are read on the host; 2 = peer      */
+                              /* memory: a kernel stores every changed 16-byte chunk of the   */
+                              /* owned rows straight into the peers' replicas (CUDA IPC over  */
+                              /* NVLink), device-side flags order the passes: no host round   */
+                              /* trip, graph-captured)                                        */
 } sacd_options;
 
 /* Per-sweep statistics (device-side ring, read by sacd_stats). */
@@ -209,6 +213,12 @@ int sacd_rmse(sacd_ctx *ctx, const uint32_t *coords, const float *vals, int64_t 
 /* Overwrite factor `mode` from host fp64 `in` (ld >= rank; columns >= rank ignored) and
  * refresh its Gram.  Values are rounded to the context precision. */
 int sacd_set_factors(sacd_ctx *ctx, int32_t mode, const double *in, int64_t ld);
+
+/* Factor `mode` as held by shard `shard`'s replica (host fp64, ld >= rank).  Shards are the
+ * ranks this context runs (one per process, or all G with emulated ranks); with the
+ * peer-memory exchange and emulated ranks every shard has its own replicas, which must stay
+ * bitwise identical.  Otherwise this is sacd_factors.  Errors: ESTATE. */
+int sacd_replica_factors(sacd_ctx *ctx, int32_t shard, int32_t mode, double *out, int64_t ld);
 
 /* Read / overwrite the previous importances z^{k-1} of `mode` (Alg 1). */
 int sacd_get_zprev(sacd_ctx *ctx, int32_t mode, double *out, int64_t ld);

@@ -327,11 +327,17 @@ static void destroy(sacd_ctx *c) {
   cudaFree(c->gram_part);
   cudaFree(c->decisions);
   for (Shard &sh : c->shards) {
+    for (void *p : sh.ipc_opened) cudaIpcCloseMemHandle(p);
     for (int n = 0; n < 3; ++n) {
       cudaFree(sh.items[n]);
       cudaFree(sh.splits[n]);
       cudaFree(sh.chunks[n]);
+      cudaFree(sh.d_peerF[n]);
+      if (sh.own_rep) cudaFree(sh.Frep[n]);
     }
+    cudaFree(sh.flags);
+    cudaFree(sh.epoch);
+    cudaFree(sh.d_peer_flags);
     cudaFree(sh.M);
     cudaFree(sh.partial);
     cudaFree(sh.row_part);
@@ -410,6 +416,104 @@ static int sync_if_device(const void *a, const void *b) {
       return SACD_OK;
     }
   }
+  return SACD_OK;
+}
+
+// Peer-memory exchange (opt.reserved[3] = 2) setup, after the factors exist and hold the
+// init: every shard's flags, pass counter and device arrays of the G ranks' replica pointers.
+//  * emulated ranks: shard q > 0 gets its own replicas (copies of the init), so the pushes
+//    of one shard into the others' replicas are real stores to other memory;
+//  * NCCL ranks (one shard per process): the CUDA IPC handles of every rank's three factors
+//    and flag array are all-gathered over NCCL and opened (NVLink peer mappings).
+static int setup_p2p(Context *c) {
+  const size_t rs = real_size(*c);
+  cudaStream_t s = c->stream;
+  const int G = c->G;
+  for (Shard &sh : c->shards) {
+    SACD_CUDA_TRY(cudaMalloc(&sh.flags, (size_t)G * 8));
+    SACD_CUDA_TRY(cudaMemsetAsync(sh.flags, 0, (size_t)G * 8, s));
+    SACD_CUDA_TRY(cudaMalloc(&sh.epoch, 8));
+    SACD_CUDA_TRY(cudaMemsetAsync(sh.epoch, 0, 8, s));
+    for (int n = 0; n < 3; ++n) {
+      if (c->opt.emulate_ranks > 1 && sh.rank > 0) {
+        const size_t b = (size_t)c->m[n].I * c->pitch * rs;
+        SACD_CUDA_TRY(cudaMalloc(&sh.Frep[n], b));
+        SACD_CUDA_TRY(cudaMemcpyAsync(sh.Frep[n], c->m[n].F, b, cudaMemcpyDeviceToDevice, s));
+        sh.own_rep = true;
+        c->device_bytes += (long long)b;
+      } else {
+        sh.Frep[n] = c->m[n].F;
+      }
+    }
+  }
+  // host tables: ptrF[q][n], ptrFlag[q] for every rank q
+  std::vector<void *> ptrF((size_t)G * 3, nullptr), ptrFlag((size_t)G, nullptr);
+  if (c->opt.emulate_ranks > 1 || G == 1) {
+    for (Shard &sh : c->shards) {
+      for (int n = 0; n < 3; ++n) ptrF[(size_t)sh.rank * 3 + n] = sh.Frep[n];
+      ptrFlag[(size_t)sh.rank] = sh.flags;
+    }
+  } else {
+    Shard &sh = c->shards[0];
+    cudaIpcMemHandle_t mine[4];
+    for (int n = 0; n < 3; ++n) SACD_CUDA_TRY(cudaIpcGetMemHandle(&mine[n], sh.Frep[n]));
+    SACD_CUDA_TRY(cudaIpcGetMemHandle(&mine[3], sh.flags));
+    const size_t hb = sizeof(mine);
+    char *dh = nullptr;
+    SACD_CUDA_TRY(cudaMalloc(&dh, hb * G));
+    SACD_CUDA_TRY(cudaMemcpyAsync(dh + hb * c->me, mine, hb, cudaMemcpyHostToDevice, s));
+    const ncclResult_t r = ncclAllGather(dh + hb * c->me, dh, hb, ncclChar, reinterpret_cast<ncclComm_t>(c->comm), s);
+    if (r != ncclSuccess) {
+      set_error(std::string("ncclAllGather (IPC handles): ") + ncclGetErrorString(r));
+      cudaFree(dh);
+      return SACD_ENCCL;
+    }
+    std::vector<cudaIpcMemHandle_t> all((size_t)G * 4);
+    SACD_CUDA_TRY(cudaMemcpyAsync(all.data(), dh, hb * G, cudaMemcpyDeviceToHost, s));
+    SACD_CUDA_TRY(cudaStreamSynchronize(s));
+    cudaFree(dh);
+    for (int q = 0; q < G; ++q) {
+      for (int k = 0; k < 4; ++k) {
+        void *ptr = nullptr;
+        if (q == c->me) {
+          ptr = k < 3 ? sh.Frep[k] : (void *)sh.flags;
+        } else {
+          const cudaError_t e = cudaIpcOpenMemHandle(&ptr, all[(size_t)q * 4 + k], cudaIpcMemLazyEnablePeerAccess);
+          if (e != cudaSuccess) {
+            cudaGetLastError();
+            set_error(std::string("sacd_init: peer-memory exchange needs CUDA IPC / P2P between the ranks' GPUs (") +
+                      cudaGetErrorString(e) + "); use the NCCL exchange (opt.reserved[3] = 0 or 1)");
+            return SACD_ECUDA;
+          }
+          sh.ipc_opened.push_back(ptr);
+        }
+        if (k < 3) ptrF[(size_t)q * 3 + k] = ptr;
+        else ptrFlag[(size_t)q] = ptr;
+      }
+    }
+  }
+  for (Shard &sh : c->shards) {
+    for (int n = 0; n < 3; ++n) {
+      std::vector<void *> v((size_t)G);
+      for (int q = 0; q < G; ++q) v[(size_t)q] = ptrF[(size_t)q * 3 + n];
+      SACD_CUDA_TRY(cudaMalloc(&sh.d_peerF[n], (size_t)G * sizeof(void *)));
+      SACD_CUDA_TRY(cudaMemcpy(sh.d_peerF[n], v.data(), (size_t)G * sizeof(void *), cudaMemcpyHostToDevice));
+    }
+    SACD_CUDA_TRY(cudaMalloc(&sh.d_peer_flags, (size_t)G * sizeof(void *)));
+    SACD_CUDA_TRY(cudaMemcpy(sh.d_peer_flags, ptrFlag.data(), (size_t)G * sizeof(void *), cudaMemcpyHostToDevice));
+  }
+  SACD_CUDA_TRY(cudaStreamSynchronize(s));
+  return SACD_OK;
+}
+
+// Copy factor `mode` (replica of shard 0) into the other shards' replicas (emulated ranks with
+// the peer-memory exchange) after a host write (sacd_set_factors).
+static int sync_replicas(Context *c, int mode) {
+  if (!c->p2p) return SACD_OK;
+  const size_t b = (size_t)c->m[mode].I * c->pitch * real_size(*c);
+  for (Shard &sh : c->shards)
+    if (sh.own_rep && sh.Frep[mode] != c->m[mode].F)
+      SACD_CUDA_TRY(cudaMemcpyAsync(sh.Frep[mode], c->m[mode].F, b, cudaMemcpyDeviceToDevice, c->stream));
   return SACD_OK;
 }
 
@@ -590,6 +694,11 @@ static int init_impl(Context *c, const uint32_t *coords, const float *vals, uint
   c->max_row_blocks = (maxI + 31) / 32 + 1;  // >= ceil(I / rows_per_block) for every pitch
   // delta exchange buffers: list slot q holds up to rank q's owned elements
   c->delta = c->sharded && c->opt.reserved[3] == 1 && (double)maxI * P < 4294967295.0;
+  c->p2p = c->sharded && c->opt.reserved[3] == 2;
+  if (c->p2p && !c->Fold) {  // pass-start snapshot of the owned rows (change detection)
+    SACD_CUDA_TRY(cudaMalloc(&c->Fold, (size_t)maxI * P * rs));
+    c->device_bytes += (long long)((size_t)maxI * P * rs);
+  }
   if (c->delta) {
     c->doff.assign(c->G, 0);
     c->dcap.assign(c->G, 0);
@@ -658,6 +767,7 @@ static int init_impl(Context *c, const uint32_t *coords, const float *vals, uint
   tm.mark(s, "work items, buffers");
   SACD_TRY(launch_setup(*c));
   SACD_TRY(launch_init_factors(*c, seed));
+  if (c->p2p) SACD_TRY(setup_p2p(c));
   for (int n = 0; n < 3; ++n) SACD_TRY(launch_gram(*c, n));
   SACD_TRY(c->sharded ? launch_sharded_initial_fit(*c) : launch_initial_fit(*c));
   SACD_CUDA_TRY(cudaStreamSynchronize(s));
@@ -872,6 +982,10 @@ int sacd_init(sacd_ctx **out, const uint32_t *coords, const float *vals, int64_t
     }
   }
 #endif
+  if (o.reserved[3] < 0 || o.reserved[3] > 2) {
+    set_error("sacd_init: exchange (reserved[3]) must be 0 (rows), 1 (delta lists) or 2 (peer memory)");
+    return SACD_EINVAL;
+  }
   if (o.world_size < 1 || o.rank < 0 || o.rank >= o.world_size || o.emulate_ranks < 0 ||
       (o.emulate_ranks > 1 && o.world_size != 1)) {
     set_error("sacd_init: bad world_size / rank / emulate_ranks");
@@ -974,6 +1088,17 @@ int sacd_factors(sacd_ctx *c, int32_t mode, double *out, int64_t ld) {
   return sticky(c, read_matrix(c, c->m[mode].F, c->m[mode].I, out, ld));
 }
 
+int sacd_replica_factors(sacd_ctx *c, int32_t shard, int32_t mode, double *out, int64_t ld) {
+  CTX_CHECK(c);
+  if (mode < 0 || mode > 2 || ld < c->R || !out || shard < 0 || shard >= (int)c->shards.size()) {
+    set_error("sacd_replica_factors: bad shard/mode/ld/out");
+    return SACD_ESTATE;
+  }
+  const Shard &sh = c->shards[(size_t)shard];
+  const void *src = (c->p2p && sh.Frep[mode]) ? sh.Frep[mode] : c->m[mode].F;
+  return sticky(c, read_matrix(c, src, c->m[mode].I, out, ld));
+}
+
 int sacd_get_zprev(sacd_ctx *c, int32_t mode, double *out, int64_t ld) {
   CTX_CHECK(c);
   if (mode < 0 || mode > 2 || ld < c->R || !out) {
@@ -999,6 +1124,7 @@ int sacd_set_factors(sacd_ctx *c, int32_t mode, const double *in, int64_t ld) {
     return SACD_ESTATE;
   }
   int rc = write_matrix(c, c->m[mode].F, c->m[mode].I, in, ld);
+  if (rc == SACD_OK) rc = sync_replicas(c, mode);
   if (rc == SACD_OK) rc = launch_gram(*c, mode);
   if (rc == SACD_OK && cudaStreamSynchronize(c->stream) != cudaSuccess) rc = SACD_ECUDA;
   return sticky(c, rc);

@@ -204,6 +204,67 @@ __global__ void __launch_bounds__(1024) k_snapshot_branch(int mode, long long nb
   }
 }
 
+// ------------------------------------------------------------------ peer-memory exchange
+// After the owner's row update, every 16-byte chunk of its owned rows [lo, hi) (element
+// indices of the row-major factor) that differs bit for bit from the pass-start snapshot Fo
+// is stored directly into every peer's replica at the same offset (NVLink stores through
+// IPC-mapped pointers across processes; other shards' replicas with emulated ranks).  No
+// lists, no counts on the host, no NCCL: the whole exchange is kernels, so the sweep graph
+// captures it.  Unchanged chunks are already equal on every replica (all start equal and
+// receive the same stores), so the replicas stay bitwise identical.
+template <typename Real>
+__global__ void __launch_bounds__(256) k_p2p_push(long long lo, long long hi, const Real *__restrict__ F,
+                                                  const Real *__restrict__ Fo, Real *const *__restrict__ peers,
+                                                  int G, int me) {
+  constexpr int PER = 16 / (int)sizeof(Real);
+  const long long c0 = lo / PER, c1 = hi / PER;  // lo, hi are whole rows (multiples of the pitch)
+  const uint4 *Fc = reinterpret_cast<const uint4 *>(F);
+  const uint4 *Oc = reinterpret_cast<const uint4 *>(Fo);
+  for (long long k = c0 + (long long)blockIdx.x * blockDim.x + threadIdx.x; k < c1;
+       k += (long long)gridDim.x * blockDim.x) {
+    const uint4 a = Fc[k], b = Oc[k];
+    if (a.x != b.x || a.y != b.y || a.z != b.z || a.w != b.w) {
+      for (int p = 0; p < G; ++p)
+        if (p != me) reinterpret_cast<uint4 *>(peers[p])[k] = a;
+    }
+  }
+}
+
+// This rank has pushed its rows: make them visible system-wide, advance the pass counter and
+// raise flag[me] = counter in every peer's flag array.
+__global__ void k_p2p_signal(unsigned long long *const *__restrict__ peer_flags, int G, int me,
+                             unsigned long long *__restrict__ epoch) {
+  if (threadIdx.x != 0) return;
+  __threadfence_system();
+  const unsigned long long e = *epoch + 1;
+  *epoch = e;
+  for (int p = 0; p < G; ++p)
+    if (p != me) {
+      unsigned long long *f = peer_flags[p] + me;
+      asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(e) : "memory");
+    }
+}
+
+// Wait until every peer has raised its flag for this pass (flags live in this rank's memory);
+// a peer that never arrives traps after ~20 s (a sticky ECUDA instead of a hang).
+__global__ void k_p2p_wait(const unsigned long long *__restrict__ flags, int G, int me,
+                           const unsigned long long *__restrict__ epoch) {
+  if (threadIdx.x != 0) return;
+  const unsigned long long e = *epoch;
+  const unsigned long long t0 = globaltimer_ns();
+  for (int p = 0; p < G; ++p) {
+    if (p == me) continue;
+    for (;;) {
+      unsigned long long v;
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flags + p) : "memory");
+      if (v >= e) break;
+      if (globaltimer_ns() - t0 > 20000000000ULL) __trap();
+      __nanosleep(200);
+    }
+  }
+  __threadfence_system();
+}
+
 // ------------------------------------------------------------------ sharded-engine kernels
 // Every rank q writes its head row id / partial row into slot q of the exchange buffers
 // and its (ti, md, E, Ech, Gram partial) into slot q of the stats buffer; NCCL all-gathers

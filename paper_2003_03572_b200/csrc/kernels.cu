@@ -382,13 +382,32 @@ struct Impl {
   }
 
   // ---- sharded engine -------------------------------------------------
+  // With the peer-memory exchange and emulated ranks, every shard has its own factor
+  // replicas: while a shard's kernels are launched the context's factor pointers are that
+  // shard's replicas (restored to shard 0's on scope exit).
+  struct ReplicaScope {
+    Context &c;
+    void *saved[3];
+    ReplicaScope(Context &cc, const Shard &sh) : c(cc) {
+      for (int k = 0; k < 3; ++k) {
+        saved[k] = c.m[k].F;
+        if (c.p2p && sh.Frep[k]) c.m[k].F = sh.Frep[k];
+      }
+    }
+    ~ReplicaScope() {
+      for (int k = 0; k < 3; ++k) c.m[k].F = saved[k];
+    }
+  };
+
   // Each rank computes the MTTKRP of its nonzero range; the head partials (rows whose
   // first nonzero is on a lower rank) are exchanged and added by the owners in rank order.
   static int sharded_mttkrp_merge(Context &c, int mode) {
-    for (Shard &sh : c.shards)
+    for (Shard &sh : c.shards) {
+      ReplicaScope rs(c, sh);
       SACD_TRY(mttkrp_on(c, mode, sh.items[mode], sh.n_items[mode], sh.splits[mode], sh.n_splits[mode],
                          sh.chunks[mode], sh.n_chunks[mode],
                          reinterpret_cast<Real *>(sh.M), reinterpret_cast<Real *>(sh.partial)));
+    }
     Real *xrow = reinterpret_cast<Real *>(c.xrow);
     for (Shard &sh : c.shards)
       k_pack_head<Real, RT><<<1, 256, 0, c.stream>>>(sh.plan[mode].head, reinterpret_cast<const Real *>(sh.M),
@@ -411,13 +430,11 @@ struct Impl {
     if (begin_sweep) k_sweep_begin<<<1, 32, 0, c.stream>>>(c.st);
     SACD_TRY(sharded_mttkrp_merge(c, mode));
     SACD_TRY(prepare(c, mode, branch_override, begin_sweep, 1));
-    if (c.delta) SACD_TRY(delta_snapshot(c, mode));
+    if (c.delta || c.p2p) SACD_TRY(delta_snapshot(c, mode));
     const long long TR = rows_tr(c, 0);
-    constexpr int GT = gram_gt<RT>();
-    constexpr int TG = gram_tg<GT>();
-    constexpr int NBP = RT / GT;
     const long long slot = 4 + (long long)c.R * c.R;
     for (Shard &sh : c.shards) {
+      ReplicaScope rs(c, sh);
       const long long rlo = sh.plan[mode].rlo, rhi = sh.plan[mode].rhi;
       const long long nblk = (rhi - rlo + TR - 1) / TR;
       double *ti_part = sh.row_part, *md_part = sh.row_part + c.max_row_blocks;
@@ -441,6 +458,16 @@ struct Impl {
       k_finalize<<<1, 1024, 0, c.stream>>>(mode, nblk, ti_part, md_part, e_part, ech_part, nullptr, nullptr,
                                            nullptr, c.R, c.st, 8, sl);
       SACD_CUDA_TRY(cudaGetLastError());
+      if (c.p2p && rhi > rlo && c.G > 1)  // this shard's changed chunks into the peers' replicas
+        k_p2p_push<Real><<<4 * c.num_sms, 256, 0, c.stream>>>(
+            rlo * RT, rhi * RT, reinterpret_cast<const Real *>(md.F), reinterpret_cast<const Real *>(c.Fold),
+            reinterpret_cast<Real *const *>(sh.d_peerF[mode]), c.G, sh.rank);
+      SACD_CUDA_TRY(cudaGetLastError());
+    }
+    if (c.p2p && c.G > 1) {  // every shard signals before any waits (emulated ranks share a stream)
+      for (Shard &sh : c.shards) k_p2p_signal<<<1, 32, 0, c.stream>>>(sh.d_peer_flags, c.G, sh.rank, sh.epoch);
+      for (Shard &sh : c.shards) k_p2p_wait<<<1, 32, 0, c.stream>>>(sh.flags, c.G, sh.rank, sh.epoch);
+      SACD_CUDA_TRY(cudaGetLastError());
     }
     if (c.comm) SACD_TRY(nccl_allgather_inplace(c, c.xstats, (size_t)slot, 0));
     int pe = prof_begin(c, 5);
@@ -448,8 +475,13 @@ struct Impl {
                                                 32 | 1 | (end_sweep ? 6 : 0));
     SACD_CUDA_TRY(cudaGetLastError());
     SACD_TRY(prof_end(c, 5, pe));
-    if (c.delta) SACD_TRY(delta_exchange(c, mode));
-    else if (c.comm) SACD_TRY(nccl_broadcast_rows(c, mode));
+    if (c.p2p) {
+      // rows already exchanged through peer memory
+    } else if (c.delta) {
+      SACD_TRY(delta_exchange(c, mode));
+    } else if (c.comm) {
+      SACD_TRY(nccl_broadcast_rows(c, mode));
+    }
     SACD_TRY(chunk_mask(c, mode));
     return SACD_OK;
   }

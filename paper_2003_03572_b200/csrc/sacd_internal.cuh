@@ -156,6 +156,17 @@ struct Shard {
   double *row_part = nullptr;    // 2 * max row blocks
   long long *cnt_part = nullptr; // 2 * max row blocks
   double *gram_part = nullptr;   // gram blocks * R * R
+  // peer-memory exchange (opt.reserved[3] = 2): this rank's factor replicas (its own device
+  // memory; with emulated ranks every shard has separate replicas), device arrays of the G
+  // ranks' replica base pointers per mode (IPC-mapped peers across processes), the flags the
+  // peers raise in this rank's memory after pushing, and this rank's pass counter
+  void *Frep[3] = {nullptr, nullptr, nullptr};
+  void **d_peerF[3] = {nullptr, nullptr, nullptr};
+  unsigned long long *flags = nullptr;      // [G]
+  unsigned long long **d_peer_flags = nullptr;
+  unsigned long long *epoch = nullptr;
+  bool own_rep = false;                     // Frep allocated by this shard (emulation, q > 0)
+  std::vector<void *> ipc_opened;
 };
 
 struct Context {
@@ -212,6 +223,8 @@ struct Context {
   // delta exchange (opt.reserved[3] = 1): per mode pass each owner sends only the
   // elements of its rows that changed, as (element index, value) lists
   bool delta = false;
+  bool p2p = false;               // opt.reserved[3] = 2: changed 16-byte chunks pushed to peers'
+                                  // replicas by a kernel, device-side flags (graph-capturable)
   bool capturing = false;         // inside capture_graph (no host synchronisation allowed)
   void *Fold = nullptr;           // Real [maxI * pitch]: owned rows before the pass
   uint32_t *didx = nullptr;       // [sum_q cap_q] list of rank q at doff[q]

@@ -33,7 +33,7 @@ EXPORTS = ("sacd_default_options", "sacd_init", "sacd_iterate", "sacd_sync", "sa
            "sacd_stats", "sacd_get_info", "sacd_free", "sacd_last_error", "sacd_set_factors", "sacd_get_zprev",
            "sacd_set_zprev", "sacd_mttkrp", "sacd_time_mttkrp", "sacd_gram", "sacd_hessian", "sacd_mode_update",
            "sacd_layout", "sacd_profile_read", "sacd_profile_reset", "sacd_shard_plan", "sacd_abi_sizes",
-           "sacd_nccl_unique_id", "sacd_predict", "sacd_rmse", "sacd_set_profile")
+           "sacd_nccl_unique_id", "sacd_predict", "sacd_rmse", "sacd_set_profile", "sacd_replica_factors")
 
 
 class Options(C.Structure):
@@ -93,6 +93,7 @@ def load_library(path: str = LIB_PATH):
     L.sacd_last_error.restype = C.c_char_p
     L.sacd_set_factors.argtypes = [P, i32, P, i64]
     L.sacd_get_zprev.argtypes = [P, i32, P, i64]
+    L.sacd_replica_factors.argtypes = [P, i32, i32, P, i64]
     L.sacd_set_zprev.argtypes = [P, i32, P, i64]
     L.sacd_mttkrp.argtypes = [P, i32, P, i64]
     L.sacd_time_mttkrp.argtypes = [P, i32, i32, C.POINTER(d)]
@@ -204,7 +205,7 @@ class Sacd:
         o.reserved[0] = int(rows_variant)
         o.reserved[1] = int(ablk_rows)
         o.reserved[2] = int(gram_variant)
-        o.reserved[3] = {"full": 0, "delta": 1}[exchange]
+        o.reserved[3] = {"full": 0, "delta": 1, "p2p": 2}[exchange]
         self._nccl_id = None
         if nccl_id is not None:
             self._nccl_id = C.create_string_buffer(bytes(nccl_id), 128)
@@ -289,6 +290,13 @@ class Sacd:
         F = _np(F, np.float64)
         assert F.shape == (self.dims[mode], self.rank)
         _check(load_library().sacd_set_factors(self._h, int(mode), _ptr(F), self.rank))
+
+    def replica_factors(self, shard, mode):
+        """Factor `mode` as held by shard `shard` (its own replica with exchange='p2p' and
+        emulated ranks)."""
+        out = np.zeros((self.dims[mode], self.rank), np.float64)
+        _check(load_library().sacd_replica_factors(self._h, int(shard), int(mode), _ptr(out), self.rank))
+        return out
 
     def get_zprev(self, mode):
         out = np.zeros((self.dims[mode], self.rank), np.float64)

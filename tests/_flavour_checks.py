@@ -24,7 +24,8 @@ def debug():
         ((300, 200, 50), 20000, ((2, 1, 3000), (0, 5, 900), (1, 199, 1500)),
          [dict(R=5), dict(R=40), dict(R=64), dict(R=200), dict(R=40, precision="f32"),
           dict(R=40, variant="snapshot"), dict(R=12, variant="jacobi"), dict(R=64, emulate_ranks=3),
-          dict(R=40, emulate_ranks=8, exchange="delta"), dict(R=64, nnz_per_item=16)]),
+          dict(R=40, emulate_ranks=8, exchange="delta"), dict(R=64, emulate_ranks=3, exchange="p2p"),
+          dict(R=64, nnz_per_item=16)]),
         ((120, 80, 16), 60000, ((2, 1, 900), (0, 5, 700)), [dict(R=24), dict(R=32), dict(R=64)]),
         ((90, 70, 40), -12000, ((2, 3, 1500), (0, 7, 900)), [dict(R=64), dict(R=100), dict(R=256)]),  # binary
     ]

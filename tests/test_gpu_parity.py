@@ -662,6 +662,54 @@ def test_sharded_nccl_world1_matches_unsharded():
 
 @pytest.mark.parametrize("G", [2, 3, 8])
 @pytest.mark.parametrize("precision", ["f64", "f32"])
+@pytest.mark.parametrize("R", [5, 64])
+def test_p2p_exchange_emulated_replicas(G, precision, R):
+    """The peer-memory exchange with G emulated ranks, each holding its OWN factor replicas:
+    every pass, each shard's kernel stores the changed 16-byte chunks of its owned rows into
+    the other shards' replicas, and device flags order the passes.  After 8 sweeps all
+    replicas are bitwise identical, equal the full-row exchange's factors bitwise, and (fp64)
+    meet the oracle bar; the captured sweep graph equals eager sweeps."""
+    dims = (300, 200, 50)
+    c, v = ragged_tensor(dims, 20000, 8, heavy_rows=((2, 1, 3000), (0, 5, 900), (1, 199, 1500)))
+    res = {}
+    for ex, graph in (("full", True), ("p2p", True), ("p2p", False)):
+        with S(c, v, dims, R, 17, nnz_per_item=256, emulate_ranks=G, exchange=ex, precision=precision,
+               use_graph=graph) as g:
+            f0 = g.fit()[0]
+            g.iterate(8)
+            st = g.stats()
+            Fs = g.factors()
+            if ex == "p2p":
+                for q in range(G):
+                    for n in range(3):
+                        assert np.array_equal(g.replica_factors(q, n), Fs[n]), (q, n)
+            res[(ex, graph)] = (np.array([f0] + [s["objective"] for s in st]), Fs, st)
+    for key in (("p2p", True), ("p2p", False)):
+        assert np.array_equal(res[key][0], res[("full", True)][0])
+        for n in range(3):
+            assert np.array_equal(res[key][1][n], res[("full", True)][1][n])
+    if precision == "f64":
+        fg, Fg, st = res[("p2p", True)]
+        ora = O.sacd_run(c, v, dims, R, 17, 8)
+        check_pair(fg, Fg, np.array([s["E"] for s in st]), np.array([s["branch"] for s in st]), ora)
+
+
+def test_p2p_exchange_world1_matches_unsharded():
+    """exchange='p2p' on the one-rank sharded engine (no peers) equals the unsharded engine."""
+    cfg = SI.CONFIGS["c1"]
+    c, v = SI.make_tensor(cfg)
+    c, v = c.numpy(), v.numpy()
+    out = []
+    for kw in ({}, {"force_sharded": True, "exchange": "p2p"}):
+        with S(c, v, cfg.dims, cfg.rank, cfg.seed, **kw) as g:
+            g.iterate(6)
+            out.append(g.factors())
+    for n in range(3):
+        assert np.array_equal(out[0][n], out[1][n])
+
+
+@pytest.mark.parametrize("G", [2, 3, 8])
+@pytest.mark.parametrize("precision", ["f64", "f32"])
 def test_delta_exchange_emulated_bitwise_equals_full(G, precision):
     """with the delta exchange every pass resets the owned rows to their
     pre-pass values and rebuilds them from the owners' (index, value) lists of changed

@@ -8,6 +8,9 @@
   row owners in rank order, owners run the row pass on their rows, the updated rows are
   all-gathered, Grams / ti / E are reduced in rank order.  The result must equal the
   unsharded oracle run (same decisions, same branch, f to 1e-12).
+* The peer-memory exchange (exchange "p2p": changed 16-byte chunks stored into every peer's
+  replica, device flags) is emulated with per-rank replicas, which must stay bitwise
+  identical.
 * The delta exchange is emulated the same way: each owner lists the elements of
   its rows that changed bit for bit (flat index, value), the list lengths are all-gathered
   and every rank takes the lists when they are smaller than the rows (12 vs 8 bytes per
@@ -87,7 +90,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, K, q, delta=False):
+def _worker(rank, world, port, K, q, exchange="rows"):
     try:
         os.environ["MASTER_ADDR"] = "127.0.0.1"
         os.environ["MASTER_PORT"] = str(port)
@@ -131,7 +134,24 @@ def _worker(rank, world, port, K, q, delta=False):
                 Fn, zn, ti, E, Ech, md, _ = O.mode_pass(M[rlo:rhi], H, F[n][rlo:rhi], zp[n][rlo:rhi], br)
                 zp[n][rlo:rhi] = zn
                 # (4) updated rows all-gathered into the replicated factor
-                if delta:
+                if exchange == "p2p":
+                    # peer-memory exchange: every 16-byte chunk (2 fp64) of the owned rows that
+                    # changed against the pass-start snapshot is stored into every peer's
+                    # replica; the all-gather stands for the stores + the flag barrier
+                    old = F[n][rlo:rhi].copy()
+                    F[n][rlo:rhi] = Fn
+                    a_new = F[n][rlo:rhi].reshape(-1, 2).view(np.int64)
+                    a_old = old.reshape(-1, 2).view(np.int64)
+                    ch = np.nonzero((a_new != a_old).any(axis=1))[0]
+                    msg = (ch + rlo * R // 2, F[n][rlo:rhi].reshape(-1, 2)[ch].copy())
+                    msgs = [None] * world
+                    dist.all_gather_object(msgs, msg)
+                    chunks = F[n].reshape(-1, 2)
+                    for p2, (ix, vals) in enumerate(msgs):
+                        if p2 != rank:
+                            chunks[ix] = vals
+                    used_delta[0] += 1
+                elif exchange == "delta":
                     old = F[n][rlo:rhi]
                     ch = (Fn.view(np.int64) != old.view(np.int64)).reshape(-1)
                     idx = np.nonzero(ch)[0] + rlo * R
@@ -180,29 +200,34 @@ def _worker(rank, world, port, K, q, delta=False):
             fs.append(xn2 - 2 * mdot + float((G[0] * G[1] * G[2]).sum()))
             Es.append(Erow)
             brs.append(brrow)
+        reps = [None] * world
+        dist.all_gather_object(reps, [x.copy() for x in F])
+        same = all(np.array_equal(reps[p2][n], reps[0][n]) for p2 in range(world) for n in range(3))
         if rank == 0:
-            q.put((fs, Es, brs, [x.copy() for x in F], used_delta[0]))
+            q.put((fs, Es, brs, [x.copy() for x in F], used_delta[0], same))
         dist.destroy_process_group()
     except Exception as ex:  # surface worker failures to the parent
         q.put(("error", repr(ex)))
         raise
 
 
-@pytest.mark.parametrize("world,delta", [(2, False), (3, False), (2, True), (3, True)])
-def test_sharded_sweeps_equal_unsharded_oracle(plan, world, delta):
-    K = 6 if delta else 4
+@pytest.mark.parametrize("world,exchange", [(2, "rows"), (3, "rows"), (2, "delta"), (3, "delta"), (2, "p2p"),
+                                            (3, "p2p")])
+def test_sharded_sweeps_equal_unsharded_oracle(plan, world, exchange):
+    K = 6 if exchange != "rows" else 4
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, K, q, delta)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, K, q, exchange)) for r in range(world)]
     for p in procs:
         p.start()
     res = q.get(timeout=300)
     for p in procs:
         p.join(timeout=120)
     assert res[0] != "error", res
-    fs, Es, brs, F, used = res
-    if delta:
+    fs, Es, brs, F, used, same = res
+    assert same  # every rank's replica is bitwise identical
+    if exchange != "rows":
         assert used > 0
     dims, R, seed = (40, 30, 20), 4, 3
     c, v = SI.tiny_tensor(dims, 0.08, 5)
