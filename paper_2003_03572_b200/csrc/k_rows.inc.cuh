@@ -251,7 +251,8 @@ __device__ __forceinline__ void rows_mma_block(long long rb, long long row_begin
                     const long long *__restrict__ row_ptr, const double *__restrict__ M, double *__restrict__ F,
                     double *__restrict__ Z, const double *__restrict__ H, const DevState *__restrict__ st,
                     uint8_t *__restrict__ dec, double *__restrict__ ti_part, double *__restrict__ md_part,
-                    long long *__restrict__ e_part, long long *__restrict__ ech_part) {
+                    long long *__restrict__ e_part, long long *__restrict__ ech_part,
+                    double *const *__restrict__ peers = nullptr, int G = 0, int me = 0) {
   constexpr int TR = WPB * 32;
   constexpr int US = RT + 2;
   constexpr int C = 8;
@@ -404,7 +405,25 @@ __device__ __forceinline__ void rows_mma_block(long long rb, long long row_begin
   }
   __syncthreads();
   double *Fo = F + row0 * RT;
-  for (int x = tid; x < nrows * RT; x += TR) Fo[x] = Us[(x / RT) * US + (x % RT)];
+  if (peers) {
+    // peer-memory exchange fused into the write-back (sharded engine, exchange = p2p): every
+    // 16-byte chunk of the block's rows that differs from the pass-start value still in F is
+    // also stored into every peer's replica, so the NVLink traffic of one block overlaps the
+    // compute of the others
+    for (int x = tid; x < nrows * RT / 2; x += TR) {
+      const int r = (2 * x) / RT, col = (2 * x) % RT;
+      const double2 nv = make_double2(Us[r * US + col], Us[r * US + col + 1]);
+      const double2 ov = reinterpret_cast<const double2 *>(Fo)[x];
+      if (__double_as_longlong(nv.x) != __double_as_longlong(ov.x) ||
+          __double_as_longlong(nv.y) != __double_as_longlong(ov.y)) {
+        for (int p = 0; p < G; ++p)
+          if (p != me) reinterpret_cast<double2 *>(peers[p] + row0 * RT)[x] = nv;
+      }
+      reinterpret_cast<double2 *>(Fo)[x] = nv;
+    }
+  } else {
+    for (int x = tid; x < nrows * RT; x += TR) Fo[x] = Us[(x / RT) * US + (x % RT)];
+  }
 
   // fixed-order block reduction of (ti, md, E, Ech)
 #pragma unroll
@@ -549,7 +568,8 @@ __global__ void __launch_bounds__(WPB * 32)
                          double *__restrict__ Z, const double *__restrict__ H, const DevState *__restrict__ st,
                          uint8_t *__restrict__ dec, double *__restrict__ ti_part, double *__restrict__ md_part,
                          long long *__restrict__ e_part, long long *__restrict__ ech_part, long long nblk,
-                         double *__restrict__ gram_part) {
+                         double *__restrict__ gram_part, double *const *__restrict__ peers = nullptr, int G = 0,
+                         int me = 0) {
   constexpr int TR = WPB * 32;
   constexpr int US = RT + 2;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -560,7 +580,7 @@ __global__ void __launch_bounds__(WPB * 32)
   const long long b0 = nblk * blockIdx.x / gridDim.x, b1 = nblk * (blockIdx.x + 1) / gridDim.x;
   for (long long rb = b0; rb < b1; ++rb) {
     rows_mma_block<RT, WPB>(rb, row_begin, row_end, R, mode, l_mode, row_ptr, M, F, Z, H, st, dec, ti_part, md_part,
-                            e_part, ech_part);
+                            e_part, ech_part, peers, G, me);
     // Us holds the block's final rows (rows past the range are zero): add them to the Gram
     const int nrows = (int)min((long long)TR, row_end - (row_begin + rb * TR));
     acc.add_block(Us, US, (nrows + 3) & ~3, wp, lane);

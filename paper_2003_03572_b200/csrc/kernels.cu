@@ -430,7 +430,10 @@ struct Impl {
     if (begin_sweep) k_sweep_begin<<<1, 32, 0, c.stream>>>(c.st);
     SACD_TRY(sharded_mttkrp_merge(c, mode));
     SACD_TRY(prepare(c, mode, branch_override, begin_sweep, 1));
-    if (c.delta || c.p2p) SACD_TRY(delta_snapshot(c, mode));
+    // p2p: the fused row kernel (fp64, R <= 64) stores the changed chunks into the peers
+    // itself; the other row kernels are followed by k_p2p_push against a pass-start snapshot
+    const bool fused_push = c.p2p && c.G > 1 && gram_fused(c);
+    if (c.delta || (c.p2p && !fused_push)) SACD_TRY(delta_snapshot(c, mode));
     const long long TR = rows_tr(c, 0);
     const long long slot = 4 + (long long)c.R * c.R;
     for (Shard &sh : c.shards) {
@@ -441,9 +444,12 @@ struct Impl {
       long long *e_part = sh.cnt_part, *ech_part = sh.cnt_part + c.max_row_blocks;
       int pe = prof_begin(c, 3);
       int gn = 0;
+      c.rows_peers = fused_push ? reinterpret_cast<void *const *>(sh.d_peerF[mode]) : nullptr;
+      c.rows_me = sh.rank;
       if (nblk > 0)
         SACD_TRY(rows(c, nblk, rlo, rhi, mode, reinterpret_cast<const Real *>(sh.M), dec, ti_part, md_part, e_part,
                       ech_part, 0, gram_fused(c) ? sh.gram_part : nullptr, &gn));
+      c.rows_peers = nullptr;
       SACD_CUDA_TRY(cudaGetLastError());
       SACD_TRY(prof_end(c, 3, pe));
       pe = prof_begin(c, 4);
@@ -458,7 +464,7 @@ struct Impl {
       k_finalize<<<1, 1024, 0, c.stream>>>(mode, nblk, ti_part, md_part, e_part, ech_part, nullptr, nullptr,
                                            nullptr, c.R, c.st, 8, sl);
       SACD_CUDA_TRY(cudaGetLastError());
-      if (c.p2p && rhi > rlo && c.G > 1)  // this shard's changed chunks into the peers' replicas
+      if (c.p2p && !fused_push && rhi > rlo && c.G > 1)  // this shard's changed chunks into the peers' replicas
         k_p2p_push<Real><<<4 * c.num_sms, 256, 0, c.stream>>>(
             rlo * RT, rhi * RT, reinterpret_cast<const Real *>(md.F), reinterpret_cast<const Real *>(c.Fold),
             reinterpret_cast<Real *const *>(sh.d_peerF[mode]), c.G, sh.rank);
@@ -801,7 +807,8 @@ struct Impl {
           kern<<<(unsigned)grid, kMmaWarps * 32, rows_mma_smem_bytes<RT, kMmaWarps>(), c.stream>>>(
               rlo, rhi, c.R, mode, c.opt.l_mode, md.row_ptr, reinterpret_cast<const double *>(M),
               reinterpret_cast<double *>(md.F), reinterpret_cast<double *>(md.Z),
-              reinterpret_cast<const double *>(c.Hr), c.st, dec, ti_part, md_part, e_part, ech_part, nblk, gram_out);
+              reinterpret_cast<const double *>(c.Hr), c.st, dec, ti_part, md_part, e_part, ech_part, nblk, gram_out,
+              reinterpret_cast<double *const *>(c.rows_peers), c.G, c.rows_me);
           if (gram_n) *gram_n = (int)grid;
         }
         SACD_CUDA_TRY(cudaGetLastError());

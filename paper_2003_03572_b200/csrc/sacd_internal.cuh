@@ -225,6 +225,8 @@ struct Context {
   bool delta = false;
   bool p2p = false;               // opt.reserved[3] = 2: changed 16-byte chunks pushed to peers'
                                   // replicas by a kernel, device-side flags (graph-capturable)
+  void *const *rows_peers = nullptr;  // set around a shard's fused row-update launch (p2p)
+  int rows_me = 0;
   bool capturing = false;         // inside capture_graph (no host synchronisation allowed)
   void *Fold = nullptr;           // Real [maxI * pitch]: owned rows before the pass
   uint32_t *didx = nullptr;       // [sum_q cap_q] list of rank q at doff[q]
