@@ -563,15 +563,15 @@ static int init_impl(Context *c, const uint32_t *coords, const float *vals, uint
   // 2%); 256 for mid-size tensors (c2 0.25 -> 0.08 ms, c3 1.21 -> 1.08, c5 R=8/16 -14..16%)
   // and for a sharded rank (c4, 8 emulated ranks: 17.2 -> 13.2 ms summed); 64 under 1e5
   // nonzeros (c1 0.095 -> 0.041 ms).
-  // The same T for the sharded engine as for one GPU (by the whole tensor's size): split rows
-  // then have the same row-relative segments, so a one-rank sharded run sums every row of M in
-  // the unsharded order (bitwise equal results, test_sharded_nccl_world1_matches_unsharded).
-  // The dynamically scheduled kernels removed the last-wave tail that made 256-nonzero items
-  // worth it for a sharded rank in round 1.
+  // T follows the nonzeros ONE rank processes (nnz / G): a sharded rank's launch then has
+  // enough items to fill the GPU (c4 over 8 ranks: 256, 1.25e7 nonzeros each), and a one-rank
+  // sharded run uses exactly the unsharded items, so it sums every row of M in the unsharded
+  // order (bitwise equal results, test_sharded_nccl_world1_matches_unsharded).
+  const long long nnz_rank = c->nnz / std::max(1, c->G);
   long long T = 1024;
   if (c->opt.nnz_per_item > 0) T = c->opt.nnz_per_item;
-  else if (c->pitch >= 128 || c->nnz >= 50000000LL) T = 1024;
-  else if (c->nnz < 100000) T = 64;
+  else if (c->pitch >= 128 || nnz_rank >= 50000000LL) T = 1024;
+  else if (nnz_rank < 100000) T = 64;
   else T = 256;
   long long max_slots = 1, maxI = 1, max_chunks = 1;
   std::vector<long long> rps[3];

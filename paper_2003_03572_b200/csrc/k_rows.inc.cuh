@@ -519,23 +519,56 @@ struct GramAcc {
 #pragma unroll
     for (int k = 0; k < TPW; ++k) c[k][0] = c[k][1] = 0.0;
   }
-  __device__ __forceinline__ void add_block(const double *Us, int US, int nrows_pad, int wp, int lane) {
-    const int g = lane >> 2, t = lane & 3;
-#pragma unroll
-    for (int k = 0; k < TPW; ++k) {
-      const int q = wp + WPB * k;
-      if (q < NT) {
-        int ti, tj;
-        tile_ij(q, ti, tj);
-        const double *pa = Us + t * US + 8 * ti + g;
-        const double *pb = Us + t * US + 8 * tj + g;
-        for (int r0 = 0; r0 < nrows_pad; r0 += 4) {
-          const double a = pa[r0 * US], b = pb[r0 * US];
-          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                       : "+d"(c[k][0]), "+d"(c[k][1])
-                       : "d"(a), "d"(b));
-        }
+  // k-steps outer, tiles inner: the warp's TPW accumulator chains are independent, so their
+  // DMMAs overlap (a tile-outer loop made one dependent chain of TPW * rows / 4 DMMAs); the
+  // P panel fragments of a k-step are loaded once and shared by the tiles.  The warp index is
+  // a template argument so that every tile's two panels are compile-time register picks.
+  __host__ __device__ static constexpr int tile_i(int q) {
+    int ti = 0;
+    while (q >= P - ti) {
+      q -= P - ti;
+      ++ti;
+    }
+    return ti;
+  }
+  __host__ __device__ static constexpr int tile_j(int q) {
+    int ti = 0;
+    while (q >= P - ti) {
+      q -= P - ti;
+      ++ti;
+    }
+    return ti + q;
+  }
+  template <int W, int K>
+  __device__ __forceinline__ void mma_tiles(const double (&pf)[P]) {
+    if constexpr (K < TPW) {
+      constexpr int q = W + WPB * K;
+      if constexpr (q < NT) {
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                     : "+d"(c[K][0]), "+d"(c[K][1])
+                     : "d"(pf[tile_i(q)]), "d"(pf[tile_j(q)]));
       }
+      mma_tiles<W, K + 1>(pf);
+    }
+  }
+  template <int W>
+  __device__ __forceinline__ void add_block_w(const double *Us, int US, int nrows_pad, int lane) {
+    const int g = lane >> 2, t = lane & 3;
+    const double *p0 = Us + t * US + g;
+    for (int r0 = 0; r0 < nrows_pad; r0 += 4) {
+      double pf[P];
+#pragma unroll
+      for (int j = 0; j < P; ++j) pf[j] = p0[r0 * US + 8 * j];
+      mma_tiles<W, 0>(pf);
+    }
+  }
+  __device__ __forceinline__ void add_block(const double *Us, int US, int nrows_pad, int wp, int lane) {
+    static_assert(WPB == 4, "add_block dispatches 4 warps");
+    switch (wp) {
+      case 0: add_block_w<0>(Us, US, nrows_pad, lane); break;
+      case 1: add_block_w<1>(Us, US, nrows_pad, lane); break;
+      case 2: add_block_w<2>(Us, US, nrows_pad, lane); break;
+      default: add_block_w<3>(Us, US, nrows_pad, lane); break;
     }
   }
   // upper-triangle entries (r <= t) of this CTA's partial: the k_gram_reduce contract

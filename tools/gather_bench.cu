@@ -197,7 +197,10 @@ static std::vector<uint32_t> make_idx(long long n, long long T, double s, uint64
 }
 
 int main(int argc, char **argv) {
+  // gather_bench [n] [table filter] [dist filter] [kernel filter]: filters are substrings
+  // (e.g. "L2_5MB" "zipf" "ldg_w32" for one case under ncu)
   const long long n = argc > 1 ? atoll(argv[1]) : (1LL << 26);
+  const std::string ftab = argc > 2 ? argv[2] : "", fdist = argc > 3 ? argv[3] : "", fker = argc > 4 ? argv[4] : "";
   int dev = 0, sms = 0;
   CK(cudaSetDevice(dev));
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -230,10 +233,13 @@ int main(int argc, char **argv) {
   const Tab tabs[] = {{"L1_100KB", 200}, {"L2_5MB", 10000}, {"HBM_256MB", 500000}, {"HBM_512MB", 1000000}};
   const double dists[] = {0.0, 1.2};
   for (const Tab &tb : tabs) {
+    if (!ftab.empty() && std::string(tb.name).find(ftab) == std::string::npos) continue;
     for (double s : dists) {
+      if (!fdist.empty() && std::string(s > 0 ? "zipf1.2" : "uniform").find(fdist) == std::string::npos) continue;
       std::vector<uint32_t> hi = make_idx(n, tb.T, s, 12345);
       CK(cudaMemcpy(idx, hi.data(), hi.size() * 4, cudaMemcpyHostToDevice));
       auto run = [&](const char *kname, auto launch) {
+        if (!fker.empty() && std::string(kname) != fker) return;
         launch();
         CK(cudaGetLastError());
         CK(cudaDeviceSynchronize());
