@@ -191,13 +191,18 @@ class OracleSweepSample:
 
     def step_seconds(self):
         O = self.O
+        T = O.max_threads()
         spent, full = 0.0, 0.0
         for n, a, b, w, (ia, ib, vv, rp) in self.strata:
             t0 = time.perf_counter()
             O.mttkrp_layout(rp, ia, ib, vv, self.F[a], self.F[b])
             dt = time.perf_counter() - t0
             spent += dt
-            full += dt * w
+            # ora_mttkrp hands rows to threads in chunks of 64 (schedule(dynamic, 64)): a
+            # stratum sample of few (heavy) rows runs on p < T threads, while in the full sweep
+            # those rows run beside all the others, so its share is its CPU time / T
+            p = min(T, max(1, (len(rp) - 1 + 63) // 64))
+            full += dt * w * p / T
         for n in range(3):
             H, Fs, M = self.rows[n]
             t0 = time.perf_counter()
