@@ -458,7 +458,7 @@ struct Impl {
         gn = gram_ranges(c, rlo, rhi);
         gram_partial(c, rlo, rhi, reinterpret_cast<const Real *>(md.F), sh.gram_part);
       }
-      k_gram_reduce<<<(c.R * c.R + 255) / 256, 256, 0, c.stream>>>(c.R, gn, sh.gram_part, sl + 4);
+      k_gram_reduce<<<gram_reduce_blocks(c.R), 256, 0, c.stream>>>(c.R, gn, sh.gram_part, sl + 4);
       SACD_CUDA_TRY(cudaGetLastError());
       SACD_TRY(prof_end(c, 4, pe));
       k_finalize<<<1, 1024, 0, c.stream>>>(mode, nblk, ti_part, md_part, e_part, ech_part, nullptr, nullptr,
@@ -649,7 +649,7 @@ struct Impl {
     ModeData &md = c.m[mode];
     int pe = prof_begin(c, 4);
     gram_partial(c, 0, md.I, reinterpret_cast<const Real *>(md.F), c.gram_part);
-    k_gram_reduce<<<(c.R * c.R + 255) / 256, 256, 0, c.stream>>>(c.R, gram_ranges(c, 0, md.I), c.gram_part, md.G);
+    k_gram_reduce<<<gram_reduce_blocks(c.R), 256, 0, c.stream>>>(c.R, gram_ranges(c, 0, md.I), c.gram_part, md.G);
     SACD_CUDA_TRY(cudaGetLastError());
     SACD_TRY(chunk_mask(c, mode));
     return prof_end(c, 4, pe);
@@ -713,7 +713,7 @@ struct Impl {
     SACD_TRY(prof_end(c, 3, pe));
     if (gn > 0) {  // the row kernel wrote one Gram partial per CTA: fixed-order reduce only
       pe = prof_begin(c, 4);
-      k_gram_reduce<<<(c.R * c.R + 255) / 256, 256, 0, c.stream>>>(c.R, gn, c.gram_part, md.G);
+      k_gram_reduce<<<gram_reduce_blocks(c.R), 256, 0, c.stream>>>(c.R, gn, c.gram_part, md.G);
       SACD_CUDA_TRY(cudaGetLastError());
       SACD_TRY(prof_end(c, 4, pe));
     } else {

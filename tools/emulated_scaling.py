@@ -27,5 +27,11 @@ for G in (1, 2, 4, 8):
         g.sync()
         ms = (time.perf_counter() - t) / K * 1e3
         f = g.fit()[0]
+        g.set_profile(True)
+        g.profile_reset()
+        g.iterate(K)
+        g.sync()
+        p = g.profile_read()
+        br = " ".join(f"{k} {p[k][0] / K:.3f}" for k in p)
     print(f"{name} G={G} ({'unsharded' if G == 1 else 'emulated, ' + exchange}): {ms:.2f} ms per sweep "
-          f"(sum over ranks), f = {f:.10e}", flush=True)
+          f"(sum over ranks), f = {f:.10e}; eager per class: {br}", flush=True)
