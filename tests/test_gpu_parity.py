@@ -494,8 +494,9 @@ def test_c4_end_to_end_10_sweeps():
       * at that first pass, every element decided differently is a near-tie at fp64
         resolution in the oracle's own trajectory: its gradient
         g = -m + sum_j u_j h_jr (Eq 14, the Gauss-Seidel row at column r) is below
-        1e-12 x (|m| + sum_j |u_j h_jr|), i.e. g, and with it the step d and the importance z
-        (Eq 20), is rounding noise of the cancellation, on either side.  After that pass the
+        1e-12 x (|m| + sum_j |u_j h_jr|), or its z and z_prev are below 1e-12 x the pass's
+        largest importance -- g, and with it the step d and the importance z (Eq 20), is
+        rounding noise of the cancellation, on either side.  After that pass the
         trajectories are different valid SaCD runs (reading C19): later mismatches and the
         final factor error are reported, not bounded.
     tools/flip_census.py / flip_census_oracle.py (profiles/r02_flip_census_*) show that neither
@@ -537,9 +538,10 @@ def test_c4_end_to_end_10_sweeps():
                             terms = u * H[:, r]
                             g_o = -M[i, r] + terms.sum()
                             rel_g = abs(g_o) / max(abs(M[i, r]) + np.abs(terms).sum(), 1e-300)
+                            rel_z = max(abs(z0), abs(z1)) / max(np.abs(zp).max(), np.abs(Z[n]).max(), 1e-300)
                             report.append((k, n, int(i), int(r), float(z0), float(z1), float(sp), float(rel_g),
-                                           float(Zg0[i, r] - z0)))
-                            assert rel_g <= 1e-12, report[-1]
+                                           float(rel_z), float(Zg0[i, r] - z0)))
+                            assert rel_g <= 1e-12 or rel_z <= 1e-12, report[-1]
                     else:
                         assert out["E"] == E and out["E_changed"] == Ech
                         assert factor_err(g.factors(n), Fn) <= FACTOR_TOL
@@ -555,7 +557,7 @@ def test_c4_end_to_end_10_sweeps():
             assert abs(f_g - f_o) <= F_TOL * f_o, (k, f_g, f_o)
         errs = [factor_err(g.factors(n), F[n]) for n in range(3)]
     print(f"c4 10 sweeps: first pass decided differently {first}; its near-ties (sweep, mode, row, col, z_prev, "
-          f"z, sp (oracle), |g| / sum of |terms|, z_prev gpu - oracle): {report[:20]}; final factor err {errs}")
+          f"z, sp (oracle), |g| / sum of |terms|, max(|z|, |z_prev|) / pass max, z_prev gpu - oracle): {report[:20]}; final factor err {errs}")
 
 
 # ----------------------------------------------------------------------------- sharded engine
