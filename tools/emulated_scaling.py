@@ -14,11 +14,14 @@ from paper_2003_03572_b200.sacd import Sacd  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 and not sys.argv[1].startswith("--") else "c4"
 exchange = sys.argv[sys.argv.index("--exchange") + 1] if "--exchange" in sys.argv else "delta"
+npi = int(sys.argv[sys.argv.index("--nnz-per-item") + 1]) if "--nnz-per-item" in sys.argv else 0
 cfg = SI.CONFIGS[name]
 c, v = SI.make_tensor(cfg, device="cuda")
 K, W = 10, 3
 for G in (1, 2, 4, 8):
     kw = {} if G == 1 else dict(emulate_ranks=G, exchange=exchange)
+    if npi:
+        kw["nnz_per_item"] = npi
     with Sacd(c, v, cfg.dims, cfg.rank, cfg.seed, **kw) as g:
         g.iterate(W)
         g.sync()
