@@ -145,12 +145,16 @@ class OracleSweepSample:
     Layouts of the samples are built untimed in the constructor.  step_seconds() returns
     (seconds actually spent, estimated full-sweep seconds)."""
 
-    def __init__(self, c, v, dims, R, seed, budget=3_000_000, rstep=None):
+    def __init__(self, c, v, dims, R, seed, budget=3_000_000, rstep=None, rsub=8):
         import oracle as O
         O.build()
         self.O, self.dims, self.R = O, dims, R
         F = O.init_factors(dims, R, seed)
         self.F = F
+        # ora_mttkrp walks a slice once per column (for r: for e in slice), so its cost is
+        # linear in R: the MTTKRP samples run on the first rsub columns and are scaled by R/rsub
+        self.rsub = min(R, rsub)
+        self.Fs = [np.ascontiguousarray(F[n][:, :self.rsub]) for n in range(3)]
         self.rstep = rstep or max(1, int(round(sum(dims) / 100_000)))
         self.strata = []   # (mode, weight, layout, nnz)
         self.nnz = len(v)
@@ -195,9 +199,10 @@ class OracleSweepSample:
         spent, full = 0.0, 0.0
         for n, a, b, w, (ia, ib, vv, rp) in self.strata:
             t0 = time.perf_counter()
-            O.mttkrp_layout(rp, ia, ib, vv, self.F[a], self.F[b])
+            O.mttkrp_layout(rp, ia, ib, vv, self.Fs[a], self.Fs[b])
             dt = time.perf_counter() - t0
             spent += dt
+            dt *= self.R / self.rsub
             # ora_mttkrp hands rows to threads in chunks of 64 (schedule(dynamic, 64)): a
             # stratum sample of few (heavy) rows runs on p < T threads, while in the full sweep
             # those rows run beside all the others, so its share is its CPU time / T
@@ -217,8 +222,9 @@ class OracleSweepSample:
     def describe(self):
         return (f"oracle sweep functions as they stand: mttkrp_layout on slice-length-stratified row samples "
                 f"({len(self.strata)} strata, {self.nnz_s} of 3x{self.nnz} slice nonzeros, weighted by rows / "
-                f"sampled rows per stratum) + mode_pass and 3 x gram on every {self.rstep}th row (scaled by the "
-                f"row share); sample layouts built untimed")
+                f"sampled rows per stratum, {self.rsub} of {self.R} columns scaled by R / {self.rsub}: the oracle "
+                f"walks each slice once per column) + mode_pass and 3 x gram on every {self.rstep}th row (scaled "
+                f"by the row share); sample layouts built untimed")
 
 
 def cpu_baseline(c, v, dims, R, seed, nnz, reps=3):
