@@ -451,6 +451,29 @@ def test_device_inputs_from_torch_stream_are_complete():
         assert r_dev == r_host
 
 
+def test_per_sweep_device_time():
+    """sacd_iter_stats.ms (%globaltimer from the sweep's first kernel to the end of its
+    objective kernel, SPEC FitReport S:251-254) is positive for every sweep and, summed over
+    back-to-back captured sweeps, matches the CUDA-event time of sacd_iterate."""
+    import torch
+    cfg = SI.CONFIGS["c3"]
+    c, v = SI.make_tensor(cfg, device="cuda")
+    stream = torch.cuda.Stream()
+    with S(c, v, cfg.dims, cfg.rank, cfg.seed, stream=stream.cuda_stream) as g:
+        g.iterate(2)
+        g.sync()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        g.iterate(10)
+        e1.record(stream)
+        e1.synchronize()
+        ms = e0.elapsed_time(e1)
+        st = g.stats()
+    dev = [s["ms"] for s in st]
+    assert len(dev) == 12 and all(0 < x < 1e3 for x in dev)
+    assert abs(sum(dev[2:]) - ms) <= 0.1 * ms + 0.05, (dev, ms)
+
+
 def test_profile_mode_counts_launches():
     cfg = SI.CONFIGS["c1"]
     c, v = SI.make_tensor(cfg)
