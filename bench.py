@@ -130,22 +130,27 @@ def algorithmic_bytes(cfg_dims, nnz, R, s):
 class OracleSweepSample:
     """The fp64 oracle's sweep (oracle.sacd_run, as it stands) on a bounded sample.
 
-    Per sweep, ora_sacd_run does for each mode n: the Grams of the two other factors, their
-    Hadamard product, the MTTKRP of every row of mode n over its full slice, and the row pass;
-    then the three Grams for the objective (every factor's Gram three times).  A step runs
-    exactly those oracle functions on samples, and estimates the full sweep:
-      * MTTKRP: the rows of each mode are stratified by slice length (classes [2^j, 2^(j+1)));
-        in every class a systematic sample of rows (with their FULL slices) gets the
-        oracle's mttkrp_layout, weighted by rows in class / rows sampled.  The oracle's cost
-        per nonzero depends on the slice length (it walks a slice once per column, so long
-        Zipf slices fall out of cache), which is why a single systematic sample scaled by the
-        nonzero share misestimates it;
-      * row pass and Grams (cost per row independent of the data): every `rstep`-th row,
-        scaled by the row share.
+    Per sweep, ora_sacd_run does, for each mode n: the Grams of the two other factors, their
+    Hadamard product, the MTTKRP of every row of mode n over its full slice, and the row pass.
+    It then does the three Grams for the objective, so every factor's Gram runs three times.
+    A step runs exactly those oracle functions on samples and models the full sweep from
+    them (calibrated on the GPU box, profiles/r02_oracle_slice_cost.txt):
+      * MTTKRP.  The rows of each mode are stratified by slice length (classes
+        [2^j, 2^(j+1))).  In every class a systematic sample of rows, with their full slices,
+        gets the oracle's mttkrp_layout.  A slice longer than `cap` nonzeros is timed on its
+        first `cap` nonzeros and scaled by length: its cost per nonzero does not depend on the
+        length.  ora_mttkrp hands rows to threads (dynamic, chunks of 64), so the mode takes
+        max(total CPU time / threads, its heaviest row), and the Zipf heads make the second
+        term bind.
+      * Gram.  One full-length strided pass per column pair, over a row subset of at least
+        128 MB (every k-th row; smaller subsets stay in cache and run too fast), scaled by k,
+        x 3 per factor.
+      * Row pass.  Cost per row is independent of the data: every `rstep`-th row, scaled by the
+        row share.
     Layouts of the samples are built untimed in the constructor.  step_seconds() returns
-    (seconds actually spent, estimated full-sweep seconds)."""
+    (seconds actually spent, modelled full-sweep seconds)."""
 
-    def __init__(self, c, v, dims, R, seed, budget=3_000_000, rstep=None, cap=1 << 20):
+    def __init__(self, c, v, dims, R, seed, budget=3_000_000, rstep=None, cap=1 << 20, gram_bytes=128 << 20):
         import oracle as O
         O.build()
         self.O, self.dims, self.R = O, dims, R
@@ -153,7 +158,7 @@ class OracleSweepSample:
         self.F = F
         self.cap = cap
         self.rstep = rstep or max(1, int(round(sum(dims) / 100_000)))
-        self.strata = []   # (mode, weight, layout, nnz)
+        self.strata = []   # (mode, a, b, weight, layout, longest row's share of the stratum's nonzeros, length scale)
         self.nnz = len(v)
         self.nnz_s = 0
         for n in range(3):
@@ -182,17 +187,16 @@ class OracleSweepSample:
                 d2 = list(dims)
                 d2[n] = len(sel)
                 ia, ib, vv, rp = O.layout(cj, vj, d2, n)
-                # a slice longer than `cap` nonzeros (the Zipf heads) is timed on its first `cap`
-                # nonzeros and scaled by length / cap: past a few MB the oracle's per-nonzero cost
-                # no longer depends on the slice length (every column pass streams from memory)
                 ln_s = np.diff(rp)
+                longest = float(ln_s.max(initial=0)) / max(1.0, float(ln_s.sum()))
+                scale = 1.0
                 if ln_s.max(initial=0) > cap:
                     keep = np.concatenate([np.arange(rp[i], rp[i] + min(ln_s[i], cap)) for i in range(len(ln_s))])
                     rp2 = np.concatenate([[0], np.cumsum(np.minimum(ln_s, cap))]).astype(np.int64)
-                    w *= float(ln_s.sum()) / float(rp2[-1])
+                    scale = float(ln_s.sum()) / float(rp2[-1])
                     ia, ib, vv, rp = (np.ascontiguousarray(ia[keep]), np.ascontiguousarray(ib[keep]),
                                       np.ascontiguousarray(vv[keep]), rp2)
-                self.strata.append((n, a, b, w, (ia, ib, vv, rp)))
+                self.strata.append((n, a, b, w, (ia, ib, vv, rp), longest, scale))
                 self.nnz_s += int(rp[-1])
         self.rows = []
         for n in range(3):
@@ -200,38 +204,46 @@ class OracleSweepSample:
             H = O.hadamard(O.gram(F[a]), O.gram(F[b]))
             Fs = np.ascontiguousarray(F[n][::self.rstep])
             self.rows.append((H, Fs, np.zeros_like(Fs)))
+        self.gk = [max(1, int(dims[n] * R * 8 // gram_bytes)) for n in range(3)]
+        self.gF = [np.ascontiguousarray(F[n][::self.gk[n]]) for n in range(3)]
 
     def step_seconds(self):
         O = self.O
         T = O.max_threads()
         spent, full = 0.0, 0.0
-        for n, a, b, w, (ia, ib, vv, rp) in self.strata:
+        cpu = [0.0, 0.0, 0.0]
+        heavy = [0.0, 0.0, 0.0]
+        for n, a, b, w, (ia, ib, vv, rp), longest, scale in self.strata:
             t0 = time.perf_counter()
             O.mttkrp_layout(rp, ia, ib, vv, self.F[a], self.F[b])
             dt = time.perf_counter() - t0
             spent += dt
-            # ora_mttkrp hands rows to threads in chunks of 64 (schedule(dynamic, 64)): a
-            # stratum sample of few (heavy) rows runs on p < T threads, while in the full sweep
-            # those rows run beside all the others, so its share is its CPU time / T
-            p = min(T, max(1, (len(rp) - 1 + 63) // 64))
-            full += dt * w * p / T
+            p = min(T, max(1, (len(rp) - 1 + 63) // 64))   # threads the sample's rows ran on
+            c_s = dt * p * scale                              # CPU seconds of the sampled rows (full length)
+            cpu[n] += c_s * w
+            heavy[n] = max(heavy[n], c_s * longest)          # ~ the stratum's longest row alone
+        for n in range(3):
+            full += max(cpu[n] / T, heavy[n])
         for n in range(3):
             H, Fs, M = self.rows[n]
             t0 = time.perf_counter()
             O.mode_pass(M, H, Fs, np.zeros_like(Fs), O.BR_FIRST)
-            for _ in range(3):
-                O.gram(Fs)
             dt = time.perf_counter() - t0
             spent += dt
             full += dt * (self.dims[n] / len(Fs))
+            t0 = time.perf_counter()
+            O.gram(self.gF[n])
+            dt = time.perf_counter() - t0
+            spent += dt
+            full += 3.0 * dt * self.gk[n]
         return spent, full
 
     def describe(self):
         return (f"oracle sweep functions as they stand: mttkrp_layout on slice-length-stratified row samples "
-                f"({len(self.strata)} strata, {self.nnz_s} of 3x{self.nnz} slice nonzeros, weighted by rows / "
-                f"sampled rows per stratum; slices longer than {self.cap} nonzeros timed on their first {self.cap} "
-                f"and scaled by length) + mode_pass and 3 x gram on every {self.rstep}th row (scaled by the row "
-                f"share); sample layouts built untimed")
+                f"({len(self.strata)} strata, {self.nnz_s} of 3x{self.nnz} slice nonzeros; slices longer than "
+                f"{self.cap} timed on their first {self.cap} and scaled by length; per mode max(CPU time / threads, "
+                f"heaviest row)) + mode_pass on every {self.rstep}th row + one gram per factor on every "
+                f"{self.gk}-th row (>= 128 MB, x k x 3); sample layouts built untimed")
 
 
 def cpu_baseline(c, v, dims, R, seed, nnz, reps=3):
