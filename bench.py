@@ -532,6 +532,7 @@ def main():
         d2h = sum(x.nbytes for x in Fs) + 16
         e2e = {"value": K / t_e2e, "unit": UNIT, "h2d_bytes_per_step": h2d / K, "d2h_bytes_per_step": d2h / K,
                "seconds": t_e2e, "phases": phases, "runs_seconds": [r[0] for r in runs],
+               "runs_phases": [r[1] for r in runs],
                "what": "sacd_init from pinned host COO (H2D + device layout sort) + sacd_iterate(K) + "
                        "sacd_factors (D2H, all modes) + sacd_fit; bytes per step = totals / K; median of the runs"}
 
