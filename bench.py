@@ -139,9 +139,10 @@ class OracleSweepSample:
         [2^j, 2^(j+1))).  In every class a systematic sample of rows, with their full slices,
         gets the oracle's mttkrp_layout.  A slice longer than `cap` nonzeros is timed on its
         first `cap` nonzeros and scaled by length: its cost per nonzero does not depend on the
-        length.  ora_mttkrp hands rows to threads (dynamic, chunks of 64), so the mode takes
-        max(total CPU time / threads, its heaviest row), and the Zipf heads make the second
-        term bind.
+        length.  ora_mttkrp hands rows to threads in chunks of 64 consecutive rows (dynamic), so
+        the mode takes max(total CPU time / threads, its heaviest chunk), every row's time
+        coming from its class's measured cost per nonzero; the Zipf heads (the first chunks)
+        make the second term bind (profiles/r02_oracle_breakdown_c4.txt).
       * Gram.  One full-length strided pass per column pair, over a row subset of at least
         128 MB (every k-th row; smaller subsets stay in cache and run too fast), scaled by k,
         x 3 per factor.
@@ -158,7 +159,8 @@ class OracleSweepSample:
         self.F = F
         self.cap = cap
         self.rstep = rstep or max(1, int(round(sum(dims) / 100_000)))
-        self.strata = []   # (mode, a, b, weight, layout, longest row's share of the stratum's nonzeros, length scale)
+        self.strata = []   # (mode, a, b, weight, layout, class, nonzeros of the sampled rows (full length), length scale)
+        self.row_len, self.row_cls = [], []
         self.nnz = len(v)
         self.nnz_s = 0
         for n in range(3):
@@ -167,6 +169,8 @@ class OracleSweepSample:
             ln = np.bincount(ci, minlength=dims[n])
             cls = np.where(ln > 0, np.floor(np.log2(np.maximum(ln, 1))).astype(np.int64), -1)
             classes = [k for k in np.unique(cls) if k >= 0]
+            self.row_len.append(ln)
+            self.row_cls.append(cls)
             per = budget / max(1, len(classes))
             pick = np.zeros(dims[n], np.int64)   # stratum id + 1 of each sampled row, 0 = not sampled
             info = []
@@ -188,7 +192,7 @@ class OracleSweepSample:
                 d2[n] = len(sel)
                 ia, ib, vv, rp = O.layout(cj, vj, d2, n)
                 ln_s = np.diff(rp)
-                longest = float(ln_s.max(initial=0)) / max(1.0, float(ln_s.sum()))
+                nz_full = float(ln_s.sum())
                 scale = 1.0
                 if ln_s.max(initial=0) > cap:
                     keep = np.concatenate([np.arange(rp[i], rp[i] + min(ln_s[i], cap)) for i in range(len(ln_s))])
@@ -196,7 +200,7 @@ class OracleSweepSample:
                     scale = float(ln_s.sum()) / float(rp2[-1])
                     ia, ib, vv, rp = (np.ascontiguousarray(ia[keep]), np.ascontiguousarray(ib[keep]),
                                       np.ascontiguousarray(vv[keep]), rp2)
-                self.strata.append((n, a, b, w, (ia, ib, vv, rp), longest, scale))
+                self.strata.append((n, a, b, w, (ia, ib, vv, rp), int(classes[j]), nz_full, scale))
                 self.nnz_s += int(rp[-1])
         self.rows = []
         for n in range(3):
@@ -211,19 +215,26 @@ class OracleSweepSample:
         O = self.O
         T = O.max_threads()
         spent, full = 0.0, 0.0
-        cpu = [0.0, 0.0, 0.0]
-        heavy = [0.0, 0.0, 0.0]
-        for n, a, b, w, (ia, ib, vv, rp), longest, scale in self.strata:
+        cpn = [dict(), dict(), dict()]   # CPU seconds per nonzero, per slice-length class
+        for n, a, b, w, (ia, ib, vv, rp), k, nz_full, scale in self.strata:
             t0 = time.perf_counter()
             O.mttkrp_layout(rp, ia, ib, vv, self.F[a], self.F[b])
             dt = time.perf_counter() - t0
             spent += dt
             p = min(T, max(1, (len(rp) - 1 + 63) // 64))   # threads the sample's rows ran on
-            c_s = dt * p * scale                              # CPU seconds of the sampled rows (full length)
-            cpu[n] += c_s * w
-            heavy[n] = max(heavy[n], c_s * longest)          # ~ the stratum's longest row alone
+            cpn[n][k] = dt * p * scale / max(nz_full, 1.0)
         for n in range(3):
-            full += max(cpu[n] / T, heavy[n])
+            # every row's CPU time from its class's cost per nonzero; ora_mttkrp hands out chunks
+            # of 64 consecutive rows (schedule(dynamic, 64)), so the mode takes at least its
+            # heaviest chunk -- the Zipf heads sit in the first chunks (c4's W: 15 s of 16)
+            ln, cls = self.row_len[n], self.row_cls[n]
+            cost = np.zeros(len(ln))
+            for k, v in cpn[n].items():
+                cost[cls == k] = v
+            row_t = ln * cost
+            pad = (-len(row_t)) % 64
+            chunk_t = np.concatenate([row_t, np.zeros(pad)]).reshape(-1, 64).sum(axis=1)
+            full += max(float(row_t.sum()) / T, float(chunk_t.max()))
         for n in range(3):
             H, Fs, M = self.rows[n]
             t0 = time.perf_counter()
@@ -242,7 +253,7 @@ class OracleSweepSample:
         return (f"oracle sweep functions as they stand: mttkrp_layout on slice-length-stratified row samples "
                 f"({len(self.strata)} strata, {self.nnz_s} of 3x{self.nnz} slice nonzeros; slices longer than "
                 f"{self.cap} timed on their first {self.cap} and scaled by length; per mode max(CPU time / threads, "
-                f"heaviest row)) + mode_pass on every {self.rstep}th row + one gram per factor on every "
+                f"heaviest 64-row chunk)) + mode_pass on every {self.rstep}th row + one gram per factor on every "
                 f"{self.gk}-th row (>= 128 MB, x k x 3); sample layouts built untimed")
 
 
