@@ -338,6 +338,14 @@ static void destroy(sacd_ctx *c) {
     cudaFree(sh.flags);
     cudaFree(sh.epoch);
     cudaFree(sh.d_peer_flags);
+    cudaFree(sh.d_px);
+    cudaFree(sh.d_pr);
+    cudaFree(sh.d_ps);
+    if (sh.xid_r && sh.xid_r != c->xid) {
+      cudaFree(sh.xid_r);
+      cudaFree(sh.xrow_r);
+      cudaFree(sh.xstats_r);
+    }
     cudaFree(sh.M);
     cudaFree(sh.partial);
     cudaFree(sh.row_part);
@@ -429,7 +437,17 @@ static int setup_p2p(Context *c) {
   const size_t rs = real_size(*c);
   cudaStream_t s = c->stream;
   const int G = c->G;
+  const size_t xrow_bytes = (size_t)G * c->pitch * rs, xst_bytes = (size_t)G * (4 + (size_t)c->R * c->R) * 8;
   for (Shard &sh : c->shards) {
+    if (sh.rank == c->shards[0].rank) {  // the context's own exchange arrays
+      sh.xid_r = c->xid;
+      sh.xrow_r = c->xrow;
+      sh.xstats_r = c->xstats;
+    } else {  // emulated ranks: every shard its own arrays
+      SACD_CUDA_TRY(cudaMalloc(&sh.xid_r, (size_t)G * 8));
+      SACD_CUDA_TRY(cudaMalloc(&sh.xrow_r, xrow_bytes));
+      SACD_CUDA_TRY(cudaMalloc(&sh.xstats_r, xst_bytes));
+    }
     SACD_CUDA_TRY(cudaMalloc(&sh.flags, (size_t)G * 8));
     SACD_CUDA_TRY(cudaMemsetAsync(sh.flags, 0, (size_t)G * 8, s));
     SACD_CUDA_TRY(cudaMalloc(&sh.epoch, 8));
@@ -446,18 +464,26 @@ static int setup_p2p(Context *c) {
       }
     }
   }
-  // host tables: ptrF[q][n], ptrFlag[q] for every rank q
-  std::vector<void *> ptrF((size_t)G * 3, nullptr), ptrFlag((size_t)G, nullptr);
+  // host tables for every rank q: ptrF[q][n] (factor replicas), ptrX[q][k] (k = 0 flags,
+  // 1 head ids, 2 head rows, 3 stats)
+  constexpr int NH = 7;  // IPC handles per rank: 3 factors + 4 exchange arrays
+  std::vector<void *> ptrF((size_t)G * 3, nullptr), ptrX((size_t)G * 4, nullptr);
   if (c->opt.emulate_ranks > 1 || G == 1) {
     for (Shard &sh : c->shards) {
       for (int n = 0; n < 3; ++n) ptrF[(size_t)sh.rank * 3 + n] = sh.Frep[n];
-      ptrFlag[(size_t)sh.rank] = sh.flags;
+      ptrX[(size_t)sh.rank * 4 + 0] = sh.flags;
+      ptrX[(size_t)sh.rank * 4 + 1] = sh.xid_r;
+      ptrX[(size_t)sh.rank * 4 + 2] = sh.xrow_r;
+      ptrX[(size_t)sh.rank * 4 + 3] = sh.xstats_r;
     }
   } else {
     Shard &sh = c->shards[0];
-    cudaIpcMemHandle_t mine[4];
+    cudaIpcMemHandle_t mine[NH];
     for (int n = 0; n < 3; ++n) SACD_CUDA_TRY(cudaIpcGetMemHandle(&mine[n], sh.Frep[n]));
     SACD_CUDA_TRY(cudaIpcGetMemHandle(&mine[3], sh.flags));
+    SACD_CUDA_TRY(cudaIpcGetMemHandle(&mine[4], sh.xid_r));
+    SACD_CUDA_TRY(cudaIpcGetMemHandle(&mine[5], sh.xrow_r));
+    SACD_CUDA_TRY(cudaIpcGetMemHandle(&mine[6], sh.xstats_r));
     const size_t hb = sizeof(mine);
     char *dh = nullptr;
     SACD_CUDA_TRY(cudaMalloc(&dh, hb * G));
@@ -468,17 +494,18 @@ static int setup_p2p(Context *c) {
       cudaFree(dh);
       return SACD_ENCCL;
     }
-    std::vector<cudaIpcMemHandle_t> all((size_t)G * 4);
+    std::vector<cudaIpcMemHandle_t> all((size_t)G * NH);
     SACD_CUDA_TRY(cudaMemcpyAsync(all.data(), dh, hb * G, cudaMemcpyDeviceToHost, s));
     SACD_CUDA_TRY(cudaStreamSynchronize(s));
     cudaFree(dh);
+    void *own[NH] = {sh.Frep[0], sh.Frep[1], sh.Frep[2], sh.flags, sh.xid_r, sh.xrow_r, sh.xstats_r};
     for (int q = 0; q < G; ++q) {
-      for (int k = 0; k < 4; ++k) {
+      for (int k = 0; k < NH; ++k) {
         void *ptr = nullptr;
         if (q == c->me) {
-          ptr = k < 3 ? sh.Frep[k] : (void *)sh.flags;
+          ptr = own[k];
         } else {
-          const cudaError_t e = cudaIpcOpenMemHandle(&ptr, all[(size_t)q * 4 + k], cudaIpcMemLazyEnablePeerAccess);
+          const cudaError_t e = cudaIpcOpenMemHandle(&ptr, all[(size_t)q * NH + k], cudaIpcMemLazyEnablePeerAccess);
           if (e != cudaSuccess) {
             cudaGetLastError();
             set_error(std::string("sacd_init: peer-memory exchange needs CUDA IPC / P2P between the ranks' GPUs (") +
@@ -488,7 +515,7 @@ static int setup_p2p(Context *c) {
           sh.ipc_opened.push_back(ptr);
         }
         if (k < 3) ptrF[(size_t)q * 3 + k] = ptr;
-        else ptrFlag[(size_t)q] = ptr;
+        else ptrX[(size_t)q * 4 + (k - 3)] = ptr;
       }
     }
   }
@@ -499,8 +526,14 @@ static int setup_p2p(Context *c) {
       SACD_CUDA_TRY(cudaMalloc(&sh.d_peerF[n], (size_t)G * sizeof(void *)));
       SACD_CUDA_TRY(cudaMemcpy(sh.d_peerF[n], v.data(), (size_t)G * sizeof(void *), cudaMemcpyHostToDevice));
     }
-    SACD_CUDA_TRY(cudaMalloc(&sh.d_peer_flags, (size_t)G * sizeof(void *)));
-    SACD_CUDA_TRY(cudaMemcpy(sh.d_peer_flags, ptrFlag.data(), (size_t)G * sizeof(void *), cudaMemcpyHostToDevice));
+    void **tabs[4] = {reinterpret_cast<void **>(&sh.d_peer_flags), reinterpret_cast<void **>(&sh.d_px),
+                      reinterpret_cast<void **>(&sh.d_pr), reinterpret_cast<void **>(&sh.d_ps)};
+    for (int k = 0; k < 4; ++k) {
+      std::vector<void *> v((size_t)G);
+      for (int q = 0; q < G; ++q) v[(size_t)q] = ptrX[(size_t)q * 4 + k];
+      SACD_CUDA_TRY(cudaMalloc(tabs[k], (size_t)G * sizeof(void *)));
+      SACD_CUDA_TRY(cudaMemcpy(*tabs[k], v.data(), (size_t)G * sizeof(void *), cudaMemcpyHostToDevice));
+    }
   }
   SACD_CUDA_TRY(cudaStreamSynchronize(s));
   return SACD_OK;

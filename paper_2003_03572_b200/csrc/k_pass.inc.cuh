@@ -287,6 +287,28 @@ __global__ void k_copy_rows_tt(long long rlo, long long rhi, const Real *__restr
 }
 
 // The owner adds the head partials of the other ranks to its rows, in rank order.
+// Peer-memory exchange of the small per-rank slots (exchange = p2p): this rank's head
+// partial (row id + row) into slot `me` of EVERY rank's exchange arrays (its own included),
+// and its stats slot [ti, md, E, Ech, Gram] into every other rank's stats array.  A flag
+// barrier (k_p2p_signal / k_p2p_wait) follows before anyone reads them, so a sweep needs no
+// NCCL at all.
+template <typename Real, int RT>
+__global__ void k_pack_head_p2p(long long head, const Real *__restrict__ M, long long *const *__restrict__ ids,
+                                Real *const *__restrict__ rows, int G, int me) {
+  for (int p = 0; p < G; ++p) {
+    for (int c = threadIdx.x; c < RT; c += blockDim.x) rows[p][(long long)me * RT + c] = head >= 0 ? M[head * RT + c] : Real(0);
+    if (threadIdx.x == 0) ids[p][me] = head;
+  }
+}
+
+__global__ void k_push_slot(const double *__restrict__ src, double *const *__restrict__ dst, long long count,
+                            long long off, int G, int me) {
+  for (int p = 0; p < G; ++p)
+    if (p != me)
+      for (long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x; x < count; x += (long long)gridDim.x * blockDim.x)
+        dst[p][off + x] = src[x];
+}
+
 template <typename Real, int RT>
 __global__ void k_merge_heads(int G, long long rlo, long long rhi, const long long *__restrict__ ids,
                               const Real *__restrict__ rows, Real *__restrict__ M) {

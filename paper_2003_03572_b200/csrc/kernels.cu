@@ -399,6 +399,16 @@ struct Impl {
     }
   };
 
+  // flag barrier of the peer-memory exchange: every shard signals before any waits (emulated
+  // ranks share one stream; across processes each rank has one shard)
+  static void p2p_barrier(Context &c) {
+    for (Shard &sh : c.shards) k_p2p_signal<<<1, 32, 0, c.stream>>>(sh.d_peer_flags, c.G, sh.rank, sh.epoch);
+    for (Shard &sh : c.shards) k_p2p_wait<<<1, 32, 0, c.stream>>>(sh.flags, c.G, sh.rank, sh.epoch);
+  }
+
+  // the stats slots [ti, md, E, Ech, Gram] of the G ranks as this context reads them
+  static double *stats_array(Context &c) { return (c.p2p && c.G > 1) ? c.shards[0].xstats_r : c.xstats; }
+
   // Each rank computes the MTTKRP of its nonzero range; the head partials (rows whose
   // first nonzero is on a lower rank) are exchanged and added by the owners in rank order.
   static int sharded_mttkrp_merge(Context &c, int mode) {
@@ -407,6 +417,21 @@ struct Impl {
       SACD_TRY(mttkrp_on(c, mode, sh.items[mode], sh.n_items[mode], sh.splits[mode], sh.n_splits[mode],
                          sh.chunks[mode], sh.n_chunks[mode],
                          reinterpret_cast<Real *>(sh.M), reinterpret_cast<Real *>(sh.partial)));
+    }
+    if (c.p2p && c.G > 1) {
+      // peer memory: every rank stores its head partial into slot `rank` of every rank's
+      // arrays, then a flag barrier; each rank merges from its own arrays
+      for (Shard &sh : c.shards)
+        k_pack_head_p2p<Real, RT><<<1, 256, 0, c.stream>>>(sh.plan[mode].head, reinterpret_cast<const Real *>(sh.M),
+                                                           sh.d_px, reinterpret_cast<Real *const *>(sh.d_pr), c.G,
+                                                           sh.rank);
+      p2p_barrier(c);
+      for (Shard &sh : c.shards)
+        k_merge_heads<Real, RT><<<1, 256, 0, c.stream>>>(c.G, sh.plan[mode].rlo, sh.plan[mode].rhi, sh.xid_r,
+                                                         reinterpret_cast<const Real *>(sh.xrow_r),
+                                                         reinterpret_cast<Real *>(sh.M));
+      SACD_CUDA_TRY(cudaGetLastError());
+      return SACD_OK;
     }
     Real *xrow = reinterpret_cast<Real *>(c.xrow);
     for (Shard &sh : c.shards)
@@ -453,7 +478,7 @@ struct Impl {
       SACD_CUDA_TRY(cudaGetLastError());
       SACD_TRY(prof_end(c, 3, pe));
       pe = prof_begin(c, 4);
-      double *sl = c.xstats + sh.rank * slot;
+      double *sl = ((c.p2p && c.G > 1) ? sh.xstats_r : c.xstats) + sh.rank * slot;
       if (gn == 0) {
         gn = gram_ranges(c, rlo, rhi);
         gram_partial(c, rlo, rhi, reinterpret_cast<const Real *>(md.F), sh.gram_part);
@@ -464,21 +489,23 @@ struct Impl {
       k_finalize<<<1, 1024, 0, c.stream>>>(mode, nblk, ti_part, md_part, e_part, ech_part, nullptr, nullptr,
                                            nullptr, c.R, c.st, 8, sl);
       SACD_CUDA_TRY(cudaGetLastError());
+      if (c.p2p && c.G > 1)  // this shard's stats slot into the other ranks' arrays
+        k_push_slot<<<4, 256, 0, c.stream>>>(sl, sh.d_ps, slot, sh.rank * slot, c.G, sh.rank);
       if (c.p2p && !fused_push && rhi > rlo && c.G > 1)  // this shard's changed chunks into the peers' replicas
         k_p2p_push<Real><<<4 * c.num_sms, 256, 0, c.stream>>>(
             rlo * RT, rhi * RT, reinterpret_cast<const Real *>(md.F), reinterpret_cast<const Real *>(c.Fold),
             reinterpret_cast<Real *const *>(sh.d_peerF[mode]), c.G, sh.rank);
       SACD_CUDA_TRY(cudaGetLastError());
     }
-    if (c.p2p && c.G > 1) {  // every shard signals before any waits (emulated ranks share a stream)
-      for (Shard &sh : c.shards) k_p2p_signal<<<1, 32, 0, c.stream>>>(sh.d_peer_flags, c.G, sh.rank, sh.epoch);
-      for (Shard &sh : c.shards) k_p2p_wait<<<1, 32, 0, c.stream>>>(sh.flags, c.G, sh.rank, sh.epoch);
+    if (c.p2p && c.G > 1) {  // rows and stats pushed: one flag barrier
+      p2p_barrier(c);
       SACD_CUDA_TRY(cudaGetLastError());
+    } else if (c.comm) {
+      SACD_TRY(nccl_allgather_inplace(c, c.xstats, (size_t)slot, 0));
     }
-    if (c.comm) SACD_TRY(nccl_allgather_inplace(c, c.xstats, (size_t)slot, 0));
     int pe = prof_begin(c, 5);
-    k_finalize_global<<<1, 1024, 0, c.stream>>>(mode, c.G, c.R, c.xstats, md.G, c.m[0].G, c.m[1].G, c.m[2].G, c.st,
-                                                32 | 1 | (end_sweep ? 6 : 0));
+    k_finalize_global<<<1, 1024, 0, c.stream>>>(mode, c.G, c.R, stats_array(c), md.G, c.m[0].G, c.m[1].G, c.m[2].G,
+                                                c.st, 32 | 1 | (end_sweep ? 6 : 0));
     SACD_CUDA_TRY(cudaGetLastError());
     SACD_TRY(prof_end(c, 5, pe));
     if (c.p2p) {
@@ -595,13 +622,16 @@ struct Impl {
                                                                 reinterpret_cast<const Real *>(md.F),
                                                                 reinterpret_cast<const Real *>(sh.M), ti_part,
                                                                 md_part, e_part, ech_part);
+      double *sl = ((c.p2p && c.G > 1) ? sh.xstats_r : c.xstats) + sh.rank * slot;
       k_finalize<<<1, 1024, 0, c.stream>>>(2, nblk, ti_part, md_part, e_part, ech_part, nullptr, nullptr, nullptr,
-                                           c.R, c.st, 8, c.xstats + sh.rank * slot);
+                                           c.R, c.st, 8, sl);
+      if (c.p2p && c.G > 1) k_push_slot<<<4, 256, 0, c.stream>>>(sl, sh.d_ps, slot, sh.rank * slot, c.G, sh.rank);
     }
     SACD_CUDA_TRY(cudaGetLastError());
-    if (c.comm) SACD_TRY(nccl_allgather_inplace(c, c.xstats, (size_t)slot, 0));
-    k_finalize_global<<<1, 1024, 0, c.stream>>>(2, c.G, c.R, c.xstats, nullptr, c.m[0].G, c.m[1].G, c.m[2].G, c.st,
-                                                2);
+    if (c.p2p && c.G > 1) p2p_barrier(c);
+    else if (c.comm) SACD_TRY(nccl_allgather_inplace(c, c.xstats, (size_t)slot, 0));
+    k_finalize_global<<<1, 1024, 0, c.stream>>>(2, c.G, c.R, stats_array(c), nullptr, c.m[0].G, c.m[1].G, c.m[2].G,
+                                                c.st, 2);
     SACD_CUDA_TRY(cudaGetLastError());
     return SACD_OK;
   }

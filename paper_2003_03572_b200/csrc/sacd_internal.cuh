@@ -166,6 +166,14 @@ struct Shard {
   unsigned long long **d_peer_flags = nullptr;
   unsigned long long *epoch = nullptr;
   bool own_rep = false;                     // Frep allocated by this shard (emulation, q > 0)
+  // this rank's exchange arrays (G slots each: head ids, head rows, stats) and device tables
+  // of every rank's arrays (p2p; shard 0 / a process's own shard uses the context's arrays)
+  long long *xid_r = nullptr;
+  void *xrow_r = nullptr;
+  double *xstats_r = nullptr;
+  long long **d_px = nullptr;
+  void **d_pr = nullptr;
+  double **d_ps = nullptr;
   std::vector<void *> ipc_opened;
 };
 
