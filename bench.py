@@ -563,8 +563,9 @@ def main():
                            "parallelism": (f"slice-sharded x{world} (factor exchange: "
                                            + {"delta": "NCCL lists of changed elements, rows when smaller)",
                                               "full": "NCCL all-gather-v of owned rows)",
-                                              "p2p": "changed 16-byte chunks stored into peer replicas over "
-                                                     "NVLink by a kernel; NCCL for the small stats)"}[args.exchange])
+                                              "p2p": "changed 16-byte chunks, head partials and stats stored "
+                                                     "into the peers' memory over NVLink by kernels, device flags; "
+                                                     "no NCCL per sweep)"}[args.exchange])
                            if world > 1 else "single GPU",
                            **({"exchange_elems_sent": info_end["delta_elems_sent"],
                                "exchange_elems_full_equiv": info_end["full_elems_equiv"]}

@@ -105,8 +105,9 @@ typedef struct {
                               /* because the list lengths are read on the host; 2 = peer      */
                               /* memory: a kernel stores every changed 16-byte chunk of the   */
                               /* owned rows straight into the peers' replicas (CUDA IPC over  */
-                              /* NVLink), device-side flags order the passes: no host round   */
-                              /* trip, graph-captured)                                        */
+                              /* NVLink), the head partials and stats slots likewise, and     */
+                              /* device-side flags order the passes: no NCCL call and no host */
+                              /* round trip per sweep, graph-captured)                        */
 } sacd_options;
 
 /* Per-sweep statistics (device-side ring, read by sacd_stats). */
