@@ -233,18 +233,52 @@ __global__ void __launch_bounds__(rows_per_block<RT>())
   }
 }
 
-// Fused row update with the out-of-block gradient on the fp64 tensor cores (Real = double,
-// RT <= 64).  Same semantics and per-row order of operations as k_sacd_rows: for column block
-// [c0, c0+8) the out-of-block part acc_q = sum_{j not in block} u_j h_(j,c0+q) of every row
-// of a warp (32 rows) is one (32 x RT) x (RT x 8) product of the CURRENT rows (columns < c0
-// already updated this pass, Gauss-Seidel C9) with H, issued as DMMA m8n8k4 (4 row tiles x
-// the k-steps outside the block, in ascending k); the in-block Gauss-Seidel step then runs
-// one thread per row exactly as in k_sacd_rows.  Fragments: A[m][k] = u[8mt+m][4kk+k] held
-// by lane (g = lane >> 2, t = lane & 3) as Us[8mt+g][4kk+t]; B[k][n] = H[4kk+k][c0+n] as
-// H[4kk+t][c0+g] (from L1: H is read-only and shared by every block); C[g][2t + {0,1}].
-// The accumulator tile and the block's M tile are transposed to one-row-per-thread through
-// a per-warp shared tile.  Shared memory: Us (rows x (RT+2), conflict-free for both the
-// fragment reads and the 16-byte row walks) + 32 x 18 doubles per warp.
+// Fused row update with the gradient on the fp64 tensor cores (Real = double, RT <= 64).
+// Same semantics and per-row order of the column steps as k_sacd_rows (Gauss-Seidel C9).
+// For column block [c0, c0+8) the out-of-block part acc_q = sum_{j not in block} u_j h_(j,c0+q)
+// of every row of a warp (32 rows) is one (32 x RT) x (RT x 8) product of the CURRENT rows
+// (columns < c0 already updated this pass) with H, issued as DMMA m8n8k4 (4 row tiles x the
+// k-steps outside the block, in ascending k).  The in-block Gauss-Seidel step then runs one
+// thread per row: the in-block terms of the columns not yet visited are added up front, the
+// term of column q' with its final value right after column q' is decided, so g of column q
+// (Eq 14) sees every earlier update and the dependent chain per column is one FMA deep.
+// g / h is the correctly rounded quotient: q0 = g * (1/h), r = fma(-q0, h, g) (exact),
+// q = fma(r, 1/h, q0) with 1/h correctly rounded (Markstein's theorem; 1/h once per CTA).
+// Fragments: A[m][k] = u[8mt+m][4kk+k] held by lane (g = lane >> 2, t = lane & 3) as
+// Us[8mt+g][4kk+t]; B[k][n] = H[4kk+k][c0+n] as H[4kk+t][c0+g] (from L1: H is read-only and
+// shared by every block); C[g][2t + {0,1}].  The accumulator tile and the block's M tile are
+// transposed to one-row-per-thread through a per-warp shared tile.  Shared memory: Us (rows x
+// (RT+4): the row pitch is 4 mod 16 doubles, so the fragment reads of a half-warp (4 rows x 4
+// columns) and the Gram panel reads hit 16 distinct bank pairs, and 16-byte chunks stay
+// aligned) + 32 x 18 doubles per warp + the 8 x 8 diagonal blocks of H and 1 / h_rr (loaded
+// once per CTA by rows_mma_prologue).
+template <int RT>
+__host__ __device__ constexpr int rows_mma_us() {
+  return RT + 4;
+}
+template <int RT, int WPB>
+__device__ __forceinline__ double *rows_mma_hd(unsigned char *smem_raw) {
+  return reinterpret_cast<double *>(smem_raw) + WPB * 32 * rows_mma_us<RT>() + WPB * 32 * 18;
+}
+// H's diagonal 8 x 8 blocks ([RT/8][8][8]) and the reciprocals 1 / h_rr (0 where h_rr = 0)
+// into shared memory; H is fixed for the whole pass.  Ends with __syncthreads.
+template <int RT, int WPB>
+__device__ __forceinline__ void rows_mma_prologue(const double *__restrict__ H) {
+  constexpr int C = 8;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double *Hd = rows_mma_hd<RT, WPB>(smem_raw);
+  double *Ri = Hd + RT * C;
+  for (int x = threadIdx.x; x < RT * C; x += WPB * 32) {
+    const int b = x / (C * C), q = (x / C) % C, qq = x % C;
+    Hd[x] = H[(b * C + q) * RT + b * C + qq];
+  }
+  for (int r = threadIdx.x; r < RT; r += WPB * 32) {
+    const double h = H[r * RT + r];
+    Ri[r] = h != 0.0 ? 1.0 / h : 0.0;
+  }
+  __syncthreads();
+}
+
 template <int RT, int WPB>
 __device__ __forceinline__ void rows_mma_block(long long rb, long long row_begin, long long row_end, int R, int mode,
                     int l_mode,
@@ -254,13 +288,14 @@ __device__ __forceinline__ void rows_mma_block(long long rb, long long row_begin
                     long long *__restrict__ e_part, long long *__restrict__ ech_part,
                     double *const *__restrict__ peers = nullptr, int G = 0, int me = 0) {
   constexpr int TR = WPB * 32;
-  constexpr int US = RT + 2;
+  constexpr int US = rows_mma_us<RT>();
   constexpr int C = 8;
   constexpr int TS = 2 * C + 2;
   constexpr int NKS = RT / 4;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double *Us = reinterpret_cast<double *>(smem_raw);
-  double *Hd = Us + TR * US + WPB * 32 * TS;  // the 8 x 8 diagonal blocks of H: [RT/8][8][8]
+  const double *Hd = rows_mma_hd<RT, WPB>(smem_raw);  // [RT/8][8][8], then 1 / h_rr [RT]
+  const double *Ri = Hd + RT * C;
   __shared__ double red_d[2][WPB];
   __shared__ long long red_l[2][WPB];
 
@@ -271,28 +306,19 @@ __device__ __forceinline__ void rows_mma_block(long long rb, long long row_begin
   const long long row0 = row_begin + rb * TR;
   const int nrows = (int)min((long long)TR, row_end - row0);
   const double *Fg = F + row0 * RT;
-  static_assert(((RT + 2) * 8) % 16 == 0, "row stride must keep 16-byte chunks aligned");
+  static_assert((US * 8) % 16 == 0, "row stride must keep 16-byte chunks aligned");
+  const bool active = tid < nrows;
+  const long long row = row0 + tid;
+  // issued before the staging wait: the empty-slice test (m = 0) needs only row_ptr
+  const bool empty = active ? __ldg(row_ptr + row) == __ldg(row_ptr + row + 1) : true;
   for (int x = tid; x < TR * RT / 2; x += TR) {  // 16-byte chunks
     const int r = (2 * x) / RT, col = (2 * x) % RT;
     if (r < nrows) cp_async<16>(Us + r * US + col, Fg + 2 * x);
     else *reinterpret_cast<double2 *>(Us + r * US + col) = make_double2(0.0, 0.0);
   }
-  cp_async_wait_all();
-  for (int x = tid; x < RT * C; x += TR) {
-    const int b = x / (C * C), q = (x / C) % C, qq = x % C;
-    Hd[x] = H[(b * C + q) * RT + b * C + qq];
-  }
-  __syncthreads();
   const int branch = st->branch[mode];
   const double Lf = st->Lfrob[mode];
   const int kmax = (R + 3) / 4;  // k-steps past R multiply zero padding
-
-  double ti = 0.0, md = 0.0;
-  long long E = 0, Ech = 0;
-  const bool active = tid < nrows;
-  const long long row = row0 + tid;
-  double *u = Us + tid * US;
-  const bool empty = active ? row_ptr[row] == row_ptr[row + 1] : true;  // empty slice: m = 0
   double *zp = Z + tt<RT>(active ? row : row0, 0);
   const double *Uw = Us + (wp * 32 + g) * US + t;
 
@@ -300,10 +326,9 @@ __device__ __forceinline__ void rows_mma_block(long long rb, long long row_begin
   // z_prev of block c0 + 8 are loaded while block c0 is processed (all read-only here)
   double bf[NKS], mt[C], zv[C];
   auto load_block = [&](int c, double (&b)[NKS], double (&mm)[C], double (&zz)[C]) {
-    const int kb = c / 4;
 #pragma unroll
     for (int kk = 0; kk < NKS; ++kk)
-      b[kk] = (kk == kb || kk == kb + 1 || kk >= kmax) ? 0.0 : __ldg(H + (4 * kk + t) * RT + c + g);
+      b[kk] = (kk == c / 4 || kk == c / 4 + 1 || kk >= kmax) ? 0.0 : __ldg(H + (4 * kk + t) * RT + c + g);
 #pragma unroll
     for (int k = 0; k < C; ++k) {
       const int x = lane + 32 * k, rl = x / C, cl = x % C;
@@ -314,12 +339,17 @@ __device__ __forceinline__ void rows_mma_block(long long rb, long long row_begin
     for (int q = 0; q < C; ++q) zz[q] = (active && c + q < RT) ? zp[32 * (c + q)] : 0.0;
   };
   load_block(0, bf, mt, zv);
+  cp_async_wait_all();
+  __syncthreads();
+
+  double ti = 0.0, md = 0.0;
+  long long E = 0, Ech = 0;
+  double *u = Us + tid * US;
   for (int c0 = 0; c0 < R; c0 += C) {
     double bfn[NKS], mtn[C], zvn[C];
     if (c0 + C < R) load_block(c0 + C, bfn, mtn, zvn);
-    // (1) out-of-block gradient of the warp's 32 rows on the tensor cores: all k-steps
-    //     unrolled, the block's own k-steps (and those past R) with a zero B fragment (adding
-    //     0 * a leaves an accumulator unchanged); even / odd k-steps in two sets of tiles
+    // (1) gradient base of the warp's 32 rows on the tensor cores: the k-steps past R with a
+    //     zero B fragment; even / odd k-steps in two sets of tiles
     double cacc[2][4][2];
 #pragma unroll
     for (int h = 0; h < 2; ++h)
@@ -356,38 +386,54 @@ __device__ __forceinline__ void rows_mma_block(long long rb, long long row_begin
         ub[q] = u[c0 + q];
       }
       const double *Hb = Hd + (c0 / C) * C * C;
-      // (3) in-block Gauss-Seidel (C9), as k_sacd_rows
+      unsigned selbits = 0;
+      // (3) in-block Gauss-Seidel (C9).  acc_q starts as the out-of-block sum; the in-block
+      //     terms of the columns not yet visited (q' >= q: their values at block start) are
+      //     added now, independently per column, and the term of column q' < q is added with
+      //     its final value as soon as column q' is decided, so every term enters once with
+      //     the value the sequential sweep sees, an all-zero row sums to exactly 0, and the
+      //     dependent chain per column is one FMA deep
+#pragma unroll
+      for (int q = 0; q < C; ++q)
+#pragma unroll
+        for (int qq = q; qq < C; ++qq) acc[q] = fma(ub[qq], Hb[q * C + qq], acc[q]);
 #pragma unroll
       for (int q = 0; q < C; ++q) {
         const int r = c0 + q;
         if (r < R) {
           const double h = Hb[q * C + q];
           double z = 0.0;
-          bool sel = false;
           if (h != 0.0) {
-            double sg = acc[q];
-#pragma unroll
-            for (int qq = 0; qq < C; ++qq) sg = fma(ub[qq], Hb[q * C + qq], sg);
-            const double gr = sg - mv[q];                  // Eq 14
+            const double ri = Ri[r];
+            const double gr = acc[q] - mv[q];              // Eq 14
             const double ur = ub[q];
-            const double un = fmax(0.0, ur - gr / h);      // Eq 11-13
+            const double q0 = gr * ri;                     // gr / h, correctly rounded
+            const double qr = fma(-q0, h, gr);
+            const double un = fmax(0.0, ur - fma(qr, ri, q0));  // Eq 11-13
             const double d = un - ur;                      // Eq 12
             const double L = l_mode ? Lf : h;
             z = -gr * d - (L * 0.5) * d * d;               // Eq 20
             const double zpr = zv[q];
-            sel = (branch == SACD_BR_FIRST) ? (z > 0.0)
-                                            : ((branch == SACD_BR_EQ24) ? (z - zpr > 0.0) : (zpr - z > 0.0));
+            const bool sel = (branch == SACD_BR_FIRST) ? (z > 0.0)
+                                                       : ((branch == SACD_BR_EQ24) ? (z - zpr > 0.0) : (zpr - z > 0.0));
             if (sel) {
               ub[q] = un;
               E += 1;
               if (d != 0.0) Ech += 1;
+              selbits |= 1u << q;
             }
           }
+#pragma unroll
+          for (int q2 = q + 1; q2 < C; ++q2) acc[q2] = fma(ub[q], Hb[q * C + q2], acc[q2]);
           zv[q] = z;                                       // z_prev <- z always (C8)
           ti += z;                                         // Eq 25
           md += ub[q] * mv[q];
-          if (dec) dec[row * R + r] = (uint8_t)sel;
         }
+      }
+      if (dec) {
+#pragma unroll
+        for (int q = 0; q < C; ++q)
+          if (c0 + q < R) dec[row * R + c0 + q] = (uint8_t)((selbits >> q) & 1u);
       }
 #pragma unroll
       for (int q = 0; q < C; ++q) u[c0 + q] = ub[q];
@@ -422,7 +468,10 @@ __device__ __forceinline__ void rows_mma_block(long long rb, long long row_begin
       reinterpret_cast<double2 *>(Fo)[x] = nv;
     }
   } else {
-    for (int x = tid; x < nrows * RT; x += TR) Fo[x] = Us[(x / RT) * US + (x % RT)];
+    for (int x = tid; x < nrows * RT / 2; x += TR) {
+      const int r = (2 * x) / RT, col = (2 * x) % RT;
+      reinterpret_cast<double2 *>(Fo)[x] = *reinterpret_cast<const double2 *>(Us + r * US + col);
+    }
   }
 
   // fixed-order block reduction of (ti, md, E, Ech)
@@ -464,6 +513,7 @@ __global__ void __launch_bounds__(WPB * 32)
                     double *__restrict__ Z, const double *__restrict__ H, const DevState *__restrict__ st,
                     uint8_t *__restrict__ dec, double *__restrict__ ti_part, double *__restrict__ md_part,
                     long long *__restrict__ e_part, long long *__restrict__ ech_part) {
+  rows_mma_prologue<RT, WPB>(H);
   rows_mma_block<RT, WPB>(blockIdx.x, row_begin, row_end, R, mode, l_mode, row_ptr, M, F, Z, H, st, dec, ti_part,
                           md_part, e_part, ech_part);
 }
@@ -480,6 +530,7 @@ __global__ void __launch_bounds__(WPB * 32)
                         long long *__restrict__ e_part, long long *__restrict__ ech_part, long long nblk,
                         unsigned long long *__restrict__ counter) {
   __shared__ long long rb_s;
+  rows_mma_prologue<RT, WPB>(H);
   for (;;) {
     __syncthreads();  // the previous block's tail (thread 0's partial writes) is done with rb_s
     if (threadIdx.x == 0) rb_s = (long long)atomicAdd(counter, 1ull);
@@ -604,10 +655,11 @@ __global__ void __launch_bounds__(WPB * 32)
                          double *__restrict__ gram_part, double *const *__restrict__ peers = nullptr, int G = 0,
                          int me = 0) {
   constexpr int TR = WPB * 32;
-  constexpr int US = RT + 2;
+  constexpr int US = rows_mma_us<RT>();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const double *Us = reinterpret_cast<const double *>(smem_raw);
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  rows_mma_prologue<RT, WPB>(H);
   GramAcc<RT, WPB> acc;
   acc.zero();
   const long long b0 = nblk * blockIdx.x / gridDim.x, b1 = nblk * (blockIdx.x + 1) / gridDim.x;
@@ -789,7 +841,7 @@ __host__ __device__ constexpr size_t rows_mma_big_smem_bytes() {
 
 template <int RT, int WPB>
 __host__ __device__ constexpr size_t rows_mma_smem_bytes() {
-  return (size_t)WPB * 32 * (RT + 2) * 8 + (size_t)WPB * 32 * 18 * 8 + (size_t)RT * 8 * 8;
+  return (size_t)WPB * 32 * rows_mma_us<RT>() * 8 + (size_t)WPB * 32 * 18 * 8 + (size_t)RT * 8 * 8 + (size_t)RT * 8;
 }
 
 // sum_r F_ir M_ir per row block (initial objective f^0)
