@@ -97,8 +97,10 @@ typedef struct {
                               /* 6 = the R <= 64 DMMA kernel on a static grid);               */
                               /* [1]: MTTKRP a-blocked order: > 0 = blocks of that many      */
                               /* a-rows, <= 0 = canonical order (default);                  */
-                              /* [2]: Gram kernel (0 = default: fp64 tensor cores (DMMA) for  */
-                              /* the fp64 build with pitch >= 32, 1 = the FMA kernel);        */
+                              /* [2]: Gram kernel (0 = default: fp64 tensor cores (DMMA): for */
+                              /* pitch <= 64 a streaming kernel after the row update, for     */
+                              /* pitch >= 128 panel pairs; 1 = the FMA kernel; 2 = fused into */
+                              /* the R <= 64 row update; 3 = panel pairs also for pitch <= 64) */
                               /* [3]: sharded exchange (0 = full owned rows, graph-captured;   */
                               /* 1 = delta: only the changed elements as (index, value) lists, */
                               /* full rows when those are smaller; NCCL sweeps then run eagerly */

@@ -250,8 +250,8 @@ __global__ void __launch_bounds__(rows_per_block<RT>())
 // transposed to one-row-per-thread through a per-warp shared tile.  Shared memory: Us (rows x
 // (RT+4): the row pitch is 4 mod 16 doubles, so the fragment reads of a half-warp (4 rows x 4
 // columns) and the Gram panel reads hit 16 distinct bank pairs, and 16-byte chunks stay
-// aligned) + 32 x 18 doubles per warp + the 8 x 8 diagonal blocks of H and 1 / h_rr (loaded
-// once per CTA by rows_mma_prologue).
+// aligned) + 32 x 18 doubles per warp + the 8 x 8 diagonal blocks of H, 1 / h_rr, the branch
+// rule and ||H||_F (loaded once per CTA by rows_mma_prologue).
 template <int RT>
 __host__ __device__ constexpr int rows_mma_us() {
   return RT + 4;
@@ -263,7 +263,8 @@ __device__ __forceinline__ double *rows_mma_hd(unsigned char *smem_raw) {
 // H's diagonal 8 x 8 blocks ([RT/8][8][8]) and the reciprocals 1 / h_rr (0 where h_rr = 0)
 // into shared memory; H is fixed for the whole pass.  Ends with __syncthreads.
 template <int RT, int WPB>
-__device__ __forceinline__ void rows_mma_prologue(const double *__restrict__ H) {
+__device__ __forceinline__ void rows_mma_prologue(const double *__restrict__ H, const DevState *__restrict__ st,
+                                                  int mode, int l_mode) {
   constexpr int C = 8;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double *Hd = rows_mma_hd<RT, WPB>(smem_raw);
@@ -275,6 +276,11 @@ __device__ __forceinline__ void rows_mma_prologue(const double *__restrict__ H) 
   for (int r = threadIdx.x; r < RT; r += WPB * 32) {
     const double h = H[r * RT + r];
     Ri[r] = h != 0.0 ? 1.0 / h : 0.0;
+    Ri[RT + 2 + r] = (l_mode ? st->Lfrob[mode] : h) * 0.5;  // L / 2 of Eq 20 (exact halving)
+  }
+  if (threadIdx.x == 0) {  // the pass's branch rule and ||H||_F, also fixed for the launch
+    Ri[RT] = (double)st->branch[mode];
+    Ri[RT + 1] = st->Lfrob[mode];
   }
   __syncthreads();
 }
@@ -316,9 +322,9 @@ __device__ __forceinline__ void rows_mma_block(long long rb, long long row_begin
     if (r < nrows) cp_async<16>(Us + r * US + col, Fg + 2 * x);
     else *reinterpret_cast<double2 *>(Us + r * US + col) = make_double2(0.0, 0.0);
   }
-  const int branch = st->branch[mode];
-  const double Lf = st->Lfrob[mode];
-  const int kmax = (R + 3) / 4;  // k-steps past R multiply zero padding
+  const int branch = (int)Ri[RT];
+  const bool first = branch == SACD_BR_FIRST, eq27 = branch == SACD_BR_EQ27;
+  const double *Lh = Ri + RT + 2;
   double *zp = Z + tt<RT>(active ? row : row0, 0);
   const double *Uw = Us + (wp * 32 + g) * US + t;
 
@@ -326,17 +332,19 @@ __device__ __forceinline__ void rows_mma_block(long long rb, long long row_begin
   // z_prev of block c0 + 8 are loaded while block c0 is processed (all read-only here)
   double bf[NKS], mt[C], zv[C];
   auto load_block = [&](int c, double (&b)[NKS], double (&mm)[C], double (&zz)[C]) {
+    // unconditional loads (no select right behind them, so they stay in flight for a whole
+    // block): H's padding rows are zero, rows past the range read the last row and
+    // inactive threads read row0's z_prev (neither is used)
 #pragma unroll
-    for (int kk = 0; kk < NKS; ++kk)
-      b[kk] = (kk == c / 4 || kk == c / 4 + 1 || kk >= kmax) ? 0.0 : __ldg(H + (4 * kk + t) * RT + c + g);
+    for (int kk = 0; kk < NKS; ++kk) b[kk] = ld_keep_f64(H + (4 * kk + t) * RT + c + g);
 #pragma unroll
     for (int k = 0; k < C; ++k) {
       const int x = lane + 32 * k, rl = x / C, cl = x % C;
-      const long long rg = row0 + wp * 32 + rl;
-      mm[k] = (rg < row_end) ? __ldg(M + rg * RT + c + cl) : 0.0;
+      const long long rg = min(row0 + wp * 32 + rl, row_end - 1);
+      mm[k] = ld_stream_f64(M + rg * RT + c + cl);
     }
 #pragma unroll
-    for (int q = 0; q < C; ++q) zz[q] = (active && c + q < RT) ? zp[32 * (c + q)] : 0.0;
+    for (int q = 0; q < C; ++q) zz[q] = ld_na_f64(zp + 32 * (c + q));
   };
   load_block(0, bf, mt, zv);
   cp_async_wait_all();
@@ -348,15 +356,18 @@ __device__ __forceinline__ void rows_mma_block(long long rb, long long row_begin
   for (int c0 = 0; c0 < R; c0 += C) {
     double bfn[NKS], mtn[C], zvn[C];
     if (c0 + C < R) load_block(c0 + C, bfn, mtn, zvn);
-    // (1) gradient base of the warp's 32 rows on the tensor cores: the k-steps past R with a
-    //     zero B fragment; even / odd k-steps in two sets of tiles
+    // (1) out-of-block part of the warp's 32 rows on the tensor cores: the block's own two
+    //     k-steps are skipped (a uniform branch), the k-steps past R multiply zero padding
+    //     (A and H); even / odd k-steps in two sets of tiles
     double cacc[2][4][2];
 #pragma unroll
     for (int h = 0; h < 2; ++h)
 #pragma unroll
       for (int m = 0; m < 4; ++m) cacc[h][m][0] = cacc[h][m][1] = 0.0;
+    const int kb = c0 / 4;
 #pragma unroll
     for (int kk = 0; kk < NKS; ++kk) {
+      if (kk == kb || kk == kb + 1) continue;
 #pragma unroll
       for (int m = 0; m < 4; ++m) {
         const double a = Uw[8 * m * US + 4 * kk];
@@ -383,7 +394,12 @@ __device__ __forceinline__ void rows_mma_block(long long rb, long long row_begin
       for (int q = 0; q < C; ++q) {
         acc[q] = Tw[lane * TS + q];
         mv[q] = empty ? 0.0 : Tw[lane * TS + C + q];
-        ub[q] = u[c0 + q];
+      }
+#pragma unroll
+      for (int q = 0; q < C; q += 2) {
+        const double2 v = *reinterpret_cast<const double2 *>(u + c0 + q);
+        ub[q] = v.x;
+        ub[q + 1] = v.y;
       }
       const double *Hb = Hd + (c0 / C) * C * C;
       unsigned selbits = 0;
@@ -397,38 +413,38 @@ __device__ __forceinline__ void rows_mma_block(long long rb, long long row_begin
       for (int q = 0; q < C; ++q)
 #pragma unroll
         for (int qq = q; qq < C; ++qq) acc[q] = fma(ub[qq], Hb[q * C + qq], acc[q]);
+      // padding columns (r >= R) have h = 0 (H is zero-padded) and u = m = 0: they take the
+      // h = 0 path (z = 0, no selection) and add exact zeros, so no r < R test is needed
 #pragma unroll
       for (int q = 0; q < C; ++q) {
         const int r = c0 + q;
-        if (r < R) {
-          const double h = Hb[q * C + q];
-          double z = 0.0;
-          if (h != 0.0) {
-            const double ri = Ri[r];
-            const double gr = acc[q] - mv[q];              // Eq 14
-            const double ur = ub[q];
-            const double q0 = gr * ri;                     // gr / h, correctly rounded
-            const double qr = fma(-q0, h, gr);
-            const double un = fmax(0.0, ur - fma(qr, ri, q0));  // Eq 11-13
-            const double d = un - ur;                      // Eq 12
-            const double L = l_mode ? Lf : h;
-            z = -gr * d - (L * 0.5) * d * d;               // Eq 20
-            const double zpr = zv[q];
-            const bool sel = (branch == SACD_BR_FIRST) ? (z > 0.0)
-                                                       : ((branch == SACD_BR_EQ24) ? (z - zpr > 0.0) : (zpr - z > 0.0));
-            if (sel) {
-              ub[q] = un;
-              E += 1;
-              if (d != 0.0) Ech += 1;
-              selbits |= 1u << q;
-            }
+        const double h = Hb[q * C + q];
+        double z = 0.0;
+        if (h != 0.0) {
+          const double ri = Ri[r];
+          const double gr = acc[q] - mv[q];              // Eq 14
+          const double ur = ub[q];
+          const double q0 = gr * ri;                     // gr / h, correctly rounded
+          const double qr = fma(-q0, h, gr);
+          const double un = fmax(0.0, ur - fma(qr, ri, q0));  // Eq 11-13
+          const double d = un - ur;                      // Eq 12
+          z = -gr * d - Lh[r] * d * d;                   // Eq 20 (Lh = L / 2)
+          // FIRST: z > 0; EQ24: z - z_prev > 0; EQ27: z_prev - z > 0, i.e. z - z_prev < 0
+          // (IEEE subtraction is antisymmetric, and z - 0 = z)
+          const double dz = z - (first ? 0.0 : zv[q]);
+          const bool sel = eq27 ? (dz < 0.0) : (dz > 0.0);
+          if (sel) {
+            ub[q] = un;
+            E += 1;
+            if (d != 0.0) Ech += 1;
+            selbits |= 1u << q;
           }
-#pragma unroll
-          for (int q2 = q + 1; q2 < C; ++q2) acc[q2] = fma(ub[q], Hb[q * C + q2], acc[q2]);
-          zv[q] = z;                                       // z_prev <- z always (C8)
-          ti += z;                                         // Eq 25
-          md += ub[q] * mv[q];
         }
+#pragma unroll
+        for (int q2 = q + 1; q2 < C; ++q2) acc[q2] = fma(ub[q], Hb[q * C + q2], acc[q2]);
+        zv[q] = z;                                       // z_prev <- z always (C8)
+        ti += z;                                         // Eq 25
+        md += ub[q] * mv[q];
       }
       if (dec) {
 #pragma unroll
@@ -436,7 +452,7 @@ __device__ __forceinline__ void rows_mma_block(long long rb, long long row_begin
           if (c0 + q < R) dec[row * R + c0 + q] = (uint8_t)((selbits >> q) & 1u);
       }
 #pragma unroll
-      for (int q = 0; q < C; ++q) u[c0 + q] = ub[q];
+      for (int q = 0; q < C; q += 2) *reinterpret_cast<double2 *>(u + c0 + q) = make_double2(ub[q], ub[q + 1]);
 #pragma unroll
       for (int q = 0; q < C; ++q) zp[32 * (c0 + q)] = zv[q];
     }
@@ -513,7 +529,7 @@ __global__ void __launch_bounds__(WPB * 32)
                     double *__restrict__ Z, const double *__restrict__ H, const DevState *__restrict__ st,
                     uint8_t *__restrict__ dec, double *__restrict__ ti_part, double *__restrict__ md_part,
                     long long *__restrict__ e_part, long long *__restrict__ ech_part) {
-  rows_mma_prologue<RT, WPB>(H);
+  rows_mma_prologue<RT, WPB>(H, st, mode, l_mode);
   rows_mma_block<RT, WPB>(blockIdx.x, row_begin, row_end, R, mode, l_mode, row_ptr, M, F, Z, H, st, dec, ti_part,
                           md_part, e_part, ech_part);
 }
@@ -528,9 +544,10 @@ __global__ void __launch_bounds__(WPB * 32)
                         double *__restrict__ Z, const double *__restrict__ H, const DevState *__restrict__ st,
                         uint8_t *__restrict__ dec, double *__restrict__ ti_part, double *__restrict__ md_part,
                         long long *__restrict__ e_part, long long *__restrict__ ech_part, long long nblk,
-                        unsigned long long *__restrict__ counter) {
+                        unsigned long long *__restrict__ counter, double *const *__restrict__ peers = nullptr,
+                        int G = 0, int me = 0) {
   __shared__ long long rb_s;
-  rows_mma_prologue<RT, WPB>(H);
+  rows_mma_prologue<RT, WPB>(H, st, mode, l_mode);
   for (;;) {
     __syncthreads();  // the previous block's tail (thread 0's partial writes) is done with rb_s
     if (threadIdx.x == 0) rb_s = (long long)atomicAdd(counter, 1ull);
@@ -538,7 +555,7 @@ __global__ void __launch_bounds__(WPB * 32)
     const long long rb = rb_s;
     if (rb >= nblk) break;
     rows_mma_block<RT, WPB>(rb, row_begin, row_end, R, mode, l_mode, row_ptr, M, F, Z, H, st, dec, ti_part, md_part,
-                            e_part, ech_part);
+                            e_part, ech_part, peers, G, me);
   }
 }
 
@@ -641,6 +658,57 @@ struct GramAcc {
   }
 };
 
+// Gram partials G_b = sum of u u^T over rows [row_begin, row_end) of F (fp64, RT <= 64; Eq 10's
+// G_n = F_n^T F_n of the factor just updated), streamed through shared memory: CTA b takes
+// the 32-row chunks [b * nch / grid, (b + 1) * nch / grid) (a fixed assignment, so its
+// partial and the fixed-order k_gram_reduce are deterministic), stages them with cp.async
+// into an S-deep ring at the conflict-free row pitch of the row update, S - 1 chunks ahead,
+// and adds each chunk's u u^T on the fp64 tensor cores with GramAcc (36 upper 8 x 8 tiles
+// for R = 64, 9 per warp).  Rows past the range are zero-filled.  Partial b goes to
+// part[b] (upper entries r <= t, the k_gram_reduce contract).
+template <int RT, int S>
+__host__ __device__ constexpr size_t gram_stream_smem_bytes() {
+  return (size_t)S * 32 * rows_mma_us<RT>() * 8;
+}
+template <int RT, int S>
+__global__ void __launch_bounds__(128) k_gram_stream(long long row_begin, long long row_end, int R,
+                                                     const double *__restrict__ F, double *__restrict__ part) {
+  constexpr int US = rows_mma_us<RT>();
+  constexpr int CH = 32;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double *ring = reinterpret_cast<double *>(smem_raw);
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  const long long nch = (row_end - row_begin + CH - 1) / CH;
+  const long long c0 = nch * blockIdx.x / gridDim.x, c1 = nch * (blockIdx.x + 1) / gridDim.x;
+  auto stage = [&](long long ch) {
+    double *dst = ring + (int)((ch - c0) % S) * CH * US;
+    const long long r0 = row_begin + ch * CH;
+    const int nr = (int)min((long long)CH, row_end - r0);
+    const double *src = F + r0 * RT;
+    for (int x = threadIdx.x; x < CH * RT / 2; x += 128) {  // 16-byte chunks
+      const int r = (2 * x) / RT, col = (2 * x) % RT;
+      if (r < nr) cp_async<16>(dst + r * US + col, src + 2 * x);
+      else *reinterpret_cast<double2 *>(dst + r * US + col) = make_double2(0.0, 0.0);
+    }
+  };
+  GramAcc<RT, 4> acc;
+  acc.zero();
+#pragma unroll
+  for (int k = 0; k < S - 1; ++k) {
+    if (c0 + k < c1) stage(c0 + k);
+    cp_async_commit();
+  }
+  for (long long ch = c0; ch < c1; ++ch) {
+    if (ch + S - 1 < c1) stage(ch + S - 1);  // the slot of chunk ch - 1, released below
+    cp_async_commit();
+    cp_async_wait_group<S - 1>();  // this thread's copies of chunk ch are done
+    __syncthreads();               // ... and every thread's copies and zero fills
+    acc.add_block(ring + (int)((ch - c0) % S) * CH * US, US, CH, wp, lane);
+    __syncthreads();  // chunk ch's slot is restaged next iteration
+  }
+  acc.store(part + (long long)blockIdx.x * R * R, R, wp, lane);
+}
+
 // Row update with the fused Gram: CTA b takes the contiguous row blocks
 // [b * nblk / grid, (b + 1) * nblk / grid) in order (a fixed assignment, so the Gram partial of
 // each CTA, and the fixed-order reduce over CTAs, are deterministic), and writes its Gram
@@ -659,7 +727,7 @@ __global__ void __launch_bounds__(WPB * 32)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const double *Us = reinterpret_cast<const double *>(smem_raw);
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
-  rows_mma_prologue<RT, WPB>(H);
+  rows_mma_prologue<RT, WPB>(H, st, mode, l_mode);
   GramAcc<RT, WPB> acc;
   acc.zero();
   const long long b0 = nblk * blockIdx.x / gridDim.x, b1 = nblk * (blockIdx.x + 1) / gridDim.x;
@@ -841,7 +909,7 @@ __host__ __device__ constexpr size_t rows_mma_big_smem_bytes() {
 
 template <int RT, int WPB>
 __host__ __device__ constexpr size_t rows_mma_smem_bytes() {
-  return (size_t)WPB * 32 * rows_mma_us<RT>() * 8 + (size_t)WPB * 32 * 18 * 8 + (size_t)RT * 8 * 8 + (size_t)RT * 8;
+  return (size_t)WPB * 32 * rows_mma_us<RT>() * 8 + (size_t)WPB * 32 * 18 * 8 + (size_t)RT * 8 * 8 + (size_t)(2 * RT + 2) * 8;
 }
 
 // sum_r F_ir M_ir per row block (initial objective f^0)

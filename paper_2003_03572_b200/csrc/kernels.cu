@@ -74,6 +74,24 @@ __device__ __forceinline__ float ld_stream_f32(const float *p) {
   return v;
 }
 
+// Row-update loads (not volatile, so the compiler may batch them): M and z_prev stream through
+// once per pass and must not evict H, which every block of the pass re-reads from L1.
+__device__ __forceinline__ double ld_stream_f64(const double *p) {  // read-only in the kernel
+  double v;
+  asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double ld_na_f64(const double *p) {  // coherent, no L1 allocation
+  double v;
+  asm("ld.global.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double ld_keep_f64(const double *p) {  // read-only, kept in L1
+  double v;
+  asm("ld.global.nc.L1::evict_last.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+
 // Asynchronous global -> shared copies (LDGSTS): the row-block staging of the row-update
 // kernels keeps every load in flight at once instead of one register round trip per element.
 template <int BYTES>
@@ -85,6 +103,11 @@ __device__ __forceinline__ void cp_async(void *smem, const void *gmem) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(sa), "l"(gmem), "n"(BYTES));
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
 
 // Reading C12: rand(seed, tag, ctr) = mix64(mix64(seed ^ tag) + (ctr + 1) * golden)
 __device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
@@ -455,9 +478,9 @@ struct Impl {
     if (begin_sweep) k_sweep_begin<<<1, 32, 0, c.stream>>>(c.st);
     SACD_TRY(sharded_mttkrp_merge(c, mode));
     SACD_TRY(prepare(c, mode, branch_override, begin_sweep, 1));
-    // p2p: the fused row kernel (fp64, R <= 64) stores the changed chunks into the peers
-    // itself; the other row kernels are followed by k_p2p_push against a pass-start snapshot
-    const bool fused_push = c.p2p && c.G > 1 && gram_fused(c);
+    // p2p: the DMMA row kernels (fp64, R <= 64) store the changed chunks into the peers
+    // themselves; the other row kernels are followed by k_p2p_push against a pass-start snapshot
+    const bool fused_push = c.p2p && c.G > 1 && rows_push(c);
     if (c.delta || (c.p2p && !fused_push)) SACD_TRY(delta_snapshot(c, mode));
     const long long TR = rows_tr(c, 0);
     const long long slot = 4 + (long long)c.R * c.R;
@@ -480,8 +503,7 @@ struct Impl {
       pe = prof_begin(c, 4);
       double *sl = ((c.p2p && c.G > 1) ? sh.xstats_r : c.xstats) + sh.rank * slot;
       if (gn == 0) {
-        gn = gram_ranges(c, rlo, rhi);
-        gram_partial(c, rlo, rhi, reinterpret_cast<const Real *>(md.F), sh.gram_part);
+        gn = gram_partial(c, rlo, rhi, reinterpret_cast<const Real *>(md.F), sh.gram_part);
       }
       k_gram_reduce<<<gram_reduce_blocks(c.R), 256, 0, c.stream>>>(c.R, gn, sh.gram_part, sl + 4);
       SACD_CUDA_TRY(cudaGetLastError());
@@ -659,27 +681,46 @@ struct Impl {
     return (int)std::max<long long>(1, std::min<long long>(c.gram_blocks, (rhi - rlo + 63) / 64));
   }
 
-  static void gram_partial(Context &c, long long rlo, long long rhi, const Real *F, double *part) {
+  // Writes the partials of rows [rlo, rhi) of F to part[0 .. n) and returns n (the count
+  // k_gram_reduce sums).  fp64 R <= 64: k_gram_stream (cp.async ring + DMMA), one partial per
+  // resident CTA (at most gram_cap, at least 32 rows each); opt.reserved[2] = 3 keeps the
+  // panel-pair DMMA kernel, 1 the FMA kernel (A/B)
+  static int gram_partial(Context &c, long long rlo, long long rhi, const Real *F, double *part) {
     const int nb = gram_ranges(c, rlo, rhi);
+    if constexpr (kGramStream) {
+      if (c.opt.reserved[2] != 1 && c.opt.reserved[2] != 3) {
+        int per_sm = 0;
+        auto kern = k_gram_stream<RT, kGramStages>;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, gram_stream_smem_bytes<RT, kGramStages>());
+        const long long nch = std::max<long long>(1, (rhi - rlo + 31) / 32);
+        const int n = (int)std::min<long long>(std::min<long long>((long long)std::max(1, per_sm) * c.num_sms,
+                                                                   (long long)c.gram_cap),
+                                               nch);
+        kern<<<(unsigned)n, 128, gram_stream_smem_bytes<RT, kGramStages>(), c.stream>>>(
+            rlo, rhi, c.R, reinterpret_cast<const double *>(F), part);
+        return n;
+      }
+    }
     if constexpr (sizeof(Real) == 8 && RT >= 32) {
       if (c.opt.reserved[2] != 1) {
         constexpr int NP = RT / 32;
         k_gram_dmma<RT><<<dim3(nb, NP * (NP + 1) / 2), 128, 0, c.stream>>>(
             rlo, rhi, c.R, reinterpret_cast<const double *>(F), part);
-        return;
+        return nb;
       }
     }
     constexpr int GT = gram_gt<RT>();
     constexpr int TG = gram_tg<GT>();
     constexpr int NB = RT / GT;
     k_gram_partial<Real, RT><<<dim3(nb, NB * (NB + 1) / 2), TG * TG, 0, c.stream>>>(rlo, rhi, c.R, F, part);
+    return nb;
   }
 
   static int gram(Context &c, int mode) {
     ModeData &md = c.m[mode];
     int pe = prof_begin(c, 4);
-    gram_partial(c, 0, md.I, reinterpret_cast<const Real *>(md.F), c.gram_part);
-    k_gram_reduce<<<gram_reduce_blocks(c.R), 256, 0, c.stream>>>(c.R, gram_ranges(c, 0, md.I), c.gram_part, md.G);
+    const int nb = gram_partial(c, 0, md.I, reinterpret_cast<const Real *>(md.F), c.gram_part);
+    k_gram_reduce<<<gram_reduce_blocks(c.R), 256, 0, c.stream>>>(c.R, nb, c.gram_part, md.G);
     SACD_CUDA_TRY(cudaGetLastError());
     SACD_TRY(chunk_mask(c, mode));
     return prof_end(c, 4, pe);
@@ -792,10 +833,19 @@ struct Impl {
   static constexpr bool kRowsMma = sizeof(Real) == 8 && RT <= 64 && rows_per_block<RT>() == 128;
   static constexpr bool kRowsMmaBig = sizeof(Real) == 8 && RT >= 128;
   static constexpr int kMmaWarps = 4;  // 5 (160 rows, 2 blocks per SM) measured 2.41 vs 1.72 ms: L1 too small
-  // the Gram refresh runs inside the row update (k_sacd_rows_mma_gram) for the default fp64
-  // R <= 64 path; opt.reserved[2] = 2 keeps the separate Gram kernel (A/B, tools)
+  // the Gram of the updated factor: a separate streaming kernel (k_gram_stream) after the row
+  // update by default; opt.reserved[2] = 2 fuses it into the row update (k_sacd_rows_mma_gram,
+  // A/B: c4 rows + Gram 1.93 ms per sweep fused)
+  static constexpr bool kGramStream = sizeof(Real) == 8 && RT <= 64;
+  static constexpr int kGramStages = 4;
+  // the default fp64 R <= 64 row kernels (dynamic or with the fused Gram) push changed
+  // chunks to the peers in their write-back
+  static bool rows_push(const Context &c) {
+    if constexpr (kRowsMma) return c.opt.reserved[0] == 0;
+    return false;
+  }
   static bool gram_fused(const Context &c) {
-    if constexpr (kRowsMma) return c.opt.reserved[0] == 0 && c.opt.reserved[2] == 0;
+    if constexpr (kRowsMma) return c.opt.reserved[0] == 0 && c.opt.reserved[2] == 2;
     return false;
   }
   static int rows_tr(const Context &c, int vflags) {
@@ -858,7 +908,7 @@ struct Impl {
               rlo, rhi, c.R, mode, c.opt.l_mode, md.row_ptr, reinterpret_cast<const double *>(M),
               reinterpret_cast<double *>(md.F), reinterpret_cast<double *>(md.Z),
               reinterpret_cast<const double *>(c.Hr), c.st, dec, ti_part, md_part, e_part, ech_part, nblk,
-              c.item_ctr + 1);
+              c.item_ctr + 1, reinterpret_cast<double *const *>(c.rows_peers), c.G, c.rows_me);
         }
         SACD_CUDA_TRY(cudaGetLastError());
         return SACD_OK;
@@ -907,6 +957,10 @@ struct Impl {
       SACD_CUDA_TRY(cudaFuncSetAttribute(k_sacd_rows_mma_gram<RT, kMmaWarps>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)rows_mma_smem_bytes<RT, kMmaWarps>()));
+    }
+    if constexpr (kGramStream) {
+      SACD_CUDA_TRY(cudaFuncSetAttribute(k_gram_stream<RT, kGramStages>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)gram_stream_smem_bytes<RT, kGramStages>()));
     }
     if constexpr (kRowsMmaBig)
       SACD_CUDA_TRY(cudaFuncSetAttribute(k_sacd_rows_mma_big<RT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
