@@ -285,6 +285,25 @@ __device__ __forceinline__ void rows_mma_prologue(const double *__restrict__ H, 
   __syncthreads();
 }
 
+// Issue the staging of row block rb's factor rows into Us (cp.async, rows past the range
+// zero-filled); rows_mma_block waits for it.
+template <int RT, int WPB>
+__device__ __forceinline__ void rows_mma_stage(long long rb, long long row_begin, long long row_end,
+                                               const double *__restrict__ F) {
+  constexpr int TR = WPB * 32;
+  constexpr int US = rows_mma_us<RT>();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double *Us = reinterpret_cast<double *>(smem_raw);
+  const long long row0 = row_begin + rb * TR;
+  const int nrows = (int)min((long long)TR, row_end - row0);
+  const double *Fg = F + row0 * RT;
+  for (int x = threadIdx.x; x < TR * RT / 2; x += TR) {  // 16-byte chunks
+    const int r = (2 * x) / RT, col = (2 * x) % RT;
+    if (r < nrows) cp_async<16>(Us + r * US + col, Fg + 2 * x);
+    else *reinterpret_cast<double2 *>(Us + r * US + col) = make_double2(0.0, 0.0);
+  }
+}
+
 template <int RT, int WPB>
 __device__ __forceinline__ void rows_mma_block(long long rb, long long row_begin, long long row_end, int R, int mode,
                     int l_mode,
@@ -292,7 +311,8 @@ __device__ __forceinline__ void rows_mma_block(long long rb, long long row_begin
                     double *__restrict__ Z, const double *__restrict__ H, const DevState *__restrict__ st,
                     uint8_t *__restrict__ dec, double *__restrict__ ti_part, double *__restrict__ md_part,
                     long long *__restrict__ e_part, long long *__restrict__ ech_part,
-                    double *const *__restrict__ peers = nullptr, int G = 0, int me = 0) {
+                    double *const *__restrict__ peers = nullptr, int G = 0, int me = 0,
+                    const long long *next_rb = nullptr, long long nblk = 0) {
   constexpr int TR = WPB * 32;
   constexpr int US = rows_mma_us<RT>();
   constexpr int C = 8;
@@ -311,17 +331,12 @@ __device__ __forceinline__ void rows_mma_block(long long rb, long long row_begin
   double *Tw = Us + TR * US + wp * 32 * TS;
   const long long row0 = row_begin + rb * TR;
   const int nrows = (int)min((long long)TR, row_end - row0);
-  const double *Fg = F + row0 * RT;
   static_assert((US * 8) % 16 == 0, "row stride must keep 16-byte chunks aligned");
   const bool active = tid < nrows;
   const long long row = row0 + tid;
-  // issued before the staging wait: the empty-slice test (m = 0) needs only row_ptr
+  // the block's staging (rows_mma_stage) is in flight; the empty-slice test (m = 0) needs
+  // only row_ptr
   const bool empty = active ? __ldg(row_ptr + row) == __ldg(row_ptr + row + 1) : true;
-  for (int x = tid; x < TR * RT / 2; x += TR) {  // 16-byte chunks
-    const int r = (2 * x) / RT, col = (2 * x) % RT;
-    if (r < nrows) cp_async<16>(Us + r * US + col, Fg + 2 * x);
-    else *reinterpret_cast<double2 *>(Us + r * US + col) = make_double2(0.0, 0.0);
-  }
   const int branch = (int)Ri[RT];
   const bool first = branch == SACD_BR_FIRST, eq27 = branch == SACD_BR_EQ27;
   const double *Lh = Ri + RT + 2;
@@ -489,6 +504,12 @@ __device__ __forceinline__ void rows_mma_block(long long rb, long long row_begin
       reinterpret_cast<double2 *>(Fo)[x] = *reinterpret_cast<const double2 *>(Us + r * US + col);
     }
   }
+  if (next_rb) {  // Us is free once every thread has read it: stage the next block now, so
+                  // its loads overlap this block's reductions and the next block's start
+    __syncthreads();
+    const long long nb = *next_rb;
+    if (nb < nblk) rows_mma_stage<RT, WPB>(nb, row_begin, row_end, F);
+  }
 
   // fixed-order block reduction of (ti, md, E, Ech)
 #pragma unroll
@@ -529,6 +550,7 @@ __global__ void __launch_bounds__(WPB * 32)
                     double *__restrict__ Z, const double *__restrict__ H, const DevState *__restrict__ st,
                     uint8_t *__restrict__ dec, double *__restrict__ ti_part, double *__restrict__ md_part,
                     long long *__restrict__ e_part, long long *__restrict__ ech_part) {
+  rows_mma_stage<RT, WPB>(blockIdx.x, row_begin, row_end, F);
   rows_mma_prologue<RT, WPB>(H, st, mode, l_mode);
   rows_mma_block<RT, WPB>(blockIdx.x, row_begin, row_end, R, mode, l_mode, row_ptr, M, F, Z, H, st, dec, ti_part,
                           md_part, e_part, ech_part);
@@ -546,16 +568,20 @@ __global__ void __launch_bounds__(WPB * 32)
                         long long *__restrict__ e_part, long long *__restrict__ ech_part, long long nblk,
                         unsigned long long *__restrict__ counter, double *const *__restrict__ peers = nullptr,
                         int G = 0, int me = 0) {
-  __shared__ long long rb_s;
-  rows_mma_prologue<RT, WPB>(H, st, mode, l_mode);
-  for (;;) {
-    __syncthreads();  // the previous block's tail (thread 0's partial writes) is done with rb_s
-    if (threadIdx.x == 0) rb_s = (long long)atomicAdd(counter, 1ull);
-    __syncthreads();
-    const long long rb = rb_s;
-    if (rb >= nblk) break;
+  // the next block's index is taken at the start of the current one, and its staging is
+  // issued as soon as the current block's rows are written back (rows_mma_block)
+  __shared__ long long rb_s[2];
+  if (threadIdx.x == 0) rb_s[0] = (long long)atomicAdd(counter, 1ull);
+  rows_mma_prologue<RT, WPB>(H, st, mode, l_mode);  // ends with __syncthreads
+  long long rb = rb_s[0];
+  if (rb < nblk) rows_mma_stage<RT, WPB>(rb, row_begin, row_end, F);
+  for (int it = 1; rb < nblk; it ^= 1) {
+    // slot it was last read before the previous block's closing barrier
+    if (threadIdx.x == 0) rb_s[it] = (long long)atomicAdd(counter, 1ull);
     rows_mma_block<RT, WPB>(rb, row_begin, row_end, R, mode, l_mode, row_ptr, M, F, Z, H, st, dec, ti_part, md_part,
-                            e_part, ech_part, peers, G, me);
+                            e_part, ech_part, peers, G, me, rb_s + it, nblk);
+    __syncthreads();  // thread 0's partial writes and rb_s[it] reads are done
+    rb = rb_s[it];
   }
 }
 
@@ -628,6 +654,30 @@ struct GramAcc {
 #pragma unroll
       for (int j = 0; j < P; ++j) pf[j] = p0[r0 * US + 8 * j];
       mma_tiles<W, 0>(pf);
+    }
+  }
+  // a chunk of NR (compile-time) rows, fully unrolled so the panel loads of later k-steps
+  // are issued ahead of the DMMAs
+  template <int W, int NR, int US>
+  __device__ __forceinline__ void add_chunk_w(const double *Us, int lane) {
+    const int g = lane >> 2, t = lane & 3;
+    const double *p0 = Us + t * US + g;
+#pragma unroll
+    for (int r0 = 0; r0 < NR; r0 += 4) {
+      double pf[P];
+#pragma unroll
+      for (int j = 0; j < P; ++j) pf[j] = p0[r0 * US + 8 * j];
+      mma_tiles<W, 0>(pf);
+    }
+  }
+  template <int NR, int US>
+  __device__ __forceinline__ void add_chunk(const double *Us, int wp, int lane) {
+    static_assert(WPB == 4, "add_chunk dispatches 4 warps");
+    switch (wp) {
+      case 0: add_chunk_w<0, NR, US>(Us, lane); break;
+      case 1: add_chunk_w<1, NR, US>(Us, lane); break;
+      case 2: add_chunk_w<2, NR, US>(Us, lane); break;
+      default: add_chunk_w<3, NR, US>(Us, lane); break;
     }
   }
   __device__ __forceinline__ void add_block(const double *Us, int US, int nrows_pad, int wp, int lane) {
@@ -703,7 +753,7 @@ __global__ void __launch_bounds__(128) k_gram_stream(long long row_begin, long l
     cp_async_commit();
     cp_async_wait_group<S - 1>();  // this thread's copies of chunk ch are done
     __syncthreads();               // ... and every thread's copies and zero fills
-    acc.add_block(ring + (int)((ch - c0) % S) * CH * US, US, CH, wp, lane);
+    acc.template add_chunk<CH, US>(ring + (int)((ch - c0) % S) * CH * US, wp, lane);
     __syncthreads();  // chunk ch's slot is restaged next iteration
   }
   acc.store(part + (long long)blockIdx.x * R * R, R, wp, lane);
@@ -732,6 +782,7 @@ __global__ void __launch_bounds__(WPB * 32)
   acc.zero();
   const long long b0 = nblk * blockIdx.x / gridDim.x, b1 = nblk * (blockIdx.x + 1) / gridDim.x;
   for (long long rb = b0; rb < b1; ++rb) {
+    rows_mma_stage<RT, WPB>(rb, row_begin, row_end, F);
     rows_mma_block<RT, WPB>(rb, row_begin, row_end, R, mode, l_mode, row_ptr, M, F, Z, H, st, dec, ti_part, md_part,
                             e_part, ech_part, peers, G, me);
     // Us holds the block's final rows (rows past the range are zero): add them to the Gram
