@@ -338,7 +338,11 @@ __device__ __forceinline__ void rows_mma_block(long long rb, long long row_begin
   // only row_ptr
   const bool empty = active ? __ldg(row_ptr + row) == __ldg(row_ptr + row + 1) : true;
   const int branch = (int)Ri[RT];
-  const bool first = branch == SACD_BR_FIRST, eq27 = branch == SACD_BR_EQ27;
+  // the branch rule as one sign test: FIRST z > 0 (z_prev taken as 0), EQ24 z - z_prev > 0,
+  // EQ27 z_prev - z > 0, i.e. -(z - z_prev) > 0 (IEEE subtraction is antisymmetric, negation
+  // and z - 0 are exact)
+  const bool first = branch == SACD_BR_FIRST;
+  const double sgn = branch == SACD_BR_EQ27 ? -1.0 : 1.0;
   const double *Lh = Ri + RT + 2;
   double *zp = Z + tt<RT>(active ? row : row0, 0);
   const double *Uw = Us + (wp * 32 + g) * US + t;
@@ -359,14 +363,14 @@ __device__ __forceinline__ void rows_mma_block(long long rb, long long row_begin
       mm[k] = ld_stream_f64(M + rg * RT + c + cl);
     }
 #pragma unroll
-    for (int q = 0; q < C; ++q) zz[q] = ld_na_f64(zp + 32 * (c + q));
+    for (int q = 0; q < C; ++q) zz[q] = first ? 0.0 : ld_na_f64(zp + 32 * (c + q));  // FIRST: not read
   };
   load_block(0, bf, mt, zv);
   cp_async_wait_all();
   __syncthreads();
 
   double ti = 0.0, md = 0.0;
-  long long E = 0, Ech = 0;
+  unsigned E = 0, Ech = 0;  // per thread at most 64 x (its rows) < 2^32
   double *u = Us + tid * US;
   for (int c0 = 0; c0 < R; c0 += C) {
     double bfn[NKS], mtn[C], zvn[C];
@@ -441,13 +445,11 @@ __device__ __forceinline__ void rows_mma_block(long long rb, long long row_begin
           const double ur = ub[q];
           const double q0 = gr * ri;                     // gr / h, correctly rounded
           const double qr = fma(-q0, h, gr);
-          const double un = fmax(0.0, ur - fma(qr, ri, q0));  // Eq 11-13
+          const double ut = ur - fma(qr, ri, q0);
+          const double un = ut > 0.0 ? ut : 0.0;         // Eq 11-13 (max(0, .); a zero's sign is immaterial)
           const double d = un - ur;                      // Eq 12
           z = -gr * d - Lh[r] * d * d;                   // Eq 20 (Lh = L / 2)
-          // FIRST: z > 0; EQ24: z - z_prev > 0; EQ27: z_prev - z > 0, i.e. z - z_prev < 0
-          // (IEEE subtraction is antisymmetric, and z - 0 = z)
-          const double dz = z - (first ? 0.0 : zv[q]);
-          const bool sel = eq27 ? (dz < 0.0) : (dz > 0.0);
+          const bool sel = (z - zv[q]) * sgn > 0.0;
           if (sel) {
             ub[q] = un;
             E += 1;
