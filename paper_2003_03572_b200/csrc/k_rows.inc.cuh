@@ -433,35 +433,51 @@ __device__ __forceinline__ void rows_mma_block(long long rb, long long row_begin
 #pragma unroll
         for (int qq = q; qq < C; ++qq) acc[q] = fma(ub[qq], Hb[q * C + qq], acc[q]);
       // padding columns (r >= R) have h = 0 (H is zero-padded) and u = m = 0: they take the
-      // h = 0 path (z = 0, no selection) and add exact zeros, so no r < R test is needed
+      // h = 0 path (z = 0, no selection) and add exact zeros, so no r < R test is needed.
+      // Column q + 1's gradient depends on column q only through u_q's final value, which is
+      // u_q or the candidate u'_q: both versions of column q + 1's g and u' are computed
+      // while column q's z and gate are still in flight, and the gate picks one.  The picked
+      // values are exactly the sequential ones; the dependent chain per column shrinks to the
+      // gate (d, z, z - z_prev) and one select.
+      auto cand = [&](double gr, double ur, double h, double ri) {  // max(0, u - g / h), Eq 11-13
+        const double q0 = gr * ri;                                  // g / h, correctly rounded
+        const double qr = fma(-q0, h, gr);
+        const double ut = ur - fma(qr, ri, q0);
+        return ut > 0.0 ? ut : 0.0;                                 // a zero's sign is immaterial
+      };
+      double gr = acc[0] - mv[0];                                   // Eq 14
+      double un = cand(gr, ub[0], Hb[0], Ri[c0]);
 #pragma unroll
       for (int q = 0; q < C; ++q) {
         const int r = c0 + q;
         const double h = Hb[q * C + q];
-        double z = 0.0;
-        if (h != 0.0) {
-          const double ri = Ri[r];
-          const double gr = acc[q] - mv[q];              // Eq 14
-          const double ur = ub[q];
-          const double q0 = gr * ri;                     // gr / h, correctly rounded
-          const double qr = fma(-q0, h, gr);
-          const double ut = ur - fma(qr, ri, q0);
-          const double un = ut > 0.0 ? ut : 0.0;         // Eq 11-13 (max(0, .); a zero's sign is immaterial)
-          const double d = un - ur;                      // Eq 12
-          z = -gr * d - Lh[r] * d * d;                   // Eq 20 (Lh = L / 2)
-          const bool sel = (z - zv[q]) * sgn > 0.0;
-          if (sel) {
-            ub[q] = un;
-            E += 1;
-            if (d != 0.0) Ech += 1;
-            selbits |= 1u << q;
-          }
+        const double ur = ub[q];
+        const double d = un - ur;                                   // Eq 12
+        double z = -gr * d - Lh[r] * d * d;                         // Eq 20 (Lh = L / 2)
+        const bool sel = h != 0.0 && (z - zv[q]) * sgn > 0.0;
+        if (h == 0.0) z = 0.0;
+        double grn = 0.0, unn = 0.0;
+        if (q + 1 < C) {
+          const double hqn = Hb[q * C + q + 1], hn = Hb[(q + 1) * C + q + 1], rin = Ri[r + 1];
+          const double g0 = fma(ur, hqn, acc[q + 1]) - mv[q + 1];  // column q kept u_q
+          const double g1 = fma(un, hqn, acc[q + 1]) - mv[q + 1];  // column q took u'_q
+          const double u0 = cand(g0, ub[q + 1], hn, rin), u1 = cand(g1, ub[q + 1], hn, rin);
+          grn = sel ? g1 : g0;
+          unn = sel ? u1 : u0;
+        }
+        if (sel) {
+          ub[q] = un;
+          E += 1;
+          if (d != 0.0) Ech += 1;
+          selbits |= 1u << q;
         }
 #pragma unroll
-        for (int q2 = q + 1; q2 < C; ++q2) acc[q2] = fma(ub[q], Hb[q * C + q2], acc[q2]);
-        zv[q] = z;                                       // z_prev <- z always (C8)
-        ti += z;                                         // Eq 25
+        for (int q2 = q + 2; q2 < C; ++q2) acc[q2] = fma(ub[q], Hb[q * C + q2], acc[q2]);
+        zv[q] = z;                                                  // z_prev <- z always (C8)
+        ti += z;                                                    // Eq 25
         md += ub[q] * mv[q];
+        gr = grn;
+        un = unn;
       }
       if (dec) {
 #pragma unroll
