@@ -304,6 +304,14 @@ __device__ __forceinline__ void rows_mma_stage(long long rb, long long row_begin
   }
 }
 
+// Is this thread's row of block rb an empty slice (m = 0)?  false past the range.
+template <int WPB>
+__device__ __forceinline__ bool rows_mma_empty(long long rb, long long row_begin, long long row_end,
+                                               const long long *__restrict__ row_ptr) {
+  const long long row = row_begin + rb * (WPB * 32) + threadIdx.x;
+  return row < row_end ? __ldg(row_ptr + row) == __ldg(row_ptr + row + 1) : true;
+}
+
 template <int RT, int WPB>
 __device__ __forceinline__ void rows_mma_block(long long rb, long long row_begin, long long row_end, int R, int mode,
                     int l_mode,
@@ -312,7 +320,8 @@ __device__ __forceinline__ void rows_mma_block(long long rb, long long row_begin
                     uint8_t *__restrict__ dec, double *__restrict__ ti_part, double *__restrict__ md_part,
                     long long *__restrict__ e_part, long long *__restrict__ ech_part,
                     double *const *__restrict__ peers = nullptr, int G = 0, int me = 0,
-                    const long long *next_rb = nullptr, long long nblk = 0) {
+                    const long long *next_rb = nullptr, long long nblk = 0, bool empty_in = false,
+                    bool *empty_next = nullptr) {
   constexpr int TR = WPB * 32;
   constexpr int US = rows_mma_us<RT>();
   constexpr int C = 8;
@@ -334,9 +343,9 @@ __device__ __forceinline__ void rows_mma_block(long long rb, long long row_begin
   static_assert((US * 8) % 16 == 0, "row stride must keep 16-byte chunks aligned");
   const bool active = tid < nrows;
   const long long row = row0 + tid;
-  // the block's staging (rows_mma_stage) is in flight; the empty-slice test (m = 0) needs
-  // only row_ptr
-  const bool empty = active ? __ldg(row_ptr + row) == __ldg(row_ptr + row + 1) : true;
+  // the block's staging (rows_mma_stage) is in flight; the empty-slice flag (m = 0) comes
+  // from the caller (the dynamic kernel loads it one block ahead)
+  const bool empty = empty_next ? empty_in : rows_mma_empty<WPB>(rb, row_begin, row_end, row_ptr);
   const int branch = (int)Ri[RT];
   // the branch rule as one sign test: FIRST z > 0 (z_prev taken as 0), EQ24 z - z_prev > 0,
   // EQ27 z_prev - z > 0, i.e. -(z - z_prev) > 0 (IEEE subtraction is antisymmetric, negation
@@ -526,7 +535,10 @@ __device__ __forceinline__ void rows_mma_block(long long rb, long long row_begin
                   // its loads overlap this block's reductions and the next block's start
     __syncthreads();
     const long long nb = *next_rb;
-    if (nb < nblk) rows_mma_stage<RT, WPB>(nb, row_begin, row_end, F);
+    if (nb < nblk) {
+      rows_mma_stage<RT, WPB>(nb, row_begin, row_end, F);
+      if (empty_next) *empty_next = rows_mma_empty<WPB>(nb, row_begin, row_end, row_ptr);
+    }
   }
 
   // fixed-order block reduction of (ti, md, E, Ech)
@@ -592,12 +604,18 @@ __global__ void __launch_bounds__(WPB * 32)
   if (threadIdx.x == 0) rb_s[0] = (long long)atomicAdd(counter, 1ull);
   rows_mma_prologue<RT, WPB>(H, st, mode, l_mode);  // ends with __syncthreads
   long long rb = rb_s[0];
-  if (rb < nblk) rows_mma_stage<RT, WPB>(rb, row_begin, row_end, F);
+  bool empty = true;
+  if (rb < nblk) {
+    rows_mma_stage<RT, WPB>(rb, row_begin, row_end, F);
+    empty = rows_mma_empty<WPB>(rb, row_begin, row_end, row_ptr);
+  }
   for (int it = 1; rb < nblk; it ^= 1) {
     // slot it was last read before the previous block's closing barrier
     if (threadIdx.x == 0) rb_s[it] = (long long)atomicAdd(counter, 1ull);
+    bool empty_nx = true;
     rows_mma_block<RT, WPB>(rb, row_begin, row_end, R, mode, l_mode, row_ptr, M, F, Z, H, st, dec, ti_part, md_part,
-                            e_part, ech_part, peers, G, me, rb_s + it, nblk);
+                            e_part, ech_part, peers, G, me, rb_s + it, nblk, empty, &empty_nx);
+    empty = empty_nx;
     __syncthreads();  // thread 0's partial writes and rb_s[it] reads are done
     rb = rb_s[it];
   }

@@ -110,6 +110,10 @@ __device__ __forceinline__ void cp_async_wait_group() {
 }
 
 // Reading C12: rand(seed, tag, ctr) = mix64(mix64(seed ^ tag) + (ctr + 1) * golden)
+#ifndef SACD_ROWS_WARPS
+#define SACD_ROWS_WARPS 4  // warps (x 32 rows) per block of the dynamic fp64 row update (2: 4 CTAs/SM, 3: 6 warps/SM, both slower)
+#endif
+
 __device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
   z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
@@ -832,7 +836,8 @@ struct Impl {
   // rows per block of the row-update launch for these flags (the DMMA kernel: kMmaWarps x 32)
   static constexpr bool kRowsMma = sizeof(Real) == 8 && RT <= 64 && rows_per_block<RT>() == 128;
   static constexpr bool kRowsMmaBig = sizeof(Real) == 8 && RT >= 128;
-  static constexpr int kMmaWarps = 4;  // 5 (160 rows, 2 blocks per SM) measured 2.41 vs 1.72 ms: L1 too small
+  static constexpr int kMmaWarps = 4;  // the fused-Gram kernel; 5 (160 rows, 2 blocks per SM) measured 2.41 vs 1.72 ms: L1 too small
+  static constexpr int kDynWarps = SACD_ROWS_WARPS;  // the dynamic / static row kernels
   // the Gram of the updated factor: a separate streaming kernel (k_gram_stream) after the row
   // update by default; opt.reserved[2] = 2 fuses it into the row update (k_sacd_rows_mma_gram,
   // A/B: c4 rows + Gram 1.93 ms per sweep fused)
@@ -851,7 +856,7 @@ struct Impl {
   static int rows_tr(const Context &c, int vflags) {
     if constexpr (kRowsMma) {
       if ((c.opt.reserved[0] == 0 || c.opt.reserved[0] == 5 || c.opt.reserved[0] == 6) && vflags == 0)
-        return kMmaWarps * 32;
+        return gram_fused(c) ? kMmaWarps * 32 : kDynWarps * 32;
     }
     if constexpr (kRowsMmaBig) {
       if (c.opt.reserved[0] == 0 && vflags == 0) return 32;
@@ -899,12 +904,12 @@ struct Impl {
         // from a work counter (c4 1.684 vs 1.720 ms per sweep for the static grid, variant 6)
         if (nblk > 0) {
           int per_sm = 0;
-          auto kern = k_sacd_rows_mma_dyn<RT, kMmaWarps>;
-          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kMmaWarps * 32,
-                                                        rows_mma_smem_bytes<RT, kMmaWarps>());
+          auto kern = k_sacd_rows_mma_dyn<RT, kDynWarps>;
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kDynWarps * 32,
+                                                        rows_mma_smem_bytes<RT, kDynWarps>());
           const long long grid = std::min<long long>(nblk, (long long)std::max(1, per_sm) * c.num_sms);
           cudaMemsetAsync(c.item_ctr + 1, 0, sizeof(unsigned long long), c.stream);
-          kern<<<(unsigned)grid, kMmaWarps * 32, rows_mma_smem_bytes<RT, kMmaWarps>(), c.stream>>>(
+          kern<<<(unsigned)grid, kDynWarps * 32, rows_mma_smem_bytes<RT, kDynWarps>(), c.stream>>>(
               rlo, rhi, c.R, mode, c.opt.l_mode, md.row_ptr, reinterpret_cast<const double *>(M),
               reinterpret_cast<double *>(md.F), reinterpret_cast<double *>(md.Z),
               reinterpret_cast<const double *>(c.Hr), c.st, dec, ti_part, md_part, e_part, ech_part, nblk,
@@ -915,7 +920,7 @@ struct Impl {
       }
       if (c.opt.reserved[0] == 6 && vflags == 0) {  // the static grid (one block per row block)
         if (nblk > 0)
-          k_sacd_rows_mma<RT, kMmaWarps><<<(unsigned)nblk, kMmaWarps * 32, rows_mma_smem_bytes<RT, kMmaWarps>(),
+          k_sacd_rows_mma<RT, kDynWarps><<<(unsigned)nblk, kDynWarps * 32, rows_mma_smem_bytes<RT, kDynWarps>(),
                                             c.stream>>>(
               rlo, rhi, c.R, mode, c.opt.l_mode, md.row_ptr, reinterpret_cast<const double *>(M),
               reinterpret_cast<double *>(md.F), reinterpret_cast<double *>(md.Z),
@@ -949,11 +954,11 @@ struct Impl {
     SACD_CUDA_TRY(cudaFuncSetAttribute(k_sacd_rows<Real, RT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)rows_smem_bytes<Real, RT, false>()));
     if constexpr (kRowsMma) {
-      SACD_CUDA_TRY(cudaFuncSetAttribute(k_sacd_rows_mma<RT, kMmaWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)rows_mma_smem_bytes<RT, kMmaWarps>()));
-      SACD_CUDA_TRY(cudaFuncSetAttribute(k_sacd_rows_mma_dyn<RT, kMmaWarps>,
+      SACD_CUDA_TRY(cudaFuncSetAttribute(k_sacd_rows_mma<RT, kDynWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)rows_mma_smem_bytes<RT, kDynWarps>()));
+      SACD_CUDA_TRY(cudaFuncSetAttribute(k_sacd_rows_mma_dyn<RT, kDynWarps>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)rows_mma_smem_bytes<RT, kMmaWarps>()));
+                                         (int)rows_mma_smem_bytes<RT, kDynWarps>()));
       SACD_CUDA_TRY(cudaFuncSetAttribute(k_sacd_rows_mma_gram<RT, kMmaWarps>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)rows_mma_smem_bytes<RT, kMmaWarps>()));
