@@ -12,6 +12,7 @@
 //           UBLKCP) of the whole 512-byte row into a per-warp shared-memory ring slot with
 //           an mbarrier; the warp waits on the slot and reads it with LDS.128 (no index
 //           shuffle, no L1 allocation: every row comes from L2);
+//   ldg256: ldg with 256-bit loads, two 16-lane workers per warp (two rows per shuffle);
 //   hot   : ldg, but rows with index < HOT are read from a copy staged in shared memory at
 //           kernel start (one generic load; the Zipf head of the b-factor).
 // Index streams: uniform over the table, or Zipf(s) with rank = index (heavy rows first,
@@ -98,6 +99,57 @@ __global__ void __launch_bounds__(1024) g_ldg(const double *__restrict__ tab, co
   }
   out[w * RW + 2 * lane] = f0;
   out[w * RW + 2 * lane + 1] = f1;
+}
+
+// ------------------------------------------------------------------ ldg256
+// Two 16-lane workers per warp: every lane loads its 32-byte quarter-chunk of a 512-byte row
+// with one 256-bit load (LDG.E.ENL2.256, sm_100), so one shuffle delivers the indices of two
+// rows (each half-warp reads its own source lane) and one load instruction moves 1 KB.
+__device__ __forceinline__ void ldg256(const double *p, double &a, double &b, double &c, double &d) {
+  asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
+}
+__global__ void __launch_bounds__(1024) g_ldg256(const double *__restrict__ tab, const uint32_t *__restrict__ idx,
+                                                 const double *__restrict__ xs, long long n, long long per,
+                                                 double *__restrict__ out) {
+  __shared__ double xsb[2][1024];
+  const int lane = threadIdx.x & 31, half = lane >> 4, hl = lane & 15;
+  const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long e0 = w * per, e1 = min(n, e0 + per);
+  double f[4] = {0.0, 0.0, 0.0, 0.0};
+  int par = 0;
+  const int wbase = threadIdx.x & ~31;
+  for (long long base = e0; base < e1; base += 32) {
+    uint32_t my = 0;
+    double xl = 0.0;
+    if (base + lane < e1) {
+      my = ld_stream_u32(idx + base + lane);
+      xl = ld_stream_f64(xs + base + lane);
+    }
+    par ^= 1;
+    xsb[par][threadIdx.x] = xl;
+    __syncwarp();
+    double b[2][4];
+    {
+      const uint32_t r = __shfl_sync(0xffffffffu, my, half);
+      ldg256(tab + (size_t)r * RW + 4 * hl, b[0][0], b[0][1], b[0][2], b[0][3]);
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      if (j + 1 < 16) {
+        const uint32_t r = __shfl_sync(0xffffffffu, my, 2 * (j + 1) + half);
+        ldg256(tab + (size_t)r * RW + 4 * hl, b[(j + 1) & 1][0], b[(j + 1) & 1][1], b[(j + 1) & 1][2],
+               b[(j + 1) & 1][3]);
+      }
+      const double x = xsb[par][wbase + 2 * j + half];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) f[e] = fma(x, b[j & 1][e], f[e]);
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < 4; ++e) f[e] += __shfl_xor_sync(0xffffffffu, f[e], 16);
+  if (half == 0)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) out[w * RW + 4 * hl + e] = f[e];
 }
 
 // ------------------------------------------------------------------ bulk copies
@@ -282,6 +334,15 @@ int main(int argc, char **argv) {
         const long long nw = (long long)sms * 32;
         const long long per = ((n + nw - 1) / nw + 31) / 32 * 32;
         run("ldg_w32_1blk", [&] { g_ldg<0><<<sms, bs>>>(tab, idx, xs, n, per, out); });
+      }
+      for (int wps : {16, 32, 48, 64}) {  // 256-bit loads, two rows per warp instruction
+        const int bs = 256;
+        const int bps = wps * 32 / bs;
+        const long long nw = (long long)sms * bps * (bs / 32);
+        const long long per = ((n + nw - 1) / nw + 31) / 32 * 32;
+        char nm[64];
+        snprintf(nm, sizeof nm, "ldg256_w%d", wps);
+        run(nm, [&] { g_ldg256<<<sms * bps, bs>>>(tab, idx, xs, n, per, out); });
       }
       for (int S : {4, 8, 16}) {
         for (int bps : {1, 2, 4, 6}) {
