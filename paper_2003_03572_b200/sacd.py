@@ -255,10 +255,18 @@ class Sacd:
         _check(load_library().sacd_fit(self._h, C.byref(f), C.byref(ft)))
         return f.value, ft.value
 
-    def factors(self, mode=None):
+    def factors(self, mode=None, out=None):
+        """The factors as fp64 host arrays (I_n x R).  out: optional preallocated C-contiguous
+        float64 array(s) of that shape (a list of three for mode=None); pinned memory (e.g. a
+        numpy view of a torch pin_memory tensor) is copied into directly by the library."""
         if mode is None:
-            return [self.factors(n) for n in range(3)]
-        out = np.zeros((self.dims[mode], self.rank), np.float64)
+            return [self.factors(n, None if out is None else out[n]) for n in range(3)]
+        shape = (self.dims[mode], self.rank)
+        if out is None:
+            out = np.zeros(shape, np.float64)
+        elif not (isinstance(out, np.ndarray) and out.dtype == np.float64 and out.shape == shape
+                  and out.flags.c_contiguous):
+            raise ValueError(f"factors: out must be a C-contiguous float64 array of shape {shape}")
         _check(load_library().sacd_factors(self._h, int(mode), _ptr(out), self.rank))
         return out
 

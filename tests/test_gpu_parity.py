@@ -430,6 +430,27 @@ def test_device_pointer_inputs():
         assert np.array_equal(g1.factors(0), g2.factors(0))
 
 
+def test_factors_into_preallocated_pinned_and_pageable_buffers():
+    """Sacd.factors(out=...): pinned buffers (direct D2H) and pageable ones (the pinned ring,
+    > 8 MB) return exactly the default read; bad buffers are rejected."""
+    import torch
+    dims, R = (40000, 300, 20), 64  # mode 0 is 20 MB: the chunked ring path
+    c, v = ragged_tensor(dims, 60000, 5)
+    with S(c, v, dims, R, 3) as g:
+        g.iterate(2)
+        ref = g.factors()
+        pinned = [torch.empty((dims[n], R), dtype=torch.float64).pin_memory().numpy() for n in range(3)]
+        pageable = [np.empty((dims[n], R)) for n in range(3)]
+        for out in (pinned, pageable):
+            got = g.factors(out=out)
+            for n in range(3):
+                assert got[n] is out[n] and np.array_equal(out[n], ref[n])
+        with pytest.raises(ValueError):
+            g.factors(0, out=np.empty((dims[0], R), np.float32))
+        with pytest.raises(ValueError):
+            g.factors(0, out=np.empty((R, dims[0])).T)
+
+
 def test_device_inputs_from_torch_stream_are_complete():
     """sacd_init / sacd_rmse read device inputs after a device synchronisation, so tensors
     produced on PyTorch's stream right before the call are complete (the library stream is
