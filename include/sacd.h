@@ -98,9 +98,10 @@ typedef struct {
                               /* [1]: MTTKRP a-blocked order: > 0 = blocks of that many      */
                               /* a-rows, <= 0 = canonical order (default);                  */
                               /* [2]: Gram kernel (0 = default: fp64 tensor cores (DMMA): for */
-                              /* pitch <= 64 a streaming kernel after the row update, for     */
-                              /* pitch >= 128 panel pairs; 1 = the FMA kernel; 2 = fused into */
-                              /* the R <= 64 row update; 3 = panel pairs also for pitch <= 64) */
+                              /* pitch <= 64 fused into the row update while max I_n x R <=    */
+                              /* 2^20, else a streaming kernel after it; for pitch >= 128 panel */
+                              /* pairs; 1 = the FMA kernel; 2 = always fused; 3 = panel pairs  */
+                              /* also for pitch <= 64; 4 = always the streaming kernel)        */
                               /* [3]: sharded exchange (0 = full owned rows, graph-captured;   */
                               /* 1 = delta: only the changed elements as (index, value) lists, */
                               /* full rows when those are smaller; NCCL sweeps then run eagerly */

@@ -839,8 +839,8 @@ struct Impl {
   static constexpr int kMmaWarps = 4;  // the fused-Gram kernel; 5 (160 rows, 2 blocks per SM) measured 2.41 vs 1.72 ms: L1 too small
   static constexpr int kDynWarps = SACD_ROWS_WARPS;  // the dynamic / static row kernels
   // the Gram of the updated factor: a separate streaming kernel (k_gram_stream) after the row
-  // update by default; opt.reserved[2] = 2 fuses it into the row update (k_sacd_rows_mma_gram,
-  // A/B: c4 rows + Gram 1.93 ms per sweep fused)
+  // update, or fused into the row update (k_sacd_rows_mma_gram; c4 rows + Gram 1.93 ms per
+  // sweep fused vs 1.87 streaming)
   static constexpr bool kGramStream = sizeof(Real) == 8 && RT <= 64;
   static constexpr int kGramStages = 4;
   // the default fp64 R <= 64 row kernels (dynamic or with the fused Gram) push changed
@@ -849,8 +849,17 @@ struct Impl {
     if constexpr (kRowsMma) return c.opt.reserved[0] == 0;
     return false;
   }
+  // opt.reserved[2]: 0 = by size (fused while max I_n x R <= 2^20: small configs are launch-
+  // bound and the fused kernel saves the Gram launch, c1 / c2 / c5 R <= 32; the streaming
+  // kernel is faster from c3 / c5 R = 64 up), 2 = fused, 4 = streaming
   static bool gram_fused(const Context &c) {
-    if constexpr (kRowsMma) return c.opt.reserved[0] == 0 && c.opt.reserved[2] == 2;
+    if constexpr (kRowsMma) {
+      if (c.opt.reserved[0] != 0) return false;
+      if (c.opt.reserved[2] == 2) return true;
+      if (c.opt.reserved[2] != 0) return false;
+      const long long imax = std::max(c.m[0].I, std::max(c.m[1].I, c.m[2].I));
+      return imax * (long long)c.R <= (1LL << 20);
+    }
     return false;
   }
   static int rows_tr(const Context &c, int vflags) {
