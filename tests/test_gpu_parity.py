@@ -124,6 +124,21 @@ def test_mttkrp_gram_hessian(R, precision):
             assert np.abs(g.hessian(n) - Ho).max() <= tol * np.abs(Ho).max()
 
 
+@pytest.mark.parametrize("gram_variant", [0, 2, 3, 4])
+@pytest.mark.parametrize("R", [5, 40, 64])
+def test_gram_refresh_after_update(gram_variant, R):
+    """The Gram refresh of the factor a mode update just wrote (Eq 10's G_n = F_n^T F_n): by
+    size (0), fused into the row update (2), panel pairs (3) and the streaming kernel (4), on
+    mode lengths that are not multiples of the 32-row chunk or the 128-row block."""
+    dims = (1000, 77, 333)
+    c, v = ragged_tensor(dims, 20000, 13, heavy_rows=((0, 3, 900),))
+    with S(c, v, dims, R, 5, gram_variant=gram_variant) as g:
+        for n in range(3):
+            g.mode_update(n, branch=0)
+            Go = O.gram(g.factors(n))
+            assert np.abs(g.gram(n) - Go).max() <= 1e-12 * np.abs(Go).max()
+
+
 @pytest.mark.parametrize("R", [33, 64, 100, 256])
 def test_uniform_values_tensor(R):
     """A tensor whose values are all equal (binary, like c4) takes the MTTKRP path without a
