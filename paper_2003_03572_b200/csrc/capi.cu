@@ -8,6 +8,7 @@
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
 #include <new>
 #include <thread>
 #include <vector>
@@ -287,6 +288,36 @@ static int sweep_eager(Context &c) {
   return SACD_OK;
 }
 
+// The library's device memory pool (sacd_internal.cuh): one per device, created on first
+// use, never destroyed (its memory is reused by every later context on that device).
+cudaMemPool_t device_pool(int device) {
+  static std::mutex mu;
+  static std::vector<cudaMemPool_t> pools;
+  std::lock_guard<std::mutex> lock(mu);
+  if (device < 0) device = 0;
+  if ((int)pools.size() <= device) pools.resize(device + 1, nullptr);
+  if (!pools[device]) {
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.handleTypes = cudaMemHandleTypeNone;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = device;
+    cudaMemPool_t pool = nullptr;
+    if (cudaMemPoolCreate(&pool, &props) != cudaSuccess) {  // fall back to the default pool
+      cudaGetLastError();
+      if (cudaDeviceGetDefaultMemPool(&pool, device) != cudaSuccess) return nullptr;
+    }
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    unsigned long long thr = total_b / 4;
+    if (const char *e = getenv("SACD_POOL_RELEASE_MB")) thr = strtoull(e, nullptr, 10) << 20;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    cudaGetLastError();
+    pools[device] = pool;
+  }
+  return pools[device];
+}
+
 static void destroy(sacd_ctx *c) {
   if (!c) return;
   if (c->stream) cudaStreamSynchronize(c->stream);
@@ -360,13 +391,7 @@ static void destroy(sacd_ctx *c) {
     if (e) cudaEventDestroy(e);
   if (c->comm) ncclCommDestroy(reinterpret_cast<ncclComm_t>(c->comm));
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
-  {
-    // return the stream-ordered allocations' memory kept mapped by the pool (see init_impl)
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, c->device) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
-    cudaGetLastError();
-  }
-  delete c;
+  delete c;  // memory from the library's pool stays mapped there for the next context
 }
 
 // Layout key (i_n, i_a, i_b): a = the LONGER other mode (ties -> lower mode id), b = the
@@ -555,17 +580,6 @@ static int init_impl(Context *c, const uint32_t *coords, const float *vals, uint
   cudaStream_t s = c->stream;
   InitTimer tm;
   SACD_TRY(sync_if_device(coords, vals));
-  {
-    // keep memory returned to the device's default pool mapped while the context lives (the
-    // layout build's multi-GB temporaries are stream-ordered allocations and mapping fresh
-    // physical memory dominated sacd_init); sacd_free trims the pool again
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, c->device) == cudaSuccess) {
-      unsigned long long thr = ~0ull;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
-    cudaGetLastError();
-  }
   SACD_CUDA_TRY(cudaMalloc(&c->st, sizeof(DevState)));
   SACD_CUDA_TRY(cudaMemsetAsync(c->st, 0, sizeof(DevState), s));
   for (int n = 0; n < 3; ++n) {
@@ -576,8 +590,8 @@ static int init_impl(Context *c, const uint32_t *coords, const float *vals, uint
   uint32_t *dc = nullptr;
   float *dv = nullptr;
   const size_t ne = (size_t)(c->nnz > 0 ? c->nnz : 1);
-  SACD_CUDA_TRY(cudaMallocAsync(&dc, ne * 12, s));
-  SACD_CUDA_TRY(cudaMallocAsync(&dv, ne * 4, s));
+  SACD_CUDA_TRY(pool_alloc(&dc, ne * 12, c->device, s));
+  SACD_CUDA_TRY(pool_alloc(&dv, ne * 4, c->device, s));
   if (c->nnz > 0) {
     SACD_CUDA_TRY(cudaMemcpyAsync(dc, coords, (size_t)c->nnz * 12, cudaMemcpyDefault, s));
     SACD_CUDA_TRY(cudaMemcpyAsync(dv, vals, (size_t)c->nnz * 4, cudaMemcpyDefault, s));
@@ -717,7 +731,7 @@ static int init_impl(Context *c, const uint32_t *coords, const float *vals, uint
     ModeData &md = c->m[n];
     SACD_CUDA_TRY(cudaMalloc(&md.F, (size_t)md.I * P * rs));
     const size_t zrows = (size_t)((md.I + 31) / 32 * 32);
-    SACD_CUDA_TRY(cudaMalloc(&md.Z, zrows * P * rs));
+    SACD_CUDA_TRY(pool_alloc(&md.Z, zrows * P * rs, c->device, s));
     SACD_CUDA_TRY(cudaMemsetAsync(md.Z, 0, zrows * P * rs, s));
     SACD_CUDA_TRY(cudaMalloc(&md.G, (size_t)R * R * 8));
     SACD_CUDA_TRY(cudaMalloc(&md.cmask, (size_t)std::max(1LL, md.I) * 4));
@@ -761,15 +775,15 @@ static int init_impl(Context *c, const uint32_t *coords, const float *vals, uint
   const long long grows = (c->opt.precision == SACD_F64 && c->pitch >= 128) ? 2048 : 64;
   c->gram_blocks = (int)std::min<long long>(gcap, std::max<long long>(1, (maxI + grows - 1) / grows));
   if (getenv("SACD_GRAM_BLOCKS")) c->gram_blocks = std::max(1, atoi(getenv("SACD_GRAM_BLOCKS")));  // tuning
-  SACD_CUDA_TRY(cudaMalloc(&c->M, (size_t)((maxI + 31) / 32 * 32) * P * rs));
+  SACD_CUDA_TRY(pool_alloc(&c->M, (size_t)((maxI + 31) / 32 * 32) * P * rs, c->device, s));
   SACD_CUDA_TRY(cudaMalloc(&c->item_ctr, 2 * sizeof(unsigned long long)));  // MTTKRP items, row blocks
   SACD_CUDA_TRY(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device));
   if (c->opt.variant == SACD_VARIANT_SNAPSHOT) {  // snapshot importances of one pass (TT layout)
-    SACD_CUDA_TRY(cudaMalloc(&c->Zs, (size_t)((maxI + 31) / 32 * 32) * P * rs));
+    SACD_CUDA_TRY(pool_alloc(&c->Zs, (size_t)((maxI + 31) / 32 * 32) * P * rs, c->device, s));
     c->device_bytes += (long long)((size_t)((maxI + 31) / 32 * 32) * P * rs);
   }
-  SACD_CUDA_TRY(cudaMalloc(&c->partial, (size_t)max_slots * P * rs));
-  SACD_CUDA_TRY(cudaMalloc(&c->fixbuf, (size_t)max_chunks * P * rs));
+  SACD_CUDA_TRY(pool_alloc(&c->partial, (size_t)max_slots * P * rs, c->device, s));
+  SACD_CUDA_TRY(pool_alloc(&c->fixbuf, (size_t)max_chunks * P * rs, c->device, s));
   // sharded ranks write their own partial buffers (>= their slots); c->max_slots keeps the
   // smallest buffer any launch may index (debug bounds)
   c->max_slots = c->sharded ? c->max_slots : max_slots;
@@ -858,7 +872,7 @@ static bool is_pinned_host(const void *p) {
 static int read_matrix(Context *c, const void *src, long long rows, double *out, long long ld, bool ttl = false) {
   double *tmp = nullptr;
   cudaStream_t s = c->stream;
-  SACD_CUDA_TRY(cudaMallocAsync(&tmp, (size_t)std::max(1LL, rows) * c->R * 8, s));
+  SACD_CUDA_TRY(pool_alloc(&tmp, (size_t)std::max(1LL, rows) * c->R * 8, c->device, s));
   int rc = launch_convert_out(*c, src, rows, tmp, ttl);
   const size_t row_bytes = (size_t)c->R * 8;
   const size_t total = (size_t)rows * row_bytes;
@@ -916,7 +930,7 @@ static int read_matrix(Context *c, const void *src, long long rows, double *out,
 static int write_matrix(Context *c, void *dst, long long rows, const double *in, long long ld, bool ttl = false) {
   double *tmp = nullptr;
   cudaStream_t s = c->stream;
-  SACD_CUDA_TRY(cudaMallocAsync(&tmp, (size_t)std::max(1LL, rows) * c->R * 8, s));
+  SACD_CUDA_TRY(pool_alloc(&tmp, (size_t)std::max(1LL, rows) * c->R * 8, c->device, s));
   cudaError_t e = cudaMemcpy2DAsync(tmp, (size_t)c->R * 8, in, (size_t)ld * 8, (size_t)c->R * 8, (size_t)rows,
                                     cudaMemcpyHostToDevice, s);
   if (e != cudaSuccess) {
@@ -1182,9 +1196,9 @@ static int eval_impl(Context *c, const uint32_t *coords, const float *vals, long
     }
     return rc == SACD_OK;
   };
-  if (ck(cudaMallocAsync(&dc, nn * 12, s)) && ck(cudaMallocAsync(&dout, nn * 8, s)) &&
-      ck(cudaMallocAsync(&part, nb * 8, s)) && ck(cudaMallocAsync(&sse, 8, s)) && ck(cudaMallocAsync(&flag, 4, s)) &&
-      (!vals || ck(cudaMallocAsync(&dv, nn * 4, s))) && ck(cudaMemsetAsync(flag, 0, 4, s)) &&
+  if (ck(pool_alloc(&dc, nn * 12, c->device, s)) && ck(pool_alloc(&dout, nn * 8, c->device, s)) &&
+      ck(pool_alloc(&part, nb * 8, c->device, s)) && ck(pool_alloc(&sse, 8, c->device, s)) && ck(pool_alloc(&flag, 4, c->device, s)) &&
+      (!vals || ck(pool_alloc(&dv, nn * 4, c->device, s))) && ck(cudaMemsetAsync(flag, 0, 4, s)) &&
       (n == 0 || ck(cudaMemcpyAsync(dc, coords, (size_t)n * 12, cudaMemcpyDefault, s))) &&
       (!vals || n == 0 || ck(cudaMemcpyAsync(dv, vals, (size_t)n * 4, cudaMemcpyDefault, s)))) {
     rc = launch_range_check(*c, dc, n, flag);
@@ -1306,7 +1320,7 @@ int sacd_mode_update(sacd_ctx *c, int32_t mode, int32_t branch, uint8_t *decisio
   const size_t nd = (size_t)c->m[mode].I * c->R;
   uint8_t *dd = nullptr;
   if (decisions) {
-    SACD_CUDA_TRY(cudaMallocAsync(&dd, std::max<size_t>(1, nd), c->stream));
+    SACD_CUDA_TRY(pool_alloc(&dd, std::max<size_t>(1, nd), c->device, c->stream));
   }
   if (dd) SACD_CUDA_TRY(cudaMemsetAsync(dd, 0, std::max<size_t>(1, nd), c->stream));
   int rc = c->sharded ? launch_sharded_mode_update(*c, mode, branch, false, false, dd)

@@ -215,19 +215,19 @@ int build_blocked_order(Context &c, int n, long long ablk_rows, std::vector<long
   void *temp = nullptr;
   size_t tb = 0, tb2 = 0;
   const size_t ne = (size_t)nnz;
-  SACD_CUDA_TRY(cudaMallocAsync(&keys, ne * 4, s));
-  SACD_CUDA_TRY(cudaMallocAsync(&keys2, ne * 4, s));
-  SACD_CUDA_TRY(cudaMallocAsync(&pos, ne * 4, s));
-  SACD_CUDA_TRY(cudaMallocAsync(&perm, ne * 4, s));
-  SACD_CUDA_TRY(cudaMallocAsync(&flag, ne * 4, s));
-  SACD_CUDA_TRY(cudaMallocAsync(&flag64, ne * 8, s));
-  SACD_CUDA_TRY(cudaMallocAsync(&idx, ne * 8, s));
+  SACD_CUDA_TRY(pool_alloc(&keys, ne * 4, c.device, s));
+  SACD_CUDA_TRY(pool_alloc(&keys2, ne * 4, c.device, s));
+  SACD_CUDA_TRY(pool_alloc(&pos, ne * 4, c.device, s));
+  SACD_CUDA_TRY(pool_alloc(&perm, ne * 4, c.device, s));
+  SACD_CUDA_TRY(pool_alloc(&flag, ne * 4, c.device, s));
+  SACD_CUDA_TRY(pool_alloc(&flag64, ne * 8, c.device, s));
+  SACD_CUDA_TRY(pool_alloc(&idx, ne * 8, c.device, s));
   const long long nblk = (md.I > 0 ? (c.dims[md.a] + ablk_rows - 1) / ablk_rows : 1);
   const int end_bit = bits_for((unsigned long long)std::max(1LL, nblk - 1));
   k_block_keys<<<grid_for(nnz), 256, 0, s>>>(md.idx_a, nnz, ablk_rows, keys, pos);
   SACD_CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, keys2, pos, perm, (int)nnz, 0, end_bit, s));
   SACD_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tb2, flag64, idx, (int)nnz, s));
-  SACD_CUDA_TRY(cudaMallocAsync(&temp, std::max(tb, tb2), s));
+  SACD_CUDA_TRY(pool_alloc(&temp, std::max(tb, tb2), c.device, s));
   SACD_CUDA_TRY(cub::DeviceRadixSort::SortPairs(temp, tb, keys, keys2, pos, perm, (int)nnz, 0, end_bit, s));
   k_block_gather<<<grid_for(nnz), 256, 0, s>>>(perm, keys2, md.idx_a, md.idx_b, md.idx_n, md.val, nnz, md.nzm, flag);
   k_widen<<<grid_for(nnz), 256, 0, s>>>(flag, nnz, flag64);
@@ -238,8 +238,8 @@ int build_blocked_order(Context &c, int n, long long ablk_rows, std::vector<long
   SACD_CUDA_TRY(cudaMemcpyAsync(&lastf, flag + nnz - 1, 4, cudaMemcpyDeviceToHost, s));
   SACD_CUDA_TRY(cudaStreamSynchronize(s));
   nseg = last + lastf;
-  SACD_CUDA_TRY(cudaMallocAsync(&d_start, (size_t)nseg * 8, s));
-  SACD_CUDA_TRY(cudaMallocAsync(&d_row, (size_t)nseg * 4, s));
+  SACD_CUDA_TRY(pool_alloc(&d_start, (size_t)nseg * 8, c.device, s));
+  SACD_CUDA_TRY(pool_alloc(&d_row, (size_t)nseg * 4, c.device, s));
   k_seg_list<<<grid_for(nnz), 256, 0, s>>>(flag, idx, reinterpret_cast<const uint32_t *>(md.nzm), nnz, d_start,
                                            d_row);
   SACD_CUDA_TRY(cudaGetLastError());
@@ -267,7 +267,7 @@ int build_layouts(Context &c, const uint32_t *coords, const float *vals) {
   cudaStream_t s = c.stream;
   int *flags = nullptr;
   InitTimer tm;
-  SACD_CUDA_TRY(cudaMallocAsync(&flags, 4 * sizeof(unsigned long long), s));  // flags | fiber counts [3]
+  SACD_CUDA_TRY(pool_alloc(&flags, 4 * sizeof(unsigned long long), c.device, s));  // flags | fiber counts [3]
   SACD_CUDA_TRY(cudaMemsetAsync(flags, 0, 4 * sizeof(unsigned long long), s));
   unsigned long long *nfib = reinterpret_cast<unsigned long long *>(flags) + 1;
   if (nnz > 0)
@@ -298,13 +298,13 @@ int build_layouts(Context &c, const uint32_t *coords, const float *vals) {
   void *temp = nullptr;
   size_t temp_bytes = 0;
   const size_t ne = (size_t)(nnz > 0 ? nnz : 1);
-  SACD_CUDA_TRY(cudaMallocAsync(&keys, ne * 8, s));
-  SACD_CUDA_TRY(cudaMallocAsync(&keys2, ne * 8, s));
-  SACD_CUDA_TRY(cudaMallocAsync(&pos, ne * 4, s));
-  SACD_CUDA_TRY(cudaMallocAsync(&pos2, ne * 4, s));
+  SACD_CUDA_TRY(pool_alloc(&keys, ne * 8, c.device, s));
+  SACD_CUDA_TRY(pool_alloc(&keys2, ne * 8, c.device, s));
+  SACD_CUDA_TRY(pool_alloc(&pos, ne * 4, c.device, s));
+  SACD_CUDA_TRY(pool_alloc(&pos2, ne * 4, c.device, s));
   if (nnz > 0) {
     SACD_CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, keys, keys2, pos, pos2, (int)nnz, 0, 64, s));
-    SACD_CUDA_TRY(cudaMallocAsync(&temp, temp_bytes, s));
+    SACD_CUDA_TRY(pool_alloc(&temp, temp_bytes, c.device, s));
   }
   for (int n = 0; n < 3; n++) {
     ModeData &md = c.m[n];
@@ -312,13 +312,13 @@ int build_layouts(Context &c, const uint32_t *coords, const float *vals) {
     const unsigned long long Ia = (unsigned long long)c.dims[a], Ib = (unsigned long long)c.dims[b];
     const bool soa = layout_needs_soa(c);
     if (soa) {
-      SACD_CUDA_TRY(cudaMallocAsync(&md.idx_a, ne * 4, s));
-      SACD_CUDA_TRY(cudaMallocAsync(&md.idx_b, ne * 4, s));
-      SACD_CUDA_TRY(cudaMallocAsync(&md.idx_n, ne * 4, s));
-      SACD_CUDA_TRY(cudaMallocAsync(&md.val, ne * 4, s));
+      SACD_CUDA_TRY(pool_alloc(&md.idx_a, ne * 4, c.device, s));
+      SACD_CUDA_TRY(pool_alloc(&md.idx_b, ne * 4, c.device, s));
+      SACD_CUDA_TRY(pool_alloc(&md.idx_n, ne * 4, c.device, s));
+      SACD_CUDA_TRY(pool_alloc(&md.val, ne * 4, c.device, s));
     }
-    SACD_CUDA_TRY(cudaMallocAsync(&md.nzm, ne * 16, s));
-    SACD_CUDA_TRY(cudaMallocAsync(&md.row_ptr, (size_t)(md.I + 1) * 8, s));
+    SACD_CUDA_TRY(pool_alloc(&md.nzm, ne * 16, c.device, s));
+    SACD_CUDA_TRY(pool_alloc(&md.row_ptr, (size_t)(md.I + 1) * 8, c.device, s));
     c.device_bytes += (long long)ne * (soa ? 32 : 16) + (md.I + 1) * 8;
     tm.mark(s, "  layout: allocations");
     if (nnz > 0) {
@@ -342,7 +342,7 @@ int build_layouts(Context &c, const uint32_t *coords, const float *vals) {
   SACD_CUDA_TRY(cudaMemcpyAsync(hfib, nfib, sizeof(hfib), cudaMemcpyDeviceToHost, s));
   // ||X||^2 in mode-0 layout order
   double *part = nullptr;
-  SACD_CUDA_TRY(cudaMallocAsync(&part, kNormBlocks * sizeof(double), s));
+  SACD_CUDA_TRY(pool_alloc(&part, kNormBlocks * sizeof(double), c.device, s));
   k_norm_partial<<<kNormBlocks, 256, 0, s>>>(c.m[0].nzm, nnz, part);  // mode-0 order, canonical here
   k_norm_final<<<1, 32, 0, s>>>(part, kNormBlocks, c.st);
   SACD_CUDA_TRY(cudaGetLastError());

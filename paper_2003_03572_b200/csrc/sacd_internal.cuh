@@ -38,6 +38,22 @@ struct Status {
     if (rc_ != SACD_OK) return rc_; \
   } while (0)
 
+// ------------------------------------------------------------------ device memory pool
+// The library's stream-ordered allocations (the uploaded COO, the layout build's multi-GB
+// sort scratch, the per-mode nonzero records, M, z_prev, the split-row partials, per-call
+// temporaries) come from ONE pool per device that the library owns (cudaMemPoolCreate), not
+// from the device's default pool.  Freed memory stays mapped in it up to a release threshold
+// (a quarter of the device's memory; SACD_POOL_RELEASE_MB overrides), so the layout of mode 2
+// reuses mode 1's scratch, and a later sacd_init in the same process (the next tensor, the
+// next repetition) finds its buffers mapped instead of paying the page-mapping cost of fresh
+// device memory again, which dominated sacd_init (c4: ~80 ms of ~180).  Buffers shared with
+// peers through CUDA IPC (factor replicas, flags, exchange slots) stay on cudaMalloc.
+cudaMemPool_t device_pool(int device);
+template <typename T>
+inline cudaError_t pool_alloc(T **p, size_t bytes, int device, cudaStream_t s) {
+  return cudaMallocFromPoolAsync(reinterpret_cast<void **>(p), bytes, device_pool(device), s);
+}
+
 // SACD_INIT_TIMING=1 prints the wall time of each sacd_init phase to stderr (diagnostics)
 struct InitTimer {
   bool on = getenv("SACD_INIT_TIMING") != nullptr;
