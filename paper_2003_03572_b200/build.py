@@ -70,6 +70,9 @@ def build(force: bool = False, verbose: bool = False, flavour: str = "default") 
     OUT, STAMP = _paths(flavour)
     if not force and not _stale(flavour):
         return OUT
+    # fingerprint of the sources as they are BEFORE nvcc reads them: an edit made while the
+    # compile runs must leave the stamp stale
+    fp = _fingerprint(flavour)
     cmd = [NVCC, *FLAGS, *FLAVOURS[flavour][1], "-o", OUT + ".tmp", *[os.path.join(CSRC, s) for s in SOURCES], *LIBS]
     log = os.path.join(HERE, f"build_{flavour}.log")
     with open(log, "w") as fh:
@@ -79,7 +82,7 @@ def build(force: bool = False, verbose: bool = False, flavour: str = "default") 
         raise RuntimeError(f"nvcc failed ({r.returncode}); see {log}")
     os.replace(OUT + ".tmp", OUT)
     with open(STAMP, "w") as fh:
-        fh.write(_fingerprint(flavour) + "\n")
+        fh.write(fp + "\n")
     if verbose:
         print(f"built {OUT}")
     return OUT

@@ -235,6 +235,32 @@ struct SubRow {
 #pragma unroll
     for (int k = 0; k < NV; ++k) VV::get(__ldg(reinterpret_cast<const VT *>(p) + k * SW), v + k * VV::N);
   }
+  // the same load with an L1 policy: H = 1 no L1 allocation, 2 L1 evict_first, 3 L1 evict_last
+  template <int H>
+  __device__ __forceinline__ void load_hint(const Real *p) {
+    if constexpr (H == 0) {
+      load(p);
+    } else {
+#pragma unroll
+      for (int k = 0; k < NV; ++k) {
+        uint4 r;
+        const void *q = reinterpret_cast<const VT *>(p) + k * SW;
+        if constexpr (H == 1)
+          asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                       : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(q));
+        else if constexpr (H == 2)
+          asm volatile("ld.global.nc.L1::evict_first.v4.u32 {%0,%1,%2,%3}, [%4];"
+                       : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(q));
+        else
+          asm volatile("ld.global.nc.L1::evict_last.v4.u32 {%0,%1,%2,%3}, [%4];"
+                       : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(q));
+        VT t;
+        static_assert(sizeof(VT) == 16, "16-byte chunks");
+        memcpy(&t, &r, 16);
+        VV::get(t, v + k * VV::N);
+      }
+    }
+  }
   __device__ __forceinline__ void store(Real *p) const { store_from(p, v); }
   __device__ static __forceinline__ void store_from(Real *p, const Real (&x)[E]) {
 #pragma unroll
@@ -418,7 +444,7 @@ __device__ __forceinline__ int xs_slot(int t) {
   return XS == 3 ? t + (t >> 4) : t;
 }
 
-template <typename Real, int RT, int SW, int D, int PF, int XS>
+template <typename Real, int RT, int SW, int D, int PFX, int XS>
 __device__ __forceinline__ void lean_item(long long item, const WorkItem *__restrict__ items,
                                           const uint4 *__restrict__ nzm, const Real *__restrict__ A,
                                           const Real *__restrict__ B, Real *__restrict__ M,
@@ -427,6 +453,12 @@ __device__ __forceinline__ void lean_item(long long item, const WorkItem *__rest
   constexpr int E = SR::E;
   constexpr int VEC = V16<Real>::N;
   static_assert(SR::NV >= 1, "row narrower than a sub-warp of 16-byte chunks");
+  // PFX >= 4 (tuning): L1 policy of the row gathers instead of a prefetch.  4: a-rows without
+  // L1 allocation, 5: a-rows evict_first, 6: a-rows without allocation + b-rows evict_last,
+  // 7: b-rows evict_last
+  constexpr int PF = PFX >= 4 ? 0 : PFX;
+  constexpr int AH = (PFX == 4 || PFX == 6) ? 1 : (PFX == 5 ? 2 : 0);
+  constexpr int BH = (PFX == 6 || PFX == 7) ? 3 : 0;
   const int lane = threadIdx.x & (SW - 1);
   const unsigned mask = SW == 32 ? 0xffffffffu : (((1u << SW) - 1u) << (threadIdx.x & 31 & ~(SW - 1)));
   const long long nz0 = items[item].nz0, nz1 = items[item].nz1;
@@ -499,13 +531,13 @@ __device__ __forceinline__ void lean_item(long long item, const WorkItem *__rest
 #pragma unroll
     for (int j = 0; j < D && j < SW; ++j) {
       fetch(j);
-      bb[j % (D + 1)].load(Bl + (long long)(fb[j] & kIdxMask) * RT);
+      bb[j % (D + 1)].template load_hint<BH>(Bl + (long long)(fb[j] & kIdxMask) * RT);
     }
 #pragma unroll
     for (int j = 0; j < SW; ++j) {
       if (j + D < SW) {
         fetch(j + D);
-        bb[(j + D) % (D + 1)].load(Bl + (long long)(fb[j + D] & kIdxMask) * RT);
+        bb[(j + D) % (D + 1)].template load_hint<BH>(Bl + (long long)(fb[j + D] & kIdxMask) * RT);
       }
       Real x;
       if constexpr (XS == 2 || XS == 3) x = xr[j % (D + 1)];
@@ -528,7 +560,7 @@ __device__ __forceinline__ void lean_item(long long item, const WorkItem *__rest
         }
         const uint32_t ai = __shfl_sync(mask, my.x, j, SW) & kIdxMask;
         SACD_DBG(SACD_DASSERT(ai < g_dbg.Ia));
-        arow.load(Al + (long long)ai * RT);
+        arow.template load_hint<AH>(Al + (long long)ai * RT);
       }
 #pragma unroll
       for (int k = 0; k < E; ++k) facc[k] = fma(x, bb[j % (D + 1)].v[k], facc[k]);

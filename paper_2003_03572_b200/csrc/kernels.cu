@@ -186,7 +186,7 @@ struct Impl {
   // only, items from c.item_ctr (reset here, stream-ordered)
   // SW = 32: one worker per warp (k_mttkrp_lean_dyn); SW < 32: 32/SW workers per warp
   // (k_mttkrp_lean_dyn_sw), each taking its own items from the counter
-  template <int D, int MINB, int XS, int SW = 32>
+  template <int D, int MINB, int XS, int SW = 32, int PF = 0>
   static void launch_dyn(Context &c, const WorkItem *items, long long n_items, const uint4 *nzm, const Real *A,
                          const Real *B, Real *out, Real *partial) {
     auto go = [&](auto kern) {
@@ -199,8 +199,8 @@ struct Impl {
       kern<<<(unsigned)std::max<long long>(1, grid), 256, 0, c.stream>>>(items, n_items, nzm, A, B, out, partial,
                                                                          c.item_ctr, (Real)c.xu);
     };
-    if constexpr (SW == 32) go(k_mttkrp_lean_dyn<Real, RT, D, MINB, 0, XS>);
-    else go(k_mttkrp_lean_dyn_sw<Real, RT, SW, D, MINB, 0, XS>);
+    if constexpr (SW == 32) go(k_mttkrp_lean_dyn<Real, RT, D, MINB, PF, XS>);
+    else go(k_mttkrp_lean_dyn_sw<Real, RT, SW, D, MINB, PF, XS>);
   }
 
   static int mttkrp_on(Context &c, int mode, const WorkItem *items, long long n_items, const SplitRow *splits,
@@ -255,6 +255,22 @@ struct Impl {
             else if (var == 55 && ux) launch_dyn<1, 4, 4, 16>(c, items, n_items, md.nzm, A, B, out, partial);
             else if (var == 56) launch_dyn<2, 4, 1>(c, items, n_items, md.nzm, A, B, out, partial);
             else if (var == 57) launch_dyn<1, 5, 1>(c, items, n_items, md.nzm, A, B, out, partial);
+            else launch_dyn<1, 6, 1>(c, items, n_items, md.nzm, A, B, out, partial);
+          }
+        }
+        else if (var >= 60 && var < 70) {
+          // L1 policy of the row gathers (the fp64 R = 64 kernel on a uniform-valued tensor, c4)
+          if constexpr (sizeof(Real) == 8 && RT == 64) {
+            const bool ux = c.uniform_x;
+            if (var == 60 && ux) launch_dyn<1, 6, 4, 32, 4>(c, items, n_items, md.nzm, A, B, out, partial);
+            else if (var == 60) launch_dyn<1, 6, 1, 32, 4>(c, items, n_items, md.nzm, A, B, out, partial);
+            else if (var == 61 && ux) launch_dyn<1, 6, 4, 32, 5>(c, items, n_items, md.nzm, A, B, out, partial);
+            else if (var == 61) launch_dyn<1, 6, 1, 32, 5>(c, items, n_items, md.nzm, A, B, out, partial);
+            else if (var == 62 && ux) launch_dyn<1, 6, 4, 32, 6>(c, items, n_items, md.nzm, A, B, out, partial);
+            else if (var == 62) launch_dyn<1, 6, 1, 32, 6>(c, items, n_items, md.nzm, A, B, out, partial);
+            else if (var == 63 && ux) launch_dyn<1, 6, 4, 32, 7>(c, items, n_items, md.nzm, A, B, out, partial);
+            else if (var == 63) launch_dyn<1, 6, 1, 32, 7>(c, items, n_items, md.nzm, A, B, out, partial);
+            else if (ux) launch_dyn<1, 6, 4>(c, items, n_items, md.nzm, A, B, out, partial);
             else launch_dyn<1, 6, 1>(c, items, n_items, md.nzm, A, B, out, partial);
           }
         }
@@ -766,7 +782,20 @@ struct Impl {
     Real *M = reinterpret_cast<Real *>(c.M);
     if (begin_sweep) k_sweep_begin<<<1, 32, 0, c.stream>>>(c.st);
     SACD_TRY(mttkrp(c, mode, M));
-    SACD_TRY(prepare(c, mode, branch_override, begin_sweep, 1));
+    if (c.join_pending) {
+      // H and the branch need the previous mode's Gram and statistics, not this MTTKRP: they
+      // stay on the side branch, which joins here
+      cudaStream_t main_stream = c.stream;
+      c.stream = c.side;
+      const int rc_prep = prepare(c, mode, branch_override, begin_sweep, 1);
+      c.stream = main_stream;
+      SACD_TRY(rc_prep);
+      SACD_CUDA_TRY(cudaEventRecord(c.ev_join, c.side));
+      SACD_CUDA_TRY(cudaStreamWaitEvent(c.stream, c.ev_join, 0));
+      c.join_pending = false;
+    } else {
+      SACD_TRY(prepare(c, mode, branch_override, begin_sweep, 1));
+    }
     const int vflags0 = c.opt.variant == SACD_VARIANT_SNAPSHOT ? 2 : (c.opt.variant == SACD_VARIANT_JACOBI ? 1 : 0);
     const long long TR = rows_tr(c, vflags0);
     const long long nblk = (md.I + TR - 1) / TR;
@@ -786,6 +815,30 @@ struct Impl {
     }
     SACD_CUDA_TRY(cudaGetLastError());
     SACD_TRY(prof_end(c, 3, pe));
+    // fork (captured sweeps, not the last mode: every branch must rejoin inside the graph)
+    const bool fork = c.capturing && c.overlap && c.side && !end_sweep && !dec;
+    cudaStream_t main_stream = c.stream;
+    if (fork) {
+      SACD_CUDA_TRY(cudaEventRecord(c.ev_fork, c.stream));
+      SACD_CUDA_TRY(cudaStreamWaitEvent(c.side, c.ev_fork, 0));
+      c.stream = c.side;
+    }
+    const int rc_tail = mode_update_tail(c, mode, gn, nblk, end_sweep);
+    c.stream = main_stream;
+    SACD_TRY(rc_tail);
+    if (fork) {
+      SACD_CUDA_TRY(cudaEventRecord(c.ev_join, c.side));
+      c.join_pending = true;
+    }
+    return SACD_OK;
+  }
+
+  // the Gram of the updated factor and the pass statistics, on c.stream
+  static int mode_update_tail(Context &c, int mode, int gn, long long nblk, bool end_sweep) {
+    ModeData &md = c.m[mode];
+    double *ti_part = c.row_part, *md_part = c.row_part + c.max_row_blocks;
+    long long *e_part = c.cnt_part, *ech_part = c.cnt_part + c.max_row_blocks;
+    int pe = 0;
     if (gn > 0) {  // the row kernel wrote one Gram partial per CTA: fixed-order reduce only
       pe = prof_begin(c, 4);
       k_gram_reduce<<<gram_reduce_blocks(c.R), 256, 0, c.stream>>>(c.R, gn, c.gram_part, md.G);

@@ -61,8 +61,10 @@ def tuning():
             F = O.init_factors(dims, R, 5)
             Mo = [O.mttkrp(c, v, dims, n, F) for n in range(3)]
             ref = None
-            for var in (1, 10, 13, 20, 22, 24, 26, 27, 39, 40, 43, 0):
+            for var in (1, 10, 13, 20, 22, 24, 26, 27, 39, 40, 43, 60, 62, 0):
                 if var == 39 and precision == "f32":
+                    continue
+                if var >= 50 and not (precision == "f64" and R in (33, 64)):
                     continue
                 with Sacd(c, v, dims, R, 5, precision=precision, nnz_per_item=48, mttkrp_variant=var) as g:
                     Ms = [g.mttkrp(n) for n in range(3)]

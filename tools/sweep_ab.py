@@ -22,10 +22,16 @@ c, v = SI.make_tensor(cfg, device="cuda")
 stream = torch.cuda.Stream()
 for spec in a.variants.split(";"):
     kw = {}
+    env = {}
     for item in spec.split(","):
-        if "=" in item:
+        if item.startswith("env:"):  # e.g. env:SACD_NO_OVERLAP=1 (read by sacd_init)
+            k, val = item[4:].split("=")
+            env[k] = val
+        elif "=" in item:
             k, val = item.split("=")
             kw[k] = int(val)
+    saved = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
     with Sacd(c, v, cfg.dims, cfg.rank, cfg.seed, stream=stream.cuda_stream, **kw) as g:
         g.iterate(a.warmup)
         g.sync()
@@ -42,5 +48,10 @@ for spec in a.variants.split(";"):
         g.sync()
         p = g.profile_read()
         br = " ".join(f"{k} {p[k][0] / a.sweeps:.3f}" for k in p)
+    for k, val in saved.items():
+        if val is None:
+            os.environ.pop(k, None)
+        else:
+            os.environ[k] = val
     print(f"{a.config} [{spec}]: {ms:.3f} ms/sweep ({1e3 / ms:.2f} sweeps/s), f after {a.warmup + a.sweeps} = {f:.12e}; "
           f"eager ms/sweep: {br}", flush=True)
