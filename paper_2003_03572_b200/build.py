@@ -46,11 +46,14 @@ def _fingerprint(flavour="default") -> str:
     h = hashlib.sha256()
     deps = sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC)) + [os.path.join(ROOT, "include", "sacd.h"),
                                                                         os.path.abspath(__file__)]
+    # names relative to the repo root and flags with the root / NCCL prefixes removed: the
+    # checkout's location (a scratch path on the GPU box) must not make a matching .so stale
+    rel = lambda x: x.replace(ROOT, "<root>").replace(NCCL, "<nccl>")
     for d in deps:
-        h.update(d.encode())
+        h.update(rel(d).encode())
         with open(d, "rb") as fh:
             h.update(fh.read())
-    h.update(repr((FLAGS, LIBS, SOURCES, FLAVOURS[flavour])).encode())
+    h.update(repr(([rel(f) for f in FLAGS], [rel(f) for f in LIBS], SOURCES, FLAVOURS[flavour])).encode())
     try:
         h.update(subprocess.run([NVCC, "--version"], capture_output=True, text=True).stdout.encode())
     except OSError:

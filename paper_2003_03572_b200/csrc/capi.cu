@@ -244,12 +244,10 @@ static int capture_graph(Context &c) {
   SACD_CUDA_TRY(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
   int rc = SACD_OK;
   c.capturing = true;
-  c.join_pending = false;
   for (int n = 0; n < 3 && rc == SACD_OK; ++n)
     rc = c.sharded ? launch_sharded_mode_update(c, n, SACD_BR_AUTO, n == 0, n == 2, nullptr)
                    : launch_mode_update(c, n, SACD_BR_AUTO, n == 0, n == 2, nullptr);
   c.capturing = false;
-  c.join_pending = false;
   c.opt.profile = saved_profile;
   cudaGraph_t g = nullptr;
   cudaError_t e = cudaStreamEndCapture(c.stream, &g);
@@ -326,9 +324,6 @@ static void destroy(sacd_ctx *c) {
   if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
   if (c->graph) cudaGraphDestroy(c->graph);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
-  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
-  if (c->ev_join) cudaEventDestroy(c->ev_join);
-  if (c->side) cudaStreamDestroy(c->side);
   for (int n = 0; n < 3; ++n) {
     ModeData &m = c->m[n];
     cudaFree(m.idx_a);
@@ -1080,19 +1075,6 @@ int sacd_init(sacd_ctx **out, const uint32_t *coords, const float *vals, int64_t
       return SACD_ECUDA;
     }
     c->own_stream = true;
-  }
-  if (!c->sharded) {  // side branch of the captured sweep (sacd_internal.cuh: Context::side)
-    const char *no = getenv("SACD_NO_OVERLAP");
-    c->overlap = !(no && no[0] == '1');
-    int least = 0, greatest = 0;
-    cudaDeviceGetStreamPriorityRange(&least, &greatest);
-    if (cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, greatest) != cudaSuccess ||
-        cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess) {
-      set_error("sacd_init: side stream creation failed");
-      destroy(c);
-      return SACD_ECUDA;
-    }
   }
   const int rc = init_impl(c, coords, vals, seed);
   if (rc != SACD_OK) {

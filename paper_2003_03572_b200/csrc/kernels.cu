@@ -782,20 +782,7 @@ struct Impl {
     Real *M = reinterpret_cast<Real *>(c.M);
     if (begin_sweep) k_sweep_begin<<<1, 32, 0, c.stream>>>(c.st);
     SACD_TRY(mttkrp(c, mode, M));
-    if (c.join_pending) {
-      // H and the branch need the previous mode's Gram and statistics, not this MTTKRP: they
-      // stay on the side branch, which joins here
-      cudaStream_t main_stream = c.stream;
-      c.stream = c.side;
-      const int rc_prep = prepare(c, mode, branch_override, begin_sweep, 1);
-      c.stream = main_stream;
-      SACD_TRY(rc_prep);
-      SACD_CUDA_TRY(cudaEventRecord(c.ev_join, c.side));
-      SACD_CUDA_TRY(cudaStreamWaitEvent(c.stream, c.ev_join, 0));
-      c.join_pending = false;
-    } else {
-      SACD_TRY(prepare(c, mode, branch_override, begin_sweep, 1));
-    }
+    SACD_TRY(prepare(c, mode, branch_override, begin_sweep, 1));
     const int vflags0 = c.opt.variant == SACD_VARIANT_SNAPSHOT ? 2 : (c.opt.variant == SACD_VARIANT_JACOBI ? 1 : 0);
     const long long TR = rows_tr(c, vflags0);
     const long long nblk = (md.I + TR - 1) / TR;
@@ -815,30 +802,6 @@ struct Impl {
     }
     SACD_CUDA_TRY(cudaGetLastError());
     SACD_TRY(prof_end(c, 3, pe));
-    // fork (captured sweeps, not the last mode: every branch must rejoin inside the graph)
-    const bool fork = c.capturing && c.overlap && c.side && !end_sweep && !dec;
-    cudaStream_t main_stream = c.stream;
-    if (fork) {
-      SACD_CUDA_TRY(cudaEventRecord(c.ev_fork, c.stream));
-      SACD_CUDA_TRY(cudaStreamWaitEvent(c.side, c.ev_fork, 0));
-      c.stream = c.side;
-    }
-    const int rc_tail = mode_update_tail(c, mode, gn, nblk, end_sweep);
-    c.stream = main_stream;
-    SACD_TRY(rc_tail);
-    if (fork) {
-      SACD_CUDA_TRY(cudaEventRecord(c.ev_join, c.side));
-      c.join_pending = true;
-    }
-    return SACD_OK;
-  }
-
-  // the Gram of the updated factor and the pass statistics, on c.stream
-  static int mode_update_tail(Context &c, int mode, int gn, long long nblk, bool end_sweep) {
-    ModeData &md = c.m[mode];
-    double *ti_part = c.row_part, *md_part = c.row_part + c.max_row_blocks;
-    long long *e_part = c.cnt_part, *ech_part = c.cnt_part + c.max_row_blocks;
-    int pe = 0;
     if (gn > 0) {  // the row kernel wrote one Gram partial per CTA: fixed-order reduce only
       pe = prof_begin(c, 4);
       k_gram_reduce<<<gram_reduce_blocks(c.R), 256, 0, c.stream>>>(c.R, gn, c.gram_part, md.G);

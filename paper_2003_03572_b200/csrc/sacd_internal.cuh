@@ -252,14 +252,6 @@ struct Context {
   void *const *rows_peers = nullptr;  // set around a shard's fused row-update launch (p2p)
   int rows_me = 0;
   bool capturing = false;         // inside capture_graph (no host synchronisation allowed)
-  // Captured unsharded sweeps fork the Gram refresh + pass statistics of modes 0 and 1 onto a
-  // side branch of the graph: the next mode's MTTKRP needs the updated factor, not its Gram,
-  // so the HBM-streaming Gram runs under the L1-bound MTTKRP and joins before that mode's H.
-  // The same kernels on the same data in the same per-kernel order: results are unchanged.
-  cudaStream_t side = nullptr;    // highest priority: its CTAs are placed before the MTTKRP's
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  bool join_pending = false;
-  bool overlap = true;            // SACD_NO_OVERLAP=1 (A/B measurements) turns the fork off
   void *Fold = nullptr;           // Real [maxI * pitch]: owned rows before the pass
   uint32_t *didx = nullptr;       // [sum_q cap_q] list of rank q at doff[q]
   void *dval = nullptr;           // Real [sum_q cap_q]

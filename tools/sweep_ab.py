@@ -24,7 +24,7 @@ for spec in a.variants.split(";"):
     kw = {}
     env = {}
     for item in spec.split(","):
-        if item.startswith("env:"):  # e.g. env:SACD_NO_OVERLAP=1 (read by sacd_init)
+        if item.startswith("env:"):  # an environment variable set around that variant's sacd_init, e.g. env:SACD_POOL_RELEASE_MB=0
             k, val = item[4:].split("=")
             env[k] = val
         elif "=" in item:
