@@ -438,8 +438,7 @@ __device__ __forceinline__ void prefetch_rows(const uint4 &m, bool valid, const 
 // shared-memory broadcast per nonzero, 3 = as 2 with the workers' slots padded apart (two
 // workers of a warp read different banks: one wavefront serves both), 4 = every value of the
 // tensor equals xu (e.g. binary tensors; detected at sacd_init): no x broadcast at all, x =
-// xu for the batch's nonzeros and 0 past the item's end; 5 = as 4 and 6 = as 1, with the b
-// indices of the batch staged in shared memory and read back four per 16-byte broadcast.
+// xu for the batch's nonzeros and 0 past the item's end.
 template <int XS>
 __device__ __forceinline__ int xs_slot(int t) {
   return XS == 3 ? t + (t >> 4) : t;
@@ -467,17 +466,8 @@ __device__ __forceinline__ void lean_item(long long item, const WorkItem *__rest
   SACD_DBG(SACD_DASSERT(nz0 >= 0 && nz0 < nz1 && nz1 <= g_dbg.nnz && slot < g_dbg.nslots));
   const Real *Al = A + lane * VEC;
   const Real *Bl = B + lane * VEC;
-  __shared__ __align__(16) Real xsb[(XS == 1 || XS == 6) ? 2 : 1][(XS == 1 || XS == 6) ? 256 : 1];
+  __shared__ __align__(16) Real xsb[XS == 1 ? 2 : 1][XS == 1 ? 256 : 1];
   __shared__ __align__(16) uint4 rsb[(XS == 2 || XS == 3) ? 2 : 1][(XS == 2 || XS == 3) ? 272 : 1];
-  // XS = 5 / 6: the batch's b indices staged in shared memory and read back four at a time
-  // (one 16-byte broadcast, one L1 wavefront, per four nonzeros instead of one shuffle each)
-  // The a indices and row ids of the batch go the same way (read back one at a time, at the
-  // fiber / row starts, as the shuffles were): no register of the batch's records stays live
-  // while the batch is consumed, which pays for the four registers of the broadcast.  One
-  // buffer, two __syncwarp per batch.
-  constexpr bool IS = XS == 5 || XS == 6 || XS == 7;  // 7: as 5, two indices per 8-byte broadcast
-  __shared__ __align__(16) uint32_t isb[IS ? 256 : 4], iax[IS ? 256 : 1], irw[IS ? 256 : 1];
-  uint4 iq = make_uint4(0u, 0u, 0u, 0u);
   const int wbase = threadIdx.x & ~(SW - 1);
   int par = 0;
   SR arow;
@@ -505,17 +495,9 @@ __device__ __forceinline__ void lean_item(long long item, const WorkItem *__rest
     // x of this lane's nonzero, converted once per batch (F2F runs on the narrow XU pipe:
     // converting per nonzero in every lane of the worker made the fp64 kernel XU-bound)
     const Real xl = (Real)__uint_as_float(my.z);
-    if constexpr (IS) {
-      __syncwarp(mask);  // every lane is done with the previous batch's slots
-      isb[threadIdx.x] = my.y;
-      iax[threadIdx.x] = my.x;
-      irw[threadIdx.x] = my.w;
-    }
-    if constexpr (XS == 1 || XS == 6) {
+    if constexpr (XS == 1) {
       par ^= 1;
       xsb[par][threadIdx.x] = xl;
-      __syncwarp(mask);
-    } else if constexpr (XS == 5 || XS == 7) {
       __syncwarp(mask);
     } else if constexpr (XS == 2 || XS == 3) {
       par ^= 1;
@@ -541,23 +523,6 @@ __device__ __forceinline__ void lean_item(long long item, const WorkItem *__rest
         fb[j] = r.x;
         if constexpr (sizeof(Real) == 8) xr[j % (D + 1)] = __hiloint2double((int)r.w, (int)r.z);
         else xr[j % (D + 1)] = __uint_as_float(r.z);
-      } else if constexpr (IS) {
-        // volatile: issued where the pipeline needs it (hoisted to the top of the batch, the
-        // eight 16-byte loads would hold 32 registers and spill)
-        if constexpr (XS == 7) {
-          if ((j & 1) == 0) {
-            const unsigned sa = (unsigned)__cvta_generic_to_shared(&isb[wbase + j]);
-            asm volatile("ld.volatile.shared.v2.u32 {%0,%1}, [%2];" : "=r"(iq.x), "=r"(iq.y) : "r"(sa));
-          }
-          fb[j] = (j & 1) == 0 ? iq.x : iq.y;
-        } else {
-          if ((j & 3) == 0) {
-            const unsigned sa = (unsigned)__cvta_generic_to_shared(&isb[wbase + j]);
-            asm volatile("ld.volatile.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
-                         : "=r"(iq.x), "=r"(iq.y), "=r"(iq.z), "=r"(iq.w) : "r"(sa));
-          }
-          fb[j] = (j & 3) == 0 ? iq.x : ((j & 3) == 1 ? iq.y : ((j & 3) == 2 ? iq.z : iq.w));
-        }
       } else {
         fb[j] = __shfl_sync(mask, my.y, j, SW);
       }
@@ -576,8 +541,8 @@ __device__ __forceinline__ void lean_item(long long item, const WorkItem *__rest
       }
       Real x;
       if constexpr (XS == 2 || XS == 3) x = xr[j % (D + 1)];
-      else if constexpr (XS == 1 || XS == 6) x = xsb[par][wbase + j];
-      else if constexpr (XS == 4 || XS == 5 || XS == 7) x = (base + j < nz1) ? xu : Real(0);
+      else if constexpr (XS == 1) x = xsb[par][wbase + j];
+      else if constexpr (XS == 4) x = (base + j < nz1) ? xu : Real(0);
       else x = __shfl_sync(mask, xl, j, SW);
       if (fb[j] & kFiberStart) {
 #pragma unroll
@@ -590,13 +555,10 @@ __device__ __forceinline__ void lean_item(long long item, const WorkItem *__rest
           else if (cur_row >= 0) SR::store_from(M + (long long)cur_row * RT + lane * VEC, acc);
 #pragma unroll
           for (int k = 0; k < E; ++k) acc[k] = Real(0);
-          if constexpr (IS) cur_row = (int)irw[wbase + j];
-          else cur_row = (int)__shfl_sync(mask, my.w, j, SW);
+          cur_row = (int)__shfl_sync(mask, my.w, j, SW);
           SACD_DBG(SACD_DASSERT(cur_row >= 0 && cur_row < g_dbg.In));
         }
-        uint32_t ai;
-        if constexpr (IS) ai = iax[wbase + j] & kIdxMask;
-        else ai = __shfl_sync(mask, my.x, j, SW) & kIdxMask;
+        const uint32_t ai = __shfl_sync(mask, my.x, j, SW) & kIdxMask;
         SACD_DBG(SACD_DASSERT(ai < g_dbg.Ia));
         arow.template load_hint<AH>(Al + (long long)ai * RT);
       }

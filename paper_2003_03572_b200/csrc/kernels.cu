@@ -270,13 +270,6 @@ struct Impl {
             else if (var == 62) launch_dyn<1, 6, 1, 32, 6>(c, items, n_items, md.nzm, A, B, out, partial);
             else if (var == 63 && ux) launch_dyn<1, 6, 4, 32, 7>(c, items, n_items, md.nzm, A, B, out, partial);
             else if (var == 63) launch_dyn<1, 6, 1, 32, 7>(c, items, n_items, md.nzm, A, B, out, partial);
-            else if (var == 64 && ux) launch_dyn<1, 6, 5>(c, items, n_items, md.nzm, A, B, out, partial);
-            else if (var == 64) launch_dyn<1, 6, 6>(c, items, n_items, md.nzm, A, B, out, partial);
-            else if (var == 65 && ux) launch_dyn<2, 6, 5>(c, items, n_items, md.nzm, A, B, out, partial);
-            else if (var == 65) launch_dyn<2, 6, 6>(c, items, n_items, md.nzm, A, B, out, partial);
-            else if (var == 67 && ux) launch_dyn<1, 6, 7>(c, items, n_items, md.nzm, A, B, out, partial);
-            else if (var == 66 && ux) launch_dyn<1, 5, 5>(c, items, n_items, md.nzm, A, B, out, partial);
-            else if (var == 66) launch_dyn<1, 5, 6>(c, items, n_items, md.nzm, A, B, out, partial);
             else if (ux) launch_dyn<1, 6, 4>(c, items, n_items, md.nzm, A, B, out, partial);
             else launch_dyn<1, 6, 1>(c, items, n_items, md.nzm, A, B, out, partial);
           }

@@ -115,3 +115,31 @@ def test_torch_inputs_are_validated(lib):
     for c, v in bad:
         with pytest.raises((TypeError, ValueError)):
             sacd.Sacd(c, v, (2, 2, 2), 2, 1)
+
+
+def test_build_stamp_is_path_independent_and_taken_before_compile(tmp_path):
+    """A prebuilt .so travels to the GPU box into a scratch checkout: its stamp must match
+    there (no silent 3-minute rebuild inside the bench or the tests), and an edit made while
+    nvcc runs must leave the stamp stale (the stamp is the fingerprint taken before nvcc
+    reads the sources)."""
+    import importlib.util
+    import inspect
+    import shutil
+    from paper_2003_03572_b200 import build as B
+    here = B._fingerprint("default")
+    root2 = tmp_path / "elsewhere"
+    (root2 / "paper_2003_03572_b200").mkdir(parents=True)
+    shutil.copytree(os.path.join(B.ROOT, "include"), root2 / "include")
+    shutil.copytree(B.CSRC, root2 / "paper_2003_03572_b200" / "csrc")
+    shutil.copy(os.path.join(B.HERE, "build.py"), root2 / "paper_2003_03572_b200" / "build.py")
+    spec = importlib.util.spec_from_file_location("build_elsewhere", root2 / "paper_2003_03572_b200" / "build.py")
+    B2 = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(B2)
+    assert B2.ROOT != B.ROOT
+    assert B2._fingerprint("default") == here
+    assert B2._fingerprint("tuning") != here
+    with open(root2 / "paper_2003_03572_b200" / "csrc" / "kernels.cu", "a") as fh:
+        fh.write("// edited\n")
+    assert B2._fingerprint("default") != here
+    src = inspect.getsource(B.build)
+    assert src.index("fp = _fingerprint(flavour)") < src.index("subprocess.run(cmd")
